@@ -1,0 +1,566 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes front-end over the two CPU checkers.
+
+``Port`` wraps the C restatement (oracle/tsgm_oracle.c); ``Reference`` wraps
+the reference's own sources compiled in place (oracle/Makefile +
+oracle/ref_runner.cpp). Both expose the same numpy-level API so a test can run
+the same comparison against either. Parameter objects are duck-typed: anything
+with the attribute names of ``Calib`` / ``SgmParams`` / ``FilterConfig``
+(including the product's own dataclasses) is accepted.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_DIR = os.path.join(HERE, "_ref")
+PORT_SO = os.path.join(REF_DIR, "liboracle.so")
+REF_SO = os.path.join(REF_DIR, "libtsgm_ref.so")
+REFERENCE_SRC = "/root/reference/proj"
+
+
+@dataclass
+class Calib:
+    focal_px: float = 720.0
+    cx: float = 621.0
+    cy: float = 187.5
+    baseline_m: float = 0.54
+    width: int = 1242
+    height: int = 375
+    d_max: int = 128
+
+
+@dataclass
+class SgmParams:
+    p1: int = 6
+    p2: int = 65
+    paths: int = 8
+    path_set: int = 0  # 0 nondiagonal, 1 diagonal (sgm.hpp:10-13)
+    d_max: int = 128
+
+
+@dataclass
+class FilterConfig:
+    q: float = 0.5
+    r: float = 1.0
+    p_init: float = 4096.0
+    disc_thresh: float = 2.0
+    min_range_halfwidth: int = 2
+    range_use_stddev: bool = False
+    range_stddev_gain: float = 2.0
+
+
+def build(reference: bool = True) -> None:
+    """Compile the checkers (``make -C oracle``); the reference only when its
+    sources are present (this container, not the GPU box)."""
+    targets = ["oracle"]
+    if reference and os.path.isdir(os.path.join(REFERENCE_SRC, "src")):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _u8(a):
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _sgm_arr(p):
+    return np.array([p.p1, p.p2, p.paths, int(p.path_set), p.d_max], dtype=np.int32)
+
+
+def _filter_arr(f):
+    return np.array([f.q, f.r, f.p_init, f.disc_thresh, f.min_range_halfwidth,
+                     1.0 if f.range_use_stddev else 0.0, f.range_stddev_gain], dtype=np.float64)
+
+
+def offsets_of(lo, hi):
+    n = (hi.astype(np.int64) - lo.astype(np.int64) + 1).ravel()
+    off = np.zeros(n.size + 1, dtype=np.int64)
+    np.cumsum(n, out=off[1:])
+    return off.astype(np.uint32) if off[-1] <= 0xFFFFFFFF else off
+
+
+class _Lib:
+    so_path = ""
+
+    def __init__(self):
+        if not os.path.exists(self.so_path):
+            raise FileNotFoundError(f"{self.so_path} missing: run `make -C oracle`")
+        self.lib = C.CDLL(self.so_path)
+
+    def _check(self, rc, errfn):
+        if rc == 0:
+            return
+        msg = errfn().decode()
+        if rc == 1:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+
+class Reference(_Lib):
+    """The reference's own code (oracle/_ref/libtsgm_ref.so)."""
+
+    so_path = REF_SO
+    kind = "reference"
+
+    def __init__(self):
+        super().__init__()
+        self.lib.ref_last_error.restype = C.c_char_p
+
+    def _c(self, rc):
+        self._check(rc, self.lib.ref_last_error)
+
+    def census(self, img):
+        img = _u8(img)
+        h, w = img.shape
+        sig = np.zeros((h, w), np.uint32)
+        self._c(self.lib.ref_census(_p(img), w, h, _p(sig)))
+        return sig
+
+    def cost_volume(self, left, right, lo, hi, threads=1):
+        left, right = _u8(left), _u8(right)
+        h, w = left.shape
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        off = offsets_of(lo, hi)
+        cap = int(off[-1])
+        cost = np.zeros(cap + 1, np.uint8)
+        off32 = np.zeros(w * h + 1, np.uint32)
+        self._c(self.lib.ref_cost_volume(_p(left), _p(right), w, h, _p(lo), _p(hi), _p(off32),
+                                         _p(cost), C.c_uint64(cap + 1), threads))
+        return off32, cost[:cap]
+
+    def aggregate(self, cost, lo, hi, params):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        h, w = lo.shape
+        cost = _u8(cost)
+        agg = np.zeros(max(cost.size, 1), np.uint16)
+        sp = _sgm_arr(params)
+        self._c(self.lib.ref_aggregate(_p(cost), _p(lo), _p(hi), w, h, _p(sp), _p(agg)))
+        return agg[: cost.size]
+
+    def wta(self, agg, lo, hi):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        h, w = lo.shape
+        agg = np.ascontiguousarray(agg, np.uint16)
+        d = np.zeros((h, w), np.int32)
+        v = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_wta(_p(agg), _p(lo), _p(hi), w, h, _p(d), _p(v)))
+        return d, v
+
+    def median(self, d, valid):
+        d = np.ascontiguousarray(d, np.int32)
+        valid = _u8(valid)
+        h, w = d.shape
+        od = np.zeros((h, w), np.int32)
+        ov = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_median(_p(d), _p(valid), w, h, _p(od), _p(ov)))
+        return od, ov
+
+    def sgm_match(self, left, right, lo, hi, params, threads=1):
+        left, right = _u8(left), _u8(right)
+        h, w = left.shape
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        d = np.zeros((h, w), np.int32)
+        v = np.zeros((h, w), np.uint8)
+        sp = _sgm_arr(params)
+        self._c(self.lib.ref_sgm_match(_p(left), _p(right), w, h, _p(lo), _p(hi), _p(sp),
+                                       threads, _p(d), _p(v)))
+        return d, v
+
+    def relative_motion(self, prev12, cur12):
+        prev12, cur12 = _f64(prev12).ravel(), _f64(cur12).ravel()
+        r = np.zeros(9)
+        t = np.zeros(3)
+        self._c(self.lib.ref_relative_motion(_p(prev12), _p(cur12), _p(r), _p(t)))
+        return r.reshape(3, 3), t
+
+    def homography(self, R, t, calib):
+        R, t = _f64(R).ravel(), _f64(t).ravel()
+        c4 = np.array([calib.focal_px, calib.cx, calib.cy, calib.baseline_m])
+        H = np.zeros(16)
+        self._c(self.lib.ref_homography(_p(R), _p(t), _p(c4), calib.width, calib.height,
+                                        calib.d_max, _p(H)))
+        return H.reshape(4, 4)
+
+    def warp(self, d, p, valid, H, d_max):
+        d, p, valid, H = _f64(d), _f64(p), _u8(valid), _f64(H).ravel()
+        h, w = d.shape
+        od, op, osrc = (np.zeros((h, w)) for _ in range(3))
+        ov = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_warp(_p(d), _p(p), _p(valid), w, h, _p(H), d_max, _p(od), _p(op),
+                                  _p(ov), _p(osrc)))
+        return od, op, ov, osrc
+
+    def predict(self, d, p, valid, R, t, calib, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        R, t = _f64(R).ravel(), _f64(t).ravel()
+        h, w = d.shape
+        c4 = np.array([calib.focal_px, calib.cx, calib.cy, calib.baseline_m])
+        fa = _filter_arr(filt)
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_predict(_p(d), _p(p), _p(valid), w, h, _p(R), _p(t), _p(c4),
+                                     calib.d_max, _p(fa), _p(od), _p(op), _p(ov)))
+        return od, op, ov
+
+    def reject(self, d, p, valid, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        h, w = d.shape
+        fa = _filter_arr(filt)
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_reject(_p(d), _p(p), _p(valid), w, h, _p(fa), _p(od), _p(op),
+                                    _p(ov)))
+        return od, op, ov
+
+    def fill(self, d, p, valid):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        h, w = d.shape
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_fill(_p(d), _p(p), _p(valid), w, h, _p(od), _p(op), _p(ov)))
+        return od, op, ov
+
+    def ranges(self, d, p, valid, calib, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        h, w = d.shape
+        c4 = np.array([calib.focal_px, calib.cx, calib.cy, calib.baseline_m])
+        fa = _filter_arr(filt)
+        lo = np.zeros((h, w), np.uint16)
+        hi = np.zeros((h, w), np.uint16)
+        self._c(self.lib.ref_ranges(_p(d), _p(p), _p(valid), w, h, _p(c4), calib.d_max, _p(fa),
+                                    _p(lo), _p(hi)))
+        return lo, hi
+
+    def correct(self, d, p, valid, md, mv, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        md, mv = np.ascontiguousarray(md, np.int32), _u8(mv)
+        h, w = d.shape
+        fa = _filter_arr(filt)
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_correct(_p(d), _p(p), _p(valid), _p(md), _p(mv), w, h, _p(fa),
+                                     _p(od), _p(op), _p(ov)))
+        return od, op, ov
+
+    def diff(self, d, p, valid, md, mv):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        md, mv = np.ascontiguousarray(md, np.int32), _u8(mv)
+        h, w = d.shape
+        out = np.zeros((h, w))
+        self._c(self.lib.ref_disparity_difference(_p(d), _p(p), _p(valid), _p(md), _p(mv), w, h,
+                                                  _p(out)))
+        return out
+
+    def step(self, state, left, right, R, t, calib, params, filt, threads=1):
+        """tsgm::step. ``state`` = (d, p, valid) or None for the default state."""
+        left, right = _u8(left), _u8(right)
+        h, w = left.shape
+        R, t = _f64(R).ravel(), _f64(t).ravel()
+        c4 = np.array([calib.focal_px, calib.cx, calib.cy, calib.baseline_m])
+        sp, fa = _sgm_arr(params), _filter_arr(filt)
+        if state is None:
+            sd = sp_ = sv = None
+            sw = sh = 0
+        else:
+            sd, sp_, sv = _f64(state[0]), _f64(state[1]), _u8(state[2])
+            sh, sw = sd.shape
+        od, op, diff = np.zeros((h, w)), np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        ed = np.zeros((h, w), np.int32)
+        ev = np.zeros((h, w), np.uint8)
+        self._c(self.lib.ref_step(_p(sd), _p(sp_), _p(sv), sw, sh, _p(left), _p(right), w, h,
+                                  _p(R), _p(t), _p(c4), calib.d_max, _p(sp), _p(fa), threads,
+                                  _p(od), _p(op), _p(ov), _p(ed), _p(ev), _p(diff)))
+        return dict(d=od, p=op, valid=ov, export_d=ed, export_valid=ev, diff=diff)
+
+
+class _OrCalib(C.Structure):
+    _fields_ = [("focal_px", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("baseline_m", C.c_double), ("width", C.c_int), ("height", C.c_int),
+                ("d_max", C.c_int)]
+
+
+class _OrSgm(C.Structure):
+    _fields_ = [("p1", C.c_int), ("p2", C.c_int), ("paths", C.c_int), ("path_set", C.c_int),
+                ("d_max", C.c_int)]
+
+
+class _OrFilter(C.Structure):
+    _fields_ = [("q", C.c_double), ("r", C.c_double), ("p_init", C.c_double),
+                ("disc_thresh", C.c_double), ("min_range_halfwidth", C.c_int),
+                ("range_use_stddev", C.c_int), ("range_stddev_gain", C.c_double)]
+
+
+class _OrDebug(C.Structure):
+    _fields_ = [("pred_d", C.c_void_p), ("pred_p", C.c_void_p), ("pred_v", C.c_void_p),
+                ("lo", C.c_void_p), ("hi", C.c_void_p), ("meas_d", C.c_void_p),
+                ("meas_v", C.c_void_p), ("mask", C.c_void_p), ("mask_tau", C.c_double)]
+
+
+def _calib(c):
+    return _OrCalib(c.focal_px, c.cx, c.cy, c.baseline_m, c.width, c.height, c.d_max)
+
+
+def _sgm(p):
+    return _OrSgm(p.p1, p.p2, p.paths, int(p.path_set), p.d_max)
+
+
+def _filt(f):
+    return _OrFilter(f.q, f.r, f.p_init, f.disc_thresh, f.min_range_halfwidth,
+                     1 if f.range_use_stddev else 0, f.range_stddev_gain)
+
+
+class Port(_Lib):
+    """The C restatement (oracle/_ref/liboracle.so)."""
+
+    so_path = PORT_SO
+    kind = "port"
+
+    def __init__(self):
+        super().__init__()
+        self.lib.or_last_error.restype = C.c_char_p
+        self.lib.or_offsets.restype = C.c_int64
+
+    def _c(self, rc):
+        self._check(rc, self.lib.or_last_error)
+
+    def census(self, img):
+        img = _u8(img)
+        h, w = img.shape
+        sig = np.zeros((h, w), np.uint32)
+        self.lib.or_census(_p(img), w, h, _p(sig))
+        return sig
+
+    def offsets(self, lo, hi):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        off = np.zeros(lo.size + 1, np.uint32)
+        n = self.lib.or_offsets(_p(lo), _p(hi), C.c_size_t(lo.size), _p(off))
+        if n < 0:
+            self._c(1)
+        return off
+
+    def cost_volume(self, left, right, lo, hi, threads=1):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        h, w = lo.shape
+        sl, sr = self.census(left), self.census(right)
+        off = self.offsets(lo, hi)
+        cost = np.zeros(int(off[-1]) + 1, np.uint8)
+        self.lib.or_cost_volume(_p(sl), _p(sr), w, h, _p(lo), _p(off), _p(cost))
+        return off, cost[: int(off[-1])]
+
+    def aggregate(self, cost, lo, hi, params):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        h, w = lo.shape
+        off = self.offsets(lo, hi)
+        cost = _u8(cost)
+        agg = np.zeros(max(cost.size, 1), np.uint16)
+        sp = _sgm(params)
+        self._c(self.lib.or_aggregate(_p(cost), _p(lo), _p(off), w, h, C.byref(sp), _p(agg)))
+        return agg[: cost.size]
+
+    def aggregate_direction(self, cost, lo, hi, dx, dy, p1, p2):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        h, w = lo.shape
+        off = self.offsets(lo, hi)
+        cost = _u8(cost)
+        out = np.zeros(max(cost.size, 1), np.uint16)
+        self.lib.or_aggregate_direction(_p(cost), _p(lo), _p(off), w, h, dx, dy, p1, p2, _p(out))
+        return out[: cost.size]
+
+    def wta(self, agg, lo, hi):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        h, w = lo.shape
+        off = self.offsets(lo, hi)
+        agg = np.ascontiguousarray(agg, np.uint16)
+        d = np.zeros((h, w), np.int32)
+        v = np.zeros((h, w), np.uint8)
+        self.lib.or_wta(_p(agg), _p(lo), _p(off), w, h, _p(d), _p(v))
+        return d, v
+
+    def median(self, d, valid):
+        d = np.ascontiguousarray(d, np.int32)
+        valid = _u8(valid)
+        h, w = d.shape
+        od = np.zeros((h, w), np.int32)
+        ov = np.zeros((h, w), np.uint8)
+        self.lib.or_median(_p(d), _p(valid), w, h, _p(od), _p(ov))
+        return od, ov
+
+    def sgm_match(self, left, right, lo, hi, params, threads=1):
+        left, right = _u8(left), _u8(right)
+        h, w = left.shape
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        d = np.zeros((h, w), np.int32)
+        v = np.zeros((h, w), np.uint8)
+        sp = _sgm(params)
+        self._c(self.lib.or_sgm_match(_p(left), _p(right), w, h, _p(lo), _p(hi), C.byref(sp),
+                                      _p(d), _p(v)))
+        return d, v
+
+    def relative_motion(self, prev12, cur12):
+        prev12, cur12 = _f64(prev12).ravel(), _f64(cur12).ravel()
+        r = np.zeros(9)
+        t = np.zeros(3)
+        self._c(self.lib.or_relative_motion(_p(prev12), _p(cur12), _p(r), _p(t)))
+        return r.reshape(3, 3), t
+
+    def homography(self, R, t, calib):
+        R, t = _f64(R).ravel(), _f64(t).ravel()
+        H = np.zeros(16)
+        c = _calib(calib)
+        self._c(self.lib.or_homography(_p(R), _p(t), C.byref(c), _p(H)))
+        return H.reshape(4, 4)
+
+    def warp(self, d, p, valid, H, d_max):
+        d, p, valid, H = _f64(d), _f64(p), _u8(valid), _f64(H).ravel()
+        h, w = d.shape
+        od, op, osrc = (np.zeros((h, w)) for _ in range(3))
+        ov = np.zeros((h, w), np.uint8)
+        self.lib.or_warp(_p(d), _p(p), _p(valid), w, h, _p(H), d_max, _p(od), _p(op), _p(ov),
+                         _p(osrc))
+        return od, op, ov, osrc
+
+    def predict(self, d, p, valid, R, t, calib, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        R, t = _f64(R).ravel(), _f64(t).ravel()
+        h, w = d.shape
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        c, f = _calib(calib), _filt(filt)
+        self._c(self.lib.or_predict(_p(d), _p(p), _p(valid), w, h, _p(R), _p(t), C.byref(c),
+                                    C.byref(f), _p(od), _p(op), _p(ov)))
+        return od, op, ov
+
+    def reject(self, d, p, valid, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        h, w = d.shape
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        self.lib.or_reject(_p(d), _p(p), _p(valid), w, h, C.c_double(filt.disc_thresh), _p(od),
+                           _p(op), _p(ov))
+        return od, op, ov
+
+    def fill(self, d, p, valid):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        h, w = d.shape
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        self.lib.or_fill(_p(d), _p(p), _p(valid), w, h, _p(od), _p(op), _p(ov))
+        return od, op, ov
+
+    def ranges(self, d, p, valid, calib, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        h, w = d.shape
+        lo = np.zeros((h, w), np.uint16)
+        hi = np.zeros((h, w), np.uint16)
+        f = _filt(filt)
+        self.lib.or_ranges(_p(d), _p(p), _p(valid), w, h, calib.d_max, C.byref(f), _p(lo),
+                           _p(hi))
+        return lo, hi
+
+    def correct(self, d, p, valid, md, mv, filt):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        md, mv = np.ascontiguousarray(md, np.int32), _u8(mv)
+        h, w = d.shape
+        od, op = np.zeros((h, w)), np.zeros((h, w))
+        ov = np.zeros((h, w), np.uint8)
+        self.lib.or_correct(_p(d), _p(p), _p(valid), _p(md), _p(mv), w, h, C.c_double(filt.r),
+                            _p(od), _p(op), _p(ov))
+        return od, op, ov
+
+    def diff(self, d, p, valid, md, mv):
+        d, valid = _f64(d), _u8(valid)
+        md, mv = np.ascontiguousarray(md, np.int32), _u8(mv)
+        h, w = d.shape
+        out = np.zeros((h, w))
+        self.lib.or_diff(_p(d), _p(valid), _p(md), _p(mv), w, h, _p(out))
+        return out
+
+    def mask(self, d, p, valid, md, mv, r, tau):
+        d, p, valid = _f64(d), _f64(p), _u8(valid)
+        md, mv = np.ascontiguousarray(md, np.int32), _u8(mv)
+        h, w = d.shape
+        out = np.zeros((h, w), np.uint8)
+        self.lib.or_mask(_p(d), _p(p), _p(valid), _p(md), _p(mv), w, h, C.c_double(r),
+                         C.c_double(tau), _p(out))
+        return out
+
+    def render(self, d, valid):
+        d, valid = _f64(d), _u8(valid)
+        h, w = d.shape
+        od = np.zeros((h, w), np.int32)
+        ov = np.zeros((h, w), np.uint8)
+        self.lib.or_render(_p(d), _p(valid), w, h, _p(od), _p(ov))
+        return od, ov
+
+    def step(self, state, left, right, R, t, calib, params, filt, threads=1, debug=False,
+             mask_tau=3.0):
+        """tsgm::step; with ``debug`` also returns pred/ranges/meas/mask."""
+        left, right = _u8(left), _u8(right)
+        h, w = left.shape
+        R, t = _f64(R).ravel(), _f64(t).ravel()
+        c, sp, f = _calib(calib), _sgm(params), _filt(filt)
+        if state is None:
+            sd = sp_ = sv = None
+            sw = sh = 0
+        else:
+            sd, sp_, sv = _f64(state[0]), _f64(state[1]), _u8(state[2])
+            sh, sw = sd.shape
+        out = dict(d=np.zeros((h, w)), p=np.zeros((h, w)), valid=np.zeros((h, w), np.uint8),
+                   export_d=np.zeros((h, w), np.int32),
+                   export_valid=np.zeros((h, w), np.uint8), diff=np.zeros((h, w)))
+        dbg = None
+        if debug:
+            out.update(pred_d=np.zeros((h, w)), pred_p=np.zeros((h, w)),
+                       pred_valid=np.zeros((h, w), np.uint8), lo=np.zeros((h, w), np.uint16),
+                       hi=np.zeros((h, w), np.uint16), meas_d=np.zeros((h, w), np.int32),
+                       meas_valid=np.zeros((h, w), np.uint8), mask=np.zeros((h, w), np.uint8))
+            dbg = _OrDebug(*(out[k].ctypes.data for k in
+                             ("pred_d", "pred_p", "pred_valid", "lo", "hi", "meas_d",
+                              "meas_valid", "mask")), mask_tau)
+        self._c(self.lib.or_step(_p(sd), _p(sp_), _p(sv), sw, sh, _p(left), _p(right), w, h,
+                                 _p(R), _p(t), C.byref(c), C.byref(sp), C.byref(f),
+                                 _p(out["d"]), _p(out["p"]), _p(out["valid"]),
+                                 _p(out["export_d"]), _p(out["export_valid"]), _p(out["diff"]),
+                                 C.byref(dbg) if dbg is not None else None))
+        return out
+
+
+_port = None
+_reference = None
+
+
+def port() -> Port:
+    global _port
+    if _port is None:
+        _port = Port()
+    return _port
+
+
+def reference() -> Reference:
+    global _reference
+    if _reference is None:
+        _reference = Reference()
+    return _reference
