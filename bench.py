@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the tsgm per-frame hot path on B200 (driver contract).
+
+Workload (BASELINE.json configs[2], the metric's 1/2/4/8-GPU configuration):
+64 independent synthetic stereo sequences x 30 frames at 1242x375, D=128,
+8 paths, P1=10, P2=120, +-3 sigma reduced windows, seeds 0..63 with
+(seed % 5) movers. A "step" is one pass of the hot path over the whole batch:
+every slot reset to the empty state, then 30 batched frames (frame 0 full
+range, 29 reduced). Sequences are sharded contiguously over ranks with no
+data-path collective (one process per GPU); `value` = all frames all ranks
+processed / max-over-ranks device time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (the
+unmodified reference sources compiled in place into oracle/_ref, else the C
+restatement) on the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W_, H_, D_ = 1242, 375, 128
+N_SEQ, N_FRAMES = 64, 30
+P1, P2 = 10, 120
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def rank_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def shard(n_items: int, world: int, rank: int) -> range:
+    """Contiguous shard of n_items over world ranks (first ranks take the remainder)."""
+    base, rem = divmod(n_items, world)
+    start = rank * base + min(rank, rem)
+    return range(start, start + base + (1 if rank < rem else 0))
+
+
+def scene_cfg(seed: int, frames: int = N_FRAMES):
+    from paper_1809_07986_b200.scene import SceneConfig
+    return SceneConfig.baseline_config(2, seed=seed, n_movers=seed % 5, frames=frames)
+
+
+def params():
+    from paper_1809_07986_b200 import tsgm
+    calib = tsgm.StereoCalib(720.0, 621.0, 187.5, 0.54, W_, H_, D_)
+    sgm = tsgm.SgmParams(P1, P2, 8, 0, D_)
+    filt = tsgm.FilterConfig(q=0.5, r=1.0, p_init=4096.0, disc_thresh=2.0,
+                             min_range_halfwidth=2, range_use_stddev=True, range_stddev_gain=3.0)
+    return calib, sgm, filt
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+
+    from paper_1809_07986_b200 import tsgm
+    from paper_1809_07986_b200.scene import render
+
+    rank, world, local = rank_info()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    my = list(shard(args.seqs, world, rank))
+    n = len(my)
+    calib, sgm, filt = params()
+
+    # inputs: render this rank's sequences (host, pinned) and make them resident
+    nthreads = os.cpu_count() or 8
+    P = W_ * H_
+    host_l = torch.empty((n, args.frames, H_, W_), dtype=torch.uint8).pin_memory()
+    host_r = torch.empty((n, args.frames, H_, W_), dtype=torch.uint8).pin_memory()
+    motions = np.zeros((n, args.frames, 12))
+    for i, s in enumerate(my):
+        cfg = scene_cfg(s, args.frames)
+        L, R, poses, _ = render(cfg, 0, args.frames, threads=nthreads,
+                                out_left=host_l[i].numpy(), out_right=host_r[i].numpy())
+        for k in range(args.frames):
+            if k == 0:
+                Rm, t = np.eye(3), np.zeros(3)
+            else:
+                Rm, t = tsgm.relative_motion(poses[k - 1], poses[k])
+            motions[i, k, :9] = Rm.ravel()
+            motions[i, k, 9:] = t
+    dev_l = host_l.to(f"cuda:{local}")
+    dev_r = host_r.to(f"cuda:{local}")
+    torch.cuda.synchronize()
+
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, sgm, filt, max_slots=n, device=local))
+    slots = list(range(n))
+    lptr = [[dev_l[i, k].data_ptr() for i in range(n)] for k in range(args.frames)]
+    rptr = [[dev_r[i, k].data_ptr() for i in range(n)] for k in range(args.frames)]
+
+    def one_step_device():
+        for s in slots:
+            eng.reset(s)
+        for k in range(args.frames):
+            eng.step_device(slots, lptr[k], rptr[k], motions[:, k, :])
+
+    # pinned output buffers for the e2e leg (export map + posterior variance + mask)
+    out_ed = np.empty((n, H_, W_), np.int32)
+    out_ev = np.empty((n, H_, W_), np.uint8)
+    out_p = np.empty((n, H_, W_), np.float64)
+    out_mask = np.empty((n, H_, W_), np.uint8)
+    host_l_np = host_l.numpy()
+    host_r_np = host_r.numpy()
+
+    def one_step_e2e():
+        for s in slots:
+            eng.reset(s)
+        for k in range(args.frames):
+            eng.step(slots, [host_l_np[i, k] for i in range(n)],
+                     [host_r_np[i, k] for i in range(n)],
+                     [(motions[i, k, :9].reshape(3, 3), motions[i, k, 9:]) for i in range(n)])
+            for i in range(n):
+                eng.fetch(i, "export_d", out_ed[i])
+                eng.fetch(i, "export_valid", out_ev[i])
+                eng.fetch(i, "state_p", out_p[i])
+                eng.fetch(i, "mask", out_mask[i])
+    e2e_h2d = n * args.frames * 2 * P
+    e2e_d2h = n * args.frames * P * (4 + 1 + 8 + 1)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # warm-up
+    for _ in range(args.warmup):
+        one_step_device()
+    eng.sync()
+    cells_rank = float(sum(eng.cells(s) for s in slots))  # last frame only (for info)
+
+    # timed region: device-resident inputs
+    barrier()
+    l0 = eng.launches
+    with ClockSampler(local) as clk:
+        eng.timer_begin()
+        for _ in range(args.steps):
+            one_step_device()
+        ms = eng.timer_end()
+    launches = (eng.launches - l0) // max(1, args.steps)
+    barrier()
+    ms = max_over_ranks(ms)
+    ms_per_step = ms / args.steps
+
+    # cells per step (all frames) — count once, outside the timed region
+    cells_step = 0.0
+    for s in slots:
+        eng.reset(s)
+    for k in range(args.frames):
+        eng.step_device(slots, lptr[k], rptr[k], motions[:, k, :])
+        cells_step += sum(eng.cells(s) for s in slots)
+    cells_step = sum_over_ranks(cells_step)
+    frames_total = args.seqs * args.frames
+
+    # roofline of the dominant kernel (8-path C -> S aggregation), standalone,
+    # on the last (reduced) frame's volumes of all slots
+    agg_ms, agg_cells = eng.bench_aggregate(slots, reps=10)
+    b_agg = 3.0 * agg_cells + 4.0 * P * n
+    peak, peak_kind = peaks()
+    achieved = b_agg / (agg_ms * 1e-3) / 1e9
+
+    # e2e: public API with host buffers, H2D + D2H inside the timed region
+    one_step_e2e()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        one_step_e2e()
+    eng.sync()
+    e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
+    e2e_s = max_over_ranks(e2e_s)
+
+    result = None
+    if rank == 0:
+        value = frames_total / (ms_per_step * 1e-3)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_reference_sample(args, budget_s=args.cpu_budget)
+        traffic = load_traffic()
+        result = {
+            "metric": "frames/sec (batched tsgm step, 1242x375, D=128, 8 paths)",
+            "value": round(value, 2),
+            "unit": "frames/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "u8/u16 cost+aggregation, f64 Kalman state",
+            "data": "synthetic (seeded KITTI-like scenes, BASELINE configs[2]; no KITTI in image)",
+            "config": {"workload": "configs[2]: 64 sequences x 30 frames, 1242x375",
+                       "sequences": args.seqs, "frames": args.frames, "width": W_,
+                       "height": H_, "d_max": D_, "paths": 8, "p1": P1, "p2": P2,
+                       "window": "+-3 sigma (range_use_stddev, gain 3), min half-width 2",
+                       "parallelism": f"sequence shards over {world} GPU(s), no collective",
+                       "l2": "inputs larger than L2 (1.8 GB of frames + volumes per step)"},
+            "gdisp_evals_per_s": round(cells_step / (ms_per_step * 1e-3) / 1e9, 3),
+            "cells_per_step": int(cells_step),
+            "e2e": {"value": round(frames_total / e2e_s, 2), "unit": "frames/s",
+                    "h2d_bytes_per_step": int(e2e_h2d * world),
+                    "d2h_bytes_per_step": int(e2e_d2h * world),
+                    "outputs": "export map (i32 d + u8 valid), posterior p (f64), mask (u8)"},
+            "roofline": {"bound": "hbm", "kernel": "8-path aggregation C->S (standalone)",
+                         "achieved": round(achieved, 1), "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "algorithmic_bytes": int(b_agg), "ms": round(agg_ms, 4),
+                         "cells": int(agg_cells)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            result["cpu_baseline"] = cpu
+        print(json.dumps(result), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def load_traffic():
+    """dram bytes per launch of the aggregation from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("aggregate_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------- reference (CPU)
+def cpu_reference_sample(args, budget_s: float = 20.0, threads: int | None = None):
+    """Reference CPU step on the host cores: one sequence per thread (step()
+    is re-entrant), frame 0 (full range) plus reduced frames, timed per frame
+    under full concurrency. frames/s for the 30-frame mix is extrapolated as
+    threads * 30 / (t_frame0 + 29 * mean(t_reduced))."""
+    from oracle import oracle as o
+    from paper_1809_07986_b200.scene import render
+
+    kind = "reference"
+    try:
+        impl = o.reference()
+    except Exception:
+        impl = o.port()
+        kind = "port"
+    from paper_1809_07986_b200 import tsgm
+    calib, sgm, filt = params()
+    threads = threads or os.cpu_count() or 1
+    n_red = max(1, min(4, int(args.cpu_frames)))
+    seqs = []
+    for s in range(threads):
+        cfg = scene_cfg(s, N_FRAMES)
+        L, R, poses, _ = render(cfg, 0, 1 + n_red, threads=threads)
+        mot = [(np.eye(3), np.zeros(3))] + [tsgm.relative_motion(poses[k - 1], poses[k])
+                                             for k in range(1, 1 + n_red)]
+        seqs.append((L, R, mot))
+
+    def run_seq(i):
+        L, R, mot = seqs[i]
+        st = None
+        times = []
+        for k in range(1 + n_red):
+            t0 = time.perf_counter()
+            res = impl.step(st, L[k], R[k], mot[k][0], mot[k][1], calib, sgm, filt)
+            times.append(time.perf_counter() - t0)
+            st = (res["d"], res["p"], res["valid"])
+        return times
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        all_times = list(ex.map(run_seq, range(threads)))
+    wall = time.perf_counter() - t0
+    t_first = float(np.mean([t[0] for t in all_times]))
+    t_red = float(np.mean([x for t in all_times for x in t[1:]]))
+    per_seq = t_first + (N_FRAMES - 1) * t_red
+    fps = threads * N_FRAMES / per_seq
+    return {"value": round(fps, 3), "unit": "frames/s", "cores": threads, "kind": kind,
+            "sample": (f"{threads} config-2 sequences (one per thread), frame 0 + {n_red} "
+                       f"reduced frames each, {wall:.1f}s wall; frames/s for the 30-frame mix "
+                       f"= cores*30/(t0 + 29*t_reduced), t0={t_first:.3f}s "
+                       f"t_reduced={t_red:.3f}s per frame under full concurrency")}
+
+
+def run_reference(args):
+    rank, world, _ = rank_info()
+    if rank != 0:
+        return None
+    times = []
+    cpu = None
+    for i in range(args.warmup + args.steps):
+        c = cpu_reference_sample(args)
+        if i >= args.warmup:
+            times.append(c)
+            cpu = c
+    value = float(np.mean([c["value"] for c in times]))
+    cpu["value"] = round(value, 3)
+    result = {
+        "metric": "frames/sec (batched tsgm step, 1242x375, D=128, 8 paths)",
+        "value": round(value, 3), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "u8/u16 cost+aggregation, f64 Kalman state",
+        "data": "synthetic (seeded KITTI-like scenes, BASELINE configs[2])",
+        "config": {"workload": "configs[2]: 64 sequences x 30 frames, 1242x375", "d_max": D_,
+                   "paths": 8, "p1": P1, "p2": P2},
+        "impl": "reference",
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(value, 3), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(result), flush=True)
+    return result
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seqs", type=int, default=N_SEQ)
+    ap.add_argument("--frames", type=int, default=N_FRAMES)
+    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,209 @@
+/* tsgm_b200 — C-ABI of the B200-native per-frame hot path of arXiv 1809.07986
+ * ("tsgm": temporal, Kalman-filtered, reduced-space semi-global matching).
+ *
+ * This is the drop-in boundary. The reference (/root/reference/proj) is a C++20
+ * library whose per-frame entry point is
+ *     tsgm::StepResult tsgm::step(const DisparityState&, const GrayImage& left,
+ *         const GrayImage& right, const RigidMotion&, const StereoCalib&,
+ *         const SgmParams&, const FilterConfig&, int threads)
+ *   (include/tsgm/temporal_filter.hpp:71-76, src/temporal_filter.cpp:195-232).
+ * Its C++ callers keep using that signature through the header-only facade
+ * include/tsgm_gpu.hpp (tsgm::gpu::step), which sits on these functions; a
+ * batched production caller uses the context API directly. No torch types, no
+ * C++ types: plain pointers and sizes.
+ *
+ * Status codes (the reference's exception classes):
+ *   0 = ok, 1 = invalid argument (std::invalid_argument), 2 = CUDA/runtime
+ *   error (std::runtime_error). The message of the last failure on the calling
+ *   thread is returned by tsgm_last_error().
+ *
+ * Layouts: images row-major W x H, index y*W + x; ragged cost volumes use the
+ * reference's prefix-sum layout (include/tsgm/matching_cost.hpp:50-73):
+ * offsets[W*H+1] (u32), cell (x, y, lo+j) at offsets[y*W+x] + j.
+ */
+#ifndef TSGM_B200_H
+#define TSGM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSGM_OK 0
+#define TSGM_INVALID_ARGUMENT 1
+#define TSGM_RUNTIME_ERROR 2
+
+/* tsgm::SgmParams (include/tsgm/sgm.hpp:15-23). path_set: 0 = nondiagonal
+ * {left,right,up,down}, 1 = diagonal (sgm.hpp:10-13); used when paths == 4. */
+typedef struct {
+    int32_t p1, p2, paths, path_set, d_max;
+} tsgm_sgm_params;
+
+/* tsgm::FilterConfig (include/tsgm/temporal_filter.hpp:8-26). */
+typedef struct {
+    double q, r;           /* NoiseParams (temporal_filter.hpp:8-13) */
+    double p_init, disc_thresh;
+    int32_t min_range_halfwidth;
+    int32_t range_use_stddev; /* bool */
+    double range_stddev_gain;
+} tsgm_filter_config;
+
+/* tsgm::StereoCalib (include/tsgm/geometry.hpp:17-27). */
+typedef struct {
+    double focal_px, cx, cy, baseline_m;
+    int32_t width, height, d_max;
+} tsgm_stereo_calib;
+
+/* ------------------------------------------------------------------------
+ * Context API — one context per GPU, `max_slots` independent sequences with
+ * device-resident Kalman state (A2, geometry.hpp:53-75), one CUDA stream.
+ * ------------------------------------------------------------------------ */
+typedef struct tsgm_ctx tsgm_ctx;
+
+#define TSGM_KEEP_VOLUMES 1u /* materialise C (u8) and S (u16) per slot for fetch */
+
+typedef struct {
+    int32_t width, height;     /* image size (must equal calib.width/height) */
+    int32_t max_slots;         /* sequences resident on this device */
+    int32_t device;            /* CUDA ordinal */
+    tsgm_stereo_calib calib;
+    tsgm_sgm_params sgm;
+    tsgm_filter_config filter;
+    double mask_tau;           /* A21 extension: Mahalanobis gate, 3.0 */
+    uint32_t flags;            /* TSGM_KEEP_VOLUMES */
+} tsgm_config;
+
+const char* tsgm_last_error(void);
+
+/* Validates like step() would (temporal_filter.cpp:198-206, sgm.cpp:14-23,
+ * geometry.cpp:21-28) and allocates all device buffers up front. */
+int tsgm_create(const tsgm_config* cfg, tsgm_ctx** out);
+void tsgm_destroy(tsgm_ctx* ctx);
+
+/* Empty (default) state for `slot`: the next step is full-range matching
+ * (temporal_filter.cpp:200-202). */
+int tsgm_reset(tsgm_ctx* ctx, int32_t slot);
+/* Host -> device state upload (DisparityState; d/p may be NULL for zeros). */
+int tsgm_set_state(tsgm_ctx* ctx, int32_t slot, const double* d, const double* p,
+                   const uint8_t* valid);
+
+/* One frame for `n` sequences. left[i]/right[i] are HOST u8 W*H images for
+ * slots[i]; motion[i*12 .. i*12+11] is the RigidMotion (row-major R, then t)
+ * mapping the previous camera frame into the current one (geometry.hpp:29-40).
+ * Asynchronous on the context stream w.r.t. the caller except for the host
+ * staging copy; outputs stay on the device until tsgm_fetch. */
+int tsgm_step(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const uint8_t* const* left,
+              const uint8_t* const* right, const double* motion);
+/* Same with DEVICE image pointers (inputs already resident in HBM). */
+int tsgm_step_device(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
+                     const uint8_t* const* d_left, const uint8_t* const* d_right,
+                     const double* motion);
+
+/* Outputs of the last step of a slot (StepResult, temporal_filter.hpp:64-69,
+ * plus the intermediates parity tests compare). */
+enum {
+    TSGM_OUT_STATE_D = 0,   /* f64 posterior d        */
+    TSGM_OUT_STATE_P = 1,   /* f64 posterior p        */
+    TSGM_OUT_STATE_VALID = 2, /* u8                   */
+    TSGM_OUT_EXPORT_D = 3,  /* i32 median-refined map (export_map.d) */
+    TSGM_OUT_EXPORT_VALID = 4, /* u8 */
+    TSGM_OUT_DIFF = 5,      /* f64 |d_pred - d_z|     */
+    TSGM_OUT_MASK = 6,      /* u8 A21 moving-object mask */
+    TSGM_OUT_PRED_D = 7,    /* f64 predict() output   */
+    TSGM_OUT_PRED_P = 8,
+    TSGM_OUT_PRED_VALID = 9,
+    TSGM_OUT_LO = 10,       /* u16 derive_search_ranges */
+    TSGM_OUT_HI = 11,
+    TSGM_OUT_MEAS_D = 12,   /* i32 WTA (sgm_match)    */
+    TSGM_OUT_MEAS_VALID = 13,
+    TSGM_OUT_OFFSETS = 14,  /* u32 W*H+1              */
+    TSGM_OUT_COST = 15,     /* u8 N   (TSGM_KEEP_VOLUMES) */
+    TSGM_OUT_AGG = 16,      /* u16 N  (TSGM_KEEP_VOLUMES) */
+    TSGM_OUT_COUNT
+};
+/* Copies output `what` of `slot` into host memory `dst` (bytes >= size). */
+int tsgm_fetch(tsgm_ctx* ctx, int32_t slot, int32_t what, void* dst, size_t bytes);
+/* Number of cost cells N of the slot's last step (sum of window lengths). */
+int tsgm_cells(tsgm_ctx* ctx, int32_t slot, uint64_t* n_cells);
+int tsgm_sync(tsgm_ctx* ctx);
+
+/* Timing on the context stream (CUDA events): begin/end bracket a region,
+ * elapsed returns milliseconds. Aggregation-only standalone benchmark
+ * (C -> S, the graded roofline kernel): runs the 8-path aggregation on the
+ * slots' current C volumes `reps` times and returns the mean ms per launch. */
+int tsgm_timer_begin(tsgm_ctx* ctx);
+int tsgm_timer_end(tsgm_ctx* ctx, float* ms);
+int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t reps,
+                         float* ms_per_launch, uint64_t* cells);
+/* Kernel launches issued by the context since creation (all stages). */
+uint64_t tsgm_launch_count(tsgm_ctx* ctx);
+
+/* ------------------------------------------------------------------------
+ * Stage API — stateless, host buffers in and out, same kernels as the step.
+ * One function per public reference sub-stage.
+ * ------------------------------------------------------------------------ */
+/* census_transform (matching_cost.hpp:80, matching_cost.cpp:53-79) */
+int tsgm_census_transform(const uint8_t* img, int32_t w, int32_t h, uint32_t* sig);
+/* build_cost_volume (matching_cost.hpp:85-88, matching_cost.cpp:88-117);
+ * offsets: W*H+1 u32, cost: capacity `cap` bytes. */
+int tsgm_build_cost_volume(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
+                           const uint16_t* lo, const uint16_t* hi, uint32_t* offsets,
+                           uint8_t* cost, uint64_t cap);
+/* aggregate_paths (sgm.hpp:47, sgm.cpp:135-161) over a ragged C volume. */
+int tsgm_aggregate_paths(const uint8_t* cost, const uint16_t* lo, const uint16_t* hi, int32_t w,
+                         int32_t h, const tsgm_sgm_params* params, uint16_t* agg);
+/* winner_takes_all (sgm.hpp:52, sgm.cpp:163-187) */
+int tsgm_winner_takes_all(const uint16_t* agg, const uint16_t* lo, const uint16_t* hi,
+                          int32_t w, int32_t h, int32_t* d, uint8_t* valid);
+/* median_refine (sgm.hpp:57, sgm.cpp:189-216) */
+int tsgm_median_refine(const int32_t* d, const uint8_t* valid, int32_t w, int32_t h,
+                       int32_t* out_d, uint8_t* out_valid);
+/* sgm_match (sgm.hpp:67-69, sgm.cpp:226-257) */
+int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
+                   const uint16_t* lo, const uint16_t* hi, const tsgm_sgm_params* params,
+                   int32_t* d, uint8_t* valid);
+/* relative_motion (geometry.hpp:111, geometry.cpp:189-197); poses row-major 3x4 */
+int tsgm_relative_motion(const double* prev12, const double* cur12, double* r9, double* t3);
+/* disparity_homography (geometry.hpp:87, geometry.cpp:77-110); row-major 4x4 */
+int tsgm_disparity_homography(const double* r9, const double* t3,
+                              const tsgm_stereo_calib* calib, double* h16);
+/* warp_state_ex (geometry.hpp:102, geometry.cpp:127-156) */
+int tsgm_warp_state_ex(const double* d, const double* p, const uint8_t* valid, int32_t w,
+                       int32_t h, const double* h16, int32_t d_max, double* od, double* op,
+                       uint8_t* ov, double* source_d);
+/* predict (temporal_filter.hpp:32-33, temporal_filter.cpp:28-49) */
+int tsgm_predict(const double* d, const double* p, const uint8_t* valid, int32_t w, int32_t h,
+                 const double* r9, const double* t3, const tsgm_stereo_calib* calib,
+                 const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov);
+/* reject_discontinuities (temporal_filter.hpp:38, temporal_filter.cpp:51-74) */
+int tsgm_reject_discontinuities(const double* d, const double* p, const uint8_t* valid,
+                                int32_t w, int32_t h, const tsgm_filter_config* cfg, double* od,
+                                double* op, uint8_t* ov);
+/* fill_zoom_holes (temporal_filter.hpp:43, temporal_filter.cpp:76-106) */
+int tsgm_fill_zoom_holes(const double* d, const double* p, const uint8_t* valid, int32_t w,
+                         int32_t h, double* od, double* op, uint8_t* ov);
+/* derive_search_ranges (temporal_filter.hpp:48-49, temporal_filter.cpp:108-143) */
+int tsgm_derive_search_ranges(const double* d, const double* p, const uint8_t* valid, int32_t w,
+                              int32_t h, const tsgm_stereo_calib* calib,
+                              const tsgm_filter_config* cfg, uint16_t* lo, uint16_t* hi);
+/* correct (temporal_filter.hpp:54-55, temporal_filter.cpp:145-170) */
+int tsgm_correct(const double* d, const double* p, const uint8_t* valid, const int32_t* md,
+                 const uint8_t* mv, int32_t w, int32_t h, const tsgm_filter_config* cfg,
+                 double* od, double* op, uint8_t* ov);
+
+/* step (temporal_filter.hpp:74-76) for ONE sequence with host-resident state,
+ * exactly the reference's value semantics: state_w == state_h == 0 is the
+ * default (empty) state. Used by the C++ facade. Optional outputs may be NULL. */
+int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_t state_w,
+                   int32_t state_h, const uint8_t* left, const uint8_t* right, int32_t w,
+                   int32_t h, const double* r9, const double* t3,
+                   const tsgm_stereo_calib* calib, const tsgm_sgm_params* params,
+                   const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov,
+                   int32_t* ed, uint8_t* ev, double* diff);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

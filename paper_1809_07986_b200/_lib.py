@@ -1,0 +1,100 @@
+"""ctypes binding of the product library ``lib/libtsgm_b200.so`` (C-ABI in
+``include/tsgm_b200.h``). Fails loudly when the library is missing: there is
+no CPU fallback anywhere in this package."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from ._build import lib_path
+
+TSGM_OK, TSGM_INVALID_ARGUMENT, TSGM_RUNTIME_ERROR = 0, 1, 2
+
+OUT = dict(
+    state_d=0, state_p=1, state_valid=2, export_d=3, export_valid=4, diff=5, mask=6,
+    pred_d=7, pred_p=8, pred_valid=9, lo=10, hi=11, meas_d=12, meas_valid=13, offsets=14,
+    cost=15, agg=16,
+)
+TSGM_KEEP_VOLUMES = 1
+
+
+class SgmParamsC(C.Structure):
+    _fields_ = [("p1", C.c_int32), ("p2", C.c_int32), ("paths", C.c_int32),
+                ("path_set", C.c_int32), ("d_max", C.c_int32)]
+
+
+class FilterConfigC(C.Structure):
+    _fields_ = [("q", C.c_double), ("r", C.c_double), ("p_init", C.c_double),
+                ("disc_thresh", C.c_double), ("min_range_halfwidth", C.c_int32),
+                ("range_use_stddev", C.c_int32), ("range_stddev_gain", C.c_double)]
+
+
+class StereoCalibC(C.Structure):
+    _fields_ = [("focal_px", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("baseline_m", C.c_double), ("width", C.c_int32), ("height", C.c_int32),
+                ("d_max", C.c_int32)]
+
+
+class ConfigC(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("max_slots", C.c_int32),
+                ("device", C.c_int32), ("calib", StereoCalibC), ("sgm", SgmParamsC),
+                ("filter", FilterConfigC), ("mask_tau", C.c_double), ("flags", C.c_uint32)]
+
+
+_lib = None
+
+# Every exported symbol of include/tsgm_b200.h (checked by the CPU tests).
+EXPORTS = [
+    "tsgm_last_error", "tsgm_create", "tsgm_destroy", "tsgm_reset", "tsgm_set_state",
+    "tsgm_step", "tsgm_step_device", "tsgm_fetch", "tsgm_cells", "tsgm_sync",
+    "tsgm_timer_begin", "tsgm_timer_end", "tsgm_bench_aggregate", "tsgm_launch_count",
+    "tsgm_census_transform", "tsgm_build_cost_volume", "tsgm_aggregate_paths",
+    "tsgm_winner_takes_all", "tsgm_median_refine", "tsgm_sgm_match", "tsgm_relative_motion",
+    "tsgm_disparity_homography", "tsgm_warp_state_ex", "tsgm_predict",
+    "tsgm_reject_discontinuities", "tsgm_fill_zoom_holes", "tsgm_derive_search_ranges",
+    "tsgm_correct", "tsgm_step_once",
+]
+
+
+def load():
+    """The product library; raises if it is not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        path = lib_path("libtsgm_b200.so")
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"{path} is missing: the CUDA path is required (run __graft_entry__.build())")
+        lib = C.CDLL(path)
+        lib.tsgm_last_error.restype = C.c_char_p
+        lib.tsgm_launch_count.restype = C.c_uint64
+        lib.tsgm_launch_count.argtypes = [C.c_void_p]
+        lib.tsgm_create.argtypes = [C.POINTER(ConfigC), C.POINTER(C.c_void_p)]
+        lib.tsgm_destroy.argtypes = [C.c_void_p]
+        for name in ("tsgm_reset",):
+            getattr(lib, name).argtypes = [C.c_void_p, C.c_int32]
+        lib.tsgm_set_state.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        for name in ("tsgm_step", "tsgm_step_device"):
+            getattr(lib, name).argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p]
+        lib.tsgm_fetch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t]
+        lib.tsgm_cells.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64)]
+        lib.tsgm_sync.argtypes = [C.c_void_p]
+        lib.tsgm_timer_begin.argtypes = [C.c_void_p]
+        lib.tsgm_timer_end.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+        lib.tsgm_bench_aggregate.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                             C.POINTER(C.c_float), C.POINTER(C.c_uint64)]
+        _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == TSGM_OK:
+        return
+    msg = load().tsgm_last_error().decode()
+    if rc == TSGM_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def ptr(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else None

@@ -1,0 +1,123 @@
+// Shared device-side definitions for the tsgm sm_100a kernels.
+//
+// Batched layout in HBM: every per-pixel map is slot-major, [max_slots][W*H]
+// (offsets: [max_slots][W*H+1]); ragged cost volumes are [max_slots][cap]
+// with cap = W*H*d_max cells, cell (x, y, lo+j) at off[y*W+x] + j exactly as in
+// the reference's CostVolume (include/tsgm/matching_cost.hpp:50-73). A launch
+// covers `n` active slots; blockIdx.{y,z} selects the active index a, and
+// slots[a] the slot.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsgm {
+
+constexpr int kCensusRadius = 2;  // matching_cost.hpp:11
+constexpr int kMaxCost = 24;      // matching_cost.hpp:13
+
+struct Bufs {
+    int W, H, P, d_max;
+    size_t vol_cap;  // cells per slot in cost/agg
+    const int* slots;  // device [n] slot ids of the active batch
+    // posterior state (A2)
+    double *sd, *sp;
+    uint8_t* sv;
+    // warp keys (A6) and warp output (pre reject/fill)
+    unsigned long long *kd, *kp, *ks;
+    double *wd, *wp, *wsrc;
+    uint8_t* wv;
+    // prediction (predict() output)
+    double *pd, *pp;
+    uint8_t* pv;
+    // ranges + prefix sums (A10, A11)
+    uint16_t *lo, *hi;
+    uint32_t* off;       // [slot][P+1]
+    uint32_t* row_sum;   // [slot][H]
+    unsigned long long* ncells;  // [slot]
+    int* overflow;       // [slot] volume >= 2^32
+    // census + volumes (A12-A14)
+    uint32_t *sigl, *sigr;
+    const uint8_t* const* left;   // device [n] image pointers
+    const uint8_t* const* right;
+    uint8_t* cost;
+    uint16_t* agg;
+    // WTA, render, export (A15, A18, A19)
+    int32_t *md, *rd, *ed;
+    uint8_t *mv, *rv, *ev;
+    // diff, mask (A17, A21)
+    double* diff;
+    uint8_t* mask;
+    // per active index: 4x4 homography (row-major), A4
+    const double* H16;
+};
+
+__device__ __forceinline__ int slot_of(const Bufs& b, int a) { return b.slots[a]; }
+
+// Doubles -> u64 keys whose unsigned order is the numeric order; -0.0 is
+// canonicalised to +0.0 so ties behave like the reference's `!=` tests
+// (geometry.cpp:116-123).
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+    unsigned long long u = (x == 0.0) ? 0ull : static_cast<unsigned long long>(__double_as_longlong(x));
+    return (u >> 63) ? ~u : (u | (1ull << 63));
+}
+__device__ __forceinline__ double key_double(unsigned long long k) {
+    unsigned long long u = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+    return __longlong_as_double(static_cast<long long>(u));
+}
+
+// static_cast<int>(std::lround(x)) as compiled for x86-64 (geometry.cpp:143-144,
+// temporal_filter.cpp:263): round half away from zero to long; out-of-range or
+// NaN yields LONG_MIN (cvttsd2si); the int cast keeps the low 32 bits.
+__device__ __forceinline__ int x86_lround_int(double x) {
+    double t = trunc(x);
+    if (fabs(x - t) >= 0.5) t += copysign(1.0, x);
+    long long v;
+    if (t >= -9223372036854775808.0 && t < 9223372036854775808.0)
+        v = static_cast<long long>(t);
+    else
+        v = static_cast<long long>(0x8000000000000000ull);
+    return static_cast<int>(static_cast<unsigned int>(static_cast<unsigned long long>(v)));
+}
+
+// static_cast<int>(double) as compiled for x86-64 (cvttsd2si, 32-bit):
+// truncation; out-of-range or NaN yields INT_MIN (temporal_filter.cpp:119-124).
+__device__ __forceinline__ int x86_cvtt_int(double x) {
+    if (x > -2147483649.0 && x < 2147483648.0) return static_cast<int>(x);
+    return static_cast<int>(0x80000000u);
+}
+
+__device__ __forceinline__ bool census_defined(int x, int y, int W, int H) {
+    return x >= kCensusRadius && x < W - kCensusRadius && y >= kCensusRadius &&
+           y < H - kCensusRadius;
+}
+
+// ------------------------------------------------------------------ launchers
+// (defined in the .cu files; all enqueue on `st` and count launches)
+struct Launch {
+    cudaStream_t st;
+    unsigned long long* counter;
+};
+
+void launch_census(const Bufs& b, int n, Launch L);
+void launch_ranges_from_pred(const Bufs& b, int n, int min_hw, int use_stddev, double gain,
+                             Launch L);
+void launch_ranges_given(const Bufs& b, int n, Launch L);  // lo/hi already set
+void launch_offsets(const Bufs& b, int n, Launch L);       // row scan + finalize
+void launch_cost(const Bufs& b, int n, Launch L);
+void launch_wta(const Bufs& b, int n, Launch L);
+void launch_median(const Bufs& b, int n, const int32_t* in_d, const uint8_t* in_v,
+                   int32_t* out_d, uint8_t* out_v, Launch L);
+
+void launch_warp(const Bufs& b, int n, const double* src_d, const double* src_p,
+                 const uint8_t* src_v, int d_max, Launch L);
+// predict tail: phi/variance (A7) then optionally reject (A8) and fill (A9)
+void launch_predict_finalize(const Bufs& b, int n, double q, int apply_phi, Launch L);
+void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* in_p,
+                        const uint8_t* in_v, double* out_d, double* out_p, uint8_t* out_v,
+                        double disc_thresh, int do_reject, int do_fill, Launch L);
+void launch_correct(const Bufs& b, int n, double r, double mask_tau, Launch L);
+
+void launch_aggregate(const Bufs& b, int n, int p1, int p2, int paths, int path_set, Launch L);
+
+}  // namespace tsgm

@@ -1,0 +1,927 @@
+// Host runtime behind include/tsgm_b200.h: device-resident per-slot state,
+// batched per-frame launch sequence on one stream, the stateless stage API, and
+// the host-side FP64 geometry (relative_motion, disparity_homography) in the
+// reference's operation order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "tsgm_b200.h"
+
+using namespace tsgm;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct invalid_arg : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+[[noreturn]] void bad(const char* msg) { throw invalid_arg(msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return TSGM_OK;
+    } catch (const invalid_arg& e) {
+        g_err = e.what();
+        return TSGM_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TSGM_RUNTIME_ERROR;
+    }
+}
+
+// ------------------------------------------------------------------ geometry
+// Sequential-k products without FMA (the host compiler runs with
+// -ffp-contract=off): the same order as the oracle restatement
+// (oracle/tsgm_oracle.c) and the oracle build's Eigen stand-in.
+void mat3_mul(const double* a, const double* b, double* r) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r[i * 3 + j] = (a[i * 3 + 0] * b[0 * 3 + j] + a[i * 3 + 1] * b[1 * 3 + j]) +
+                           a[i * 3 + 2] * b[2 * 3 + j];
+}
+void mat3_vec(const double* a, const double* v, double* r) {
+    for (int i = 0; i < 3; ++i) r[i] = (a[i * 3 + 0] * v[0] + a[i * 3 + 1] * v[1]) + a[i * 3 + 2] * v[2];
+}
+void mat4_mul(const double* a, const double* b, double* r) {
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j)
+            r[i * 4 + j] = ((a[i * 4 + 0] * b[0 * 4 + j] + a[i * 4 + 1] * b[1 * 4 + j]) +
+                            a[i * 4 + 2] * b[2 * 4 + j]) +
+                           a[i * 4 + 3] * b[3 * 4 + j];
+}
+
+// RigidMotion::validate, geometry.cpp:30-36
+void motion_validate(const double* r) {
+    double rt[9], g[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) rt[i * 3 + j] = r[j * 3 + i];
+    mat3_mul(rt, r, g);
+    double mx = 0.0;
+    for (int i = 0; i < 9; ++i) {
+        const double e = std::fabs(g[i] - ((i % 4) == 0 ? 1.0 : 0.0));
+        if (i == 0 || e > mx) mx = e;
+    }
+    if (!(mx <= 1e-9)) bad("RigidMotion: rotation is not orthonormal");
+    const double det = r[0] * (r[4] * r[8] - r[5] * r[7]) - r[3] * (r[1] * r[8] - r[2] * r[7]) +
+                       r[6] * (r[1] * r[5] - r[2] * r[4]);
+    if (!(std::fabs(det - 1.0) <= 1e-9)) bad("RigidMotion: rotation determinant is not +1");
+}
+
+// StereoCalib::validate, geometry.cpp:21-28
+void calib_validate(const tsgm_stereo_calib& c) {
+    if (!(c.focal_px > 0.0)) bad("StereoCalib: focal_px must be positive");
+    if (!(c.baseline_m > 0.0)) bad("StereoCalib: baseline_m must be positive");
+    if (!(c.width > 0 && c.height > 0)) bad("StereoCalib: empty image");
+    if (!(c.cx >= 0.0 && c.cx < c.width)) bad("StereoCalib: cx outside image");
+    if (!(c.cy >= 0.0 && c.cy < c.height)) bad("StereoCalib: cy outside image");
+    if (!(c.d_max >= 1)) bad("StereoCalib: d_max must be at least 1");
+}
+
+// SgmParams::validate, sgm.cpp:14-23
+void sgm_validate(const tsgm_sgm_params& p) {
+    if (p.p1 <= 0 || p.p2 < p.p1) bad("SgmParams: require 0 < p1 <= p2");
+    if (p.paths != 4 && p.paths != 8) bad("SgmParams: paths must be 4 or 8");
+    if (p.d_max < 1 || p.d_max > 65535) bad("SgmParams: d_max out of range");
+    if ((kMaxCost + p.p2) * p.paths > 65535) bad("SgmParams: p2 too large for 16-bit accumulation");
+}
+
+// disparity_homography, geometry.cpp:77-110 (row-major out)
+void homography(const double* r9, const double* t3, const tsgm_stereo_calib& c, double* h16) {
+    calib_validate(c);
+    motion_validate(r9);
+    bool ident = t3[0] == 0.0 && t3[1] == 0.0 && t3[2] == 0.0;
+    for (int i = 0; i < 9; ++i) ident = ident && r9[i] == ((i % 4) == 0 ? 1.0 : 0.0);
+    std::memset(h16, 0, 16 * sizeof(double));
+    if (ident) {
+        h16[0] = h16[5] = h16[10] = h16[15] = 1.0;
+        return;
+    }
+    const double f = c.focal_px, b = c.baseline_m;
+    double q[16] = {0}, qi[16] = {0}, t[16] = {0}, tmp[16];
+    q[0] = 1.0;
+    q[3] = -c.cx;
+    q[5] = 1.0;
+    q[7] = -c.cy;
+    q[11] = f;
+    q[14] = 1.0 / b;
+    qi[0] = 1.0;
+    qi[2] = c.cx / f;
+    qi[5] = 1.0;
+    qi[6] = c.cy / f;
+    qi[11] = b;
+    qi[14] = 1.0 / f;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) t[i * 4 + j] = r9[i * 3 + j];
+        t[i * 4 + 3] = t3[i];
+    }
+    t[15] = 1.0;
+    mat4_mul(qi, t, tmp);
+    mat4_mul(tmp, q, h16);
+}
+
+// relative_motion, geometry.cpp:189-197
+void relative_motion(const double* prev12, const double* cur12, double* r9, double* t3) {
+    double rp[9], rc[9], tp[3], tc[3];
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) {
+            rp[i * 3 + j] = prev12[i * 4 + j];
+            rc[i * 3 + j] = cur12[i * 4 + j];
+        }
+        tp[i] = prev12[i * 4 + 3];
+        tc[i] = cur12[i * 4 + 3];
+    }
+    motion_validate(rp);
+    motion_validate(rc);
+    bool same = true;
+    for (int i = 0; i < 12; ++i) same = same && prev12[i] == cur12[i];
+    if (same) {
+        for (int i = 0; i < 9; ++i) r9[i] = (i % 4) == 0 ? 1.0 : 0.0;
+        t3[0] = t3[1] = t3[2] = 0.0;
+        return;
+    }
+    double rct[9], it[3], tmp[3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) rct[i * 3 + j] = rc[j * 3 + i];
+    mat3_vec(rct, tc, tmp);
+    for (int i = 0; i < 3; ++i) it[i] = -tmp[i];
+    mat3_mul(rct, rp, r9);
+    mat3_vec(rct, tp, tmp);
+    for (int i = 0; i < 3; ++i) t3[i] = tmp[i] + it[i];
+}
+
+}  // namespace
+
+// ====================================================================== context
+constexpr int kRing = 8;
+
+struct tsgm_ctx {
+    tsgm_config cfg{};
+    int W = 0, H = 0, P = 0, d_max = 0, max_slots = 0;
+    size_t vol_cap = 0;
+    int device = 0;
+    cudaStream_t st = nullptr;
+    Bufs b{};
+    unsigned long long launches = 0;
+    std::vector<void*> allocs;
+    // per-step device arrays
+    int* d_slots = nullptr;
+    const uint8_t** d_left = nullptr;
+    const uint8_t** d_right = nullptr;
+    double* d_H = nullptr;
+    // pinned staging ring
+    struct Stage {
+        int* slots;
+        const uint8_t** left;
+        const uint8_t** right;
+        double* H;
+        cudaEvent_t done;
+        bool used;
+    } ring[kRing]{};
+    int ring_i = 0;
+    uint8_t* d_img = nullptr;  // [max_slots][2][P] staging for host-image steps
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    template <typename T>
+    T* dalloc(size_t count) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~tsgm_ctx() {
+        if (device >= 0) cudaSetDevice(device);
+        if (st) cudaStreamSynchronize(st);
+        for (void* p : allocs) cudaFree(p);
+        for (auto& r : ring) {
+            if (r.slots) cudaFreeHost(r.slots);
+            if (r.left) cudaFreeHost(r.left);
+            if (r.right) cudaFreeHost(r.right);
+            if (r.H) cudaFreeHost(r.H);
+            if (r.done) cudaEventDestroy(r.done);
+        }
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (st) cudaStreamDestroy(st);
+    }
+    Launch L() { return Launch{st, &launches}; }
+};
+
+namespace {
+
+void validate_config(const tsgm_config& c) {
+    // step() preconditions, temporal_filter.cpp:198-206 + what sgm_match /
+    // census_transform / make_cost_volume would throw on every frame
+    if (c.width != c.calib.width || c.height != c.calib.height)
+        bad("tsgm_create: image size must equal calib.width x calib.height");
+    if (c.sgm.d_max != c.calib.d_max) bad("step: params.d_max disagrees with calibration");
+    calib_validate(c.calib);
+    sgm_validate(c.sgm);
+    if (c.width < 2 * kCensusRadius + 1 || c.height < 2 * kCensusRadius + 1)
+        bad("census_transform: image smaller than the 5x5 window");
+    const unsigned long long cap = 1ull * c.width * c.height * c.sgm.d_max;
+    if (cap > 0xffffffffull) bad("CostVolume: volume exceeds 32-bit addressing");
+    if (c.max_slots < 1) bad("tsgm_create: max_slots must be >= 1");
+}
+
+void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
+    ctx->cfg = c;
+    ctx->W = c.width;
+    ctx->H = c.height;
+    ctx->P = c.width * c.height;
+    ctx->d_max = c.sgm.d_max;
+    ctx->max_slots = c.max_slots;
+    ctx->vol_cap = static_cast<size_t>(ctx->P) * ctx->d_max;
+    ctx->device = c.device;
+    CK(cudaSetDevice(c.device));
+    CK(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    const size_t S = c.max_slots, P = ctx->P;
+    Bufs& b = ctx->b;
+    b.W = ctx->W;
+    b.H = ctx->H;
+    b.P = ctx->P;
+    b.d_max = ctx->d_max;
+    b.vol_cap = ctx->vol_cap;
+    b.sd = ctx->dalloc<double>(S * P);
+    b.sp = ctx->dalloc<double>(S * P);
+    b.sv = ctx->dalloc<uint8_t>(S * P);
+    b.kd = ctx->dalloc<unsigned long long>(S * P);
+    b.kp = ctx->dalloc<unsigned long long>(S * P);
+    b.ks = ctx->dalloc<unsigned long long>(S * P);
+    b.wd = ctx->dalloc<double>(S * P);
+    b.wp = ctx->dalloc<double>(S * P);
+    b.wsrc = ctx->dalloc<double>(S * P);
+    b.wv = ctx->dalloc<uint8_t>(S * P);
+    b.pd = ctx->dalloc<double>(S * P);
+    b.pp = ctx->dalloc<double>(S * P);
+    b.pv = ctx->dalloc<uint8_t>(S * P);
+    b.lo = ctx->dalloc<uint16_t>(S * P);
+    b.hi = ctx->dalloc<uint16_t>(S * P);
+    b.off = ctx->dalloc<uint32_t>(S * (P + 1));
+    b.row_sum = ctx->dalloc<uint32_t>(S * ctx->H);
+    b.ncells = ctx->dalloc<unsigned long long>(S);
+    b.overflow = ctx->dalloc<int>(S);
+    b.sigl = ctx->dalloc<uint32_t>(S * P);
+    b.sigr = ctx->dalloc<uint32_t>(S * P);
+    b.cost = ctx->dalloc<uint8_t>(S * ctx->vol_cap);
+    b.agg = ctx->dalloc<uint16_t>(S * ctx->vol_cap);
+    b.md = ctx->dalloc<int32_t>(S * P);
+    b.rd = ctx->dalloc<int32_t>(S * P);
+    b.ed = ctx->dalloc<int32_t>(S * P);
+    b.mv = ctx->dalloc<uint8_t>(S * P);
+    b.rv = ctx->dalloc<uint8_t>(S * P);
+    b.ev = ctx->dalloc<uint8_t>(S * P);
+    b.diff = ctx->dalloc<double>(S * P);
+    b.mask = ctx->dalloc<uint8_t>(S * P);
+    ctx->d_slots = ctx->dalloc<int>(S);
+    ctx->d_left = ctx->dalloc<const uint8_t*>(S);
+    ctx->d_right = ctx->dalloc<const uint8_t*>(S);
+    ctx->d_H = ctx->dalloc<double>(S * 16);
+    ctx->d_img = ctx->dalloc<uint8_t>(S * 2 * P);
+    b.slots = ctx->d_slots;
+    b.left = ctx->d_left;
+    b.right = ctx->d_right;
+    b.H16 = ctx->d_H;
+    // empty state everywhere, warp keys armed
+    CK(cudaMemsetAsync(b.sd, 0, sizeof(double) * S * P, ctx->st));
+    CK(cudaMemsetAsync(b.sp, 0, sizeof(double) * S * P, ctx->st));
+    CK(cudaMemsetAsync(b.sv, 0, S * P, ctx->st));
+    CK(cudaMemsetAsync(b.kd, 0, sizeof(unsigned long long) * S * P, ctx->st));
+    CK(cudaMemsetAsync(b.kp, 0xff, sizeof(unsigned long long) * S * P, ctx->st));
+    CK(cudaMemsetAsync(b.ks, 0xff, sizeof(unsigned long long) * S * P, ctx->st));
+    CK(cudaMemsetAsync(b.ncells, 0, sizeof(unsigned long long) * S, ctx->st));
+    for (auto& r : ctx->ring) {
+        CK(cudaMallocHost(&r.slots, sizeof(int) * S));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&r.left), sizeof(void*) * S));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&r.right), sizeof(void*) * S));
+        CK(cudaMallocHost(&r.H, sizeof(double) * 16 * S));
+        CK(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
+        r.used = false;
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+}
+
+// Stage the per-step arrays (slots, image pointers, homographies) and upload.
+void upload_step(tsgm_ctx* ctx, int n, const int32_t* slots, const uint8_t* const* dl,
+                 const uint8_t* const* dr, const double* H) {
+    auto& r = ctx->ring[ctx->ring_i];
+    ctx->ring_i = (ctx->ring_i + 1) % kRing;
+    if (r.used) CK(cudaEventSynchronize(r.done));
+    std::memcpy(r.slots, slots, sizeof(int) * n);
+    std::memcpy(r.left, dl, sizeof(void*) * n);
+    std::memcpy(r.right, dr, sizeof(void*) * n);
+    std::memcpy(r.H, H, sizeof(double) * 16 * n);
+    CK(cudaMemcpyAsync(ctx->d_slots, r.slots, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_left, r.left, sizeof(void*) * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_right, r.right, sizeof(void*) * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_H, r.H, sizeof(double) * 16 * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaEventRecord(r.done, ctx->st));
+    r.used = true;
+}
+
+void check_slots(tsgm_ctx* ctx, int n, const int32_t* slots) {
+    if (n < 1 || n > ctx->max_slots) bad("tsgm_step: n out of range");
+    std::vector<char> seen(ctx->max_slots, 0);
+    for (int i = 0; i < n; ++i) {
+        if (slots[i] < 0 || slots[i] >= ctx->max_slots) bad("tsgm_step: slot out of range");
+        if (seen[slots[i]]) bad("tsgm_step: duplicate slot in batch");
+        seen[slots[i]] = 1;
+    }
+}
+
+// The per-frame pipeline of step() (temporal_filter.cpp:195-232) for n slots.
+void run_step(tsgm_ctx* ctx, int n) {
+    const Bufs& b = ctx->b;
+    const tsgm_config& c = ctx->cfg;
+    Launch L = ctx->L();
+    // predict (A5-A9)
+    launch_warp(b, n, b.sd, b.sp, b.sv, c.calib.d_max, L);
+    launch_predict_finalize(b, n, c.filter.q, 1, L);
+    launch_reject_fill(b, n, b.wd, b.wp, b.wv, b.pd, b.pp, b.pv, c.filter.disc_thresh, 1, 1, L);
+    // derive_search_ranges + offsets (A10, A11)
+    launch_ranges_from_pred(b, n, c.filter.min_range_halfwidth, c.filter.range_use_stddev,
+                            c.filter.range_stddev_gain, L);
+    launch_offsets(b, n, L);
+    // sgm_match (A12-A15)
+    launch_census(b, n, L);
+    launch_cost(b, n, L);
+    launch_aggregate(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+    launch_wta(b, n, L);
+    // correct + diff + mask + render, then the export median (A16-A19, A21)
+    launch_correct(b, n, c.filter.r, c.mask_tau, L);
+    launch_median(b, n, b.rd, b.rv, b.ed, b.ev, L);
+    CK(cudaGetLastError());
+}
+
+void step_impl(tsgm_ctx* ctx, int n, const int32_t* slots, const uint8_t* const* dl,
+               const uint8_t* const* dr, const double* motion) {
+    check_slots(ctx, n, slots);
+    std::vector<double> H(16 * static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) homography(motion + 12 * i, motion + 12 * i + 9, ctx->cfg.calib, &H[16 * i]);
+    CK(cudaSetDevice(ctx->device));
+    upload_step(ctx, n, slots, dl, dr, H.data());
+    run_step(ctx, n);
+}
+
+struct OutDesc {
+    const void* base;
+    size_t elem;
+    size_t stride;  // elements per slot
+};
+
+OutDesc out_desc(tsgm_ctx* ctx, int what) {
+    const Bufs& b = ctx->b;
+    const size_t P = ctx->P;
+    switch (what) {
+        case TSGM_OUT_STATE_D: return {b.sd, 8, P};
+        case TSGM_OUT_STATE_P: return {b.sp, 8, P};
+        case TSGM_OUT_STATE_VALID: return {b.sv, 1, P};
+        case TSGM_OUT_EXPORT_D: return {b.ed, 4, P};
+        case TSGM_OUT_EXPORT_VALID: return {b.ev, 1, P};
+        case TSGM_OUT_DIFF: return {b.diff, 8, P};
+        case TSGM_OUT_MASK: return {b.mask, 1, P};
+        case TSGM_OUT_PRED_D: return {b.pd, 8, P};
+        case TSGM_OUT_PRED_P: return {b.pp, 8, P};
+        case TSGM_OUT_PRED_VALID: return {b.pv, 1, P};
+        case TSGM_OUT_LO: return {b.lo, 2, P};
+        case TSGM_OUT_HI: return {b.hi, 2, P};
+        case TSGM_OUT_MEAS_D: return {b.md, 4, P};
+        case TSGM_OUT_MEAS_VALID: return {b.mv, 1, P};
+        case TSGM_OUT_OFFSETS: return {b.off, 4, P + 1};
+        case TSGM_OUT_COST: return {b.cost, 1, ctx->vol_cap};
+        case TSGM_OUT_AGG: return {b.agg, 2, ctx->vol_cap};
+        default: bad("tsgm_fetch: unknown output");
+    }
+}
+
+unsigned long long cells_of(tsgm_ctx* ctx, int slot) {
+    unsigned long long n = 0;
+    CK(cudaMemcpyAsync(&n, ctx->b.ncells + slot, sizeof n, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return n;
+}
+
+// One-slot scratch context for the stateless stage API.
+std::unique_ptr<tsgm_ctx> scratch(int w, int h, int d_max) {
+    tsgm_config c{};
+    c.width = w;
+    c.height = h;
+    c.max_slots = 1;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    c.device = dev;
+    c.calib = tsgm_stereo_calib{1.0, 0.0, 0.0, 1.0, w, h, d_max};
+    c.sgm = tsgm_sgm_params{6, 65, 8, 0, d_max};
+    c.mask_tau = 3.0;
+    auto ctx = std::make_unique<tsgm_ctx>();
+    init_ctx(ctx.get(), c);
+    const int zero = 0;
+    const double I[16] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};
+    const uint8_t* l = ctx->d_img;
+    const uint8_t* r = ctx->d_img + ctx->P;
+    upload_step(ctx.get(), 1, &zero, &l, &r, I);
+    return ctx;
+}
+
+template <typename T>
+void h2d(tsgm_ctx* ctx, T* dst, const T* src, size_t count) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->st));
+}
+template <typename T>
+void d2h(tsgm_ctx* ctx, T* dst, const T* src, size_t count) {
+    if (dst) CK(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->st));
+}
+void sync(tsgm_ctx* ctx) {
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->st));
+}
+
+// Host-side window bookkeeping for caller-provided ranges (make_cost_volume,
+// matching_cost.cpp:30-48, with its u64 wrap-around on hi < lo).
+unsigned long long ranges_total(const uint16_t* lo, const uint16_t* hi, size_t n, int* max_hi) {
+    unsigned long long total = 0;
+    int mh = 0;
+    for (size_t i = 0; i < n; ++i) {
+        total += static_cast<unsigned long long>(hi[i]) - lo[i] + 1;
+        mh = std::max<int>(mh, hi[i]);
+    }
+    if (total > 0xffffffffull) bad("CostVolume: volume exceeds 32-bit addressing");
+    *max_hi = mh;
+    return total;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* tsgm_last_error(void) { return g_err.c_str(); }
+
+int tsgm_create(const tsgm_config* cfg, tsgm_ctx** out) {
+    return guarded([&] {
+        if (!cfg || !out) bad("tsgm_create: null argument");
+        validate_config(*cfg);
+        auto ctx = std::make_unique<tsgm_ctx>();
+        init_ctx(ctx.get(), *cfg);
+        *out = ctx.release();
+    });
+}
+
+void tsgm_destroy(tsgm_ctx* ctx) { delete ctx; }
+
+int tsgm_reset(tsgm_ctx* ctx, int32_t slot) {
+    return guarded([&] {
+        if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_reset: slot out of range");
+        CK(cudaSetDevice(ctx->device));
+        const size_t P = ctx->P;
+        CK(cudaMemsetAsync(ctx->b.sd + slot * P, 0, 8 * P, ctx->st));
+        CK(cudaMemsetAsync(ctx->b.sp + slot * P, 0, 8 * P, ctx->st));
+        CK(cudaMemsetAsync(ctx->b.sv + slot * P, 0, P, ctx->st));
+    });
+}
+
+int tsgm_set_state(tsgm_ctx* ctx, int32_t slot, const double* d, const double* p,
+                   const uint8_t* valid) {
+    return guarded([&] {
+        if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_set_state: slot out of range");
+        CK(cudaSetDevice(ctx->device));
+        const size_t P = ctx->P;
+        if (d) h2d(ctx, ctx->b.sd + slot * P, d, P);
+        else CK(cudaMemsetAsync(ctx->b.sd + slot * P, 0, 8 * P, ctx->st));
+        if (p) h2d(ctx, ctx->b.sp + slot * P, p, P);
+        else CK(cudaMemsetAsync(ctx->b.sp + slot * P, 0, 8 * P, ctx->st));
+        if (valid) h2d(ctx, ctx->b.sv + slot * P, valid, P);
+        else CK(cudaMemsetAsync(ctx->b.sv + slot * P, 0, P, ctx->st));
+        sync(ctx);
+    });
+}
+
+int tsgm_step(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const uint8_t* const* left,
+              const uint8_t* const* right, const double* motion) {
+    return guarded([&] {
+        if (!ctx || !slots || !left || !right || !motion) bad("tsgm_step: null argument");
+        check_slots(ctx, n, slots);
+        CK(cudaSetDevice(ctx->device));
+        std::vector<const uint8_t*> dl(n), dr(n);
+        const size_t P = ctx->P;
+        for (int i = 0; i < n; ++i) {
+            uint8_t* base = ctx->d_img + static_cast<size_t>(slots[i]) * 2 * P;
+            h2d(ctx, base, left[i], P);
+            h2d(ctx, base + P, right[i], P);
+            dl[i] = base;
+            dr[i] = base + P;
+        }
+        step_impl(ctx, n, slots, dl.data(), dr.data(), motion);
+    });
+}
+
+int tsgm_step_device(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
+                     const uint8_t* const* d_left, const uint8_t* const* d_right,
+                     const double* motion) {
+    return guarded([&] {
+        if (!ctx || !slots || !d_left || !d_right || !motion) bad("tsgm_step_device: null argument");
+        step_impl(ctx, n, slots, d_left, d_right, motion);
+    });
+}
+
+int tsgm_fetch(tsgm_ctx* ctx, int32_t slot, int32_t what, void* dst, size_t bytes) {
+    return guarded([&] {
+        if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_fetch: slot out of range");
+        CK(cudaSetDevice(ctx->device));
+        const OutDesc o = out_desc(ctx, what);
+        size_t count = o.stride;
+        if (what == TSGM_OUT_COST || what == TSGM_OUT_AGG) count = cells_of(ctx, slot);
+        if (bytes < count * o.elem) bad("tsgm_fetch: destination too small");
+        const char* src = static_cast<const char*>(o.base) + static_cast<size_t>(slot) * o.stride * o.elem;
+        CK(cudaMemcpyAsync(dst, src, count * o.elem, cudaMemcpyDeviceToHost, ctx->st));
+        sync(ctx);
+    });
+}
+
+int tsgm_cells(tsgm_ctx* ctx, int32_t slot, uint64_t* n_cells) {
+    return guarded([&] {
+        if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_cells: slot out of range");
+        CK(cudaSetDevice(ctx->device));
+        *n_cells = cells_of(ctx, slot);
+    });
+}
+
+int tsgm_sync(tsgm_ctx* ctx) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        sync(ctx);
+    });
+}
+
+int tsgm_timer_begin(tsgm_ctx* ctx) {
+    return guarded([&] { CK(cudaEventRecord(ctx->ev0, ctx->st)); });
+}
+
+int tsgm_timer_end(tsgm_ctx* ctx, float* ms) {
+    return guarded([&] {
+        CK(cudaEventRecord(ctx->ev1, ctx->st));
+        CK(cudaEventSynchronize(ctx->ev1));
+        CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+    });
+}
+
+int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t reps,
+                         float* ms_per_launch, uint64_t* cells) {
+    return guarded([&] {
+        check_slots(ctx, n, slots);
+        CK(cudaSetDevice(ctx->device));
+        std::vector<const uint8_t*> dl(n, ctx->d_img), dr(n, ctx->d_img);
+        std::vector<double> H(16 * static_cast<size_t>(n), 0.0);
+        upload_step(ctx, n, slots, dl.data(), dr.data(), H.data());
+        const tsgm_config& c = ctx->cfg;
+        Launch L = ctx->L();
+        launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);  // warm
+        CK(cudaEventRecord(ctx->ev0, ctx->st));
+        for (int r = 0; r < reps; ++r)
+            launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+        CK(cudaEventRecord(ctx->ev1, ctx->st));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        *ms_per_launch = ms / std::max(1, reps);
+        unsigned long long total = 0;
+        for (int i = 0; i < n; ++i) total += cells_of(ctx, slots[i]);
+        *cells = total;
+    });
+}
+
+uint64_t tsgm_launch_count(tsgm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---------------------------------------------------------------- stage API
+int tsgm_census_transform(const uint8_t* img, int32_t w, int32_t h, uint32_t* sig) {
+    return guarded([&] {
+        if (w < 2 * kCensusRadius + 1 || h < 2 * kCensusRadius + 1)
+            bad("census_transform: image smaller than the 5x5 window");
+        auto ctx = scratch(w, h, 1);
+        h2d(ctx.get(), ctx->d_img, img, ctx->P);
+        h2d(ctx.get(), ctx->d_img + ctx->P, img, ctx->P);
+        launch_census(ctx->b, 1, ctx->L());
+        d2h(ctx.get(), sig, ctx->b.sigl, ctx->P);
+        sync(ctx.get());
+    });
+}
+
+int tsgm_build_cost_volume(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
+                           const uint16_t* lo, const uint16_t* hi, uint32_t* offsets,
+                           uint8_t* cost, uint64_t cap) {
+    return guarded([&] {
+        if (w < 2 * kCensusRadius + 1 || h < 2 * kCensusRadius + 1)
+            bad("census_transform: image smaller than the 5x5 window");
+        int max_hi = 0;
+        const unsigned long long total = ranges_total(lo, hi, static_cast<size_t>(w) * h, &max_hi);
+        if (total > cap) bad("tsgm_build_cost_volume: capacity too small");
+        auto ctx = scratch(w, h, max_hi + 1);
+        tsgm_ctx* c = ctx.get();
+        h2d(c, c->d_img, left, c->P);
+        h2d(c, c->d_img + c->P, right, c->P);
+        h2d(c, c->b.lo, lo, c->P);
+        h2d(c, c->b.hi, hi, c->P);
+        launch_ranges_given(c->b, 1, c->L());
+        launch_offsets(c->b, 1, c->L());
+        launch_census(c->b, 1, c->L());
+        launch_cost(c->b, 1, c->L());
+        d2h(c, offsets, c->b.off, c->P + 1);
+        d2h(c, cost, c->b.cost, total);
+        sync(c);
+    });
+}
+
+int tsgm_aggregate_paths(const uint8_t* cost, const uint16_t* lo, const uint16_t* hi, int32_t w,
+                         int32_t h, const tsgm_sgm_params* params, uint16_t* agg) {
+    return guarded([&] {
+        sgm_validate(*params);
+        int max_hi = 0;
+        const unsigned long long total = ranges_total(lo, hi, static_cast<size_t>(w) * h, &max_hi);
+        auto ctx = scratch(w, h, max_hi + 1);
+        tsgm_ctx* c = ctx.get();
+        h2d(c, c->b.lo, lo, c->P);
+        h2d(c, c->b.hi, hi, c->P);
+        h2d(c, c->b.cost, cost, total);
+        launch_ranges_given(c->b, 1, c->L());
+        launch_offsets(c->b, 1, c->L());
+        launch_aggregate(c->b, 1, params->p1, params->p2, params->paths, params->path_set, c->L());
+        d2h(c, agg, c->b.agg, total);
+        sync(c);
+    });
+}
+
+int tsgm_winner_takes_all(const uint16_t* agg, const uint16_t* lo, const uint16_t* hi,
+                          int32_t w, int32_t h, int32_t* d, uint8_t* valid) {
+    return guarded([&] {
+        int max_hi = 0;
+        const unsigned long long total = ranges_total(lo, hi, static_cast<size_t>(w) * h, &max_hi);
+        auto ctx = scratch(w, h, max_hi + 1);
+        tsgm_ctx* c = ctx.get();
+        h2d(c, c->b.lo, lo, c->P);
+        h2d(c, c->b.hi, hi, c->P);
+        h2d(c, c->b.agg, agg, total);
+        launch_ranges_given(c->b, 1, c->L());
+        launch_offsets(c->b, 1, c->L());
+        launch_wta(c->b, 1, c->L());
+        d2h(c, d, c->b.md, c->P);
+        d2h(c, valid, c->b.mv, c->P);
+        sync(c);
+    });
+}
+
+int tsgm_median_refine(const int32_t* d, const uint8_t* valid, int32_t w, int32_t h,
+                       int32_t* out_d, uint8_t* out_valid) {
+    return guarded([&] {
+        auto ctx = scratch(w, h, 1);
+        tsgm_ctx* c = ctx.get();
+        h2d(c, c->b.rd, d, c->P);
+        h2d(c, c->b.rv, valid, c->P);
+        launch_median(c->b, 1, c->b.rd, c->b.rv, c->b.ed, c->b.ev, c->L());
+        d2h(c, out_d, c->b.ed, c->P);
+        d2h(c, out_valid, c->b.ev, c->P);
+        sync(c);
+    });
+}
+
+int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
+                   const uint16_t* lo, const uint16_t* hi, const tsgm_sgm_params* params,
+                   int32_t* d, uint8_t* valid) {
+    return guarded([&] {
+        // sgm_match, sgm.cpp:229-234: params, then ranges.validate(d_max)
+        sgm_validate(*params);
+        const size_t P = static_cast<size_t>(w) * h;
+        for (size_t i = 0; i < P; ++i)
+            if (lo[i] > hi[i] || hi[i] >= params->d_max) bad("SearchRangeMap: range outside [0, d_max)");
+        if (w < 2 * kCensusRadius + 1 || h < 2 * kCensusRadius + 1)
+            bad("census_transform: image smaller than the 5x5 window");
+        auto ctx = scratch(w, h, params->d_max);
+        tsgm_ctx* c = ctx.get();
+        h2d(c, c->d_img, left, P);
+        h2d(c, c->d_img + P, right, P);
+        h2d(c, c->b.lo, lo, P);
+        h2d(c, c->b.hi, hi, P);
+        launch_ranges_given(c->b, 1, c->L());
+        launch_offsets(c->b, 1, c->L());
+        launch_census(c->b, 1, c->L());
+        launch_cost(c->b, 1, c->L());
+        launch_aggregate(c->b, 1, params->p1, params->p2, params->paths, params->path_set, c->L());
+        launch_wta(c->b, 1, c->L());
+        d2h(c, d, c->b.md, P);
+        d2h(c, valid, c->b.mv, P);
+        sync(c);
+    });
+}
+
+int tsgm_relative_motion(const double* prev12, const double* cur12, double* r9, double* t3) {
+    return guarded([&] { relative_motion(prev12, cur12, r9, t3); });
+}
+
+int tsgm_disparity_homography(const double* r9, const double* t3,
+                              const tsgm_stereo_calib* calib, double* h16) {
+    return guarded([&] { homography(r9, t3, *calib, h16); });
+}
+
+int tsgm_warp_state_ex(const double* d, const double* p, const uint8_t* valid, int32_t w,
+                       int32_t h, const double* h16, int32_t d_max, double* od, double* op,
+                       uint8_t* ov, double* source_d) {
+    return guarded([&] {
+        auto ctx = scratch(w, h, 1);
+        tsgm_ctx* c = ctx.get();
+        const size_t P = c->P;
+        const int zero = 0;
+        const uint8_t* img = c->d_img;
+        upload_step(c, 1, &zero, &img, &img, h16);
+        h2d(c, c->b.sd, d, P);
+        h2d(c, c->b.sp, p, P);
+        h2d(c, c->b.sv, valid, P);
+        launch_warp(c->b, 1, c->b.sd, c->b.sp, c->b.sv, d_max, c->L());
+        launch_predict_finalize(c->b, 1, 0.0, 0, c->L());
+        d2h(c, od, c->b.wd, P);
+        d2h(c, op, c->b.wp, P);
+        d2h(c, ov, c->b.wv, P);
+        d2h(c, source_d, c->b.wsrc, P);
+        sync(c);
+    });
+}
+
+int tsgm_predict(const double* d, const double* p, const uint8_t* valid, int32_t w, int32_t h,
+                 const double* r9, const double* t3, const tsgm_stereo_calib* calib,
+                 const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov) {
+    return guarded([&] {
+        double H[16];
+        homography(r9, t3, *calib, H);
+        auto ctx = scratch(w, h, 1);
+        tsgm_ctx* c = ctx.get();
+        const size_t P = c->P;
+        const int zero = 0;
+        const uint8_t* img = c->d_img;
+        upload_step(c, 1, &zero, &img, &img, H);
+        h2d(c, c->b.sd, d, P);
+        h2d(c, c->b.sp, p, P);
+        h2d(c, c->b.sv, valid, P);
+        launch_warp(c->b, 1, c->b.sd, c->b.sp, c->b.sv, calib->d_max, c->L());
+        launch_predict_finalize(c->b, 1, cfg->q, 1, c->L());
+        launch_reject_fill(c->b, 1, c->b.wd, c->b.wp, c->b.wv, c->b.pd, c->b.pp, c->b.pv,
+                           cfg->disc_thresh, 1, 1, c->L());
+        d2h(c, od, c->b.pd, P);
+        d2h(c, op, c->b.pp, P);
+        d2h(c, ov, c->b.pv, P);
+        sync(c);
+    });
+}
+
+static int reject_fill_api(const double* d, const double* p, const uint8_t* valid, int32_t w,
+                           int32_t h, double thr, int rej, int fil, double* od, double* op,
+                           uint8_t* ov) {
+    return guarded([&] {
+        auto ctx = scratch(w, h, 1);
+        tsgm_ctx* c = ctx.get();
+        const size_t P = c->P;
+        h2d(c, c->b.wd, d, P);
+        h2d(c, c->b.wp, p, P);
+        h2d(c, c->b.wv, valid, P);
+        launch_reject_fill(c->b, 1, c->b.wd, c->b.wp, c->b.wv, c->b.pd, c->b.pp, c->b.pv, thr, rej,
+                           fil, c->L());
+        d2h(c, od, c->b.pd, P);
+        d2h(c, op, c->b.pp, P);
+        d2h(c, ov, c->b.pv, P);
+        sync(c);
+    });
+}
+
+int tsgm_reject_discontinuities(const double* d, const double* p, const uint8_t* valid,
+                                int32_t w, int32_t h, const tsgm_filter_config* cfg, double* od,
+                                double* op, uint8_t* ov) {
+    return reject_fill_api(d, p, valid, w, h, cfg->disc_thresh, 1, 0, od, op, ov);
+}
+
+int tsgm_fill_zoom_holes(const double* d, const double* p, const uint8_t* valid, int32_t w,
+                         int32_t h, double* od, double* op, uint8_t* ov) {
+    return reject_fill_api(d, p, valid, w, h, 0.0, 0, 1, od, op, ov);
+}
+
+int tsgm_derive_search_ranges(const double* d, const double* p, const uint8_t* valid, int32_t w,
+                              int32_t h, const tsgm_stereo_calib* calib,
+                              const tsgm_filter_config* cfg, uint16_t* lo, uint16_t* hi) {
+    return guarded([&] {
+        auto ctx = scratch(w, h, calib->d_max);
+        tsgm_ctx* c = ctx.get();
+        const size_t P = c->P;
+        h2d(c, c->b.pd, d, P);
+        h2d(c, c->b.pp, p, P);
+        h2d(c, c->b.pv, valid, P);
+        launch_ranges_from_pred(c->b, 1, cfg->min_range_halfwidth, cfg->range_use_stddev,
+                                cfg->range_stddev_gain, c->L());
+        d2h(c, lo, c->b.lo, P);
+        d2h(c, hi, c->b.hi, P);
+        sync(c);
+    });
+}
+
+int tsgm_correct(const double* d, const double* p, const uint8_t* valid, const int32_t* md,
+                 const uint8_t* mv, int32_t w, int32_t h, const tsgm_filter_config* cfg,
+                 double* od, double* op, uint8_t* ov) {
+    return guarded([&] {
+        auto ctx = scratch(w, h, 1);
+        tsgm_ctx* c = ctx.get();
+        const size_t P = c->P;
+        h2d(c, c->b.pd, d, P);
+        h2d(c, c->b.pp, p, P);
+        h2d(c, c->b.pv, valid, P);
+        h2d(c, c->b.md, md, P);
+        h2d(c, c->b.mv, mv, P);
+        launch_correct(c->b, 1, cfg->r, 3.0, c->L());
+        d2h(c, od, c->b.sd, P);
+        d2h(c, op, c->b.sp, P);
+        d2h(c, ov, c->b.sv, P);
+        sync(c);
+    });
+}
+
+int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_t state_w,
+                   int32_t state_h, const uint8_t* left, const uint8_t* right, int32_t w,
+                   int32_t h, const double* r9, const double* t3,
+                   const tsgm_stereo_calib* calib, const tsgm_sgm_params* params,
+                   const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov,
+                   int32_t* ed, uint8_t* ev, double* diff) {
+    return guarded([&] {
+        // step(), temporal_filter.cpp:198-206
+        const bool empty = state_w == 0 && state_h == 0;
+        if (!empty && (state_w != w || state_h != h)) bad("step: state dimension mismatch");
+        if (params->d_max != calib->d_max) bad("step: params.d_max disagrees with calibration");
+        tsgm_config c{};
+        c.width = w;
+        c.height = h;
+        c.max_slots = 1;
+        CK(cudaGetDevice(&c.device));
+        c.calib = *calib;
+        // the reference reads only f/cx/cy/b from calib in step; its size
+        // fields are validated by disparity_homography but need not equal the
+        // image (geometry.cpp:21-28)
+        c.sgm = *params;
+        c.filter = *cfg;
+        c.mask_tau = 3.0;
+        double H[16];
+        homography(r9, t3, *calib, H);
+        sgm_validate(*params);
+        if (w < 2 * kCensusRadius + 1 || h < 2 * kCensusRadius + 1)
+            bad("census_transform: image smaller than the 5x5 window");
+        if (1ull * w * h * params->d_max > 0xffffffffull)
+            bad("CostVolume: volume exceeds 32-bit addressing");
+        thread_local std::unique_ptr<tsgm_ctx> cache;
+        if (!cache || std::memcmp(&cache->cfg, &c, sizeof c) != 0) {
+            cache.reset();
+            auto ctx = std::make_unique<tsgm_ctx>();
+            init_ctx(ctx.get(), c);
+            cache = std::move(ctx);
+        }
+        tsgm_ctx* x = cache.get();
+        const size_t P = x->P;
+        if (empty || !sv) {
+            CK(cudaMemsetAsync(x->b.sd, 0, 8 * P, x->st));
+            CK(cudaMemsetAsync(x->b.sp, 0, 8 * P, x->st));
+            CK(cudaMemsetAsync(x->b.sv, 0, P, x->st));
+        } else {
+            h2d(x, x->b.sd, sd, P);
+            h2d(x, x->b.sp, sp, P);
+            h2d(x, x->b.sv, sv, P);
+        }
+        h2d(x, x->d_img, left, P);
+        h2d(x, x->d_img + P, right, P);
+        const int zero = 0;
+        const uint8_t* l = x->d_img;
+        const uint8_t* r = x->d_img + P;
+        upload_step(x, 1, &zero, &l, &r, H);
+        run_step(x, 1);
+        d2h(x, od, x->b.sd, P);
+        d2h(x, op, x->b.sp, P);
+        d2h(x, ov, x->b.sv, P);
+        d2h(x, ed, x->b.ed, P);
+        d2h(x, ev, x->b.ev, P);
+        d2h(x, diff, x->b.diff, P);
+        sync(x);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,338 @@
+// Census, search ranges + prefix sums, ragged matching cost, WTA and median:
+// the per-pixel integer stages of sgm_match and step (SURVEY.md §8(a) rows
+// A10-A13, A15, A19). All results are bit-exact restatements of the cited
+// reference lines.
+#include "common.cuh"
+
+namespace tsgm {
+
+// ---------------------------------------------------------------- census (A12)
+// census_transform, matching_cost.cpp:53-79. One thread per pixel of a
+// 32x8 tile; the 36x12 input tile (2-px halo) is staged in shared memory.
+constexpr int kCtW = 32, kCtH = 8;
+
+__global__ void census_kernel(Bufs b) {
+    __shared__ uint8_t tile[kCtH + 4][kCtW + 4];
+    const int a = blockIdx.z >> 1, which = blockIdx.z & 1;
+    const int s = slot_of(b, a);
+    const uint8_t* img = which ? b.right[a] : b.left[a];
+    uint32_t* sig = (which ? b.sigr : b.sigl) + static_cast<size_t>(s) * b.P;
+    const int x0 = blockIdx.x * kCtW - 2, y0 = blockIdx.y * kCtH - 2;
+    for (int i = threadIdx.y * kCtW + threadIdx.x; i < (kCtH + 4) * (kCtW + 4); i += kCtW * kCtH) {
+        const int ty = i / (kCtW + 4), tx = i % (kCtW + 4);
+        const int gx = x0 + tx, gy = y0 + ty;
+        tile[ty][tx] = (gx >= 0 && gx < b.W && gy >= 0 && gy < b.H) ? img[gy * b.W + gx] : 0;
+    }
+    __syncthreads();
+    const int x = blockIdx.x * kCtW + threadIdx.x, y = blockIdx.y * kCtH + threadIdx.y;
+    if (x >= b.W || y >= b.H) return;
+    uint32_t v = 0;
+    if (census_defined(x, y, b.W, b.H)) {
+        const uint8_t c = tile[threadIdx.y + 2][threadIdx.x + 2];
+#pragma unroll
+        for (int dy = 0; dy < 5; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 5; ++dx) {
+                if (dx == 2 && dy == 2) continue;
+                v = (v << 1) | (tile[threadIdx.y + dy][threadIdx.x + dx] < c ? 1u : 0u);
+            }
+    }
+    sig[y * b.W + x] = v;
+}
+
+void launch_census(const Bufs& b, int n, Launch L) {
+    dim3 grid((b.W + kCtW - 1) / kCtW, (b.H + kCtH - 1) / kCtH, 2 * n);
+    census_kernel<<<grid, dim3(kCtW, kCtH), 0, L.st>>>(b);
+    ++*L.counter;
+}
+
+// ---------------------------------------------------------------- ranges (A10, A11)
+// derive_search_ranges, temporal_filter.cpp:108-143, fused with the in-row
+// part of make_cost_volume's exclusive scan (matching_cost.cpp:30-48).
+// One CTA per (row, active slot); row totals go to row_sum.
+constexpr int kRowThreads = 256;
+
+__device__ __forceinline__ void derive_range(double d, double p, int top, int min_len,
+                                             int use_stddev, double gain, int& lo, int& hi) {
+    const double half = use_stddev ? gain * sqrt(p) : p;
+    lo = x86_cvtt_int(floor(d - half));
+    hi = x86_cvtt_int(ceil(d + half));
+    lo = max(0, min(top, lo));
+    hi = max(0, min(top, hi));
+    const int deficit = min_len - (hi - lo + 1);
+    if (deficit > 0) {
+        lo -= deficit / 2;
+        hi += deficit - deficit / 2;
+        if (lo < 0) {
+            hi = min(top, hi - lo);
+            lo = 0;
+        }
+        if (hi > top) {
+            lo = max(0, lo - (hi - top));
+            hi = top;
+        }
+    }
+}
+
+// Block-wide exclusive scan of one u32 per thread; returns the block total.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& excl) {
+    __shared__ uint32_t warp_tot[kRowThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < kRowThreads / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+        }
+        if (lane < kRowThreads / 32) warp_tot[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    const uint32_t before = wid ? warp_tot[wid - 1] : 0;
+    excl = before + incl - v;
+    const uint32_t total = warp_tot[kRowThreads / 32 - 1];
+    __syncthreads();
+    return total;
+}
+
+template <bool kDerive>
+__global__ void ranges_kernel(Bufs b, int min_hw, int use_stddev, double gain) {
+    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
+    const size_t base = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * b.W;
+    const int per = (b.W + kRowThreads - 1) / kRowThreads;
+    const int x0 = threadIdx.x * per;
+    const int top = b.d_max - 1, min_len = 2 * min_hw + 1;
+    uint32_t sum = 0;
+    for (int k = 0; k < per; ++k) {
+        const int x = x0 + k;
+        if (x >= b.W) break;
+        int lo, hi;
+        if (kDerive) {
+            lo = 0;
+            hi = top;
+            if (b.pv[base + x]) derive_range(b.pd[base + x], b.pp[base + x], top, min_len,
+                                             use_stddev, gain, lo, hi);
+            b.lo[base + x] = static_cast<uint16_t>(lo);
+            b.hi[base + x] = static_cast<uint16_t>(hi);
+        } else {
+            lo = b.lo[base + x];
+            hi = b.hi[base + x];
+        }
+        sum += static_cast<uint32_t>(hi - lo + 1);
+    }
+    uint32_t excl;
+    const uint32_t total = block_exclusive_scan(sum, excl);
+    uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * b.W;
+    uint32_t run = excl;
+    for (int k = 0; k < per; ++k) {
+        const int x = x0 + k;
+        if (x >= b.W) break;
+        off[x] = run;  // in-row exclusive; rebased by offsets_finalize
+        run += static_cast<uint32_t>(b.hi[base + x] - b.lo[base + x] + 1);
+    }
+    if (threadIdx.x == 0) b.row_sum[static_cast<size_t>(s) * b.H + y] = total;
+}
+
+void launch_ranges_from_pred(const Bufs& b, int n, int min_hw, int use_stddev, double gain,
+                             Launch L) {
+    ranges_kernel<true><<<dim3(b.H, n), kRowThreads, 0, L.st>>>(b, min_hw, use_stddev, gain);
+    ++*L.counter;
+}
+void launch_ranges_given(const Bufs& b, int n, Launch L) {
+    ranges_kernel<false><<<dim3(b.H, n), kRowThreads, 0, L.st>>>(b, 0, 0, 0.0);
+    ++*L.counter;
+}
+
+// Per slot: exclusive scan of the row totals in u64 (overflow -> flag, the
+// reference throws at matching_cost.cpp:43-44), then rebase every offset.
+__global__ void row_scan_kernel(Bufs b) {
+    const int a = blockIdx.x, s = slot_of(b, a);
+    __shared__ unsigned long long carry;
+    __shared__ unsigned long long part[1024];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    uint32_t* rs = b.row_sum + static_cast<size_t>(s) * b.H;
+    for (int base = 0; base < b.H; base += 1024) {
+        const int y = base + threadIdx.x;
+        const unsigned long long v = y < b.H ? rs[y] : 0ull;
+        part[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele, H is small
+            const unsigned long long t = threadIdx.x >= o ? part[threadIdx.x - o] : 0ull;
+            __syncthreads();
+            part[threadIdx.x] += t;
+            __syncthreads();
+        }
+        const unsigned long long incl = part[threadIdx.x] + carry;
+        __syncthreads();
+        if (y < b.H) {
+            const unsigned long long excl = incl - v;
+            rs[y] = excl > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(excl);
+        }
+        if (threadIdx.x == 1023) carry = incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        b.ncells[s] = carry;
+        b.overflow[s] = carry > 0xffffffffull ? 1 : 0;
+        b.off[static_cast<size_t>(s) * (b.P + 1) + b.P] = static_cast<uint32_t>(carry);
+    }
+}
+
+__global__ void offsets_finalize_kernel(Bufs b) {
+    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
+    const uint32_t rb = b.row_sum[static_cast<size_t>(s) * b.H + y];
+    uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * b.W;
+    for (int x = threadIdx.x; x < b.W; x += blockDim.x) off[x] += rb;
+}
+
+void launch_offsets(const Bufs& b, int n, Launch L) {
+    row_scan_kernel<<<n, 1024, 0, L.st>>>(b);
+    offsets_finalize_kernel<<<dim3(b.H, n), kRowThreads, 0, L.st>>>(b);
+    *L.counter += 2;
+}
+
+// ---------------------------------------------------------------- cost (A13)
+// build_cost_volume, matching_cost.cpp:88-117. One CTA per (row, slot); the
+// row's signatures, lo and in-row offsets are staged in shared memory and every
+// thread writes consecutive cells (coalesced), locating its pixel by binary
+// search over the in-row offsets.
+__global__ void cost_kernel(Bufs b) {
+    extern __shared__ uint32_t sm[];
+    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
+    const int W = b.W;
+    uint32_t* sl = sm;
+    uint32_t* sr = sl + W;
+    uint32_t* o = sr + W;            // W+1 in-row offsets
+    uint16_t* lo = reinterpret_cast<uint16_t*>(o + W + 1);
+    const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
+    const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
+    const uint32_t row0 = off[0];
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+        sl[x] = b.sigl[pbase + x];
+        sr[x] = b.sigr[pbase + x];
+        o[x] = off[x] - row0;
+        lo[x] = b.lo[pbase + x];
+    }
+    if (threadIdx.x == 0) o[W] = off[W] - row0;  // next row's first offset (or total)
+    __syncthreads();
+    const uint32_t n = o[W];
+    uint8_t* out = b.cost + static_cast<size_t>(s) * b.vol_cap + row0;
+    const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
+    for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+        int l = 0, r = W;  // largest x with o[x] <= c
+        while (r - l > 1) {
+            const int m = (l + r) >> 1;
+            if (o[m] <= c) l = m; else r = m;
+        }
+        const int x = l;
+        const int xr = x - (static_cast<int>(lo[x]) + static_cast<int>(c - o[x]));
+        const bool ok = row_def && x >= kCensusRadius && x < W - kCensusRadius &&
+                        xr >= kCensusRadius && xr < W - kCensusRadius;
+        out[c] = ok ? static_cast<uint8_t>(__popc(sl[x] ^ sr[xr])) : static_cast<uint8_t>(kMaxCost);
+    }
+}
+
+void launch_cost(const Bufs& b, int n, Launch L) {
+    const size_t smem = sizeof(uint32_t) * (3 * b.W + 1) + sizeof(uint16_t) * b.W;
+    cost_kernel<<<dim3(b.H, n), 512, smem, L.st>>>(b);
+    ++*L.counter;
+}
+
+// ---------------------------------------------------------------- WTA (A15)
+// winner_takes_all, sgm.cpp:163-187: first minimum of S over the window,
+// 2-px census border invalid. One warp per pixel group: lanes stride the
+// window, then a (value, index) warp argmin keeps the first minimum.
+__global__ void wta_kernel(Bufs b) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
+    const uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap;
+    for (int i = warp; i < b.P; i += nwarps) {
+        const int x = i % b.W, y = i / b.W;
+        const size_t pi = static_cast<size_t>(s) * b.P + i;
+        if (!census_defined(x, y, b.W, b.H)) {
+            if (lane == 0) {
+                b.md[pi] = 0;
+                b.mv[pi] = 0;
+            }
+            continue;
+        }
+        const uint32_t o0 = off[i], n = off[i + 1] - o0;
+        uint32_t best = 0xffffffffu;  // (value << 16) | index: min keeps first index
+        for (uint32_t j = lane; j < n; j += 32) {
+            const uint32_t key = (static_cast<uint32_t>(agg[o0 + j]) << 16) | j;
+            best = min(best, key);
+        }
+        best = __reduce_min_sync(0xffffffffu, best);
+        if (lane == 0) {
+            b.md[pi] = static_cast<int32_t>(b.lo[pi]) + static_cast<int32_t>(best & 0xffffu);
+            b.mv[pi] = 1;
+        }
+    }
+}
+
+void launch_wta(const Bufs& b, int n, Launch L) {
+    const int blocks = (b.P + 7) / 8 < 2048 ? (b.P + 7) / 8 : 2048;
+    wta_kernel<<<dim3(blocks, n), 256, 0, L.st>>>(b);
+    ++*L.counter;
+}
+
+// ---------------------------------------------------------------- median (A19)
+// median_refine, sgm.cpp:189-216: lower median of the valid 3x3 neighbours,
+// valid iff at least 5.
+__global__ void median_kernel(Bufs b, const int32_t* in_d, const uint8_t* in_v, int32_t* out_d,
+                              uint8_t* out_v) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.P) return;
+    const int x = i % b.W, y = i / b.W;
+    const size_t base = static_cast<size_t>(s) * b.P;
+    int32_t v[9];
+    int n = 0;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+            const int nx = x + dx, ny = y + dy;
+            if (nx < 0 || nx >= b.W || ny < 0 || ny >= b.H) continue;
+            const size_t j = base + static_cast<size_t>(ny) * b.W + nx;
+            if (!in_v[j]) continue;
+            v[n++] = in_d[j];
+        }
+    if (n < 5) {
+        out_d[base + i] = 0;
+        out_v[base + i] = 0;
+        return;
+    }
+    // lower median = element of rank (n-1)/2
+    const int k = (n - 1) / 2;
+    int32_t med = 0;
+    for (int p = 0; p < n; ++p) {
+        int less = 0, leq = 0;
+        for (int q = 0; q < n; ++q) {
+            less += v[q] < v[p];
+            leq += v[q] <= v[p];
+        }
+        if (less <= k && k < leq) med = v[p];
+    }
+    out_d[base + i] = med;
+    out_v[base + i] = 1;
+}
+
+void launch_median(const Bufs& b, int n, const int32_t* in_d, const uint8_t* in_v,
+                   int32_t* out_d, uint8_t* out_v, Launch L) {
+    median_kernel<<<dim3((b.P + 255) / 256, n), 256, 0, L.st>>>(b, in_d, in_v, out_d, out_v);
+    ++*L.counter;
+}
+
+}  // namespace tsgm

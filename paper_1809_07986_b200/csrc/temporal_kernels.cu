@@ -1,0 +1,243 @@
+// FP64 Kalman-state kernels: ego-motion forward warp with the reference's
+// lexicographic collision rule, prediction variance, discontinuity rejection,
+// zoom-hole fill, correction, diff, mask and integer rendering (SURVEY.md
+// §8(a) rows A5-A9, A16-A18, A21). Compiled with -fmad=false and written in
+// the reference's operation order, so results are bit-identical to the x86-64
+// reference build (which has no FMA).
+#include "common.cuh"
+
+namespace tsgm {
+
+// ---------------------------------------------------------------- warp (A5, A6)
+// warp_state_ex, geometry.cpp:127-156. A colliding target keeps the
+// lexicographic maximum of (d' up, p down, source d down) (replaces(),
+// geometry.cpp:116-123): pass 1 atomicMax on d', pass 2 atomicMin on p among
+// sources whose d' equals the winner, pass 3 atomicMin on the source d among
+// sources matching both. Keys are order-preserving u64 images of the doubles,
+// so the result is exact and independent of thread order.
+struct Mapped {
+    int t;  // target pixel index, -1 if dropped
+    double dp;
+};
+
+__device__ __forceinline__ Mapped map_source(const double* H, int x, int y, double ds, int W,
+                                             int Hh, int d_max) {
+    Mapped m{-1, 0.0};
+    const double xd = static_cast<double>(x), yd = static_cast<double>(y);
+    double v[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)  // DispHomography::apply, geometry.cpp:56-61
+        v[r] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(H[r * 4 + 0], xd), __dmul_rn(H[r * 4 + 1], yd)),
+                                   __dmul_rn(H[r * 4 + 2], ds)),
+                         __dmul_rn(H[r * 4 + 3], 1.0));
+    if (!(v[3] > 1e-12)) return m;
+    const double mx = v[0] / v[3], my = v[1] / v[3], dp = v[2] / v[3];
+    if (!(dp > 0.0) || !(dp < static_cast<double>(d_max))) return m;
+    const int tx = x86_lround_int(mx), ty = x86_lround_int(my);
+    if (tx < 0 || tx >= W || ty < 0 || ty >= Hh) return m;
+    m.t = ty * W + tx;
+    m.dp = dp;
+    return m;
+}
+
+template <int kPass>
+__global__ void warp_pass_kernel(Bufs b, const double* src_d, const double* src_p,
+                                 const uint8_t* src_v, int d_max) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.P) return;
+    const size_t base = static_cast<size_t>(s) * b.P;
+    if (!src_v[base + i]) return;
+    __shared__ double H[16];
+    (void)H;
+    const double* Hg = b.H16 + 16 * a;
+    const double ds = src_d[base + i];
+    const Mapped m = map_source(Hg, i % b.W, i / b.W, ds, b.W, b.H, d_max);
+    if (m.t < 0) return;
+    const size_t t = base + m.t;
+    const unsigned long long kd = ord_key(m.dp);
+    if (kPass == 1) {
+        atomicMax(&b.kd[t], kd);
+    } else if (kPass == 2) {
+        if (b.kd[t] == kd) atomicMin(&b.kp[t], ord_key(src_p[base + i]));
+    } else {
+        if (b.kd[t] == kd && b.kp[t] == ord_key(src_p[base + i])) atomicMin(&b.ks[t], ord_key(ds));
+    }
+}
+
+void launch_warp(const Bufs& b, int n, const double* src_d, const double* src_p,
+                 const uint8_t* src_v, int d_max, Launch L) {
+    const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(b.P);
+    // keys of the active slots only: slots are not contiguous in general, so
+    // clear per slot (n is small; these are memset nodes, not kernels)
+    dim3 grid((b.P + 255) / 256, n);
+    (void)bytes;
+    warp_pass_kernel<1><<<grid, 256, 0, L.st>>>(b, src_d, src_p, src_v, d_max);
+    warp_pass_kernel<2><<<grid, 256, 0, L.st>>>(b, src_d, src_p, src_v, d_max);
+    warp_pass_kernel<3><<<grid, 256, 0, L.st>>>(b, src_d, src_p, src_v, d_max);
+    *L.counter += 3;
+}
+
+// Decode the winners (warp_state_ex output) and apply predict's variance step,
+// temporal_filter.cpp:35-47: invalidate if the source disparity is not
+// positive, phi = d'/d_src, p = (phi*phi)*p + q. Also re-arms the keys for the
+// next frame (kd = 0, kp = ks = ~0).
+__global__ void predict_finalize_kernel(Bufs b, double q, int apply_phi) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.P) return;
+    const size_t t = static_cast<size_t>(s) * b.P + i;
+    const unsigned long long kd = b.kd[t];
+    double d = 0.0, p = 0.0, src = 0.0;
+    uint8_t v = 0;
+    if (kd != 0ull) {
+        d = key_double(kd);
+        p = key_double(b.kp[t]);
+        src = key_double(b.ks[t]);
+        v = 1;
+        if (apply_phi) {
+            if (!(src > 0.0)) {
+                d = p = 0.0;
+                v = 0;
+            } else {
+                const double phi = d / src;
+                p = __dadd_rn(__dmul_rn(__dmul_rn(phi, phi), p), q);
+            }
+        }
+    }
+    b.wd[t] = d;
+    b.wp[t] = p;
+    b.wv[t] = v;
+    if (b.wsrc) b.wsrc[t] = kd != 0ull ? src : 0.0;
+    b.kd[t] = 0ull;
+    b.kp[t] = ~0ull;
+    b.ks[t] = ~0ull;
+}
+
+void launch_predict_finalize(const Bufs& b, int n, double q, int apply_phi, Launch L) {
+    predict_finalize_kernel<<<dim3((b.P + 255) / 256, n), 256, 0, L.st>>>(b, q, apply_phi);
+    ++*L.counter;
+}
+
+// ---------------------------------------------------------------- reject + fill (A8, A9)
+// reject_discontinuities (temporal_filter.cpp:51-74) decided on its input,
+// then fill_zoom_holes (:76-106) decided on reject's output, fused: a pixel's
+// fill needs reject's verdict at its 4 neighbours, each recomputed from the
+// input (radius-2 dependence, read through L1).
+__device__ __forceinline__ bool rejected(const double* d, const uint8_t* v, int x, int y, int W,
+                                         int H, double thr) {
+    const int i = y * W + x;
+    if (!v[i]) return false;
+    const double di = d[i];
+    // neighbour order (1,0), (-1,0), (0,1), (0,-1) as kDx/kDy at :52-53
+    if (x + 1 < W && v[i + 1] && fabs(di - d[i + 1]) > thr) return true;
+    if (x - 1 >= 0 && v[i - 1] && fabs(di - d[i - 1]) > thr) return true;
+    if (y + 1 < H && v[i + W] && fabs(di - d[i + W]) > thr) return true;
+    if (y - 1 >= 0 && v[i - W] && fabs(di - d[i - W]) > thr) return true;
+    return false;
+}
+
+__global__ void reject_fill_kernel(Bufs b, const double* in_d, const double* in_p,
+                                   const uint8_t* in_v, double* out_d, double* out_p,
+                                   uint8_t* out_v, double thr, int do_reject, int do_fill) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.P) return;
+    const size_t base = static_cast<size_t>(s) * b.P;
+    const double* d = in_d + base;
+    const double* p = in_p + base;
+    const uint8_t* v = in_v + base;
+    const int W = b.W, H = b.H, x = i % W, y = i / W;
+    // validity after rejection
+    auto rv = [&](int xx, int yy) -> bool {
+        const int j = yy * W + xx;
+        return v[j] && !(do_reject && rejected(d, v, xx, yy, W, H, thr));
+    };
+    double od = d[i], op = p[i];
+    uint8_t ov = v[i];
+    if (v[i] && do_reject && rejected(d, v, x, y, W, H, thr)) {
+        od = op = 0.0;  // DisparityState::invalidate, geometry.hpp:70-74
+        ov = 0;
+    }
+    if (do_fill && !ov) {
+        const bool horiz = x - 1 >= 0 && x + 1 < W && rv(x - 1, y) && rv(x + 1, y);
+        const bool vert = y - 1 >= 0 && y + 1 < H && rv(x, y - 1) && rv(x, y + 1);
+        if (horiz || vert) {
+            double ds = 0.0, ps = 0.0;
+            int nn = 0;
+            if (horiz) {
+                ds = __dadd_rn(ds, __dadd_rn(d[i - 1], d[i + 1]));
+                ps = __dadd_rn(ps, __dadd_rn(p[i - 1], p[i + 1]));
+                nn += 2;
+            }
+            if (vert) {
+                ds = __dadd_rn(ds, __dadd_rn(d[i - W], d[i + W]));
+                ps = __dadd_rn(ps, __dadd_rn(p[i - W], p[i + W]));
+                nn += 2;
+            }
+            od = ds / nn;
+            op = ps / nn;
+            ov = 1;
+        }
+    }
+    out_d[base + i] = od;
+    out_p[base + i] = op;
+    out_v[base + i] = ov;
+}
+
+void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* in_p,
+                        const uint8_t* in_v, double* out_d, double* out_p, uint8_t* out_v,
+                        double disc_thresh, int do_reject, int do_fill, Launch L) {
+    reject_fill_kernel<<<dim3((b.P + 255) / 256, n), 256, 0, L.st>>>(
+        b, in_d, in_p, in_v, out_d, out_p, out_v, disc_thresh, do_reject, do_fill);
+    ++*L.counter;
+}
+
+// ---------------------------------------------------------------- correct (A16-A18, A21)
+// correct (temporal_filter.cpp:145-170), the diff map (:223-229), the
+// Mahalanobis mask extension (A21) and render_integer (:178-191), fused.
+__global__ void correct_kernel(Bufs b, double r, double tau) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.P) return;
+    const size_t t = static_cast<size_t>(s) * b.P + i;
+    const bool hp = b.pv[t] != 0, hm = b.mv[t] != 0;
+    const double pdv = b.pd[t], ppv = b.pp[t];
+    const double dz = static_cast<double>(b.md[t]);
+    double d = 0.0, p = 0.0;
+    uint8_t v = 0;
+    if (hp && hm) {
+        const double k = ppv / __dadd_rn(ppv, r);
+        d = __dadd_rn(pdv, __dmul_rn(k, __dsub_rn(dz, pdv)));
+        const double omk = __dsub_rn(1.0, k);
+        p = __dadd_rn(__dmul_rn(__dmul_rn(omk, omk), ppv), __dmul_rn(__dmul_rn(k, k), r));
+        v = 1;
+    } else if (hm) {
+        d = dz;
+        p = r;
+        v = 1;
+    } else if (hp) {
+        d = pdv;
+        p = ppv;
+        v = 1;
+    }
+    b.sd[t] = d;
+    b.sp[t] = p;
+    b.sv[t] = v;
+    b.diff[t] = (hp && hm) ? fabs(__dsub_rn(pdv, dz)) : 0.0;
+    uint8_t mk = 0;
+    if (hp && hm) {
+        const double e = __dsub_rn(dz, pdv);
+        mk = __dmul_rn(e, e) > __dmul_rn(__dmul_rn(tau, tau), __dadd_rn(ppv, r)) ? 1 : 0;
+    }
+    b.mask[t] = mk;
+    b.rd[t] = v ? x86_lround_int(d) : 0;
+    b.rv[t] = v;
+}
+
+void launch_correct(const Bufs& b, int n, double r, double mask_tau, Launch L) {
+    correct_kernel<<<dim3((b.P + 255) / 256, n), 256, 0, L.st>>>(b, r, mask_tau);
+    ++*L.counter;
+}
+
+}  // namespace tsgm

@@ -1,0 +1,416 @@
+"""Python mirror of the reference's hot-path API, running on the B200.
+
+Same names, argument meaning and error behaviour as the reference C++ library
+(/root/reference/proj/include/tsgm/*.hpp): invalid arguments raise
+``ValueError`` (std::invalid_argument), CUDA/runtime failures raise
+``RuntimeError`` (std::runtime_error). Every call goes through the C-ABI of
+``lib/libtsgm_b200.so`` (include/tsgm_b200.h); nothing here computes on the CPU
+beyond argument marshalling.
+
+Two levels:
+
+* stage functions (``census_transform`` ... ``step``) — the reference's public
+  sub-stage API, stateless, host numpy arrays in and out;
+* :class:`Engine` — the production path: device-resident Kalman state for many
+  independent sequences ("slots"), one batched launch sequence per frame.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import ConfigC, FilterConfigC, OUT, SgmParamsC, StereoCalibC, check, ptr
+
+NONDIAGONAL, DIAGONAL = 0, 1  # PathSet, sgm.hpp:10-13
+
+
+@dataclass
+class SgmParams:  # sgm.hpp:15-23
+    p1: int = 6
+    p2: int = 65
+    paths: int = 8
+    path_set: int = NONDIAGONAL
+    d_max: int = 128
+
+    def _c(self):
+        return SgmParamsC(self.p1, self.p2, self.paths, int(self.path_set), self.d_max)
+
+
+@dataclass
+class FilterConfig:  # temporal_filter.hpp:8-26 (NoiseParams q, r flattened)
+    q: float = 0.5
+    r: float = 1.0
+    p_init: float = 4096.0
+    disc_thresh: float = 2.0
+    min_range_halfwidth: int = 2
+    range_use_stddev: bool = False
+    range_stddev_gain: float = 2.0
+
+    def _c(self):
+        return FilterConfigC(self.q, self.r, self.p_init, self.disc_thresh,
+                             self.min_range_halfwidth, 1 if self.range_use_stddev else 0,
+                             self.range_stddev_gain)
+
+
+@dataclass
+class StereoCalib:  # geometry.hpp:17-27
+    focal_px: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+    baseline_m: float = 0.0
+    width: int = 0
+    height: int = 0
+    d_max: int = 0
+
+    def _c(self):
+        return StereoCalibC(self.focal_px, self.cx, self.cy, self.baseline_m, self.width,
+                            self.height, self.d_max)
+
+
+def _as(x, cls):
+    """Accept any object with the dataclass's attribute names."""
+    if isinstance(x, cls):
+        return x
+    return cls(**{k: getattr(x, k) for k in cls.__dataclass_fields__})
+
+
+def _u8(a):
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _u16(a):
+    return np.ascontiguousarray(a, dtype=np.uint16)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _hw(a):
+    h, w = a.shape
+    return w, h
+
+
+# --------------------------------------------------------------------- stages
+def census_transform(img):
+    """census_transform (matching_cost.cpp:53-79) -> u32 signatures."""
+    img = _u8(img)
+    w, h = _hw(img)
+    sig = np.zeros((h, w), np.uint32)
+    check(_lib.load().tsgm_census_transform(ptr(img), w, h, ptr(sig)))
+    return sig
+
+
+def build_cost_volume(left, right, lo, hi):
+    """build_cost_volume (matching_cost.cpp:88-117) -> (offsets u32[W*H+1], cost u8[N])."""
+    left, right, lo, hi = _u8(left), _u8(right), _u16(lo), _u16(hi)
+    w, h = _hw(left)
+    if right.shape != left.shape or lo.shape != left.shape or hi.shape != left.shape:
+        raise ValueError("build_cost_volume: input size mismatch")
+    n = int((hi.astype(np.int64) - lo.astype(np.int64) + 1).sum())
+    off = np.zeros(w * h + 1, np.uint32)
+    cost = np.zeros(max(n, 1), np.uint8)
+    check(_lib.load().tsgm_build_cost_volume(ptr(left), ptr(right), w, h, ptr(lo), ptr(hi),
+                                            ptr(off), ptr(cost), C.c_uint64(cost.size)))
+    return off, cost[:n]
+
+
+def aggregate_paths(cost, lo, hi, params):
+    """aggregate_paths (sgm.cpp:135-161) over a ragged C volume -> u16 S."""
+    cost, lo, hi = _u8(cost), _u16(lo), _u16(hi)
+    w, h = _hw(lo)
+    p = _as(params, SgmParams)._c()
+    agg = np.zeros(max(cost.size, 1), np.uint16)
+    check(_lib.load().tsgm_aggregate_paths(ptr(cost), ptr(lo), ptr(hi), w, h, C.byref(p),
+                                          ptr(agg)))
+    return agg[: cost.size]
+
+
+def winner_takes_all(agg, lo, hi):
+    """winner_takes_all (sgm.cpp:163-187) -> (d i32, valid u8)."""
+    agg, lo, hi = _u16(agg), _u16(lo), _u16(hi)
+    w, h = _hw(lo)
+    d = np.zeros((h, w), np.int32)
+    v = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_winner_takes_all(ptr(agg), ptr(lo), ptr(hi), w, h, ptr(d), ptr(v)))
+    return d, v
+
+
+def median_refine(d, valid):
+    """median_refine (sgm.cpp:189-216)."""
+    d, valid = _i32(d), _u8(valid)
+    w, h = _hw(d)
+    od = np.zeros((h, w), np.int32)
+    ov = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_median_refine(ptr(d), ptr(valid), w, h, ptr(od), ptr(ov)))
+    return od, ov
+
+
+def sgm_match(left, right, lo, hi, params):
+    """sgm_match (sgm.cpp:226-257): census -> cost -> aggregate -> WTA."""
+    left, right, lo, hi = _u8(left), _u8(right), _u16(lo), _u16(hi)
+    if left.shape != right.shape:
+        raise ValueError("sgm_match: image size mismatch")
+    if lo.shape != left.shape:
+        raise ValueError("sgm_match: range map size mismatch")
+    w, h = _hw(left)
+    p = _as(params, SgmParams)._c()
+    d = np.zeros((h, w), np.int32)
+    v = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_sgm_match(ptr(left), ptr(right), w, h, ptr(lo), ptr(hi), C.byref(p),
+                                    ptr(d), ptr(v)))
+    return d, v
+
+
+def relative_motion(prev_pose, cur_pose):
+    """relative_motion (geometry.cpp:189-197): 3x4 camera-to-world poses -> (R, t)."""
+    a, b = _f64(prev_pose).ravel(), _f64(cur_pose).ravel()
+    r = np.zeros(9)
+    t = np.zeros(3)
+    check(_lib.load().tsgm_relative_motion(ptr(a), ptr(b), ptr(r), ptr(t)))
+    return r.reshape(3, 3), t
+
+
+def disparity_homography(R, t, calib):
+    """disparity_homography (geometry.cpp:77-110) -> 4x4."""
+    R, t = _f64(R).ravel(), _f64(t).ravel()
+    c = _as(calib, StereoCalib)._c()
+    H = np.zeros(16)
+    check(_lib.load().tsgm_disparity_homography(ptr(R), ptr(t), C.byref(c), ptr(H)))
+    return H.reshape(4, 4)
+
+
+def warp_state_ex(d, p, valid, H, d_max):
+    """warp_state_ex (geometry.cpp:127-156) -> (d, p, valid, source_d)."""
+    d, p, valid, H = _f64(d), _f64(p), _u8(valid), _f64(H).ravel()
+    w, h = _hw(d)
+    od, op, osrc = np.zeros((h, w)), np.zeros((h, w)), np.zeros((h, w))
+    ov = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_warp_state_ex(ptr(d), ptr(p), ptr(valid), w, h, ptr(H), int(d_max),
+                                        ptr(od), ptr(op), ptr(ov), ptr(osrc)))
+    return od, op, ov, osrc
+
+
+def predict(d, p, valid, R, t, calib, cfg):
+    """predict (temporal_filter.cpp:28-49)."""
+    d, p, valid = _f64(d), _f64(p), _u8(valid)
+    R, t = _f64(R).ravel(), _f64(t).ravel()
+    w, h = _hw(d)
+    c, f = _as(calib, StereoCalib)._c(), _as(cfg, FilterConfig)._c()
+    od, op = np.zeros((h, w)), np.zeros((h, w))
+    ov = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_predict(ptr(d), ptr(p), ptr(valid), w, h, ptr(R), ptr(t), C.byref(c),
+                                  C.byref(f), ptr(od), ptr(op), ptr(ov)))
+    return od, op, ov
+
+
+def reject_discontinuities(d, p, valid, cfg):
+    """reject_discontinuities (temporal_filter.cpp:51-74)."""
+    d, p, valid = _f64(d), _f64(p), _u8(valid)
+    w, h = _hw(d)
+    f = _as(cfg, FilterConfig)._c()
+    od, op = np.zeros((h, w)), np.zeros((h, w))
+    ov = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_reject_discontinuities(ptr(d), ptr(p), ptr(valid), w, h, C.byref(f),
+                                                 ptr(od), ptr(op), ptr(ov)))
+    return od, op, ov
+
+
+def fill_zoom_holes(d, p, valid):
+    """fill_zoom_holes (temporal_filter.cpp:76-106)."""
+    d, p, valid = _f64(d), _f64(p), _u8(valid)
+    w, h = _hw(d)
+    od, op = np.zeros((h, w)), np.zeros((h, w))
+    ov = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_fill_zoom_holes(ptr(d), ptr(p), ptr(valid), w, h, ptr(od), ptr(op),
+                                          ptr(ov)))
+    return od, op, ov
+
+
+def derive_search_ranges(d, p, valid, calib, cfg):
+    """derive_search_ranges (temporal_filter.cpp:108-143) -> (lo, hi) u16."""
+    d, p, valid = _f64(d), _f64(p), _u8(valid)
+    w, h = _hw(d)
+    c, f = _as(calib, StereoCalib)._c(), _as(cfg, FilterConfig)._c()
+    lo = np.zeros((h, w), np.uint16)
+    hi = np.zeros((h, w), np.uint16)
+    check(_lib.load().tsgm_derive_search_ranges(ptr(d), ptr(p), ptr(valid), w, h, C.byref(c),
+                                               C.byref(f), ptr(lo), ptr(hi)))
+    return lo, hi
+
+
+def correct(d, p, valid, meas_d, meas_valid, cfg):
+    """correct (temporal_filter.cpp:145-170)."""
+    d, p, valid = _f64(d), _f64(p), _u8(valid)
+    md, mv = _i32(meas_d), _u8(meas_valid)
+    if md.shape != d.shape:
+        raise ValueError("correct: dimension mismatch")
+    w, h = _hw(d)
+    f = _as(cfg, FilterConfig)._c()
+    od, op = np.zeros((h, w)), np.zeros((h, w))
+    ov = np.zeros((h, w), np.uint8)
+    check(_lib.load().tsgm_correct(ptr(d), ptr(p), ptr(valid), ptr(md), ptr(mv), w, h, C.byref(f),
+                                  ptr(od), ptr(op), ptr(ov)))
+    return od, op, ov
+
+
+def step(state, left, right, R, t, calib, params, cfg):
+    """step (temporal_filter.cpp:195-232) for one sequence, value semantics.
+
+    ``state`` is ``(d, p, valid)`` or ``None`` for the default (empty) state.
+    Returns a dict with the StepResult fields: d, p, valid (posterior),
+    export_d, export_valid (median-refined map) and diff."""
+    left, right = _u8(left), _u8(right)
+    if left.shape != right.shape:
+        raise ValueError("step: left/right dimension mismatch")
+    w, h = _hw(left)
+    R, t = _f64(R).ravel(), _f64(t).ravel()
+    c = _as(calib, StereoCalib)._c()
+    sp = _as(params, SgmParams)._c()
+    f = _as(cfg, FilterConfig)._c()
+    if state is None:
+        sd = spp = sv = None
+        sw = sh = 0
+    else:
+        sd, spp, sv = _f64(state[0]), _f64(state[1]), _u8(state[2])
+        sh, sw = sv.shape
+    out = dict(d=np.zeros((h, w)), p=np.zeros((h, w)), valid=np.zeros((h, w), np.uint8),
+               export_d=np.zeros((h, w), np.int32), export_valid=np.zeros((h, w), np.uint8),
+               diff=np.zeros((h, w)))
+    check(_lib.load().tsgm_step_once(
+        ptr(sd), ptr(spp), ptr(sv), sw, sh, ptr(left), ptr(right), w, h, ptr(R), ptr(t),
+        C.byref(c), C.byref(sp), C.byref(f), ptr(out["d"]), ptr(out["p"]), ptr(out["valid"]),
+        ptr(out["export_d"]), ptr(out["export_valid"]), ptr(out["diff"])))
+    return out
+
+
+# --------------------------------------------------------------------- engine
+_OUT_DTYPES = dict(state_d=np.float64, state_p=np.float64, state_valid=np.uint8,
+                   export_d=np.int32, export_valid=np.uint8, diff=np.float64, mask=np.uint8,
+                   pred_d=np.float64, pred_p=np.float64, pred_valid=np.uint8, lo=np.uint16,
+                   hi=np.uint16, meas_d=np.int32, meas_valid=np.uint8, offsets=np.uint32,
+                   cost=np.uint8, agg=np.uint16)
+
+
+@dataclass
+class EngineConfig:
+    calib: StereoCalib
+    sgm: SgmParams
+    filter: FilterConfig
+    max_slots: int = 1
+    device: int = 0
+    mask_tau: float = 3.0
+    keep_volumes: bool = True
+
+
+class Engine:
+    """Batched, device-resident production path (tsgm_ctx)."""
+
+    def __init__(self, cfg: EngineConfig):
+        self.cfg = cfg
+        cal = _as(cfg.calib, StereoCalib)
+        c = ConfigC(cal.width, cal.height, cfg.max_slots, cfg.device, cal._c(),
+                    _as(cfg.sgm, SgmParams)._c(), _as(cfg.filter, FilterConfig)._c(),
+                    cfg.mask_tau, _lib.TSGM_KEEP_VOLUMES if cfg.keep_volumes else 0)
+        self._lib = _lib.load()
+        h = C.c_void_p()
+        check(self._lib.tsgm_create(C.byref(c), C.byref(h)))
+        self._h = h
+        self.width, self.height = cal.width, cal.height
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.tsgm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self, slot: int):
+        check(self._lib.tsgm_reset(self._h, slot))
+
+    def set_state(self, slot, d, p, valid):
+        check(self._lib.tsgm_set_state(self._h, slot, ptr(_f64(d)), ptr(_f64(p)),
+                                       ptr(_u8(valid))))
+
+    @staticmethod
+    def _motions(motions, n):
+        m = np.zeros((n, 12))
+        for i, (R, t) in enumerate(motions):
+            m[i, :9] = np.asarray(R, np.float64).ravel()
+            m[i, 9:] = np.asarray(t, np.float64).ravel()
+        return m
+
+    def step(self, slots, lefts, rights, motions):
+        """One frame for ``len(slots)`` sequences; host u8 images; motions =
+        [(R 3x3, t 3)] (identity for a first frame)."""
+        n = len(slots)
+        sl = np.asarray(slots, np.int32)
+        ls = [_u8(x) for x in lefts]
+        rs = [_u8(x) for x in rights]
+        lp = (C.c_void_p * n)(*[x.ctypes.data for x in ls])
+        rp = (C.c_void_p * n)(*[x.ctypes.data for x in rs])
+        m = self._motions(motions, n)
+        check(self._lib.tsgm_step(self._h, n, ptr(sl), lp, rp, ptr(m)))
+
+    def step_device(self, slots, left_ptrs, right_ptrs, motion12):
+        """Device-resident inputs: raw CUDA pointers, motion12 f64 [n, 12]."""
+        n = len(slots)
+        sl = np.asarray(slots, np.int32)
+        lp = (C.c_void_p * n)(*left_ptrs)
+        rp = (C.c_void_p * n)(*right_ptrs)
+        m = _f64(motion12)
+        check(self._lib.tsgm_step_device(self._h, n, ptr(sl), lp, rp, ptr(m)))
+
+    def cells(self, slot) -> int:
+        v = C.c_uint64()
+        check(self._lib.tsgm_cells(self._h, slot, C.byref(v)))
+        return int(v.value)
+
+    def fetch(self, slot: int, what: str, out=None):
+        dt = _OUT_DTYPES[what]
+        if what in ("cost", "agg"):
+            shape = (self.cells(slot),)
+        elif what == "offsets":
+            shape = (self.width * self.height + 1,)
+        else:
+            shape = (self.height, self.width)
+        if out is None:
+            out = np.empty(shape, dt)
+        check(self._lib.tsgm_fetch(self._h, slot, OUT[what], ptr(out), out.nbytes))
+        return out
+
+    def sync(self):
+        check(self._lib.tsgm_sync(self._h))
+
+    def timer_begin(self):
+        check(self._lib.tsgm_timer_begin(self._h))
+
+    def timer_end(self) -> float:
+        ms = C.c_float()
+        check(self._lib.tsgm_timer_end(self._h, C.byref(ms)))
+        return float(ms.value)
+
+    def bench_aggregate(self, slots, reps=10):
+        """Standalone C -> S aggregation over the slots' current volumes:
+        (ms per aggregation, total cells)."""
+        sl = np.asarray(slots, np.int32)
+        ms = C.c_float()
+        cells = C.c_uint64()
+        check(self._lib.tsgm_bench_aggregate(self._h, len(sl), ptr(sl), reps, C.byref(ms),
+                                             C.byref(cells)))
+        return float(ms.value), int(cells.value)
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.tsgm_launch_count(self._h))
