@@ -63,6 +63,7 @@ typedef struct {
 typedef struct tsgm_ctx tsgm_ctx;
 
 #define TSGM_KEEP_VOLUMES 1u /* materialise C (u8) and S (u16) per slot for fetch */
+#define TSGM_FORCE_SCANLINE_AGG 2u /* use the per-direction scanline aggregation kernels */
 
 typedef struct {
     int32_t width, height;     /* image size (must equal calib.width/height) */

@@ -1,0 +1,381 @@
+// Line-sweep 8-path aggregation over ragged windows (aggregate_paths,
+// sgm.cpp:39-161 / SURVEY.md §8(a) row A14), the fast path.
+//
+// Decomposition. The 8 directions are grouped into 4 ROLES, each a sweep over
+// LINES in which every direction's predecessor lies in the previous line:
+//   A: columns x = 0..W-1,   directions (-1,0), (-1,-1), (-1,+1)
+//   B: columns x = W-1..0,   directions (+1,0), (+1,-1), (+1,+1)
+//   C: rows    y = 0..H-1,   direction  (0,-1)
+//   D: rows    y = H-1..0,   direction  (0,+1)
+// (4-path sets keep the subset). Within a line all pixels are independent, so
+// a CTA processes a line FLAT: every pixel's window is split into aligned
+// quads of 4 levels; pixels of <= 4 quads run as 4-lane groups (8 pixels per
+// warp), wider ones as a whole warp. Arithmetic is u16x2 SIMD (VIADDMNMX /
+// VIMNMX .U16x2), two levels per instruction.
+//
+// State. Per direction, each pixel's normalised path cost
+//   M(d) = min(L(d) - min_k L(k), P2)      (P2 for levels outside the window)
+// lives in shared memory in an ABSOLUTE-level slot (level d at byte 4 + d), so
+// the recursion (sgm.cpp:100-126) becomes, with no bounds checks,
+//   L(d) = C(d) + min(M_q(d), min(M_q(d-1), M_q(d+1)) + P1)
+// (absent predecessor levels read as P2, which is exactly the reference's
+// q_min + P2 cap after normalisation). Slots are SHEARED: direction (dl, di)
+// stores pixel i of line l at slot (i + di*l) mod len, so a pixel reads and
+// rewrites the same slot its predecessor wrote: one buffer per direction, one
+// barrier per line. Levels that leave a slot's window are reset to P2 (the
+// slot's quad range is tracked), keeping "outside the window == P2" invariant.
+//
+// Output. Each role writes its partial sum per quad (A/B: u16, C/D: u8 since a
+// single path cost <= 24 + P2 <= 255) in the quad layout qoff; the combine
+// kernel adds the partials into S in the reference's ragged layout. Sums of
+// u16 values never overflow (SgmParams::validate, sgm.cpp:21-22), so the
+// grouping is exact.
+#include "common.cuh"
+
+namespace tsgm {
+
+constexpr int kSweepThreads = 512;
+constexpr int kSweepWarps = kSweepThreads / 32;
+
+__host__ __device__ inline int sweep_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 3); }
+
+struct SweepPlan {
+    size_t buf, rng, meta, lists, total;
+};
+
+__host__ __device__ inline SweepPlan sweep_plan(int W, int H, int d_max) {
+    SweepPlan p;
+    const size_t sb = sweep_slot_bytes(d_max);
+    const size_t slots = (3 * static_cast<size_t>(H) > static_cast<size_t>(W)) ? 3 * static_cast<size_t>(H) : W;
+    const size_t lmax = W > H ? W : H;
+    p.buf = slots * sb;
+    p.rng = slots * 4;
+    p.meta = 3 * lmax * 4;
+    p.lists = ((2 * lmax * 2) + 15) & ~static_cast<size_t>(15);
+    p.total = p.buf + p.rng + p.meta + p.lists;
+    return p;
+}
+
+bool sweep_supported(int W, int H, int d_max, int p2) {
+    // u8 path costs need 24 + P2 <= 255; quads per lane <= 2 (d_max <= 256)
+    return kMaxCost + p2 <= 255 && d_max <= 256 && W < 65536 && H < 65536 &&
+           sweep_plan(W, H, d_max).total <= 227 * 1024;
+}
+
+struct SweepParams {
+    int p1, p2;
+    int roles;    // bit 0 A, 1 B, 2 C, 3 D
+    int ndir_ab;  // directions in the column roles
+    int di_ab[3];
+    int n;        // active slots
+};
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+    return __byte_perm(a, b, s);
+}
+
+// One pixel of a line, processed by a group of G lanes (G = 4 or 32), each
+// lane holding up to KQ quads.
+template <int G, int KQ>
+__device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, const int* di,
+                                            uint8_t* mbuf, int SB, uint32_t* rng,
+                                            const uint32_t* m_lohi, const uint32_t* m_cell,
+                                            const uint32_t* m_qoff, const uint8_t* cost,
+                                            void* out, bool out_u16, uint32_t P1x2, uint32_t P2x2,
+                                            uint32_t P2x4) {
+    const int lane = threadIdx.x & 31;
+    const int lg = lane & (G - 1);
+    const unsigned gmask = G == 32 ? 0xffffffffu : (0xfu << (lane & ~3));
+    const uint32_t lohi = m_lohi[i];
+    const int lo = static_cast<int>(lohi & 0xffffu), hi = static_cast<int>(lohi >> 16);
+    const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
+    const uint32_t cell = m_cell[i], qo = m_qoff[i];
+
+    bool act[KQ];
+    uint32_t CA[KQ], CB[KQ], ivA[KQ], ivB[KQ], sA[KQ], sB[KQ], LA[KQ], LB[KQ];
+#pragma unroll
+    for (int t = 0; t < KQ; ++t) {
+        const int k = lg + t * G;
+        act[t] = k < nq;
+        sA[t] = sB[t] = 0u;
+        CA[t] = CB[t] = ivA[t] = ivB[t] = 0u;
+        if (act[t]) {
+            const int d0 = 4 * (q0 + k);
+            // 4 matching costs for levels d0..d0+3 (bytes outside the window are
+            // read but masked): unaligned 32-bit window via a funnel shift
+            const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + cell + (d0 - lo);
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+            const uint32_t w0 = __ldg(aw), w1 = __ldg(aw + 1);
+            const uint32_t cq = __funnelshift_r(w0, w1, 8u * static_cast<uint32_t>(addr & 3));
+            CA[t] = prmt(cq, 0u, 0x4140u);
+            CB[t] = prmt(cq, 0u, 0x4342u);
+            const uint32_t bad0 = (d0 < lo || d0 > hi) ? 0x0000ffffu : 0u;
+            const uint32_t bad1 = (d0 + 1 < lo || d0 + 1 > hi) ? 0xffff0000u : 0u;
+            const uint32_t bad2 = (d0 + 2 < lo || d0 + 2 > hi) ? 0x0000ffffu : 0u;
+            const uint32_t bad3 = (d0 + 3 > hi) ? 0xffff0000u : 0u;
+            ivA[t] = bad0 | bad1;
+            ivB[t] = bad2 | bad3;
+        }
+    }
+
+    for (int j = 0; j < ndir; ++j) {
+        const int dj = di[j];
+        const bool has_pred = l > 0 && static_cast<unsigned>(i + dj) < static_cast<unsigned>(len);
+        int sidx = (i + dj * l) % len;
+        if (sidx < 0) sidx += len;
+        uint8_t* sb = mbuf + (static_cast<size_t>(j) * len + sidx) * SB;
+        uint32_t mn = 0xffffffffu;
+#pragma unroll
+        for (int t = 0; t < KQ; ++t) {
+            if (!act[t]) continue;
+            const int d0 = 4 * (q0 + lg + t * G);
+            if (has_pred) {
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(sb + d0);
+                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+                const uint32_t e0 = prmt(w1, 0u, 0x4140u);  // M(d0),   M(d0+1)
+                const uint32_t e1 = prmt(w1, 0u, 0x4342u);  // M(d0+2), M(d0+3)
+                const uint32_t mpa = prmt(w1, 0u, 0x4241u); // M(d0+1), M(d0+2)
+                const uint32_t mma = prmt(w0 >> 24, e0, 0x5410u);  // M(d0-1), M(d0)
+                const uint32_t mpb = prmt(e1, w2 & 0xffu, 0x5432u); // M(d0+3), M(d0+4)
+                LA[t] = __vadd2(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), CA[t]);
+                LB[t] = __vadd2(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), CB[t]);
+            } else {
+                LA[t] = CA[t];  // path starts here (sgm.cpp:93-99)
+                LB[t] = CB[t];
+            }
+            mn = __vminu2(mn, __vminu2(LA[t] | ivA[t], LB[t] | ivB[t]));
+        }
+        const uint32_t m1 = min(mn & 0xffffu, mn >> 16);
+        const uint32_t m = __reduce_min_sync(gmask, m1);
+        const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
+#pragma unroll
+        for (int t = 0; t < KQ; ++t) {
+            if (!act[t]) continue;
+            const int d0 = 4 * (q0 + lg + t * G);
+            const uint32_t ma = __vmaxu2(__viaddmin_u16x2(LA[t], neg, P2x2), ivA[t] & P2x2);
+            const uint32_t mb = __vmaxu2(__viaddmin_u16x2(LB[t], neg, P2x2), ivB[t] & P2x2);
+            *reinterpret_cast<uint32_t*>(sb + 4 + d0) = prmt(ma, mb, 0x6420u);
+            sA[t] = __vadd2(sA[t], LA[t]);
+            sB[t] = __vadd2(sB[t], LB[t]);
+        }
+        // reset levels the slot held but this window does not cover
+        uint32_t* rp = rng + static_cast<size_t>(j) * len + sidx;
+        const uint32_t old = *rp;
+        const int oq0 = static_cast<int>(old & 0xffffu), oq1 = static_cast<int>(old >> 16);
+        for (int q = oq0 + lg; q <= oq1; q += G)
+            if (q < q0 || q > q1) *reinterpret_cast<uint32_t*>(sb + 4 + 4 * q) = P2x4;
+        __syncwarp(gmask);
+        if (lg == 0) *rp = static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16);
+    }
+#pragma unroll
+    for (int t = 0; t < KQ; ++t) {
+        if (!act[t]) continue;
+        const uint32_t qi = qo + lg + t * G;
+        if (out_u16)
+            reinterpret_cast<uint2*>(out)[qi] = make_uint2(sA[t], sB[t]);
+        else
+            reinterpret_cast<uint32_t*>(out)[qi] = prmt(sA[t], sB[t], 0x6420u);
+    }
+}
+
+template <int KQ>
+__global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepParams sp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int cnt[2];
+    __shared__ int item_s;
+    const SweepPlan plan = sweep_plan(b.W, b.H, b.d_max);
+    const int SB = sweep_slot_bytes(b.d_max);
+    const int lmax = b.W > b.H ? b.W : b.H;
+    uint8_t* mbuf = smem;
+    uint32_t* rng = reinterpret_cast<uint32_t*>(smem + plan.buf);
+    uint32_t* m_lohi = reinterpret_cast<uint32_t*>(smem + plan.buf + plan.rng);
+    uint32_t* m_cell = m_lohi + lmax;
+    uint32_t* m_qoff = m_cell + lmax;
+    uint16_t* l_narrow = reinterpret_cast<uint16_t*>(m_qoff + lmax);
+    uint16_t* l_wide = l_narrow + lmax;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
+    const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
+    const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
+    const int n_ab = __popc(sp.roles & 3) * sp.n, n_cd = __popc(sp.roles & 12) * sp.n;
+    const int di_cd[1] = {0};
+
+    if (threadIdx.x == 0) cnt[0] = cnt[1] = 0;
+    for (;;) {
+        if (threadIdx.x == 0) item_s = atomicAdd(b.work, 1);
+        __syncthreads();
+        const int item = item_s;
+        __syncthreads();
+        if (item >= n_ab + n_cd) break;
+        // decode (column roles first: they carry 3 directions)
+        int role, a;
+        if (item < n_ab) {
+            const int per = __popc(sp.roles & 3);
+            a = item / per;
+            const int r = item % per;
+            role = (sp.roles & 1) ? r : 1;
+        } else {
+            const int it = item - n_ab, per = __popc(sp.roles & 12);
+            a = it / per;
+            const int r = it % per;
+            role = (sp.roles & 4) ? 2 + r : 3;
+        }
+        const int s = slot_of(b, a);
+        const bool cols = role < 2;
+        const int sign = (role == 0 || role == 2) ? 1 : -1;
+        const int len = cols ? b.H : b.W, nlines = cols ? b.W : b.H;
+        const int ndir = cols ? sp.ndir_ab : 1;
+        const int* di = cols ? sp.di_ab : di_cd;
+        const uint16_t* lo = b.lo + static_cast<size_t>(s) * b.P;
+        const uint16_t* hi = b.hi + static_cast<size_t>(s) * b.P;
+        const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
+        const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1);
+        const uint8_t* cost = b.cost + static_cast<size_t>(s) * b.vol_cap;
+        void* out;
+        switch (role) {
+            case 0: out = b.pA + static_cast<size_t>(s) * b.quad_cap * 4; break;
+            case 1: out = b.pB + static_cast<size_t>(s) * b.quad_cap * 4; break;
+            case 2: out = b.pC + static_cast<size_t>(s) * b.quad_cap * 4; break;
+            default: out = b.pD + static_cast<size_t>(s) * b.quad_cap * 4; break;
+        }
+        const bool out_u16 = cols;
+
+        // all slots start as "absent" (P2) with an empty quad range
+        {
+            uint32_t* mw = reinterpret_cast<uint32_t*>(mbuf);
+            const size_t words = static_cast<size_t>(ndir) * len * SB / 4;
+            for (size_t w = threadIdx.x; w < words; w += kSweepThreads) mw[w] = P2x4;
+            for (int w = threadIdx.x; w < ndir * len; w += kSweepThreads) rng[w] = 0x0000ffffu;
+        }
+        __syncthreads();
+
+        for (int l = 0; l < nlines; ++l) {
+            const int lc = sign > 0 ? l : nlines - 1 - l;
+            // line metadata + narrow/wide classification (warp-aggregated appends)
+            for (int base = 0; base < len; base += kSweepThreads) {
+                const int i = base + threadIdx.x;
+                bool narrow = false, wide = false;
+                if (i < len) {
+                    const size_t p = cols ? static_cast<size_t>(i) * b.W + lc
+                                          : static_cast<size_t>(lc) * b.W + i;
+                    const int l0 = lo[p], h0 = hi[p];
+                    m_lohi[i] = static_cast<uint32_t>(l0) | (static_cast<uint32_t>(h0) << 16);
+                    m_cell[i] = off[p];
+                    m_qoff[i] = qoff[p];
+                    const int nq = (h0 >> 2) - (l0 >> 2) + 1;
+                    narrow = nq <= 4;
+                    wide = !narrow;
+                }
+                const unsigned bn = __ballot_sync(0xffffffffu, narrow);
+                const unsigned bw = __ballot_sync(0xffffffffu, wide);
+                int basen = 0, basew = 0;
+                if (lane == 0) {
+                    if (bn) basen = atomicAdd(&cnt[0], __popc(bn));
+                    if (bw) basew = atomicAdd(&cnt[1], __popc(bw));
+                }
+                basen = __shfl_sync(0xffffffffu, basen, 0);
+                basew = __shfl_sync(0xffffffffu, basew, 0);
+                const unsigned lt = (1u << lane) - 1u;
+                if (narrow) l_narrow[basen + __popc(bn & lt)] = static_cast<uint16_t>(i);
+                if (wide) l_wide[basew + __popc(bw & lt)] = static_cast<uint16_t>(i);
+            }
+            __syncthreads();
+            const int n_narrow = cnt[0], n_wide = cnt[1];
+            const int u_narrow = (n_narrow + 7) >> 3;
+            for (int u = warp; u < u_narrow + n_wide; u += kSweepWarps) {
+                if (u < u_narrow) {
+                    const int e = u * 8 + (lane >> 2);
+                    if (e < n_narrow)
+                        sweep_pixel<4, 1>(l_narrow[e], l, len, ndir, di, mbuf, SB, rng, m_lohi,
+                                          m_cell, m_qoff, cost, out, out_u16, P1x2, P2x2, P2x4);
+                } else {
+                    sweep_pixel<32, KQ>(l_wide[u - u_narrow], l, len, ndir, di, mbuf, SB, rng,
+                                        m_lohi, m_cell, m_qoff, cost, out, out_u16, P1x2, P2x2,
+                                        P2x4);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) cnt[0] = cnt[1] = 0;
+            __syncthreads();
+        }
+    }
+}
+
+// S = sum of the role partials, written in the reference's ragged layout. One
+// CTA per (row, slot); threads over the row's cells (coalesced S stores).
+__global__ void sweep_combine_kernel(Bufs b, int roles) {
+    extern __shared__ uint32_t sm[];
+    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x, W = b.W;
+    uint32_t* o = sm;              // W+1 in-row cell offsets
+    uint32_t* qo = o + W + 1;      // W quad offsets
+    uint16_t* lo = reinterpret_cast<uint16_t*>(qo + W);
+    const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
+    const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
+    const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
+    const uint32_t row0 = off[0];
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+        o[x] = off[x] - row0;
+        qo[x] = qoff[x];
+        lo[x] = b.lo[pbase + x];
+    }
+    if (threadIdx.x == 0) o[W] = off[W] - row0;
+    __syncthreads();
+    const uint32_t n = o[W];
+    const size_t qb = static_cast<size_t>(s) * b.quad_cap * 4;
+    const uint16_t* pA = b.pA + qb;
+    const uint16_t* pB = b.pB + qb;
+    const uint8_t* pC = b.pC + qb;
+    const uint8_t* pD = b.pD + qb;
+    uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap + row0;
+    for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+        int l = 0, r = W;
+        while (r - l > 1) {
+            const int m = (l + r) >> 1;
+            if (o[m] <= c) l = m; else r = m;
+        }
+        const int lv = lo[l] + static_cast<int>(c - o[l]);
+        const size_t e = 4 * (static_cast<size_t>(qo[l]) + (lv >> 2) - (lo[l] >> 2)) + (lv & 3);
+        uint32_t v = 0;
+        if (roles & 1) v += pA[e];
+        if (roles & 2) v += pB[e];
+        if (roles & 4) v += pC[e];
+        if (roles & 8) v += pD[e];
+        agg[c] = static_cast<uint16_t>(v);
+    }
+}
+
+void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
+                            int num_sms, Launch L) {
+    SweepParams sp{};
+    sp.p1 = p1;
+    sp.p2 = p2;
+    sp.n = n;
+    const bool nondiag = paths == 8 || path_set == 0;
+    const bool diag = paths == 8 || path_set == 1;
+    int k = 0;
+    if (nondiag) sp.di_ab[k++] = 0;
+    if (diag) {
+        sp.di_ab[k++] = -1;
+        sp.di_ab[k++] = 1;
+    }
+    sp.ndir_ab = k;
+    sp.roles = 3 | (nondiag ? 12 : 0);
+    const SweepPlan plan = sweep_plan(b.W, b.H, b.d_max);
+    const int items = (__builtin_popcount(sp.roles & 3) + __builtin_popcount(sp.roles & 12)) * n;
+    const int grid = items < num_sms ? items : num_sms;
+    cudaMemsetAsync(b.work, 0, sizeof(int), L.st);
+    if ((b.d_max + 3) / 4 <= 32) {
+        cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(plan.total));
+        sweep_kernel<1><<<grid, kSweepThreads, plan.total, L.st>>>(b, sp);
+    } else {
+        cudaFuncSetAttribute(sweep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(plan.total));
+        sweep_kernel<2><<<grid, kSweepThreads, plan.total, L.st>>>(b, sp);
+    }
+    const size_t csmem = sizeof(uint32_t) * (2 * b.W + 1) + sizeof(uint16_t) * b.W;
+    sweep_combine_kernel<<<dim3(b.H, n), 512, csmem, L.st>>>(b, sp.roles);
+    *L.counter += 2;
+}
+
+}  // namespace tsgm

@@ -34,14 +34,23 @@ struct Bufs {
     uint16_t *lo, *hi;
     uint32_t* off;       // [slot][P+1]
     uint32_t* row_sum;   // [slot][H]
+    uint32_t* qoff;      // [slot][P+1] quad-aligned offsets (aggregation partials)
+    uint32_t* qrow_sum;  // [slot][H]
     unsigned long long* ncells;  // [slot]
+    unsigned long long* nquads;  // [slot]
     int* overflow;       // [slot] volume >= 2^32
     // census + volumes (A12-A14)
     uint32_t *sigl, *sigr;
     const uint8_t* const* left;   // device [n] image pointers
     const uint8_t* const* right;
-    uint8_t* cost;
+    uint8_t* cost;   // 16 bytes of padding before slot 0 and after the last slot
     uint16_t* agg;
+    // line-sweep aggregation partials in the quad layout (qoff), per role:
+    // A/B (column sweeps, 3 directions) u16, C/D (row sweeps, 1 direction) u8
+    uint16_t *pA, *pB;
+    uint8_t *pC, *pD;
+    size_t quad_cap;  // quads per slot
+    int* work;        // persistent-CTA work counter
     // WTA, render, export (A15, A18, A19)
     int32_t *md, *rd, *ed;
     uint8_t *mv, *rv, *ev;
@@ -119,5 +128,10 @@ void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* 
 void launch_correct(const Bufs& b, int n, double r, double mask_tau, Launch L);
 
 void launch_aggregate(const Bufs& b, int n, int p1, int p2, int paths, int path_set, Launch L);
+// Line-sweep aggregation (aggregate_sweep.cu): returns false when the
+// configuration does not fit its shared-memory plan (caller falls back).
+bool sweep_supported(int W, int H, int d_max, int p2);
+void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
+                            int num_sms, Launch L);
 
 }  // namespace tsgm

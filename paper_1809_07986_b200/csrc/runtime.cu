@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -179,6 +180,8 @@ struct tsgm_ctx {
     int W = 0, H = 0, P = 0, d_max = 0, max_slots = 0;
     size_t vol_cap = 0;
     int device = 0;
+    int num_sms = 148;
+    bool use_sweep = false;  // line-sweep aggregation (else per-direction scanline kernel)
     cudaStream_t st = nullptr;
     Bufs b{};
     unsigned long long launches = 0;
@@ -280,12 +283,30 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.hi = ctx->dalloc<uint16_t>(S * P);
     b.off = ctx->dalloc<uint32_t>(S * (P + 1));
     b.row_sum = ctx->dalloc<uint32_t>(S * ctx->H);
+    b.qoff = ctx->dalloc<uint32_t>(S * (P + 1));
+    b.qrow_sum = ctx->dalloc<uint32_t>(S * ctx->H);
+    b.nquads = ctx->dalloc<unsigned long long>(S);
     b.ncells = ctx->dalloc<unsigned long long>(S);
     b.overflow = ctx->dalloc<int>(S);
     b.sigl = ctx->dalloc<uint32_t>(S * P);
     b.sigr = ctx->dalloc<uint32_t>(S * P);
-    b.cost = ctx->dalloc<uint8_t>(S * ctx->vol_cap);
+    // 16 bytes of padding on both sides: the sweep reads aligned words around
+    // each window
+    b.cost = ctx->dalloc<uint8_t>(S * ctx->vol_cap + 32) + 16;
     b.agg = ctx->dalloc<uint16_t>(S * ctx->vol_cap);
+    const char* force = std::getenv("TSGM_FORCE_SCANLINE_AGG");
+    const bool force_scan = (c.flags & TSGM_FORCE_SCANLINE_AGG) || (force && force[0] == '1');
+    ctx->use_sweep = !force_scan &&
+                     sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2);
+    b.quad_cap = P * static_cast<size_t>((ctx->d_max - 1) / 4 + 1);
+    if (ctx->use_sweep) {
+        b.pA = ctx->dalloc<uint16_t>(S * b.quad_cap * 4);
+        b.pB = ctx->dalloc<uint16_t>(S * b.quad_cap * 4);
+        b.pC = ctx->dalloc<uint8_t>(S * b.quad_cap * 4);
+        b.pD = ctx->dalloc<uint8_t>(S * b.quad_cap * 4);
+    }
+    b.work = ctx->dalloc<int>(1);
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device));
     b.md = ctx->dalloc<int32_t>(S * P);
     b.rd = ctx->dalloc<int32_t>(S * P);
     b.ed = ctx->dalloc<int32_t>(S * P);
@@ -350,6 +371,17 @@ void check_slots(tsgm_ctx* ctx, int n, const int32_t* slots) {
     }
 }
 
+// aggregate_paths for the active slots: the line-sweep kernels when the
+// configuration fits their shared-memory plan, else the scanline kernels.
+void aggregate(tsgm_ctx* ctx, int n, Launch L) {
+    const tsgm_config& c = ctx->cfg;
+    if (ctx->use_sweep && sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2))
+        launch_aggregate_sweep(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
+                               ctx->num_sms, L);
+    else
+        launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+}
+
 // The per-frame pipeline of step() (temporal_filter.cpp:195-232) for n slots.
 void run_step(tsgm_ctx* ctx, int n) {
     const Bufs& b = ctx->b;
@@ -366,7 +398,7 @@ void run_step(tsgm_ctx* ctx, int n) {
     // sgm_match (A12-A15)
     launch_census(b, n, L);
     launch_cost(b, n, L);
-    launch_aggregate(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+    aggregate(ctx, n, L);
     launch_wta(b, n, L);
     // correct + diff + mask + render, then the export median (A16-A19, A21)
     launch_correct(b, n, c.filter.r, c.mask_tau, L);
@@ -596,10 +628,10 @@ int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t
         upload_step(ctx, n, slots, dl.data(), dr.data(), H.data());
         const tsgm_config& c = ctx->cfg;
         Launch L = ctx->L();
-        launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);  // warm
+        (void)c;
+        aggregate(ctx, n, L);  // warm
         CK(cudaEventRecord(ctx->ev0, ctx->st));
-        for (int r = 0; r < reps; ++r)
-            launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+        for (int r = 0; r < reps; ++r) aggregate(ctx, n, L);
         CK(cudaEventRecord(ctx->ev1, ctx->st));
         CK(cudaEventSynchronize(ctx->ev1));
         float ms = 0.f;
@@ -665,7 +697,8 @@ int tsgm_aggregate_paths(const uint8_t* cost, const uint16_t* lo, const uint16_t
         h2d(c, c->b.cost, cost, total);
         launch_ranges_given(c->b, 1, c->L());
         launch_offsets(c->b, 1, c->L());
-        launch_aggregate(c->b, 1, params->p1, params->p2, params->paths, params->path_set, c->L());
+        c->cfg.sgm = *params;
+        aggregate(c, 1, c->L());
         d2h(c, agg, c->b.agg, total);
         sync(c);
     });
@@ -725,7 +758,8 @@ int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t
         launch_offsets(c->b, 1, c->L());
         launch_census(c->b, 1, c->L());
         launch_cost(c->b, 1, c->L());
-        launch_aggregate(c->b, 1, params->p1, params->p2, params->paths, params->path_set, c->L());
+        c->cfg.sgm = *params;
+        aggregate(c, 1, c->L());
         launch_wta(c->b, 1, c->L());
         d2h(c, d, c->b.md, P);
         d2h(c, valid, c->b.mv, P);

@@ -103,6 +103,12 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& e
     return total;
 }
 
+// Quads of a window: aligned groups of 4 levels covering [lo, hi]; the
+// aggregation partials use a quad-aligned copy of the ragged layout.
+__device__ __forceinline__ uint32_t quads_of(int lo, int hi) {
+    return static_cast<uint32_t>((hi >> 2) - (lo >> 2) + 1);
+}
+
 template <bool kDerive>
 __global__ void ranges_kernel(Bufs b, int min_hw, int use_stddev, double gain) {
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
@@ -110,7 +116,7 @@ __global__ void ranges_kernel(Bufs b, int min_hw, int use_stddev, double gain) {
     const int per = (b.W + kRowThreads - 1) / kRowThreads;
     const int x0 = threadIdx.x * per;
     const int top = b.d_max - 1, min_len = 2 * min_hw + 1;
-    uint32_t sum = 0;
+    uint32_t sum = 0, qsum = 0;
     for (int k = 0; k < per; ++k) {
         const int x = x0 + k;
         if (x >= b.W) break;
@@ -127,18 +133,28 @@ __global__ void ranges_kernel(Bufs b, int min_hw, int use_stddev, double gain) {
             hi = b.hi[base + x];
         }
         sum += static_cast<uint32_t>(hi - lo + 1);
+        qsum += quads_of(lo, hi);
     }
-    uint32_t excl;
+    uint32_t excl, qexcl;
     const uint32_t total = block_exclusive_scan(sum, excl);
-    uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * b.W;
-    uint32_t run = excl;
+    const uint32_t qtotal = block_exclusive_scan(qsum, qexcl);
+    const size_t orow = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * b.W;
+    uint32_t* off = b.off + orow;
+    uint32_t* qoff = b.qoff + orow;
+    uint32_t run = excl, qrun = qexcl;
     for (int k = 0; k < per; ++k) {
         const int x = x0 + k;
         if (x >= b.W) break;
         off[x] = run;  // in-row exclusive; rebased by offsets_finalize
-        run += static_cast<uint32_t>(b.hi[base + x] - b.lo[base + x] + 1);
+        qoff[x] = qrun;
+        const int lo = b.lo[base + x], hi = b.hi[base + x];
+        run += static_cast<uint32_t>(hi - lo + 1);
+        qrun += quads_of(lo, hi);
     }
-    if (threadIdx.x == 0) b.row_sum[static_cast<size_t>(s) * b.H + y] = total;
+    if (threadIdx.x == 0) {
+        b.row_sum[static_cast<size_t>(s) * b.H + y] = total;
+        b.qrow_sum[static_cast<size_t>(s) * b.H + y] = qtotal;
+    }
 }
 
 void launch_ranges_from_pred(const Bufs& b, int n, int min_hw, int use_stddev, double gain,
@@ -152,14 +168,15 @@ void launch_ranges_given(const Bufs& b, int n, Launch L) {
 }
 
 // Per slot: exclusive scan of the row totals in u64 (overflow -> flag, the
-// reference throws at matching_cost.cpp:43-44), then rebase every offset.
+// reference throws at matching_cost.cpp:43-44), for the cell offsets (y = 0)
+// and the quad offsets (y = 1); then rebase every offset.
 __global__ void row_scan_kernel(Bufs b) {
-    const int a = blockIdx.x, s = slot_of(b, a);
+    const int a = blockIdx.x, s = slot_of(b, a), which = blockIdx.y;
     __shared__ unsigned long long carry;
     __shared__ unsigned long long part[1024];
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    uint32_t* rs = b.row_sum + static_cast<size_t>(s) * b.H;
+    uint32_t* rs = (which ? b.qrow_sum : b.row_sum) + static_cast<size_t>(s) * b.H;
     for (int base = 0; base < b.H; base += 1024) {
         const int y = base + threadIdx.x;
         const unsigned long long v = y < b.H ? rs[y] : 0ull;
@@ -181,21 +198,31 @@ __global__ void row_scan_kernel(Bufs b) {
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        b.ncells[s] = carry;
-        b.overflow[s] = carry > 0xffffffffull ? 1 : 0;
-        b.off[static_cast<size_t>(s) * (b.P + 1) + b.P] = static_cast<uint32_t>(carry);
+        const size_t last = static_cast<size_t>(s) * (b.P + 1) + b.P;
+        if (which == 0) {
+            b.ncells[s] = carry;
+            b.overflow[s] = carry > 0xffffffffull ? 1 : 0;
+            b.off[last] = static_cast<uint32_t>(carry);
+        } else {
+            b.nquads[s] = carry;
+            b.qoff[last] = static_cast<uint32_t>(carry);
+        }
     }
 }
 
 __global__ void offsets_finalize_kernel(Bufs b) {
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const uint32_t rb = b.row_sum[static_cast<size_t>(s) * b.H + y];
-    uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * b.W;
-    for (int x = threadIdx.x; x < b.W; x += blockDim.x) off[x] += rb;
+    const uint32_t qb = b.qrow_sum[static_cast<size_t>(s) * b.H + y];
+    const size_t orow = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * b.W;
+    for (int x = threadIdx.x; x < b.W; x += blockDim.x) {
+        b.off[orow + x] += rb;
+        b.qoff[orow + x] += qb;
+    }
 }
 
 void launch_offsets(const Bufs& b, int n, Launch L) {
-    row_scan_kernel<<<n, 1024, 0, L.st>>>(b);
+    row_scan_kernel<<<dim3(n, 2), 1024, 0, L.st>>>(b);
     offsets_finalize_kernel<<<dim3(b.H, n), kRowThreads, 0, L.st>>>(b);
     *L.counter += 2;
 }

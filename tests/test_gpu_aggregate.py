@@ -1,0 +1,82 @@
+"""aggregate_paths on the GPU vs the oracle on adversarial ragged volumes:
+random narrow/wide/full windows, large window shifts between neighbours,
+odd sizes, d_max not a multiple of 4, every path set, random P1/P2 — for both
+aggregation kernels (line sweep and per-direction scanline). Bit-exact."""
+import numpy as np
+import pytest
+
+from paper_1809_07986_b200 import tsgm
+
+pytestmark = pytest.mark.gpu
+
+
+def ragged_ranges(rng, w, h, d_max, p_full=0.2, p_wide=0.05):
+    lo = np.zeros((h, w), np.int64)
+    hi = np.zeros((h, w), np.int64)
+    kind = rng.random((h, w))
+    centre = rng.integers(0, d_max, (h, w))
+    # smooth-ish centres along rows for realistic small shifts
+    centre = np.clip(np.cumsum(rng.integers(-1, 2, (h, w)), axis=1) + centre[:, :1], 0,
+                     d_max - 1)
+    half = rng.integers(0, 6, (h, w))
+    lo[:] = np.clip(centre - half, 0, d_max - 1)
+    hi[:] = np.clip(centre + half, 0, d_max - 1)
+    full = kind < p_full
+    lo[full], hi[full] = 0, d_max - 1
+    wide = (kind >= p_full) & (kind < p_full + p_wide)
+    a = rng.integers(0, d_max, (h, w))
+    b = rng.integers(0, d_max, (h, w))
+    lo[wide], hi[wide] = np.minimum(a, b)[wide], np.maximum(a, b)[wide]
+    return lo.astype(np.uint16), hi.astype(np.uint16)
+
+
+CASES = [
+    # w, h, d_max, p_full
+    (37, 23, 16, 0.2),
+    (64, 40, 5, 0.5),
+    (61, 29, 130, 0.3),
+    (200, 75, 128, 0.21),
+    (96, 33, 256, 0.1),
+    (33, 64, 64, 0.9),
+]
+
+
+@pytest.mark.parametrize("kernel", ["sweep", "scanline"])
+@pytest.mark.parametrize("w,h,d_max,p_full", CASES)
+def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
+    if kernel == "scanline":
+        monkeypatch.setenv("TSGM_FORCE_SCANLINE_AGG", "1")
+    rng = np.random.default_rng(w * 1000 + h * 7 + d_max)
+    lo, hi = ragged_ranges(rng, w, h, d_max, p_full)
+    n = int((hi.astype(np.int64) - lo + 1).sum())
+    cost = rng.integers(0, 25, n).astype(np.uint8)
+    for paths, path_set in ((8, 0), (4, 0), (4, 1)):
+        p1 = int(rng.integers(1, 12))
+        p2 = p1 + int(rng.integers(0, 120))
+        params = tsgm.SgmParams(p1, p2, paths, path_set, d_max)
+        got = tsgm.aggregate_paths(cost, lo, hi, params)
+        want = port.aggregate(cost, lo, hi, params)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_full_size_realistic(port):
+    """1242x375, D=128: 21% full-range windows, narrow ones 7-11 levels."""
+    rng = np.random.default_rng(7)
+    w, h, d = 1242, 375, 128
+    lo, hi = ragged_ranges(rng, w, h, d, p_full=0.21, p_wide=0.0)
+    n = int((hi.astype(np.int64) - lo + 1).sum())
+    cost = rng.integers(0, 25, n).astype(np.uint8)
+    params = tsgm.SgmParams(10, 120, 8, 0, d)
+    np.testing.assert_array_equal(tsgm.aggregate_paths(cost, lo, hi, params),
+                                  port.aggregate(cost, lo, hi, params))
+
+
+def test_large_p2_falls_back_to_scanline(port):
+    """P2 + 24 > 255 does not fit the u8 line state: the scanline kernel runs."""
+    rng = np.random.default_rng(3)
+    lo, hi = ragged_ranges(rng, 40, 20, 32)
+    n = int((hi.astype(np.int64) - lo + 1).sum())
+    cost = rng.integers(0, 25, n).astype(np.uint8)
+    params = tsgm.SgmParams(10, 400, 8, 0, 32)
+    np.testing.assert_array_equal(tsgm.aggregate_paths(cost, lo, hi, params),
+                                  port.aggregate(cost, lo, hi, params))
