@@ -1,0 +1,252 @@
+// tsgm::gpu — header-only C++ facade with the reference's own signatures and
+// types, running on the B200 through the C-ABI in tsgm_b200.h.
+//
+// Drop-in use: a caller of the reference library (/root/reference/proj)
+// includes this header next to "tsgm/temporal_filter.hpp" and replaces
+//     tsgm::step(state, left, right, motion, calib, params, cfg, threads)
+// with
+//     tsgm::gpu::step(state, left, right, motion, calib, params, cfg, threads)
+// (temporal_filter.hpp:74-76). Results are bit-identical (DESIGN.md,
+// "Parity"). Errors are rethrown as the reference's exception types:
+// status 1 -> std::invalid_argument, 2 -> std::runtime_error. `threads` is
+// accepted and ignored (the GPU grid replaces parallel_rows).
+//
+// For many sequences use tsgm::gpu::Engine: device-resident state per slot,
+// one batched launch sequence per frame.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tsgm/geometry.hpp"
+#include "tsgm/matching_cost.hpp"
+#include "tsgm/sgm.hpp"
+#include "tsgm/temporal_filter.hpp"
+#include "tsgm_b200.h"
+
+namespace tsgm {
+namespace gpu {
+
+namespace detail {
+
+inline void check(int rc) {
+    if (rc == TSGM_OK) return;
+    const std::string msg = tsgm_last_error();
+    if (rc == TSGM_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+inline tsgm_sgm_params to_c(const SgmParams& p) {
+    return tsgm_sgm_params{p.p1, p.p2, p.paths, p.path_set == PathSet::diagonal ? 1 : 0,
+                           p.d_max};
+}
+inline tsgm_filter_config to_c(const FilterConfig& f) {
+    return tsgm_filter_config{f.noise.q, f.noise.r, f.p_init, f.disc_thresh,
+                              f.min_range_halfwidth, f.range_use_stddev ? 1 : 0,
+                              f.range_stddev_gain};
+}
+inline tsgm_stereo_calib to_c(const StereoCalib& c) {
+    return tsgm_stereo_calib{c.focal_px, c.cx, c.cy, c.baseline_m, c.width, c.height, c.d_max};
+}
+inline void motion12(const RigidMotion& m, double* r9, double* t3) {
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) r9[i * 3 + j] = m.rotation(i, j);
+        t3[i] = m.translation(i);
+    }
+}
+
+}  // namespace detail
+
+// step (temporal_filter.hpp:74-76, temporal_filter.cpp:195-232)
+inline StepResult step(const DisparityState& state, const GrayImage& left,
+                       const GrayImage& right, const RigidMotion& motion,
+                       const StereoCalib& calib, const SgmParams& params,
+                       const FilterConfig& cfg, int threads = 1) {
+    (void)threads;
+    if (!left.same_size(right)) throw std::invalid_argument("step: left/right dimension mismatch");
+    const int w = left.width(), h = left.height();
+    double r9[9], t3[3];
+    detail::motion12(motion, r9, t3);
+    const tsgm_stereo_calib c = detail::to_c(calib);
+    const tsgm_sgm_params p = detail::to_c(params);
+    const tsgm_filter_config f = detail::to_c(cfg);
+    StepResult res;
+    res.state = DisparityState(w, h);
+    res.export_map = DisparityMap(w, h);
+    res.diff = Image<double>(w, h, 0.0);
+    detail::check(tsgm_step_once(state.d.data(), state.p.data(), state.valid.data(),
+                                 state.width(), state.height(), left.data(), right.data(), w, h,
+                                 r9, t3, &c, &p, &f, res.state.d.data(), res.state.p.data(),
+                                 res.state.valid.data(), res.export_map.d.data(),
+                                 res.export_map.valid.data(), res.diff.data()));
+    return res;
+}
+
+// census_transform (matching_cost.hpp:80)
+inline CensusMap census_transform(const GrayImage& img, int threads = 1) {
+    (void)threads;
+    CensusMap m{Image<std::uint32_t>(img.width(), img.height())};
+    detail::check(tsgm_census_transform(img.data(), img.width(), img.height(), m.sig.data()));
+    return m;
+}
+
+// sgm_match (sgm.hpp:67-69); stage timings are not reported
+inline DisparityMap sgm_match(const GrayImage& left, const GrayImage& right,
+                              const SearchRangeMap& ranges, const SgmParams& params,
+                              int threads = 1, SgmStageTimings* timings = nullptr) {
+    (void)threads;
+    (void)timings;
+    if (!left.same_size(right)) throw std::invalid_argument("sgm_match: image size mismatch");
+    if (!left.same_size(ranges.lo)) throw std::invalid_argument("sgm_match: range map size mismatch");
+    DisparityMap dm(left.width(), left.height());
+    const tsgm_sgm_params p = detail::to_c(params);
+    detail::check(tsgm_sgm_match(left.data(), right.data(), left.width(), left.height(),
+                                 ranges.lo.data(), ranges.hi.data(), &p, dm.d.data(),
+                                 dm.valid.data()));
+    return dm;
+}
+
+// aggregate_paths (sgm.hpp:47) over a reference MatchingCostVolume
+inline AggregatedCostVolume aggregate_paths(const MatchingCostVolume& vol, const SgmParams& params) {
+    AggregatedCostVolume agg;
+    agg.ranges = vol.ranges;
+    agg.offsets = vol.offsets;
+    agg.cost.assign(vol.cost.size(), 0);
+    const tsgm_sgm_params p = detail::to_c(params);
+    detail::check(tsgm_aggregate_paths(vol.cost.data(), vol.ranges.lo.data(),
+                                       vol.ranges.hi.data(), vol.width(), vol.height(), &p,
+                                       agg.cost.data()));
+    return agg;
+}
+
+// winner_takes_all (sgm.hpp:52)
+inline DisparityMap winner_takes_all(const AggregatedCostVolume& agg, int threads = 1) {
+    (void)threads;
+    DisparityMap dm(agg.width(), agg.height());
+    detail::check(tsgm_winner_takes_all(agg.cost.data(), agg.ranges.lo.data(),
+                                        agg.ranges.hi.data(), agg.width(), agg.height(),
+                                        dm.d.data(), dm.valid.data()));
+    return dm;
+}
+
+// median_refine (sgm.hpp:57)
+inline DisparityMap median_refine(const DisparityMap& dm, int threads = 1) {
+    (void)threads;
+    DisparityMap out(dm.width(), dm.height());
+    detail::check(tsgm_median_refine(dm.d.data(), dm.valid.data(), dm.width(), dm.height(),
+                                     out.d.data(), out.valid.data()));
+    return out;
+}
+
+// predict (temporal_filter.hpp:32-33)
+inline DisparityState predict(const DisparityState& state, const RigidMotion& motion,
+                              const StereoCalib& calib, const FilterConfig& cfg) {
+    double r9[9], t3[3];
+    detail::motion12(motion, r9, t3);
+    const tsgm_stereo_calib c = detail::to_c(calib);
+    const tsgm_filter_config f = detail::to_c(cfg);
+    DisparityState out(state.width(), state.height());
+    detail::check(tsgm_predict(state.d.data(), state.p.data(), state.valid.data(), state.width(),
+                               state.height(), r9, t3, &c, &f, out.d.data(), out.p.data(),
+                               out.valid.data()));
+    return out;
+}
+
+// derive_search_ranges (temporal_filter.hpp:48-49)
+inline SearchRangeMap derive_search_ranges(const DisparityState& state, const StereoCalib& calib,
+                                           const FilterConfig& cfg) {
+    const tsgm_stereo_calib c = detail::to_c(calib);
+    const tsgm_filter_config f = detail::to_c(cfg);
+    SearchRangeMap r(state.width(), state.height(), 0, 0);
+    detail::check(tsgm_derive_search_ranges(state.d.data(), state.p.data(), state.valid.data(),
+                                            state.width(), state.height(), &c, &f, r.lo.data(),
+                                            r.hi.data()));
+    return r;
+}
+
+// correct (temporal_filter.hpp:54-55)
+inline DisparityState correct(const DisparityState& pred, const DisparityMap& meas,
+                              const FilterConfig& cfg) {
+    if (!pred.valid.same_size(meas.valid)) throw std::invalid_argument("correct: dimension mismatch");
+    const tsgm_filter_config f = detail::to_c(cfg);
+    DisparityState out(pred.width(), pred.height());
+    detail::check(tsgm_correct(pred.d.data(), pred.p.data(), pred.valid.data(), meas.d.data(),
+                               meas.valid.data(), pred.width(), pred.height(), &f, out.d.data(),
+                               out.p.data(), out.valid.data()));
+    return out;
+}
+
+// Batched, device-resident production path.
+class Engine {
+public:
+    Engine(const StereoCalib& calib, const SgmParams& params, const FilterConfig& cfg,
+           int max_slots, int device = 0, double mask_tau = 3.0, unsigned flags = 0) {
+        tsgm_config c{};
+        c.width = calib.width;
+        c.height = calib.height;
+        c.max_slots = max_slots;
+        c.device = device;
+        c.calib = detail::to_c(calib);
+        c.sgm = detail::to_c(params);
+        c.filter = detail::to_c(cfg);
+        c.mask_tau = mask_tau;
+        c.flags = flags;
+        detail::check(tsgm_create(&c, &ctx_));
+        w_ = calib.width;
+        h_ = calib.height;
+    }
+    ~Engine() { tsgm_destroy(ctx_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void reset(int slot) { detail::check(tsgm_reset(ctx_, slot)); }
+
+    // One frame for slots[i] with images lefts[i]/rights[i] and motions[i].
+    void step(const std::vector<int>& slots, const std::vector<const GrayImage*>& lefts,
+              const std::vector<const GrayImage*>& rights,
+              const std::vector<RigidMotion>& motions) {
+        const int n = static_cast<int>(slots.size());
+        std::vector<const std::uint8_t*> l(n), r(n);
+        std::vector<double> m(12 * static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            l[i] = lefts[i]->data();
+            r[i] = rights[i]->data();
+            detail::motion12(motions[i], &m[12 * i], &m[12 * i + 9]);
+        }
+        detail::check(tsgm_step(ctx_, n, slots.data(), l.data(), r.data(), m.data()));
+    }
+
+    // StepResult of a slot's last frame (state, export map, diff).
+    StepResult result(int slot) const {
+        StepResult res;
+        res.state = DisparityState(w_, h_);
+        res.export_map = DisparityMap(w_, h_);
+        res.diff = Image<double>(w_, h_, 0.0);
+        fetch(slot, TSGM_OUT_STATE_D, res.state.d.data(), 8);
+        fetch(slot, TSGM_OUT_STATE_P, res.state.p.data(), 8);
+        fetch(slot, TSGM_OUT_STATE_VALID, res.state.valid.data(), 1);
+        fetch(slot, TSGM_OUT_EXPORT_D, res.export_map.d.data(), 4);
+        fetch(slot, TSGM_OUT_EXPORT_VALID, res.export_map.valid.data(), 1);
+        fetch(slot, TSGM_OUT_DIFF, res.diff.data(), 8);
+        return res;
+    }
+
+    // A21 moving-object mask of a slot's last frame.
+    Image<std::uint8_t> mask(int slot) const {
+        Image<std::uint8_t> m(w_, h_);
+        fetch(slot, TSGM_OUT_MASK, m.data(), 1);
+        return m;
+    }
+
+private:
+    void fetch(int slot, int what, void* dst, size_t elem) const {
+        detail::check(tsgm_fetch(ctx_, slot, what, dst, elem * static_cast<size_t>(w_) * h_));
+    }
+    tsgm_ctx* ctx_ = nullptr;
+    int w_ = 0, h_ = 0;
+};
+
+}  // namespace gpu
+}  // namespace tsgm

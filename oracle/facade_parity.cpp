@@ -1,0 +1,142 @@
+// TEST INFRASTRUCTURE ONLY. Drop-in check of the C++ facade: the same frames
+// go through the reference's tsgm::step (compiled in place from
+// /root/reference/proj/src) and through tsgm::gpu::step (include/tsgm_gpu.hpp
+// over libtsgm_b200.so). Every StepResult field must be identical, and the
+// facade must throw the reference's exception types. Built by
+// `make -C oracle facade` into oracle/_ref/facade_parity; run on the GPU box by
+// tests/test_gpu_facade.py. Exit 0 = parity.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+
+#include "tsgm/temporal_filter.hpp"
+#include "tsgm_gpu.hpp"
+#include "tsgm_scene.h"
+
+using namespace tsgm;
+
+static int fails = 0;
+#define EXPECT(c, msg)                                   \
+    do {                                                 \
+        if (!(c)) {                                      \
+            std::fprintf(stderr, "FAIL: %s\n", msg);     \
+            ++fails;                                     \
+        }                                                \
+    } while (0)
+
+static RigidMotion yaw(double a) {
+    RigidMotion m;
+    m.rotation(0, 0) = std::cos(a);
+    m.rotation(0, 2) = std::sin(a);
+    m.rotation(2, 0) = -std::sin(a);
+    m.rotation(2, 2) = std::cos(a);
+    m.translation(2) = -0.3;
+    return m;
+}
+
+int main() {
+    tsgm_scene_cfg sc;
+    tsgm_scene_default(&sc, 1);
+    sc.width = 320;
+    sc.height = 120;
+    sc.focal = 200.0;
+    sc.cx = 159.5;
+    sc.cy = 59.5;
+    sc.d_max = 64;
+    sc.frames = 6;
+    sc.seed = 11;
+    const int w = sc.width, h = sc.height, F = sc.frames;
+    std::vector<uint8_t> L(static_cast<size_t>(w) * h * F), R(L.size());
+    std::vector<double> poses(12 * F);
+    if (tsgm_scene_render(&sc, 0, F, L.data(), R.data(), nullptr, poses.data(), 4) != 0) return 2;
+
+    StereoCalib calib;
+    calib.focal_px = sc.focal;
+    calib.cx = sc.cx;
+    calib.cy = sc.cy;
+    calib.baseline_m = sc.baseline;
+    calib.width = w;
+    calib.height = h;
+    calib.d_max = sc.d_max;
+    SgmParams params;
+    params.p1 = 10;
+    params.p2 = 120;
+    params.d_max = sc.d_max;
+    FilterConfig cfg;
+    cfg.range_use_stddev = true;
+    cfg.range_stddev_gain = 3.0;
+
+    DisparityState s_ref, s_gpu;
+    for (int k = 0; k < F; ++k) {
+        GrayImage left(w, h), right(w, h);
+        std::copy(L.begin() + static_cast<long>(k) * w * h, L.begin() + static_cast<long>(k + 1) * w * h, left.data());
+        std::copy(R.begin() + static_cast<long>(k) * w * h, R.begin() + static_cast<long>(k + 1) * w * h, right.data());
+        RigidMotion m;
+        if (k > 0) {
+            Pose a, b;
+            for (int i = 0; i < 12; ++i) {
+                a(i / 4, i % 4) = poses[12 * (k - 1) + i];
+                b(i / 4, i % 4) = poses[12 * k + i];
+            }
+            m = relative_motion(a, b);
+        }
+        const StepResult ref = tsgm::step(s_ref, left, right, m, calib, params, cfg);
+        const StepResult gpu = tsgm::gpu::step(s_gpu, left, right, m, calib, params, cfg);
+        EXPECT(ref.state.valid == gpu.state.valid, "state.valid");
+        EXPECT(ref.state.d == gpu.state.d, "state.d");
+        EXPECT(ref.state.p == gpu.state.p, "state.p");
+        EXPECT(ref.export_map == gpu.export_map, "export_map");
+        EXPECT(ref.diff == gpu.diff, "diff");
+        s_ref = ref.state;
+        s_gpu = gpu.state;
+        // sub-stage facades on the same frame
+        const DisparityState pr = tsgm::predict(s_ref, yaw(0.01), calib, cfg);
+        const DisparityState pg = tsgm::gpu::predict(s_gpu, yaw(0.01), calib, cfg);
+        EXPECT(pr.d == pg.d && pr.p == pg.p && pr.valid == pg.valid, "predict");
+        const SearchRangeMap rr = derive_search_ranges(pr, calib, cfg);
+        const SearchRangeMap rg = tsgm::gpu::derive_search_ranges(pg, calib, cfg);
+        EXPECT(rr.lo == rg.lo && rr.hi == rg.hi, "derive_search_ranges");
+        const DisparityMap mr = sgm_match(left, right, rr, params);
+        const DisparityMap mg = tsgm::gpu::sgm_match(left, right, rg, params);
+        EXPECT(mr == mg, "sgm_match");
+        EXPECT(median_refine(mr) == tsgm::gpu::median_refine(mg), "median_refine");
+        const DisparityState cr = correct(pr, mr, cfg);
+        const DisparityState cg = tsgm::gpu::correct(pg, mg, cfg);
+        EXPECT(cr.d == cg.d && cr.p == cg.p && cr.valid == cg.valid, "correct");
+        EXPECT(census_transform(left).sig == tsgm::gpu::census_transform(left).sig, "census");
+    }
+    // error behaviour (temporal_filter.cpp:198-206)
+    try {
+        SgmParams bad = params;
+        bad.d_max = 32;
+        tsgm::gpu::step(DisparityState(), GrayImage(w, h), GrayImage(w, h), RigidMotion{}, calib,
+                        bad, cfg);
+        EXPECT(false, "d_max mismatch did not throw");
+    } catch (const std::invalid_argument&) {
+    }
+    try {
+        tsgm::gpu::step(DisparityState(), GrayImage(w, h), GrayImage(w - 1, h), RigidMotion{},
+                        calib, params, cfg);
+        EXPECT(false, "size mismatch did not throw");
+    } catch (const std::invalid_argument&) {
+    }
+    // batched engine == per-call facade
+    {
+        tsgm::gpu::Engine eng(calib, params, cfg, 2);
+        DisparityState s;
+        for (int k = 0; k < 3; ++k) {
+            GrayImage left(w, h), right(w, h);
+            std::copy(L.begin() + static_cast<long>(k) * w * h, L.begin() + static_cast<long>(k + 1) * w * h, left.data());
+            std::copy(R.begin() + static_cast<long>(k) * w * h, R.begin() + static_cast<long>(k + 1) * w * h, right.data());
+            const StepResult one = tsgm::gpu::step(s, left, right, RigidMotion{}, calib, params, cfg);
+            eng.step({1}, {&left}, {&right}, {RigidMotion{}});
+            const StepResult batched = eng.result(1);
+            EXPECT(one.state.d == batched.state.d && one.export_map == batched.export_map,
+                   "Engine vs step");
+            s = one.state;
+        }
+    }
+    std::printf("facade parity: %s (%d failures)\n", fails ? "FAIL" : "ok", fails);
+    return fails ? 1 : 0;
+}

@@ -43,6 +43,8 @@ struct SweepPlan {
     size_t buf, rng, meta, lists, total;
 };
 
+constexpr int kMetaPerThread = 4;  // line length <= kSweepThreads * 4 = 2048
+
 __host__ __device__ inline SweepPlan sweep_plan(int W, int H, int d_max) {
     SweepPlan p;
     const size_t sb = sweep_slot_bytes(d_max);
@@ -50,7 +52,7 @@ __host__ __device__ inline SweepPlan sweep_plan(int W, int H, int d_max) {
     const size_t lmax = W > H ? W : H;
     p.buf = slots * sb;
     p.rng = slots * 4;
-    p.meta = 3 * lmax * 4;
+    p.meta = 2 * 3 * lmax * 4;  // two lines in flight: lohi, cell, qoff
     p.lists = ((2 * lmax * 2) + 15) & ~static_cast<size_t>(15);
     p.total = p.buf + p.rng + p.meta + p.lists;
     return p;
@@ -58,7 +60,8 @@ __host__ __device__ inline SweepPlan sweep_plan(int W, int H, int d_max) {
 
 bool sweep_supported(int W, int H, int d_max, int p2) {
     // u8 path costs need 24 + P2 <= 255; quads per lane <= 2 (d_max <= 256)
-    return kMaxCost + p2 <= 255 && d_max <= 256 && W < 65536 && H < 65536 &&
+    const int lmax = W > H ? W : H;
+    return kMaxCost + p2 <= 255 && d_max <= 256 && lmax <= kSweepThreads * kMetaPerThread &&
            sweep_plan(W, H, d_max).total <= 227 * 1024;
 }
 
@@ -74,22 +77,56 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     return __byte_perm(a, b, s);
 }
 
+// Line metadata of one line (three u32 arrays in shared memory).
+struct LineMeta {
+    uint32_t* lohi;
+    uint32_t* cell;
+    uint32_t* qoff;
+};
+
+// Matching costs of one pixel's quads for one lane, fetched ahead of use.
+template <int KQ>
+struct CostRegs {
+    uint32_t w0[KQ], w1[KQ], sh[KQ];
+};
+
+template <int G, int KQ>
+__device__ __forceinline__ void fetch_costs(int i, const LineMeta& m, const uint8_t* cost,
+                                            CostRegs<KQ>& r) {
+    const int lg = threadIdx.x & (G - 1);
+    const uint32_t lohi = m.lohi[i];
+    const int lo = static_cast<int>(lohi & 0xffffu), hi = static_cast<int>(lohi >> 16);
+    const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
+    const uint32_t cell = m.cell[i];
+#pragma unroll
+    for (int t = 0; t < KQ; ++t) {
+        const int k = lg + t * G;
+        r.w0[t] = r.w1[t] = r.sh[t] = 0u;
+        if (k < nq) {
+            const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + cell + (4 * (q0 + k) - lo);
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+            r.w0[t] = __ldg(aw);
+            r.w1[t] = __ldg(aw + 1);
+            r.sh[t] = 8u * static_cast<uint32_t>(addr & 3);
+        }
+    }
+}
+
 // One pixel of a line, processed by a group of G lanes (G = 4 or 32), each
 // lane holding up to KQ quads.
 template <int G, int KQ>
-__device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, const int* di,
+__device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, int di0, int di1, int di2,
                                             uint8_t* mbuf, int SB, uint32_t* rng,
-                                            const uint32_t* m_lohi, const uint32_t* m_cell,
-                                            const uint32_t* m_qoff, const uint8_t* cost,
+                                            const LineMeta& meta, const CostRegs<KQ>& cr,
                                             void* out, bool out_u16, uint32_t P1x2, uint32_t P2x2,
                                             uint32_t P2x4) {
     const int lane = threadIdx.x & 31;
     const int lg = lane & (G - 1);
     const unsigned gmask = G == 32 ? 0xffffffffu : (0xfu << (lane & ~3));
-    const uint32_t lohi = m_lohi[i];
+    const uint32_t lohi = meta.lohi[i];
     const int lo = static_cast<int>(lohi & 0xffffu), hi = static_cast<int>(lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
-    const uint32_t cell = m_cell[i], qo = m_qoff[i];
+    const uint32_t qo = meta.qoff[i];
 
     bool act[KQ];
     uint32_t CA[KQ], CB[KQ], ivA[KQ], ivB[KQ], sA[KQ], sB[KQ], LA[KQ], LB[KQ];
@@ -101,12 +138,7 @@ __device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, con
         CA[t] = CB[t] = ivA[t] = ivB[t] = 0u;
         if (act[t]) {
             const int d0 = 4 * (q0 + k);
-            // 4 matching costs for levels d0..d0+3 (bytes outside the window are
-            // read but masked): unaligned 32-bit window via a funnel shift
-            const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + cell + (d0 - lo);
-            const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-            const uint32_t w0 = __ldg(aw), w1 = __ldg(aw + 1);
-            const uint32_t cq = __funnelshift_r(w0, w1, 8u * static_cast<uint32_t>(addr & 3));
+            const uint32_t cq = __funnelshift_r(cr.w0[t], cr.w1[t], cr.sh[t]);
             CA[t] = prmt(cq, 0u, 0x4140u);
             CB[t] = prmt(cq, 0u, 0x4342u);
             const uint32_t bad0 = (d0 < lo || d0 > hi) ? 0x0000ffffu : 0u;
@@ -119,7 +151,7 @@ __device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, con
     }
 
     for (int j = 0; j < ndir; ++j) {
-        const int dj = di[j];
+        const int dj = j == 0 ? di0 : (j == 1 ? di1 : di2);
         const bool has_pred = l > 0 && static_cast<unsigned>(i + dj) < static_cast<unsigned>(len);
         int sidx = (i + dj * l) % len;
         if (sidx < 0) sidx += len;
@@ -178,29 +210,88 @@ __device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, con
     }
 }
 
+// Per-slot views of one role's line geometry and metadata sources.
+struct RoleView {
+    bool cols;
+    int len, nlines, sign;
+    const uint16_t *lo, *hi;
+    const uint32_t *off, *qoff;
+    const uint32_t *t_lohi, *t_cell, *t_qoff;  // column-major copies (cols)
+    int W;
+    __device__ __forceinline__ int line_coord(int l) const { return sign > 0 ? l : nlines - 1 - l; }
+    // metadata of pixel i of line l (processing order)
+    __device__ __forceinline__ void load(int l, int i, uint32_t& lohi, uint32_t& cell,
+                                         uint32_t& qo) const {
+        const int lc = line_coord(l);
+        if (cols) {
+            const size_t p = static_cast<size_t>(lc) * len + i;
+            lohi = t_lohi[p];
+            cell = t_cell[p];
+            qo = t_qoff[p];
+        } else {
+            const size_t p = static_cast<size_t>(lc) * W + i;
+            lohi = static_cast<uint32_t>(lo[p]) | (static_cast<uint32_t>(hi[p]) << 16);
+            cell = off[p];
+            qo = qoff[p];
+        }
+    }
+};
+
+// Column-major copies of (lo|hi<<16, cell offset, quad offset) for the column
+// sweeps, via 32x32 shared-memory tiles (coalesced both ways).
+__global__ void sweep_meta_kernel(Bufs b) {
+    __shared__ uint32_t t0[32][33], t1[32][33], t2[32][33];
+    const int a = blockIdx.z, s = slot_of(b, a);
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const size_t P = b.P;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int x = x0 + threadIdx.x, y = y0 + r;
+        if (x < b.W && y < b.H) {
+            const size_t p = static_cast<size_t>(s) * P + static_cast<size_t>(y) * b.W + x;
+            const size_t po = static_cast<size_t>(s) * (P + 1) + static_cast<size_t>(y) * b.W + x;
+            t0[r][threadIdx.x] = static_cast<uint32_t>(b.lo[p]) | (static_cast<uint32_t>(b.hi[p]) << 16);
+            t1[r][threadIdx.x] = b.off[po];
+            t2[r][threadIdx.x] = b.qoff[po];
+        }
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int y = y0 + threadIdx.x, x = x0 + r;
+        if (x < b.W && y < b.H) {
+            const size_t q = static_cast<size_t>(s) * P + static_cast<size_t>(x) * b.H + y;
+            b.mt_lohi[q] = t0[threadIdx.x][r];
+            b.mt_cell[q] = t1[threadIdx.x][r];
+            b.mt_qoff[q] = t2[threadIdx.x][r];
+        }
+    }
+}
+
 template <int KQ>
 __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ int cnt[2];
+    __shared__ int cnt[2][2];
     __shared__ int item_s;
     const SweepPlan plan = sweep_plan(b.W, b.H, b.d_max);
     const int SB = sweep_slot_bytes(b.d_max);
     const int lmax = b.W > b.H ? b.W : b.H;
     uint8_t* mbuf = smem;
     uint32_t* rng = reinterpret_cast<uint32_t*>(smem + plan.buf);
-    uint32_t* m_lohi = reinterpret_cast<uint32_t*>(smem + plan.buf + plan.rng);
-    uint32_t* m_cell = m_lohi + lmax;
-    uint32_t* m_qoff = m_cell + lmax;
-    uint16_t* l_narrow = reinterpret_cast<uint16_t*>(m_qoff + lmax);
+    uint32_t* mbase = reinterpret_cast<uint32_t*>(smem + plan.buf + plan.rng);
+    auto meta_set = [&](int k) {
+        LineMeta m;
+        m.lohi = mbase + (3 * k + 0) * lmax;
+        m.cell = mbase + (3 * k + 1) * lmax;
+        m.qoff = mbase + (3 * k + 2) * lmax;
+        return m;
+    };
+    uint16_t* l_narrow = reinterpret_cast<uint16_t*>(mbase + 6 * lmax);
     uint16_t* l_wide = l_narrow + lmax;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
     const int n_ab = __popc(sp.roles & 3) * sp.n, n_cd = __popc(sp.roles & 12) * sp.n;
-    const int di_cd[1] = {0};
 
-    if (threadIdx.x == 0) cnt[0] = cnt[1] = 0;
     for (;;) {
         if (threadIdx.x == 0) item_s = atomicAdd(b.work, 1);
         __syncthreads();
@@ -221,15 +312,22 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
             role = (sp.roles & 4) ? 2 + r : 3;
         }
         const int s = slot_of(b, a);
-        const bool cols = role < 2;
-        const int sign = (role == 0 || role == 2) ? 1 : -1;
-        const int len = cols ? b.H : b.W, nlines = cols ? b.W : b.H;
-        const int ndir = cols ? sp.ndir_ab : 1;
-        const int* di = cols ? sp.di_ab : di_cd;
-        const uint16_t* lo = b.lo + static_cast<size_t>(s) * b.P;
-        const uint16_t* hi = b.hi + static_cast<size_t>(s) * b.P;
-        const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
-        const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1);
+        RoleView rv;
+        rv.cols = role < 2;
+        rv.sign = (role == 0 || role == 2) ? 1 : -1;
+        rv.len = rv.cols ? b.H : b.W;
+        rv.nlines = rv.cols ? b.W : b.H;
+        rv.W = b.W;
+        rv.lo = b.lo + static_cast<size_t>(s) * b.P;
+        rv.hi = b.hi + static_cast<size_t>(s) * b.P;
+        rv.off = b.off + static_cast<size_t>(s) * (b.P + 1);
+        rv.qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1);
+        rv.t_lohi = b.mt_lohi + static_cast<size_t>(s) * b.P;
+        rv.t_cell = b.mt_cell + static_cast<size_t>(s) * b.P;
+        rv.t_qoff = b.mt_qoff + static_cast<size_t>(s) * b.P;
+        const int len = rv.len, nlines = rv.nlines;
+        const int ndir = rv.cols ? sp.ndir_ab : 1;
+        const int di0 = rv.cols ? sp.di_ab[0] : 0, di1 = sp.di_ab[1], di2 = sp.di_ab[2];
         const uint8_t* cost = b.cost + static_cast<size_t>(s) * b.vol_cap;
         void* out;
         switch (role) {
@@ -238,7 +336,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
             case 2: out = b.pC + static_cast<size_t>(s) * b.quad_cap * 4; break;
             default: out = b.pD + static_cast<size_t>(s) * b.quad_cap * 4; break;
         }
-        const bool out_u16 = cols;
+        const bool out_u16 = rv.cols;
 
         // all slots start as "absent" (P2) with an empty quad range
         {
@@ -247,22 +345,23 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
             for (size_t w = threadIdx.x; w < words; w += kSweepThreads) mw[w] = P2x4;
             for (int w = threadIdx.x; w < ndir * len; w += kSweepThreads) rng[w] = 0x0000ffffu;
         }
+        // metadata of lines 0 and 1
+        for (int k = 0; k < 2 && k < nlines; ++k) {
+            const LineMeta m = meta_set(k);
+            for (int i = threadIdx.x; i < len; i += kSweepThreads)
+                rv.load(k, i, m.lohi[i], m.cell[i], m.qoff[i]);
+        }
+        if (threadIdx.x == 0) cnt[0][0] = cnt[0][1] = cnt[1][0] = cnt[1][1] = 0;
         __syncthreads();
 
-        for (int l = 0; l < nlines; ++l) {
-            const int lc = sign > 0 ? l : nlines - 1 - l;
-            // line metadata + narrow/wide classification (warp-aggregated appends)
+        // classify line `l` (metadata in `m`) into the narrow / wide lists
+        auto classify = [&](const LineMeta& m, int* c) {
             for (int base = 0; base < len; base += kSweepThreads) {
                 const int i = base + threadIdx.x;
                 bool narrow = false, wide = false;
                 if (i < len) {
-                    const size_t p = cols ? static_cast<size_t>(i) * b.W + lc
-                                          : static_cast<size_t>(lc) * b.W + i;
-                    const int l0 = lo[p], h0 = hi[p];
-                    m_lohi[i] = static_cast<uint32_t>(l0) | (static_cast<uint32_t>(h0) << 16);
-                    m_cell[i] = off[p];
-                    m_qoff[i] = qoff[p];
-                    const int nq = (h0 >> 2) - (l0 >> 2) + 1;
+                    const uint32_t lohi = m.lohi[i];
+                    const int nq = static_cast<int>(lohi >> 18) - static_cast<int>((lohi & 0xffffu) >> 2) + 1;
                     narrow = nq <= 4;
                     wide = !narrow;
                 }
@@ -270,8 +369,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
                 const unsigned bw = __ballot_sync(0xffffffffu, wide);
                 int basen = 0, basew = 0;
                 if (lane == 0) {
-                    if (bn) basen = atomicAdd(&cnt[0], __popc(bn));
-                    if (bw) basew = atomicAdd(&cnt[1], __popc(bw));
+                    if (bn) basen = atomicAdd(&c[0], __popc(bn));
+                    if (bw) basew = atomicAdd(&c[1], __popc(bw));
                 }
                 basen = __shfl_sync(0xffffffffu, basen, 0);
                 basew = __shfl_sync(0xffffffffu, basew, 0);
@@ -279,23 +378,87 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
                 if (narrow) l_narrow[basen + __popc(bn & lt)] = static_cast<uint16_t>(i);
                 if (wide) l_wide[basew + __popc(bw & lt)] = static_cast<uint16_t>(i);
             }
-            __syncthreads();
-            const int n_narrow = cnt[0], n_wide = cnt[1];
-            const int u_narrow = (n_narrow + 7) >> 3;
-            for (int u = warp; u < u_narrow + n_wide; u += kSweepWarps) {
-                if (u < u_narrow) {
-                    const int e = u * 8 + (lane >> 2);
-                    if (e < n_narrow)
-                        sweep_pixel<4, 1>(l_narrow[e], l, len, ndir, di, mbuf, SB, rng, m_lohi,
-                                          m_cell, m_qoff, cost, out, out_u16, P1x2, P2x2, P2x4);
-                } else {
-                    sweep_pixel<32, KQ>(l_wide[u - u_narrow], l, len, ndir, di, mbuf, SB, rng,
-                                        m_lohi, m_cell, m_qoff, cost, out, out_u16, P1x2, P2x2,
-                                        P2x4);
+        };
+        classify(meta_set(0), cnt[0]);
+        __syncthreads();
+
+        for (int l = 0; l < nlines; ++l) {
+            const LineMeta cur = meta_set(l & 1);
+            const LineMeta nxt = meta_set((l + 1) & 1);
+            // (a) metadata of line l+2 into registers (stored after this line)
+            uint32_t r_lohi[kMetaPerThread], r_cell[kMetaPerThread], r_qoff[kMetaPerThread];
+            const bool have2 = l + 2 < nlines;
+#pragma unroll
+            for (int k = 0; k < kMetaPerThread; ++k) {
+                const int i = threadIdx.x + k * kSweepThreads;
+                if (have2 && i < len) rv.load(l + 2, i, r_lohi[k], r_cell[k], r_qoff[k]);
+            }
+            // (b) pull line l+1's matching costs towards L2
+            if (l + 1 < nlines) {
+                for (int i = threadIdx.x; i < len; i += kSweepThreads) {
+                    const uint32_t lohi = nxt.lohi[i];
+                    const int n = static_cast<int>(lohi >> 16) - static_cast<int>(lohi & 0xffffu) + 1;
+                    const uint8_t* c0 = cost + nxt.cell[i];
+                    for (int o = 0; o < n + 4; o += 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(c0 + o));
                 }
             }
+            // (c) this line's pixels, next unit's costs fetched ahead
+            int* c_cur = &cnt[0][0] + 2 * (l & 1);
+            int* c_nxt = &cnt[0][0] + 2 * ((l + 1) & 1);
+            const int n_narrow = c_cur[0], n_wide = c_cur[1];
+            if (threadIdx.x == 0) c_nxt[0] = c_nxt[1] = 0;
+            const int u_narrow = (n_narrow + 7) >> 3, total = u_narrow + n_wide;
+            int u = warp;
+            CostRegs<KQ> cr_cur, cr_nxt;
+            auto fetch_unit = [&](int uu, CostRegs<KQ>& r) {
+                if (uu >= total) return;
+                if (uu < u_narrow) {
+                    const int e = uu * 8 + (lane >> 2);
+                    if (e < n_narrow) {
+                        CostRegs<1> r1;
+                        fetch_costs<4, 1>(l_narrow[e], cur, cost, r1);
+                        r.w0[0] = r1.w0[0];
+                        r.w1[0] = r1.w1[0];
+                        r.sh[0] = r1.sh[0];
+                    }
+                } else {
+                    fetch_costs<32, KQ>(l_wide[uu - u_narrow], cur, cost, r);
+                }
+            };
+            fetch_unit(u, cr_cur);
+            while (u < total) {
+                const int un = u + kSweepWarps;
+                fetch_unit(un, cr_nxt);
+                if (u < u_narrow) {
+                    const int e = u * 8 + (lane >> 2);
+                    if (e < n_narrow) {
+                        CostRegs<1> r1;
+                        r1.w0[0] = cr_cur.w0[0];
+                        r1.w1[0] = cr_cur.w1[0];
+                        r1.sh[0] = cr_cur.sh[0];
+                        sweep_pixel<4, 1>(l_narrow[e], l, len, ndir, di0, di1, di2, mbuf, SB, rng, cur, r1,
+                                          out, out_u16, P1x2, P2x2, P2x4);
+                    }
+                } else {
+                    sweep_pixel<32, KQ>(l_wide[u - u_narrow], l, len, ndir, di0, di1, di2, mbuf, SB, rng,
+                                        cur, cr_cur, out, out_u16, P1x2, P2x2, P2x4);
+                }
+                cr_cur = cr_nxt;
+                u = un;
+            }
             __syncthreads();
-            if (threadIdx.x == 0) cnt[0] = cnt[1] = 0;
+            // line l's metadata slot now takes line l+2; classify line l+1
+#pragma unroll
+            for (int k = 0; k < kMetaPerThread; ++k) {
+                const int i = threadIdx.x + k * kSweepThreads;
+                if (have2 && i < len) {
+                    cur.lohi[i] = r_lohi[k];
+                    cur.cell[i] = r_cell[k];
+                    cur.qoff[i] = r_qoff[k];
+                }
+            }
+            if (l + 1 < nlines) classify(nxt, c_nxt);
             __syncthreads();
         }
     }
@@ -364,6 +527,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int items = (__builtin_popcount(sp.roles & 3) + __builtin_popcount(sp.roles & 12)) * n;
     const int grid = items < num_sms ? items : num_sms;
     cudaMemsetAsync(b.work, 0, sizeof(int), L.st);
+    sweep_meta_kernel<<<dim3((b.W + 31) / 32, (b.H + 31) / 32, n), dim3(32, 8), 0, L.st>>>(b);
     if ((b.d_max + 3) / 4 <= 32) {
         cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(plan.total));
@@ -375,7 +539,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     }
     const size_t csmem = sizeof(uint32_t) * (2 * b.W + 1) + sizeof(uint16_t) * b.W;
     sweep_combine_kernel<<<dim3(b.H, n), 512, csmem, L.st>>>(b, sp.roles);
-    *L.counter += 2;
+    *L.counter += 3;
 }
 
 }  // namespace tsgm

@@ -51,6 +51,9 @@ struct Bufs {
     uint8_t *pC, *pD;
     size_t quad_cap;  // quads per slot
     int* work;        // persistent-CTA work counter
+    // column-major (line-major for the column sweeps) window metadata:
+    // [slot][x*H + y] = lo | hi << 16, cell offset, quad offset
+    uint32_t *mt_lohi, *mt_cell, *mt_qoff;
     // WTA, render, export (A15, A18, A19)
     int32_t *md, *rd, *ed;
     uint8_t *mv, *rv, *ev;

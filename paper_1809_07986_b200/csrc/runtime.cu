@@ -304,6 +304,9 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
         b.pB = ctx->dalloc<uint16_t>(S * b.quad_cap * 4);
         b.pC = ctx->dalloc<uint8_t>(S * b.quad_cap * 4);
         b.pD = ctx->dalloc<uint8_t>(S * b.quad_cap * 4);
+        b.mt_lohi = ctx->dalloc<uint32_t>(S * P);
+        b.mt_cell = ctx->dalloc<uint32_t>(S * P);
+        b.mt_qoff = ctx->dalloc<uint32_t>(S * P);
     }
     b.work = ctx->dalloc<int>(1);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device));
