@@ -344,7 +344,7 @@ class Port(_Lib):
         img = _u8(img)
         h, w = img.shape
         sig = np.zeros((h, w), np.uint32)
-        self.lib.or_census(_p(img), w, h, _p(sig))
+        self._c(self.lib.or_census(_p(img), w, h, _p(sig)))
         return sig
 
     def offsets(self, lo, hi):

@@ -49,7 +49,9 @@ int or_filter_validate(const or_filter* f, int d_max) {
 
 /* census_transform, src/matching_cost.cpp:53-79: 5x5 window, raster order,
  * bit 23 = (-2,-2), strict "darker than centre"; 2-px border signature 0. */
-void or_census(const uint8_t* img, int w, int h, uint32_t* sig) {
+int or_census(const uint8_t* img, int w, int h, uint32_t* sig) {
+    if (w < 2 * CENSUS_R + 1 || h < 2 * CENSUS_R + 1)
+        return fail("census_transform: image smaller than the 5x5 window");
     memset(sig, 0, sizeof(uint32_t) * (size_t)w * h);
     for (int y = CENSUS_R; y < h - CENSUS_R; ++y)
         for (int x = CENSUS_R; x < w - CENSUS_R; ++x) {
@@ -62,6 +64,7 @@ void or_census(const uint8_t* img, int w, int h, uint32_t* sig) {
                 }
             sig[(size_t)y * w + x] = s;
         }
+    return 0;
 }
 
 /* make_cost_volume offsets, src/matching_cost.cpp:30-48 */

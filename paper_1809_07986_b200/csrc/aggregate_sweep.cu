@@ -90,114 +90,123 @@ struct CostRegs {
     uint32_t w0[KQ], w1[KQ], sh[KQ];
 };
 
+// Every lane of the warp calls this (inactive lanes: i < 0 or quad beyond the
+// window) so that the group reductions can use full-warp shuffles; addresses
+// are clamped into the window, results of inactive lanes are masked later.
 template <int G, int KQ>
 __device__ __forceinline__ void fetch_costs(int i, const LineMeta& m, const uint8_t* cost,
                                             CostRegs<KQ>& r) {
     const int lg = threadIdx.x & (G - 1);
-    const uint32_t lohi = m.lohi[i];
+    const uint32_t lohi = i >= 0 ? m.lohi[i] : 0u;
     const int lo = static_cast<int>(lohi & 0xffffu), hi = static_cast<int>(lohi >> 16);
     const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
-    const uint32_t cell = m.cell[i];
+    const uint32_t cell = i >= 0 ? m.cell[i] : 0u;
 #pragma unroll
     for (int t = 0; t < KQ; ++t) {
-        const int k = lg + t * G;
-        r.w0[t] = r.w1[t] = r.sh[t] = 0u;
-        if (k < nq) {
-            const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + cell + (4 * (q0 + k) - lo);
-            const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-            r.w0[t] = __ldg(aw);
-            r.w1[t] = __ldg(aw + 1);
-            r.sh[t] = 8u * static_cast<uint32_t>(addr & 3);
-        }
+        const int k = min(lg + t * G, nq - 1);
+        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + cell + (4 * (q0 + k) - lo);
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+        r.w0[t] = __ldg(aw);
+        r.w1[t] = __ldg(aw + 1);
+        r.sh[t] = 8u * static_cast<uint32_t>(addr & 3);
     }
 }
 
+// min over the lanes of a group (G = 4: butterfly within the quad of lanes;
+// G = 32: one REDUX). All 32 lanes must call it.
+template <int G>
+__device__ __forceinline__ uint32_t group_min(uint32_t v) {
+    if (G == 32) return __reduce_min_sync(0xffffffffu, v);
+    v = min(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    v = min(v, __shfl_xor_sync(0xffffffffu, v, 2));
+    return v;
+}
+
 // One pixel of a line, processed by a group of G lanes (G = 4 or 32), each
-// lane holding up to KQ quads.
+// lane holding up to KQ quads. All lanes of the warp call it; a group with
+// i < 0 has no pixel (everything masked, nothing stored).
 template <int G, int KQ>
-__device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, int di0, int di1, int di2,
-                                            uint8_t* mbuf, int SB, uint32_t* rng,
-                                            const LineMeta& meta, const CostRegs<KQ>& cr,
-                                            void* out, bool out_u16, uint32_t P1x2, uint32_t P2x2,
-                                            uint32_t P2x4) {
+__device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, int di0, int di1,
+                                            int di2, int sb0, int sb1, int sb2, uint8_t* mbuf,
+                                            int SB, uint32_t* rng, const LineMeta& meta,
+                                            const CostRegs<KQ>& cr, void* out, bool out_u16,
+                                            uint32_t P1x2, uint32_t P2x2, uint32_t P2x4) {
     const int lane = threadIdx.x & 31;
     const int lg = lane & (G - 1);
-    const unsigned gmask = G == 32 ? 0xffffffffu : (0xfu << (lane & ~3));
-    const uint32_t lohi = meta.lohi[i];
+    const bool px = i >= 0;
+    const int ii = px ? i : 0;
+    const uint32_t lohi = px ? meta.lohi[ii] : 0u;
     const int lo = static_cast<int>(lohi & 0xffffu), hi = static_cast<int>(lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
-    const uint32_t qo = meta.qoff[i];
+    const uint32_t qo = px ? meta.qoff[ii] : 0u;
 
     bool act[KQ];
+    int dq[KQ];  // byte offset of the lane's quad in a slot (clamped into the window)
     uint32_t CA[KQ], CB[KQ], ivA[KQ], ivB[KQ], sA[KQ], sB[KQ], LA[KQ], LB[KQ];
 #pragma unroll
     for (int t = 0; t < KQ; ++t) {
         const int k = lg + t * G;
-        act[t] = k < nq;
+        act[t] = px && k < nq;
+        const int d0 = 4 * (q0 + min(k, nq - 1));
+        dq[t] = d0;
         sA[t] = sB[t] = 0u;
-        CA[t] = CB[t] = ivA[t] = ivB[t] = 0u;
-        if (act[t]) {
-            const int d0 = 4 * (q0 + k);
-            const uint32_t cq = __funnelshift_r(cr.w0[t], cr.w1[t], cr.sh[t]);
-            CA[t] = prmt(cq, 0u, 0x4140u);
-            CB[t] = prmt(cq, 0u, 0x4342u);
-            const uint32_t bad0 = (d0 < lo || d0 > hi) ? 0x0000ffffu : 0u;
-            const uint32_t bad1 = (d0 + 1 < lo || d0 + 1 > hi) ? 0xffff0000u : 0u;
-            const uint32_t bad2 = (d0 + 2 < lo || d0 + 2 > hi) ? 0x0000ffffu : 0u;
-            const uint32_t bad3 = (d0 + 3 > hi) ? 0xffff0000u : 0u;
-            ivA[t] = bad0 | bad1;
-            ivB[t] = bad2 | bad3;
-        }
+        const uint32_t cq = __funnelshift_r(cr.w0[t], cr.w1[t], cr.sh[t]);
+        CA[t] = prmt(cq, 0u, 0x4140u);
+        CB[t] = prmt(cq, 0u, 0x4342u);
+        const uint32_t bad0 = (d0 < lo) ? 0x0000ffffu : 0u;
+        const uint32_t bad1 = (d0 + 1 < lo || d0 + 1 > hi) ? 0xffff0000u : 0u;
+        const uint32_t bad2 = (d0 + 2 < lo || d0 + 2 > hi) ? 0x0000ffffu : 0u;
+        const uint32_t bad3 = (d0 + 3 > hi) ? 0xffff0000u : 0u;
+        ivA[t] = act[t] ? (bad0 | bad1) : 0xffffffffu;
+        ivB[t] = act[t] ? (bad2 | bad3) : 0xffffffffu;
     }
 
     for (int j = 0; j < ndir; ++j) {
         const int dj = j == 0 ? di0 : (j == 1 ? di1 : di2);
-        const bool has_pred = l > 0 && static_cast<unsigned>(i + dj) < static_cast<unsigned>(len);
-        int sidx = (i + dj * l) % len;
-        if (sidx < 0) sidx += len;
+        const int sbj = j == 0 ? sb0 : (j == 1 ? sb1 : sb2);
+        const bool has_pred = l > 0 && static_cast<unsigned>(ii + dj) < static_cast<unsigned>(len);
+        int sidx = ii + sbj;
+        if (sidx >= len) sidx -= len;
         uint8_t* sb = mbuf + (static_cast<size_t>(j) * len + sidx) * SB;
         uint32_t mn = 0xffffffffu;
 #pragma unroll
         for (int t = 0; t < KQ; ++t) {
-            if (!act[t]) continue;
-            const int d0 = 4 * (q0 + lg + t * G);
-            if (has_pred) {
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(sb + d0);
-                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
-                const uint32_t e0 = prmt(w1, 0u, 0x4140u);  // M(d0),   M(d0+1)
-                const uint32_t e1 = prmt(w1, 0u, 0x4342u);  // M(d0+2), M(d0+3)
-                const uint32_t mpa = prmt(w1, 0u, 0x4241u); // M(d0+1), M(d0+2)
-                const uint32_t mma = prmt(w0 >> 24, e0, 0x5410u);  // M(d0-1), M(d0)
-                const uint32_t mpb = prmt(e1, w2 & 0xffu, 0x5432u); // M(d0+3), M(d0+4)
-                LA[t] = __vadd2(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), CA[t]);
-                LB[t] = __vadd2(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), CB[t]);
-            } else {
-                LA[t] = CA[t];  // path starts here (sgm.cpp:93-99)
-                LB[t] = CB[t];
-            }
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(sb + dq[t]);
+            // no predecessor (image edge): M == 0 gives L = C (sgm.cpp:93-99)
+            const uint32_t w0 = has_pred ? w[0] : 0u;
+            const uint32_t w1 = has_pred ? w[1] : 0u;
+            const uint32_t w2 = has_pred ? w[2] : 0u;
+            const uint32_t e0 = prmt(w1, 0u, 0x4140u);  // M(d0),   M(d0+1)
+            const uint32_t e1 = prmt(w1, 0u, 0x4342u);  // M(d0+2), M(d0+3)
+            const uint32_t mpa = prmt(w1, 0u, 0x4241u); // M(d0+1), M(d0+2)
+            const uint32_t mma = prmt(w0 >> 24, e0, 0x5410u);  // M(d0-1), M(d0)
+            const uint32_t mpb = prmt(e1, w2 & 0xffu, 0x5432u); // M(d0+3), M(d0+4)
+            LA[t] = __vadd2(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), CA[t]);
+            LB[t] = __vadd2(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), CB[t]);
             mn = __vminu2(mn, __vminu2(LA[t] | ivA[t], LB[t] | ivB[t]));
         }
-        const uint32_t m1 = min(mn & 0xffffu, mn >> 16);
-        const uint32_t m = __reduce_min_sync(gmask, m1);
+        const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
         const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
 #pragma unroll
         for (int t = 0; t < KQ; ++t) {
-            if (!act[t]) continue;
-            const int d0 = 4 * (q0 + lg + t * G);
             const uint32_t ma = __vmaxu2(__viaddmin_u16x2(LA[t], neg, P2x2), ivA[t] & P2x2);
             const uint32_t mb = __vmaxu2(__viaddmin_u16x2(LB[t], neg, P2x2), ivB[t] & P2x2);
-            *reinterpret_cast<uint32_t*>(sb + 4 + d0) = prmt(ma, mb, 0x6420u);
+            if (act[t]) *reinterpret_cast<uint32_t*>(sb + 4 + dq[t]) = prmt(ma, mb, 0x6420u);
             sA[t] = __vadd2(sA[t], LA[t]);
             sB[t] = __vadd2(sB[t], LB[t]);
         }
         // reset levels the slot held but this window does not cover
-        uint32_t* rp = rng + static_cast<size_t>(j) * len + sidx;
-        const uint32_t old = *rp;
-        const int oq0 = static_cast<int>(old & 0xffffu), oq1 = static_cast<int>(old >> 16);
-        for (int q = oq0 + lg; q <= oq1; q += G)
-            if (q < q0 || q > q1) *reinterpret_cast<uint32_t*>(sb + 4 + 4 * q) = P2x4;
-        __syncwarp(gmask);
-        if (lg == 0) *rp = static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16);
+        if (px) {
+            uint32_t* rp = rng + static_cast<size_t>(j) * len + sidx;
+            const uint32_t old = *rp;
+            const int oq0 = static_cast<int>(old & 0xffffu), oq1 = static_cast<int>(old >> 16);
+            if (oq0 < q0 || oq1 > q1) {
+                for (int q = oq0 + lg; q <= oq1; q += G)
+                    if (q < q0 || q > q1) *reinterpret_cast<uint32_t*>(sb + 4 + 4 * q) = P2x4;
+            }
+            if (lg == 0 && old != (static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16)))
+                *rp = static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16);
+        }
     }
 #pragma unroll
     for (int t = 0; t < KQ; ++t) {
@@ -340,9 +349,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
 
         // all slots start as "absent" (P2) with an empty quad range
         {
-            uint32_t* mw = reinterpret_cast<uint32_t*>(mbuf);
-            const size_t words = static_cast<size_t>(ndir) * len * SB / 4;
-            for (size_t w = threadIdx.x; w < words; w += kSweepThreads) mw[w] = P2x4;
+            uint4* mw = reinterpret_cast<uint4*>(mbuf);
+            const size_t vecs = static_cast<size_t>(ndir) * len * SB / 16;
+            const uint4 fill = make_uint4(P2x4, P2x4, P2x4, P2x4);
+            for (size_t w = threadIdx.x; w < vecs; w += kSweepThreads) mw[w] = fill;
+            uint32_t* mt = reinterpret_cast<uint32_t*>(mbuf);
+            for (size_t w = vecs * 4 + threadIdx.x; w < static_cast<size_t>(ndir) * len * SB / 4;
+                 w += kSweepThreads)
+                mt[w] = P2x4;
             for (int w = threadIdx.x; w < ndir * len; w += kSweepThreads) rng[w] = 0x0000ffffu;
         }
         // metadata of lines 0 and 1
@@ -409,40 +423,57 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
             const int n_narrow = c_cur[0], n_wide = c_cur[1];
             if (threadIdx.x == 0) c_nxt[0] = c_nxt[1] = 0;
             const int u_narrow = (n_narrow + 7) >> 3, total = u_narrow + n_wide;
-            int u = warp;
-            CostRegs<KQ> cr_cur, cr_nxt;
-            auto fetch_unit = [&](int uu, CostRegs<KQ>& r) {
-                if (uu >= total) return;
+            // sheared slot bases of this line, (dj * l) mod len per direction
+            auto sbase = [&](int dj) {
+                int v = (dj * l) % len;
+                return v < 0 ? v + len : v;
+            };
+            const int sb0 = sbase(di0), sb1 = sbase(di1), sb2 = sbase(di2);
+            // pixel of this lane's group in unit uu (-1: none)
+            auto unit_pixel = [&](int uu) -> int {
                 if (uu < u_narrow) {
                     const int e = uu * 8 + (lane >> 2);
-                    if (e < n_narrow) {
-                        CostRegs<1> r1;
-                        fetch_costs<4, 1>(l_narrow[e], cur, cost, r1);
-                        r.w0[0] = r1.w0[0];
-                        r.w1[0] = r1.w1[0];
-                        r.sh[0] = r1.sh[0];
-                    }
-                } else {
-                    fetch_costs<32, KQ>(l_wide[uu - u_narrow], cur, cost, r);
+                    return e < n_narrow ? static_cast<int>(l_narrow[e]) : -1;
                 }
+                return uu < total ? static_cast<int>(l_wide[uu - u_narrow]) : -1;
             };
-            fetch_unit(u, cr_cur);
+            int u = warp;
+            CostRegs<KQ> cr_cur, cr_nxt;
+            if (u < total) {
+                if (u < u_narrow) {
+                    CostRegs<1> r1;
+                    fetch_costs<4, 1>(unit_pixel(u), cur, cost, r1);
+                    cr_cur.w0[0] = r1.w0[0];
+                    cr_cur.w1[0] = r1.w1[0];
+                    cr_cur.sh[0] = r1.sh[0];
+                } else {
+                    fetch_costs<32, KQ>(unit_pixel(u), cur, cost, cr_cur);
+                }
+            }
             while (u < total) {
                 const int un = u + kSweepWarps;
-                fetch_unit(un, cr_nxt);
-                if (u < u_narrow) {
-                    const int e = u * 8 + (lane >> 2);
-                    if (e < n_narrow) {
+                if (un < total) {
+                    if (un < u_narrow) {
                         CostRegs<1> r1;
-                        r1.w0[0] = cr_cur.w0[0];
-                        r1.w1[0] = cr_cur.w1[0];
-                        r1.sh[0] = cr_cur.sh[0];
-                        sweep_pixel<4, 1>(l_narrow[e], l, len, ndir, di0, di1, di2, mbuf, SB, rng, cur, r1,
-                                          out, out_u16, P1x2, P2x2, P2x4);
+                        fetch_costs<4, 1>(unit_pixel(un), cur, cost, r1);
+                        cr_nxt.w0[0] = r1.w0[0];
+                        cr_nxt.w1[0] = r1.w1[0];
+                        cr_nxt.sh[0] = r1.sh[0];
+                    } else {
+                        fetch_costs<32, KQ>(unit_pixel(un), cur, cost, cr_nxt);
                     }
+                }
+                if (u < u_narrow) {
+                    CostRegs<1> r1;
+                    r1.w0[0] = cr_cur.w0[0];
+                    r1.w1[0] = cr_cur.w1[0];
+                    r1.sh[0] = cr_cur.sh[0];
+                    sweep_pixel<4, 1>(unit_pixel(u), l, len, ndir, di0, di1, di2, sb0, sb1, sb2,
+                                      mbuf, SB, rng, cur, r1, out, out_u16, P1x2, P2x2, P2x4);
                 } else {
-                    sweep_pixel<32, KQ>(l_wide[u - u_narrow], l, len, ndir, di0, di1, di2, mbuf, SB, rng,
-                                        cur, cr_cur, out, out_u16, P1x2, P2x2, P2x4);
+                    sweep_pixel<32, KQ>(unit_pixel(u), l, len, ndir, di0, di1, di2, sb0, sb1,
+                                        sb2, mbuf, SB, rng, cur, cr_cur, out, out_u16, P1x2, P2x2,
+                                        P2x4);
                 }
                 cr_cur = cr_nxt;
                 u = un;
