@@ -85,24 +85,24 @@ struct LineMeta {
 };
 
 // Matching costs of one pixel's quads for one lane, fetched ahead of use.
-template <int KQ>
+template <int Q>
 struct CostRegs {
-    uint32_t w0[KQ], w1[KQ], sh[KQ];
+    uint32_t w0[Q], w1[Q], sh[Q];
 };
 
 // Every lane of the warp calls this (inactive lanes: i < 0 or quad beyond the
 // window) so that the group reductions can use full-warp shuffles; addresses
 // are clamped into the window, results of inactive lanes are masked later.
-template <int G, int KQ>
+template <int G, int Q>
 __device__ __forceinline__ void fetch_costs(int i, const LineMeta& m, const uint8_t* cost,
-                                            CostRegs<KQ>& r) {
+                                            CostRegs<Q>& r) {
     const int lg = threadIdx.x & (G - 1);
     const uint32_t lohi = i >= 0 ? m.lohi[i] : 0u;
     const int lo = static_cast<int>(lohi & 0xffffu), hi = static_cast<int>(lohi >> 16);
     const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
     const uint32_t cell = i >= 0 ? m.cell[i] : 0u;
 #pragma unroll
-    for (int t = 0; t < KQ; ++t) {
+    for (int t = 0; t < Q; ++t) {
         const int k = min(lg + t * G, nq - 1);
         const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + cell + (4 * (q0 + k) - lo);
         const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
@@ -112,24 +112,33 @@ __device__ __forceinline__ void fetch_costs(int i, const LineMeta& m, const uint
     }
 }
 
-// min over the lanes of a group (G = 4: butterfly within the quad of lanes;
-// G = 32: one REDUX). All 32 lanes must call it.
+// min over the G lanes of a group; all 32 lanes must call it.
 template <int G>
 __device__ __forceinline__ uint32_t group_min(uint32_t v) {
     if (G == 32) return __reduce_min_sync(0xffffffffu, v);
-    v = min(v, __shfl_xor_sync(0xffffffffu, v, 1));
-    v = min(v, __shfl_xor_sync(0xffffffffu, v, 2));
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 
-// One pixel of a line, processed by a group of G lanes (G = 4 or 32), each
-// lane holding up to KQ quads. All lanes of the warp call it; a group with
-// i < 0 has no pixel (everything masked, nothing stored).
-template <int G, int KQ>
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// One pixel of a line, processed by a group of G lanes, each lane holding Q
+// quads (quad k = lg + t*G). All lanes of the warp call it; a group with
+// i < 0 has no pixel (everything masked, nothing stored). `mbuf` / `rng` are
+// 32-bit shared-memory addresses.
+template <int G, int Q>
 __device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, int di0, int di1,
-                                            int di2, int sb0, int sb1, int sb2, uint8_t* mbuf,
-                                            int SB, uint32_t* rng, const LineMeta& meta,
-                                            const CostRegs<KQ>& cr, void* out, bool out_u16,
+                                            int di2, int sb0, int sb1, int sb2, uint32_t mbuf,
+                                            int SB, uint32_t rng, const LineMeta& meta,
+                                            const CostRegs<Q>& cr, void* out, bool out_u16,
                                             uint32_t P1x2, uint32_t P2x2, uint32_t P2x4) {
     const int lane = threadIdx.x & 31;
     const int lg = lane & (G - 1);
@@ -138,17 +147,17 @@ __device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, int
     const uint32_t lohi = px ? meta.lohi[ii] : 0u;
     const int lo = static_cast<int>(lohi & 0xffffu), hi = static_cast<int>(lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
-    const uint32_t qo = px ? meta.qoff[ii] : 0u;
+    const uint32_t qrange = static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16);
 
-    bool act[KQ];
-    int dq[KQ];  // byte offset of the lane's quad in a slot (clamped into the window)
-    uint32_t CA[KQ], CB[KQ], ivA[KQ], ivB[KQ], sA[KQ], sB[KQ], LA[KQ], LB[KQ];
+    bool act[Q];
+    uint32_t dq[Q];  // byte offset of the lane's quad in a slot (clamped into the window)
+    uint32_t CA[Q], CB[Q], ivA[Q], ivB[Q], sA[Q], sB[Q], LA[Q], LB[Q];
 #pragma unroll
-    for (int t = 0; t < KQ; ++t) {
+    for (int t = 0; t < Q; ++t) {
         const int k = lg + t * G;
         act[t] = px && k < nq;
         const int d0 = 4 * (q0 + min(k, nq - 1));
-        dq[t] = d0;
+        dq[t] = static_cast<uint32_t>(d0);
         sA[t] = sB[t] = 0u;
         const uint32_t cq = __funnelshift_r(cr.w0[t], cr.w1[t], cr.sh[t]);
         CA[t] = prmt(cq, 0u, 0x4140u);
@@ -167,15 +176,18 @@ __device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, int
         const bool has_pred = l > 0 && static_cast<unsigned>(ii + dj) < static_cast<unsigned>(len);
         int sidx = ii + sbj;
         if (sidx >= len) sidx -= len;
-        uint8_t* sb = mbuf + (static_cast<size_t>(j) * len + sidx) * SB;
+        const uint32_t slot = static_cast<uint32_t>(j * len + sidx);
+        const uint32_t sb = mbuf + slot * static_cast<uint32_t>(SB);
         uint32_t mn = 0xffffffffu;
 #pragma unroll
-        for (int t = 0; t < KQ; ++t) {
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(sb + dq[t]);
+        for (int t = 0; t < Q; ++t) {
             // no predecessor (image edge): M == 0 gives L = C (sgm.cpp:93-99)
-            const uint32_t w0 = has_pred ? w[0] : 0u;
-            const uint32_t w1 = has_pred ? w[1] : 0u;
-            const uint32_t w2 = has_pred ? w[2] : 0u;
+            uint32_t w0 = 0u, w1 = 0u, w2 = 0u;
+            if (has_pred) {
+                w0 = lds32(sb + dq[t]);
+                w1 = lds32(sb + dq[t] + 4);
+                w2 = lds32(sb + dq[t] + 8);
+            }
             const uint32_t e0 = prmt(w1, 0u, 0x4140u);  // M(d0),   M(d0+1)
             const uint32_t e1 = prmt(w1, 0u, 0x4342u);  // M(d0+2), M(d0+3)
             const uint32_t mpa = prmt(w1, 0u, 0x4241u); // M(d0+1), M(d0+2)
@@ -187,29 +199,28 @@ __device__ __forceinline__ void sweep_pixel(int i, int l, int len, int ndir, int
         }
         const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
         const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
+        // reset levels the slot held but this window does not cover
+        const uint32_t rp = rng + 4u * slot;
+        const uint32_t old = lds32(rp);
+        __syncwarp();
 #pragma unroll
-        for (int t = 0; t < KQ; ++t) {
+        for (int t = 0; t < Q; ++t) {
             const uint32_t ma = __vmaxu2(__viaddmin_u16x2(LA[t], neg, P2x2), ivA[t] & P2x2);
             const uint32_t mb = __vmaxu2(__viaddmin_u16x2(LB[t], neg, P2x2), ivB[t] & P2x2);
-            if (act[t]) *reinterpret_cast<uint32_t*>(sb + 4 + dq[t]) = prmt(ma, mb, 0x6420u);
+            if (act[t]) sts32(sb + 4 + dq[t], prmt(ma, mb, 0x6420u));
             sA[t] = __vadd2(sA[t], LA[t]);
             sB[t] = __vadd2(sB[t], LB[t]);
         }
-        // reset levels the slot held but this window does not cover
-        if (px) {
-            uint32_t* rp = rng + static_cast<size_t>(j) * len + sidx;
-            const uint32_t old = *rp;
+        if (px && old != qrange) {
             const int oq0 = static_cast<int>(old & 0xffffu), oq1 = static_cast<int>(old >> 16);
-            if (oq0 < q0 || oq1 > q1) {
-                for (int q = oq0 + lg; q <= oq1; q += G)
-                    if (q < q0 || q > q1) *reinterpret_cast<uint32_t*>(sb + 4 + 4 * q) = P2x4;
-            }
-            if (lg == 0 && old != (static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16)))
-                *rp = static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16);
+            for (int q = oq0 + lg; q <= oq1; q += G)
+                if (q < q0 || q > q1) sts32(sb + 4 + 4 * q, P2x4);
+            if (lg == 0) sts32(rp, qrange);
         }
     }
+    const uint32_t qo = px ? meta.qoff[ii] : 0u;
 #pragma unroll
-    for (int t = 0; t < KQ; ++t) {
+    for (int t = 0; t < Q; ++t) {
         if (!act[t]) continue;
         const uint32_t qi = qo + lg + t * G;
         if (out_u16)
@@ -275,8 +286,9 @@ __global__ void sweep_meta_kernel(Bufs b) {
     }
 }
 
-template <int KQ>
+template <int GW, int QW>
 __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepParams sp) {
+    constexpr int kWidePerWarp = 32 / GW;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int cnt[2][2];
     __shared__ int item_s;
@@ -285,6 +297,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
     const int lmax = b.W > b.H ? b.W : b.H;
     uint8_t* mbuf = smem;
     uint32_t* rng = reinterpret_cast<uint32_t*>(smem + plan.buf);
+    const uint32_t mbuf_s = static_cast<uint32_t>(__cvta_generic_to_shared(mbuf));
+    const uint32_t rng_s = static_cast<uint32_t>(__cvta_generic_to_shared(rng));
     uint32_t* mbase = reinterpret_cast<uint32_t*>(smem + plan.buf + plan.rng);
     auto meta_set = [&](int k) {
         LineMeta m;
@@ -422,7 +436,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
             int* c_nxt = &cnt[0][0] + 2 * ((l + 1) & 1);
             const int n_narrow = c_cur[0], n_wide = c_cur[1];
             if (threadIdx.x == 0) c_nxt[0] = c_nxt[1] = 0;
-            const int u_narrow = (n_narrow + 7) >> 3, total = u_narrow + n_wide;
+            const int u_narrow = (n_narrow + 7) >> 3;
+            const int u_wide = (n_wide + kWidePerWarp - 1) / kWidePerWarp;
+            const int total = u_narrow + u_wide;
             // sheared slot bases of this line, (dj * l) mod len per direction
             auto sbase = [&](int dj) {
                 int v = (dj * l) % len;
@@ -435,44 +451,36 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(Bufs b, SweepPa
                     const int e = uu * 8 + (lane >> 2);
                     return e < n_narrow ? static_cast<int>(l_narrow[e]) : -1;
                 }
-                return uu < total ? static_cast<int>(l_wide[uu - u_narrow]) : -1;
+                const int e = (uu - u_narrow) * kWidePerWarp + lane / GW;
+                return e < n_wide ? static_cast<int>(l_wide[e]) : -1;
             };
             int u = warp;
-            CostRegs<KQ> cr_cur, cr_nxt;
-            if (u < total) {
-                if (u < u_narrow) {
+            CostRegs<QW> cr_cur, cr_nxt;
+            auto fetch_unit = [&](int uu, CostRegs<QW>& r) {
+                if (uu < u_narrow) {
                     CostRegs<1> r1;
-                    fetch_costs<4, 1>(unit_pixel(u), cur, cost, r1);
-                    cr_cur.w0[0] = r1.w0[0];
-                    cr_cur.w1[0] = r1.w1[0];
-                    cr_cur.sh[0] = r1.sh[0];
+                    fetch_costs<4, 1>(unit_pixel(uu), cur, cost, r1);
+                    r.w0[0] = r1.w0[0];
+                    r.w1[0] = r1.w1[0];
+                    r.sh[0] = r1.sh[0];
                 } else {
-                    fetch_costs<32, KQ>(unit_pixel(u), cur, cost, cr_cur);
+                    fetch_costs<GW, QW>(unit_pixel(uu), cur, cost, r);
                 }
-            }
+            };
+            if (u < total) fetch_unit(u, cr_cur);
             while (u < total) {
                 const int un = u + kSweepWarps;
-                if (un < total) {
-                    if (un < u_narrow) {
-                        CostRegs<1> r1;
-                        fetch_costs<4, 1>(unit_pixel(un), cur, cost, r1);
-                        cr_nxt.w0[0] = r1.w0[0];
-                        cr_nxt.w1[0] = r1.w1[0];
-                        cr_nxt.sh[0] = r1.sh[0];
-                    } else {
-                        fetch_costs<32, KQ>(unit_pixel(un), cur, cost, cr_nxt);
-                    }
-                }
+                if (un < total) fetch_unit(un, cr_nxt);
                 if (u < u_narrow) {
                     CostRegs<1> r1;
                     r1.w0[0] = cr_cur.w0[0];
                     r1.w1[0] = cr_cur.w1[0];
                     r1.sh[0] = cr_cur.sh[0];
                     sweep_pixel<4, 1>(unit_pixel(u), l, len, ndir, di0, di1, di2, sb0, sb1, sb2,
-                                      mbuf, SB, rng, cur, r1, out, out_u16, P1x2, P2x2, P2x4);
+                                      mbuf_s, SB, rng_s, cur, r1, out, out_u16, P1x2, P2x2, P2x4);
                 } else {
-                    sweep_pixel<32, KQ>(unit_pixel(u), l, len, ndir, di0, di1, di2, sb0, sb1,
-                                        sb2, mbuf, SB, rng, cur, cr_cur, out, out_u16, P1x2, P2x2,
+                    sweep_pixel<GW, QW>(unit_pixel(u), l, len, ndir, di0, di1, di2, sb0, sb1, sb2,
+                                        mbuf_s, SB, rng_s, cur, cr_cur, out, out_u16, P1x2, P2x2,
                                         P2x4);
                 }
                 cr_cur = cr_nxt;
@@ -559,14 +567,16 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int grid = items < num_sms ? items : num_sms;
     cudaMemsetAsync(b.work, 0, sizeof(int), L.st);
     sweep_meta_kernel<<<dim3((b.W + 31) / 32, (b.H + 31) / 32, n), dim3(32, 8), 0, L.st>>>(b);
+    // wide windows: groups of 8 lanes x 4 quads (<= 128 levels, 4 pixels per
+    // warp) or 16 lanes x 4 quads (<= 256 levels)
     if ((b.d_max + 3) / 4 <= 32) {
-        cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(sweep_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(plan.total));
-        sweep_kernel<1><<<grid, kSweepThreads, plan.total, L.st>>>(b, sp);
+        sweep_kernel<8, 4><<<grid, kSweepThreads, plan.total, L.st>>>(b, sp);
     } else {
-        cudaFuncSetAttribute(sweep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(sweep_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(plan.total));
-        sweep_kernel<2><<<grid, kSweepThreads, plan.total, L.st>>>(b, sp);
+        sweep_kernel<16, 4><<<grid, kSweepThreads, plan.total, L.st>>>(b, sp);
     }
     const size_t csmem = sizeof(uint32_t) * (2 * b.W + 1) + sizeof(uint16_t) * b.W;
     sweep_combine_kernel<<<dim3(b.H, n), 512, csmem, L.st>>>(b, sp.roles);
