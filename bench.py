@@ -45,13 +45,6 @@ def rank_info():
     return rank, world, local
 
 
-def shard(n_items: int, world: int, rank: int) -> range:
-    """Contiguous shard of n_items over world ranks (first ranks take the remainder)."""
-    base, rem = divmod(n_items, world)
-    start = rank * base + min(rank, rem)
-    return range(start, start + base + (1 if rank < rem else 0))
-
-
 def scene_cfg(seed: int, frames: int = N_FRAMES):
     from paper_1809_07986_b200.scene import SceneConfig
     return SceneConfig.baseline_config(2, seed=seed, n_movers=seed % 5, frames=frames)
@@ -136,6 +129,7 @@ def run_ours(args):
 
     from paper_1809_07986_b200 import tsgm
     from paper_1809_07986_b200.scene import render
+    from paper_1809_07986_b200.sharding import RankStats, gather_stats, job_throughput, shard
 
     rank, world, local = rank_info()
     dist = None
@@ -182,10 +176,10 @@ def run_ours(args):
             eng.step_device(slots, lptr[k], rptr[k], motions[:, k, :])
 
     # pinned output buffers for the e2e leg (export map + posterior variance + mask)
-    out_ed = np.empty((n, H_, W_), np.int32)
-    out_ev = np.empty((n, H_, W_), np.uint8)
-    out_p = np.empty((n, H_, W_), np.float64)
-    out_mask = np.empty((n, H_, W_), np.uint8)
+    out_ed = torch.empty((n, H_, W_), dtype=torch.int32).pin_memory().numpy()
+    out_ev = torch.empty((n, H_, W_), dtype=torch.uint8).pin_memory().numpy()
+    out_p = torch.empty((n, H_, W_), dtype=torch.float64).pin_memory().numpy()
+    out_mask = torch.empty((n, H_, W_), dtype=torch.uint8).pin_memory().numpy()
     host_l_np = host_l.numpy()
     host_r_np = host_r.numpy()
 
@@ -196,11 +190,11 @@ def run_ours(args):
             eng.step(slots, [host_l_np[i, k] for i in range(n)],
                      [host_r_np[i, k] for i in range(n)],
                      [(motions[i, k, :9].reshape(3, 3), motions[i, k, 9:]) for i in range(n)])
-            for i in range(n):
-                eng.fetch(i, "export_d", out_ed[i])
-                eng.fetch(i, "export_valid", out_ev[i])
-                eng.fetch(i, "state_p", out_p[i])
-                eng.fetch(i, "mask", out_mask[i])
+            eng.fetch_batch(slots, "export_d", [out_ed[i] for i in range(n)])
+            eng.fetch_batch(slots, "export_valid", [out_ev[i] for i in range(n)])
+            eng.fetch_batch(slots, "state_p", [out_p[i] for i in range(n)])
+            eng.fetch_batch(slots, "mask", [out_mask[i] for i in range(n)])
+        eng.sync()
     e2e_h2d = n * args.frames * 2 * P
     e2e_d2h = n * args.frames * P * (4 + 1 + 8 + 1)
 
@@ -249,8 +243,11 @@ def run_ours(args):
     for k in range(args.frames):
         eng.step_device(slots, lptr[k], rptr[k], motions[:, k, :])
         cells_step += sum(eng.cells(s) for s in slots)
-    cells_step = sum_over_ranks(cells_step)
-    frames_total = args.seqs * args.frames
+    stats = gather_stats(RankStats(rank, n, n * args.frames, cells_step, ms_per_step),
+                         device=f"cuda:{local}")
+    job = job_throughput(stats)
+    cells_step = job["cells"]
+    frames_total = job["frames"]
 
     # roofline of the dominant kernel (8-path C -> S aggregation), standalone,
     # on the last (reduced) frame's volumes of all slots

@@ -126,6 +126,11 @@ enum {
 };
 /* Copies output `what` of `slot` into host memory `dst` (bytes >= size). */
 int tsgm_fetch(tsgm_ctx* ctx, int32_t slot, int32_t what, void* dst, size_t bytes);
+/* Asynchronous batched fetch: enqueues the device-to-host copies of output
+ * `what` for n slots into dsts[i] (pinned host memory for true overlap) on the
+ * context stream and returns; tsgm_sync() completes them. Not for COST/AGG. */
+int tsgm_fetch_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t what,
+                     void* const* dsts, size_t bytes_each);
 /* Number of cost cells N of the slot's last step (sum of window lengths). */
 int tsgm_cells(tsgm_ctx* ctx, int32_t slot, uint64_t* n_cells);
 int tsgm_sync(tsgm_ctx* ctx);

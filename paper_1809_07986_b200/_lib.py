@@ -46,7 +46,7 @@ _lib = None
 # Every exported symbol of include/tsgm_b200.h (checked by the CPU tests).
 EXPORTS = [
     "tsgm_last_error", "tsgm_create", "tsgm_destroy", "tsgm_reset", "tsgm_set_state",
-    "tsgm_step", "tsgm_step_device", "tsgm_fetch", "tsgm_cells", "tsgm_sync",
+    "tsgm_step", "tsgm_step_device", "tsgm_fetch", "tsgm_fetch_batch", "tsgm_cells", "tsgm_sync",
     "tsgm_timer_begin", "tsgm_timer_end", "tsgm_bench_aggregate", "tsgm_launch_count",
     "tsgm_census_transform", "tsgm_build_cost_volume", "tsgm_aggregate_paths",
     "tsgm_winner_takes_all", "tsgm_median_refine", "tsgm_sgm_match", "tsgm_relative_motion",
@@ -77,6 +77,8 @@ def load():
             getattr(lib, name).argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p]
         lib.tsgm_fetch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t]
+        lib.tsgm_fetch_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                         C.c_size_t]
         lib.tsgm_cells.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64)]
         lib.tsgm_sync.argtypes = [C.c_void_p]
         lib.tsgm_timer_begin.argtypes = [C.c_void_p]

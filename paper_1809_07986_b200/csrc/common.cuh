@@ -45,15 +45,12 @@ struct Bufs {
     const uint8_t* const* right;
     uint8_t* cost;   // 16 bytes of padding before slot 0 and after the last slot
     uint16_t* agg;
-    // line-sweep aggregation partials in the quad layout (qoff), per role:
-    // A/B (column sweeps, 3 directions) u16, C/D (row sweeps, 1 direction) u8
-    uint16_t *pA, *pB;
-    uint8_t *pC, *pD;
+    // scanline-group aggregation: per-direction path costs (u8) in the quad
+    // layout (qoff), [dir][slot][quad_cap][4]
+    uint8_t* pdir;
     size_t quad_cap;  // quads per slot
-    int* work;        // persistent-CTA work counter
-    // column-major (line-major for the column sweeps) window metadata:
-    // [slot][x*H + y] = lo | hi << 16, cell offset, quad offset
-    uint32_t *mt_lohi, *mt_cell, *mt_qoff;
+    int max_slots;
+    int* work;
     // WTA, render, export (A15, A18, A19)
     int32_t *md, *rd, *ed;
     uint8_t *mv, *rv, *ev;

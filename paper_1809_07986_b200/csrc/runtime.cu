@@ -299,15 +299,8 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     ctx->use_sweep = !force_scan &&
                      sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2);
     b.quad_cap = P * static_cast<size_t>((ctx->d_max - 1) / 4 + 1);
-    if (ctx->use_sweep) {
-        b.pA = ctx->dalloc<uint16_t>(S * b.quad_cap * 4);
-        b.pB = ctx->dalloc<uint16_t>(S * b.quad_cap * 4);
-        b.pC = ctx->dalloc<uint8_t>(S * b.quad_cap * 4);
-        b.pD = ctx->dalloc<uint8_t>(S * b.quad_cap * 4);
-        b.mt_lohi = ctx->dalloc<uint32_t>(S * P);
-        b.mt_cell = ctx->dalloc<uint32_t>(S * P);
-        b.mt_qoff = ctx->dalloc<uint32_t>(S * P);
-    }
+    b.max_slots = c.max_slots;
+    if (ctx->use_sweep) b.pdir = ctx->dalloc<uint8_t>(8 * S * b.quad_cap * 4);
     b.work = ctx->dalloc<int>(1);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device));
     b.md = ctx->dalloc<int32_t>(S * P);
@@ -591,6 +584,22 @@ int tsgm_fetch(tsgm_ctx* ctx, int32_t slot, int32_t what, void* dst, size_t byte
         const char* src = static_cast<const char*>(o.base) + static_cast<size_t>(slot) * o.stride * o.elem;
         CK(cudaMemcpyAsync(dst, src, count * o.elem, cudaMemcpyDeviceToHost, ctx->st));
         sync(ctx);
+    });
+}
+
+int tsgm_fetch_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t what,
+                     void* const* dsts, size_t bytes_each) {
+    return guarded([&] {
+        if (what == TSGM_OUT_COST || what == TSGM_OUT_AGG) bad("tsgm_fetch_batch: volumes need tsgm_fetch");
+        CK(cudaSetDevice(ctx->device));
+        const OutDesc o = out_desc(ctx, what);
+        if (bytes_each < o.stride * o.elem) bad("tsgm_fetch_batch: destination too small");
+        for (int i = 0; i < n; ++i) {
+            if (slots[i] < 0 || slots[i] >= ctx->max_slots) bad("tsgm_fetch_batch: slot out of range");
+            const char* src = static_cast<const char*>(o.base) +
+                              static_cast<size_t>(slots[i]) * o.stride * o.elem;
+            CK(cudaMemcpyAsync(dsts[i], src, o.stride * o.elem, cudaMemcpyDeviceToHost, ctx->st));
+        }
     });
 }
 

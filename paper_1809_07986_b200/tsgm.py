@@ -390,6 +390,14 @@ class Engine:
         check(self._lib.tsgm_fetch(self._h, slot, OUT[what], ptr(out), out.nbytes))
         return out
 
+    def fetch_batch(self, slots, what: str, outs):
+        """Asynchronously copy output ``what`` of ``slots`` into ``outs`` (pinned
+        host arrays for overlap); completes at the next :meth:`sync`."""
+        n = len(slots)
+        sl = np.asarray(slots, np.int32)
+        dp = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
+        check(self._lib.tsgm_fetch_batch(self._h, n, ptr(sl), OUT[what], dp, outs[0].nbytes))
+
     def sync(self):
         check(self._lib.tsgm_sync(self._h))
 
