@@ -120,13 +120,15 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
             CA[t] = prmt(cq, 0u, 0x4140u);
             CB[t] = prmt(cq, 0u, 0x4342u);
             act[t] = pix && k0 + t < nq;
-            const int d0 = 4 * (a0 + t);
-            const uint32_t bad0 = (d0 < lo) ? 0x0000ffffu : 0u;
-            const uint32_t bad1 = (d0 + 1 < lo || d0 + 1 > hi) ? 0xffff0000u : 0u;
-            const uint32_t bad2 = (d0 + 2 < lo || d0 + 2 > hi) ? 0x0000ffffu : 0u;
-            const uint32_t bad3 = (d0 + 3 > hi) ? 0xffff0000u : 0u;
-            ivA[t] = act[t] ? (bad0 | bad1) : 0xffffffffu;
-            ivB[t] = act[t] ? (bad2 | bad3) : 0xffffffffu;
+            // levels of the quad outside [lo, hi]: the low levels of the first
+            // window quad and the high levels of the last one
+            const int qa = a0 + t;
+            const int nlo = qa == q0 ? (lo & 3) : 0;
+            const int nhi = qa == q1 ? 3 - (hi & 3) : 0;
+            const unsigned long long valid =
+                act[t] ? ((~0ull << (16 * nlo)) & (~0ull >> (16 * nhi))) : 0ull;
+            ivA[t] = ~static_cast<uint32_t>(valid);
+            ivB[t] = ~static_cast<uint32_t>(valid >> 32);
         }
     }
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
@@ -223,18 +225,27 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         m.qo = __ldg(qoff + p);
     };
 
-    int p_nxt = 0;
-    bool act_nxt = pixel_at(0, p_nxt);
-    PixMeta m_nxt{0u, 0u, 0u};
-    if (act_nxt) load_meta(p_nxt, m_nxt);
+    // metadata two steps ahead, costs of the next step prefetched into L1
+    int p_tmp = 0;
+    bool act1 = pixel_at(0, p_tmp);
+    PixMeta m1{0u, 0u, 0u};
+    if (act1) load_meta(p_tmp, m1);
+    bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
+    PixMeta m2{0u, 0u, 0u};
+    if (act2) load_meta(p_tmp, m2);
     for (int k = 0; k < nsteps; ++k) {
-        const bool active = act_nxt;
-        const PixMeta mc = m_nxt;
-        // next step's metadata in flight while this step computes
-        if (k + 1 < nsteps) {
-            act_nxt = pixel_at(k + 1, p_nxt);
-            if (act_nxt) load_meta(p_nxt, m_nxt);
+        const bool active = act1;
+        const PixMeta mc = m1;
+        act1 = act2;
+        m1 = m2;
+        if (act1) {  // step k+1's window towards L1 (its metadata arrived a step ago)
+            const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
+            const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
+            const uint8_t* c0 = cost + m1.cell;
+            for (int o = 0; o < n_n + 4; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + o));
         }
+        act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
+        if (act2) load_meta(p_tmp, m2);
         if (__ballot_sync(0xffffffffu, active) == 0u) {
             prev_active = false;
             continue;
@@ -248,7 +259,12 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         while (bw) {
             const int gi = lane >> 3;
             const int cntw = __popc(bw);
-            const int src = gi < cntw ? static_cast<int>(__fns(bw, 0, gi + 1)) : lane;
+            // lane of the gi-th remaining wide window
+            unsigned mk = bw;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                if (t < gi) mk &= mk - 1;
+            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
             PixMeta pw;
             pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
             pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
