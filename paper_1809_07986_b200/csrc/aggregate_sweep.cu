@@ -125,10 +125,10 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
             const int qa = a0 + t;
             const int nlo = qa == q0 ? (lo & 3) : 0;
             const int nhi = qa == q1 ? 3 - (hi & 3) : 0;
-            const unsigned long long valid =
-                act[t] ? ((~0ull << (16 * nlo)) & (~0ull >> (16 * nhi))) : 0ull;
-            ivA[t] = ~static_cast<uint32_t>(valid);
-            ivB[t] = ~static_cast<uint32_t>(valid >> 32);
+            // valid levels of the quad as a nibble, expanded to u16 lanes
+            const uint32_t v = act[t] ? ((0xfu << nlo) & (0xfu >> nhi)) : 0u;
+            ivA[t] = ~((v & 1u) * 0x0000ffffu + ((v >> 1) & 1u) * 0xffff0000u);
+            ivB[t] = ~(((v >> 2) & 1u) * 0x0000ffffu + ((v >> 3) & 1u) * 0xffff0000u);
         }
     }
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
@@ -192,8 +192,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
 
-    const uint16_t* lo = b.lo + static_cast<size_t>(s) * b.P;
-    const uint16_t* hi = b.hi + static_cast<size_t>(s) * b.P;
+    const uint32_t* lohi = b.lohi + static_cast<size_t>(s) * b.P;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
     const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1);
     const uint8_t* cost = b.cost + static_cast<size_t>(s) * b.vol_cap;
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         return x >= 0 && x < W;
     };
     auto load_meta = [&](int p, PixMeta& m) {
-        m.lohi = static_cast<uint32_t>(__ldg(lo + p)) | (static_cast<uint32_t>(__ldg(hi + p)) << 16);
+        m.lohi = __ldg(lohi + p);
         m.cell = __ldg(off + p);
         m.qo = __ldg(qoff + p);
     };
@@ -281,40 +280,49 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
 }
 
 // S = sum of the per-direction path costs, written in the reference's ragged
-// layout. One CTA per (row, slot); threads over the row's cells (coalesced
-// S stores).
+// layout. One CTA per (row, slot); one thread per QUAD of the row's quad
+// layout: 8 coalesced u32 loads (4 u8 path costs each), u16x2 sums, and the
+// valid levels stored as u16 at their ragged cell positions.
 __global__ void sweep_combine_kernel(Bufs b, int ndir) {
     extern __shared__ uint32_t sm[];
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x, W = b.W;
-    uint32_t* o = sm;              // W+1 in-row cell offsets
-    uint32_t* qo = o + W + 1;      // W quad offsets
-    uint16_t* lo = reinterpret_cast<uint16_t*>(qo + W);
+    uint32_t* qo = sm;               // W+1 in-row quad offsets (relative)
+    uint32_t* cl = qo + W + 1;       // W cell offsets (absolute, per slot)
+    uint32_t* lh = cl + W;           // W lo | hi << 16
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
-    const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
-    const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
-    const uint32_t row0 = off[0];
+    const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
+    const uint32_t q_row0 = b.qoff[obase];
     for (int x = threadIdx.x; x < W; x += blockDim.x) {
-        o[x] = off[x] - row0;
-        qo[x] = qoff[x];
-        lo[x] = b.lo[pbase + x];
+        qo[x] = b.qoff[obase + x] - q_row0;
+        cl[x] = b.off[obase + x];
+        lh[x] = b.lohi[pbase + x];
     }
-    if (threadIdx.x == 0) o[W] = off[W] - row0;
+    if (threadIdx.x == 0) qo[W] = b.qoff[obase + W] - q_row0;
     __syncthreads();
-    const uint32_t n = o[W];
-    const size_t dstride = static_cast<size_t>(b.max_slots) * b.quad_cap * 4;
-    const uint8_t* pd = b.pdir + static_cast<size_t>(s) * b.quad_cap * 4;
-    uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap + row0;
-    for (uint32_t cc = threadIdx.x; cc < n; cc += blockDim.x) {
-        int l = 0, r = W;
+    const uint32_t nq = qo[W];
+    const size_t dstride = static_cast<size_t>(b.max_slots) * b.quad_cap;  // in u32 quads
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) +
+                         static_cast<size_t>(s) * b.quad_cap + q_row0;
+    uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap;
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        int l = 0, r = W;  // pixel of quad q
         while (r - l > 1) {
             const int m = (l + r) >> 1;
-            if (o[m] <= cc) l = m; else r = m;
+            if (qo[m] <= q) l = m; else r = m;
         }
-        const int lv = lo[l] + static_cast<int>(cc - o[l]);
-        const size_t e = 4 * (static_cast<size_t>(qo[l]) + (lv >> 2) - (lo[l] >> 2)) + (lv & 3);
-        uint32_t v = 0;
-        for (int d = 0; d < ndir; ++d) v += pd[d * dstride + e];
-        agg[cc] = static_cast<uint16_t>(v);
+        uint32_t sa = 0u, sb = 0u;
+        for (int d = 0; d < ndir; ++d) {
+            const uint32_t w = __ldg(pd + d * dstride + q);
+            sa = __vadd2(sa, __byte_perm(w, 0u, 0x4140u));
+            sb = __vadd2(sb, __byte_perm(w, 0u, 0x4342u));
+        }
+        const int lo = static_cast<int>(lh[l] & 0xffffu), hi = static_cast<int>(lh[l] >> 16);
+        const int d0 = 4 * ((lo >> 2) + static_cast<int>(q - qo[l]));
+        uint16_t* dst = agg + cl[l] + (d0 - lo);
+        const uint32_t v[4] = {sa & 0xffffu, sa >> 16, sb & 0xffffu, sb >> 16};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (d0 + t >= lo && d0 + t <= hi) dst[t] = static_cast<uint16_t>(v[t]);
     }
 }
 
@@ -342,7 +350,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int tasks = sp.task_off[k] * n;
     const size_t smem = static_cast<size_t>(kScanWarps) * 32 * (scan_slot_bytes(b.d_max) + 4);
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
-    const size_t csmem = sizeof(uint32_t) * (2 * b.W + 1) + sizeof(uint16_t) * b.W;
+    const size_t csmem = sizeof(uint32_t) * (3 * b.W + 1);
     sweep_combine_kernel<<<dim3(b.H, n), 512, csmem, L.st>>>(b, k);
     *L.counter += 2;
 }

@@ -32,6 +32,7 @@ struct Bufs {
     uint8_t* pv;
     // ranges + prefix sums (A10, A11)
     uint16_t *lo, *hi;
+    uint32_t* lohi;      // [slot][P] lo | hi << 16 (packed copy for the aggregation)
     uint32_t* off;       // [slot][P+1]
     uint32_t* row_sum;   // [slot][H]
     uint32_t* qoff;      // [slot][P+1] quad-aligned offsets (aggregation partials)

@@ -281,6 +281,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.pv = ctx->dalloc<uint8_t>(S * P);
     b.lo = ctx->dalloc<uint16_t>(S * P);
     b.hi = ctx->dalloc<uint16_t>(S * P);
+    b.lohi = ctx->dalloc<uint32_t>(S * P);
     b.off = ctx->dalloc<uint32_t>(S * (P + 1));
     b.row_sum = ctx->dalloc<uint32_t>(S * ctx->H);
     b.qoff = ctx->dalloc<uint32_t>(S * (P + 1));

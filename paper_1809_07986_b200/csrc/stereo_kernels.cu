@@ -148,6 +148,7 @@ __global__ void ranges_kernel(Bufs b, int min_hw, int use_stddev, double gain) {
         off[x] = run;  // in-row exclusive; rebased by offsets_finalize
         qoff[x] = qrun;
         const int lo = b.lo[base + x], hi = b.hi[base + x];
+        b.lohi[base + x] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
         run += static_cast<uint32_t>(hi - lo + 1);
         qrun += quads_of(lo, hi);
     }
@@ -229,9 +230,10 @@ void launch_offsets(const Bufs& b, int n, Launch L) {
 
 // ---------------------------------------------------------------- cost (A13)
 // build_cost_volume, matching_cost.cpp:88-117. One CTA per (row, slot); the
-// row's signatures, lo and in-row offsets are staged in shared memory and every
-// thread writes consecutive cells (coalesced), locating its pixel by binary
-// search over the in-row offsets.
+// row's signatures, lo and in-row offsets are staged in shared memory. Each
+// thread produces one ALIGNED group of 4 cells of the ragged volume (one
+// binary search for its first cell, then a walk), stored as one u32; the two
+// groups a row shares with its neighbours are stored byte by byte.
 __global__ void cost_kernel(Bufs b) {
     extern __shared__ uint32_t sm[];
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
@@ -252,19 +254,48 @@ __global__ void cost_kernel(Bufs b) {
     if (threadIdx.x == 0) o[W] = off[W] - row0;  // next row's first offset (or total)
     __syncthreads();
     const uint32_t n = o[W];
-    uint8_t* out = b.cost + static_cast<size_t>(s) * b.vol_cap + row0;
+    if (n == 0) return;
+    uint8_t* base = b.cost + static_cast<size_t>(s) * b.vol_cap;
+    const uintptr_t abs0 = reinterpret_cast<uintptr_t>(base) + row0;  // address of cell 0
+    const uintptr_t g0 = abs0 & ~static_cast<uintptr_t>(3);
+    const uint32_t ngroups = static_cast<uint32_t>(((abs0 + n + 3) & ~static_cast<uintptr_t>(3)) - g0) / 4;
+    const int lead = static_cast<int>(abs0 - g0);  // cells of group 0 before this row
     const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
-    for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
-        int l = 0, r = W;  // largest x with o[x] <= c
+    for (uint32_t gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+        const int c0 = static_cast<int>(4 * gi) - lead;  // relative cell of byte 0
+        const int cf = max(c0, 0);
+        int l = 0, r = W;  // pixel of the first valid cell
         while (r - l > 1) {
             const int m = (l + r) >> 1;
-            if (o[m] <= c) l = m; else r = m;
+            if (static_cast<int>(o[m]) <= cf) l = m; else r = m;
         }
-        const int x = l;
-        const int xr = x - (static_cast<int>(lo[x]) + static_cast<int>(c - o[x]));
-        const bool ok = row_def && x >= kCensusRadius && x < W - kCensusRadius &&
-                        xr >= kCensusRadius && xr < W - kCensusRadius;
-        out[c] = ok ? static_cast<uint8_t>(__popc(sl[x] ^ sr[xr])) : static_cast<uint8_t>(kMaxCost);
+        int x = l;
+        uint32_t word = 0u;
+        bool full = true;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int c = c0 + t;
+            if (c < 0 || c >= static_cast<int>(n)) {
+                full = false;
+                continue;
+            }
+            while (x + 1 < W && static_cast<int>(o[x + 1]) <= c) ++x;
+            const int xr = x - (static_cast<int>(lo[x]) + (c - static_cast<int>(o[x])));
+            const bool ok = row_def && x >= kCensusRadius && x < W - kCensusRadius &&
+                            xr >= kCensusRadius && xr < W - kCensusRadius;
+            const uint32_t cv = ok ? static_cast<uint32_t>(__popc(sl[x] ^ sr[xr])) : kMaxCost;
+            word |= cv << (8 * t);
+        }
+        uint8_t* gptr = reinterpret_cast<uint8_t*>(g0 + 4 * static_cast<uintptr_t>(gi));
+        if (full) {
+            *reinterpret_cast<uint32_t*>(gptr) = word;
+        } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int c = c0 + t;
+                if (c >= 0 && c < static_cast<int>(n)) gptr[t] = static_cast<uint8_t>(word >> (8 * t));
+            }
+        }
     }
 }
 
