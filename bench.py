@@ -164,7 +164,8 @@ def run_ours(args):
     dev_r = host_r.to(f"cuda:{local}")
     torch.cuda.synchronize()
 
-    eng = tsgm.Engine(tsgm.EngineConfig(calib, sgm, filt, max_slots=n, device=local))
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, sgm, filt, max_slots=n, device=local,
+                                        keep_volumes=False))
     slots = list(range(n))
     lptr = [[dev_l[i, k].data_ptr() for i in range(n)] for k in range(args.frames)]
     rptr = [[dev_r[i, k].data_ptr() for i in range(n)] for k in range(args.frames)]

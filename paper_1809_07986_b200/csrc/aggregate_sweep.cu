@@ -97,7 +97,7 @@ template <int G, int Q>
 __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has_pred,
                                            uint32_t sb, uint32_t rp, const uint8_t* cost,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
-                                           uint32_t P2x4) {
+                                           uint32_t P2x4, const uint8_t* mask_tab) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
@@ -114,21 +114,24 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         uint32_t c[Q + 1];
 #pragma unroll
         for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
+        // invalid-level masks of the lane's 16 levels from the table:
+        // row = levels below lo in the first quad, col = last valid level + 1
+        const int start = 4 * (q0 + k0);  // unclamped first level of the lane
+        const int lrel = k0 == 0 ? (lo & 3) : 0;
+        const int hrel = pix ? min(max(hi - start, -1), 16) : -1;
+        const uint4* row = reinterpret_cast<const uint4*>(
+            mask_tab + 32u * static_cast<uint32_t>(lrel * 18 + hrel + 1));
+        const uint4 m0 = row[0], m1 = row[1];
+        ivA[0] = m0.x; ivB[0] = m0.y;
+        if (Q > 1) { ivA[1] = m0.z; ivB[1] = m0.w; }
+        if (Q > 2) { ivA[2] = m1.x; ivB[2] = m1.y; }
+        if (Q > 3) { ivA[3] = m1.z; ivB[3] = m1.w; }
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
             CA[t] = prmt(cq, 0u, 0x4140u);
             CB[t] = prmt(cq, 0u, 0x4342u);
             act[t] = pix && k0 + t < nq;
-            // levels of the quad outside [lo, hi]: the low levels of the first
-            // window quad and the high levels of the last one
-            const int qa = a0 + t;
-            const int nlo = qa == q0 ? (lo & 3) : 0;
-            const int nhi = qa == q1 ? 3 - (hi & 3) : 0;
-            // valid levels of the quad as a nibble, expanded to u16 lanes
-            const uint32_t v = act[t] ? ((0xfu << nlo) & (0xfu >> nhi)) : 0u;
-            ivA[t] = ~((v & 1u) * 0x0000ffffu + ((v >> 1) & 1u) * 0xffff0000u);
-            ivB[t] = ~(((v >> 2) & 1u) * 0x0000ffffu + ((v >> 3) & 1u) * 0xffff0000u);
         }
     }
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
@@ -171,6 +174,21 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
 
 __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
+    // invalid-level masks: entry (lrel, hrel) covers 16 levels = 4 quads x
+    // (ivA, ivB); level j is invalid iff j < lrel or j > hrel (hrel in -1..16)
+    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+    for (int e = threadIdx.x; e < 4 * 18 * 8; e += blockDim.x) {
+        const int lrel = e / (18 * 8), hrel = (e / 8) % 18 - 1, word = e % 8;
+        const int t = word >> 1, half0 = 4 * t + 2 * (word & 1);
+        uint32_t m = 0u;
+        for (int h = 0; h < 2; ++h) {
+            const int j = half0 + h;
+            if (j < lrel || j > hrel) m |= 0xffffu << (16 * h);
+        }
+        mask_tab_s[e] = m;
+    }
+    __syncthreads();
+    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
     const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
     const int task = blockIdx.x * kScanWarps + warp;
     const int per_slot = sp.task_off[sp.ndir];
@@ -252,7 +270,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         const int nq = static_cast<int>(mc.lohi >> 18) - static_cast<int>((mc.lohi & 0xffffu) >> 2) + 1;
         const bool narrow = active && nq <= 4;
         // windows of <= 4 quads: the lane itself
-        scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4);
+        scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                         mask_tab);
         // wider windows: 8 lanes x 4 quads, 4 windows per pass
         unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
         while (bw) {
@@ -270,7 +289,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
             pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
             const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
             scan_pixel<8, 4>(gi < cntw, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
-                             rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2, P2x4);
+                             rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2, P2x4,
+                             mask_tab);
 #pragma unroll
             for (int t = 0; t < 4; ++t)
                 if (bw) bw &= bw - 1;
@@ -326,9 +346,102 @@ __global__ void sweep_combine_kernel(Bufs b, int ndir) {
     }
 }
 
+// Fused combine + winner_takes_all (sgm.cpp:163-187) for the production step:
+// S of each pixel is summed from the per-direction path costs in registers and
+// reduced to its first argmin; S is written to the ragged volume only when
+// requested (kept volumes / standalone C->S). One CTA per (row, slot); a lane
+// per window of <= 4 quads, 8 lanes x 4 quads per wider window.
+template <int G>
+__device__ __forceinline__ void wta_pixel(bool pix, int x, int y, const PixMeta& pm, int ndir,
+                                          const uint32_t* pd, size_t dstride, uint16_t* agg,
+                                          int32_t* md, uint8_t* mv, int W, int H, bool write_s,
+                                          bool do_wta) {
+    constexpr int Q = 4;
+    const int lg = static_cast<int>(threadIdx.x & (G - 1));
+    const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
+    const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
+    const int k0 = lg * Q;
+    uint32_t sA[Q], sB[Q];
+    uint32_t best = 0xffffffffu;  // (S << 16) | level
+#pragma unroll
+    for (int t = 0; t < Q; ++t) {
+        sA[t] = sB[t] = 0u;
+        const int k = k0 + t;
+        if (!(pix && k < nq)) continue;
+        for (int d = 0; d < ndir; ++d) {
+            const uint32_t w = __ldg(pd + d * dstride + pm.qo + k);
+            sA[t] = __vadd2(sA[t], __byte_perm(w, 0u, 0x4140u));
+            sB[t] = __vadd2(sB[t], __byte_perm(w, 0u, 0x4342u));
+        }
+        const int d0 = 4 * (q0 + k);
+        const uint32_t v[4] = {sA[t] & 0xffffu, sA[t] >> 16, sB[t] & 0xffffu, sB[t] >> 16};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int lv = d0 + u;
+            if (lv < lo || lv > hi) continue;
+            if (write_s) agg[pm.cell + (lv - lo)] = static_cast<uint16_t>(v[u]);
+            best = min(best, (v[u] << 16) | static_cast<uint32_t>(lv));
+        }
+    }
+    if (G > 1) {
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    }
+    if (do_wta && pix && lg == 0) {
+        const bool def = x >= kCensusRadius && x < W - kCensusRadius && y >= kCensusRadius &&
+                         y < H - kCensusRadius;
+        md[0] = def ? static_cast<int32_t>(best & 0xffffu) : 0;
+        mv[0] = def ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) combine_wta_kernel(Bufs b, int ndir, int write_s,
+                                                          int do_wta) {
+    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x, W = b.W;
+    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+    const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
+    const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
+    const size_t dstride = static_cast<size_t>(b.max_slots) * b.quad_cap;
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) + static_cast<size_t>(s) * b.quad_cap;
+    uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap;
+    for (int x0 = warp * 32; x0 < W; x0 += 32 * (blockDim.x >> 5)) {
+        const int x = x0 + lane;
+        const bool active = x < W;
+        PixMeta m{0u, 0u, 0u};
+        if (active) {
+            m.lohi = b.lohi[pbase + x];
+            m.cell = b.off[obase + x];
+            m.qo = b.qoff[obase + x];
+        }
+        const int nq = static_cast<int>(m.lohi >> 18) - static_cast<int>((m.lohi & 0xffffu) >> 2) + 1;
+        const bool narrow = active && nq <= 4;
+        wta_pixel<1>(narrow, x, y, m, ndir, pd, dstride, agg, b.md + pbase + x, b.mv + pbase + x,
+                     W, b.H, write_s, do_wta);
+        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
+        while (bw) {
+            const int gi = lane >> 3;
+            const int cntw = __popc(bw);
+            unsigned mk = bw;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                if (t < gi) mk &= mk - 1;
+            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
+            PixMeta pw;
+            pw.lohi = __shfl_sync(0xffffffffu, m.lohi, src);
+            pw.cell = __shfl_sync(0xffffffffu, m.cell, src);
+            pw.qo = __shfl_sync(0xffffffffu, m.qo, src);
+            const int xw = x0 + src;
+            wta_pixel<8>(gi < cntw, xw, y, pw, ndir, pd, dstride, agg, b.md + pbase + xw,
+                         b.mv + pbase + xw, W, b.H, write_s, do_wta);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (bw) bw &= bw - 1;
+        }
+    }
+}
+
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
-                            int num_sms, Launch L) {
-    (void)num_sms;
+                            int write_s, int do_wta, Launch L) {
     ScanParams sp{};
     sp.p1 = p1;
     sp.p2 = p2;
@@ -350,8 +463,12 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int tasks = sp.task_off[k] * n;
     const size_t smem = static_cast<size_t>(kScanWarps) * 32 * (scan_slot_bytes(b.d_max) + 4);
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
-    const size_t csmem = sizeof(uint32_t) * (3 * b.W + 1);
-    sweep_combine_kernel<<<dim3(b.H, n), 512, csmem, L.st>>>(b, k);
+    if (do_wta) {
+        combine_wta_kernel<<<dim3(b.H, n), 256, 0, L.st>>>(b, k, write_s, 1);
+    } else {
+        const size_t csmem = sizeof(uint32_t) * (3 * b.W + 1);
+        sweep_combine_kernel<<<dim3(b.H, n), 512, csmem, L.st>>>(b, k);
+    }
     *L.counter += 2;
 }
 

@@ -132,7 +132,9 @@ void launch_aggregate(const Bufs& b, int n, int p1, int p2, int paths, int path_
 // Line-sweep aggregation (aggregate_sweep.cu): returns false when the
 // configuration does not fit its shared-memory plan (caller falls back).
 bool sweep_supported(int W, int H, int d_max, int p2);
+// write_s: store S in the ragged volume; do_wta: fuse winner_takes_all
+// (writes md/mv). At least one of the two must be set.
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
-                            int num_sms, Launch L);
+                            int write_s, int do_wta, Launch L);
 
 }  // namespace tsgm

@@ -368,15 +368,19 @@ void check_slots(tsgm_ctx* ctx, int n, const int32_t* slots) {
     }
 }
 
-// aggregate_paths for the active slots: the line-sweep kernels when the
-// configuration fits their shared-memory plan, else the scanline kernels.
-void aggregate(tsgm_ctx* ctx, int n, Launch L) {
+// aggregate_paths for the active slots: the scanline-group kernel when the
+// configuration fits it, else the per-direction scanline kernels. With
+// fuse_wta, winner_takes_all is fused into the combine (S is then written
+// only if keep_s) and the caller skips launch_wta.
+bool aggregate(tsgm_ctx* ctx, int n, Launch L, bool fuse_wta = false, bool keep_s = true) {
     const tsgm_config& c = ctx->cfg;
-    if (ctx->use_sweep && sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2))
+    if (ctx->use_sweep && sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2)) {
         launch_aggregate_sweep(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
-                               ctx->num_sms, L);
-    else
-        launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+                               (keep_s || !fuse_wta) ? 1 : 0, fuse_wta ? 1 : 0, L);
+        return fuse_wta;
+    }
+    launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+    return false;
 }
 
 // The per-frame pipeline of step() (temporal_filter.cpp:195-232) for n slots.
@@ -395,8 +399,8 @@ void run_step(tsgm_ctx* ctx, int n) {
     // sgm_match (A12-A15)
     launch_census(b, n, L);
     launch_cost(b, n, L);
-    aggregate(ctx, n, L);
-    launch_wta(b, n, L);
+    if (!aggregate(ctx, n, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0))
+        launch_wta(b, n, L);
     // correct + diff + mask + render, then the export median (A16-A19, A21)
     launch_correct(b, n, c.filter.r, c.mask_tau, L);
     launch_median(b, n, b.rd, b.rv, b.ed, b.ev, L);
