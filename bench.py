@@ -273,7 +273,7 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_reference_sample(args, budget_s=args.cpu_budget)
-        traffic = load_traffic()
+        traffic = load_traffic(agg_cells)
         result = {
             "metric": "frames/sec (batched tsgm step, 1242x375, D=128, 8 paths)",
             "value": round(value, 2),
@@ -318,12 +318,14 @@ def run_ours(args):
     return result
 
 
-def load_traffic():
-    """dram bytes per launch of the aggregation from the committed ncu summary."""
+def load_traffic(cells: float):
+    """DRAM bytes of the aggregation launch, from the committed ncu capture
+    (profiles/traffic.json: measured bytes per cell x this launch's cells)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get("aggregate_dram_bytes_per_launch")
+            t = json.load(f)
+        return int(t["bytes_per_cell"] * cells)
     except Exception:
         return None
 
@@ -346,7 +348,7 @@ def cpu_reference_sample(args, budget_s: float = 20.0, threads: int | None = Non
     from paper_1809_07986_b200 import tsgm
     calib, sgm, filt = params()
     threads = threads or os.cpu_count() or 1
-    n_red = max(1, min(4, int(args.cpu_frames)))
+    n_red = max(1, min(12, int(args.cpu_frames)))
     seqs = []
     for s in range(threads):
         cfg = scene_cfg(s, N_FRAMES)
@@ -420,7 +422,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seqs", type=int, default=N_SEQ)
     ap.add_argument("--frames", type=int, default=N_FRAMES)
-    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--cpu-frames", type=int, default=6)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

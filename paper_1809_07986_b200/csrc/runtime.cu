@@ -203,6 +203,12 @@ struct tsgm_ctx {
     int ring_i = 0;
     uint8_t* d_img = nullptr;  // [max_slots][2][P] staging for host-image steps
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // output copies overlap the next frame: a copy stream that starts after
+    // the frame's kernels; the next frame waits for it only before the
+    // kernels that overwrite the outputs (correct, median)
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t ev_frame = nullptr, ev_copied = nullptr;
+    bool copy_pending = false;
 
     template <typename T>
     T* dalloc(size_t count) {
@@ -224,6 +230,10 @@ struct tsgm_ctx {
         }
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (copy_st) cudaStreamSynchronize(copy_st);
+        if (ev_frame) cudaEventDestroy(ev_frame);
+        if (ev_copied) cudaEventDestroy(ev_copied);
+        if (copy_st) cudaStreamDestroy(copy_st);
         if (st) cudaStreamDestroy(st);
     }
     Launch L() { return Launch{st, &launches}; }
@@ -257,6 +267,9 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     ctx->device = c.device;
     CK(cudaSetDevice(c.device));
     CK(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_frame, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_copied, cudaEventDisableTiming));
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
     const size_t S = c.max_slots, P = ctx->P;
@@ -402,9 +415,14 @@ void run_step(tsgm_ctx* ctx, int n) {
     if (!aggregate(ctx, n, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0))
         launch_wta(b, n, L);
     // correct + diff + mask + render, then the export median (A16-A19, A21)
+    if (ctx->copy_pending) {  // the previous frame's outputs are still being copied out
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_copied, 0));
+        ctx->copy_pending = false;
+    }
     launch_correct(b, n, c.filter.r, c.mask_tau, L);
     launch_median(b, n, b.rd, b.rv, b.ed, b.ev, L);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_frame, ctx->st));
 }
 
 void step_impl(tsgm_ctx* ctx, int n, const int32_t* slots, const uint8_t* const* dl,
@@ -488,6 +506,7 @@ void d2h(tsgm_ctx* ctx, T* dst, const T* src, size_t count) {
 void sync(tsgm_ctx* ctx) {
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->st));
+    if (ctx->copy_st) CK(cudaStreamSynchronize(ctx->copy_st));
 }
 
 // Host-side window bookkeeping for caller-provided ranges (make_cost_volume,
@@ -599,12 +618,17 @@ int tsgm_fetch_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t wha
         CK(cudaSetDevice(ctx->device));
         const OutDesc o = out_desc(ctx, what);
         if (bytes_each < o.stride * o.elem) bad("tsgm_fetch_batch: destination too small");
+        // after the last frame's kernels, on the copy engine
+        CK(cudaEventRecord(ctx->ev_frame, ctx->st));
+        CK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_frame, 0));
         for (int i = 0; i < n; ++i) {
             if (slots[i] < 0 || slots[i] >= ctx->max_slots) bad("tsgm_fetch_batch: slot out of range");
             const char* src = static_cast<const char*>(o.base) +
                               static_cast<size_t>(slots[i]) * o.stride * o.elem;
-            CK(cudaMemcpyAsync(dsts[i], src, o.stride * o.elem, cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaMemcpyAsync(dsts[i], src, o.stride * o.elem, cudaMemcpyDeviceToHost, ctx->copy_st));
         }
+        CK(cudaEventRecord(ctx->ev_copied, ctx->copy_st));
+        ctx->copy_pending = true;
     });
 }
 

@@ -88,3 +88,38 @@ def test_reset_restarts_full_range(port):
     np.testing.assert_array_equal(eng.fetch(0, "state_p"), ref["p"])
     assert (eng.fetch(0, "hi") == 31).all() and (eng.fetch(0, "lo") == 0).all()
     eng.close()
+
+
+def test_overlapped_fetch_captures_each_frame(port):
+    """fetch_batch copies run on the copy stream while the next frame computes;
+    every frame's copies must hold that frame's outputs."""
+    cfgs = [SceneConfig.baseline_config(1, width=256, height=96, focal=160.0, cx=127.5, cy=47.5,
+                                        d_max=48, seed=s, n_movers=2) for s in (3, 4)]
+    calib = tsgm.StereoCalib(160.0, 127.5, 47.5, cfgs[0].baseline, 256, 96, 48)
+    params, filt = tsgm.SgmParams(10, 120, 8, 0, 48), tsgm.FilterConfig(range_use_stddev=True,
+                                                                        range_stddev_gain=3.0)
+    seqs = [render(c, 0, 5) for c in cfgs]
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=2, keep_volumes=False))
+    got = []
+    for k in range(5):
+        mots = [(np.eye(3), np.zeros(3)) if k == 0 else tsgm.relative_motion(P[k - 1], P[k])
+                for (_, _, P, _) in seqs]
+        eng.step([0, 1], [s[0][k] for s in seqs], [s[1][k] for s in seqs], mots)
+        ed = [np.empty((96, 256), np.int32) for _ in range(2)]
+        pp = [np.empty((96, 256), np.float64) for _ in range(2)]
+        mk = [np.empty((96, 256), np.uint8) for _ in range(2)]
+        eng.fetch_batch([0, 1], "export_d", ed)
+        eng.fetch_batch([0, 1], "state_p", pp)
+        eng.fetch_batch([0, 1], "mask", mk)
+        got.append((ed, pp, mk))
+    eng.sync()
+    for i, (L, R, P, _) in enumerate(seqs):
+        state = None
+        for k in range(5):
+            m = (np.eye(3), np.zeros(3)) if k == 0 else tsgm.relative_motion(P[k - 1], P[k])
+            ref = port.step(state, L[k], R[k], m[0], m[1], calib, params, filt, debug=True)
+            np.testing.assert_array_equal(got[k][0][i], ref["export_d"])
+            np.testing.assert_array_equal(got[k][1][i], ref["p"])
+            np.testing.assert_array_equal(got[k][2][i], ref["mask"])
+            state = (ref["d"], ref["p"], ref["valid"])
+    eng.close()
