@@ -35,10 +35,10 @@ constexpr int kScanWarps = 4;  // warps per CTA (one task each)
 __host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
 
 bool sweep_supported(int W, int H, int d_max, int p2) {
-    // u8 path costs need 24 + P2 <= 255; a wide window is <= 8 lanes x 4 quads
+    // u8 path costs need 24 + P2 <= 255; a window is <= 16 lanes x 4 quads
     (void)W;
     (void)H;
-    return kMaxCost + p2 <= 255 && (d_max + 3) / 4 <= 32;
+    return kMaxCost + p2 <= 255 && (d_max + 3) / 4 <= 64;
 }
 
 struct ScanParams {
@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         // windows of <= 4 quads: the lane itself
         scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
                          mask_tab);
-        // wider windows: 8 lanes x 4 quads, 4 windows per pass
-        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
+        // wider windows: 8 lanes x 4 quads (<= 128 levels), 4 windows per pass
+        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow && nq <= 32);
         while (bw) {
             const int gi = lane >> 3;
             const int cntw = __popc(bw);
@@ -294,6 +294,24 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
 #pragma unroll
             for (int t = 0; t < 4; ++t)
                 if (bw) bw &= bw - 1;
+        }
+        // extra-wide windows (<= 256 levels): 16 lanes x 4 quads, 2 per pass
+        unsigned bx = __ballot_sync(0xffffffffu, active && nq > 32);
+        while (bx) {
+            const int gi = lane >> 4;
+            const int cntw = __popc(bx);
+            const unsigned mk = gi ? (bx & (bx - 1)) : bx;
+            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
+            PixMeta pw;
+            pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
+            pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
+            pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
+            const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
+            scan_pixel<16, 4>(gi < cntw, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
+                              rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2,
+                              P2x4, mask_tab);
+            if (bx) bx &= bx - 1;
+            if (bx) bx &= bx - 1;
         }
         prev_active = active;
     }
@@ -417,7 +435,7 @@ __global__ void __launch_bounds__(256) combine_wta_kernel(Bufs b, int ndir, int 
         const bool narrow = active && nq <= 4;
         wta_pixel<1>(narrow, x, y, m, ndir, pd, dstride, agg, b.md + pbase + x, b.mv + pbase + x,
                      W, b.H, write_s, do_wta);
-        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
+        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow && nq <= 32);
         while (bw) {
             const int gi = lane >> 3;
             const int cntw = __popc(bw);
@@ -436,6 +454,22 @@ __global__ void __launch_bounds__(256) combine_wta_kernel(Bufs b, int ndir, int 
 #pragma unroll
             for (int t = 0; t < 4; ++t)
                 if (bw) bw &= bw - 1;
+        }
+        unsigned bx = __ballot_sync(0xffffffffu, active && nq > 32);
+        while (bx) {
+            const int gi = lane >> 4;
+            const int cntw = __popc(bx);
+            const unsigned mk = gi ? (bx & (bx - 1)) : bx;
+            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
+            PixMeta pw;
+            pw.lohi = __shfl_sync(0xffffffffu, m.lohi, src);
+            pw.cell = __shfl_sync(0xffffffffu, m.cell, src);
+            pw.qo = __shfl_sync(0xffffffffu, m.qo, src);
+            const int xw = x0 + src;
+            wta_pixel<16>(gi < cntw, xw, y, pw, ndir, pd, dstride, agg, b.md + pbase + xw,
+                          b.mv + pbase + xw, W, b.H, write_s, do_wta);
+            if (bx) bx &= bx - 1;
+            if (bx) bx &= bx - 1;
         }
     }
 }

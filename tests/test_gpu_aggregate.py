@@ -37,6 +37,7 @@ CASES = [
     (61, 29, 130, 0.3),
     (200, 75, 128, 0.21),
     (96, 33, 256, 0.1),
+    (130, 41, 200, 0.4),
     (33, 64, 64, 0.9),
 ]
 

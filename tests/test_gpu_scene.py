@@ -123,3 +123,32 @@ def test_overlapped_fetch_captures_each_frame(port):
             np.testing.assert_array_equal(got[k][2][i], ref["mask"])
             state = (ref["d"], ref["p"], ref["valid"])
     eng.close()
+
+
+@pytest.mark.parametrize("half", [2, 4, 8, 16])
+def test_config3_fixed_window_sweep(port, half):
+    """Config 3: reduced windows of exactly 2h+1 levels (stddev ranges with a
+    vanishing gain and min_range_halfwidth = h)."""
+    cfg = SceneConfig.baseline_config(3, width=320, height=120, focal=200.0, cx=159.5, cy=59.5,
+                                      d_max=128, seed=21)
+    run_parity(port, [cfg], 4, tsgm.SgmParams(10, 120, 8, 0, 128),
+               tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=1e-9,
+                                 min_range_halfwidth=half), check_volumes=True)
+
+
+def test_config3_full_range_d256(port):
+    """Config 3's D=256 full-range baseline (p_init >= d_max^2/4)."""
+    cfg = SceneConfig.baseline_config(3, width=384, height=96, focal=240.0, cx=191.5, cy=47.5,
+                                      d_max=256, seed=22)
+    run_parity(port, [cfg], 2, tsgm.SgmParams(10, 120, 8, 0, 256),
+               tsgm.FilterConfig(p_init=16384.0, range_use_stddev=True, range_stddev_gain=3.0),
+               check_volumes=True)
+
+
+def test_config4_gain_and_occluders(port):
+    """Config 4 at reduced size: per-frame global gain +-10%, occluding movers
+    up to 30% of the image, D=256, two sequences batched."""
+    cfgs = [SceneConfig.baseline_config(4, width=512, height=256, focal=275.0, cx=255.5,
+                                        cy=127.5, seed=s) for s in (1, 2)]
+    run_parity(port, cfgs, 4, tsgm.SgmParams(10, 120, 8, 0, 256),
+               tsgm.FilterConfig(p_init=16384.0, range_use_stddev=True, range_stddev_gain=3.0))
