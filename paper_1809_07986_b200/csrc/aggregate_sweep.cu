@@ -379,26 +379,37 @@ __device__ __forceinline__ void wta_pixel(bool pix, int x, int y, const PixMeta&
     const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
     const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
     const int k0 = lg * Q;
-    uint32_t sA[Q], sB[Q];
-    uint32_t best = 0xffffffffu;  // (S << 16) | level
+    const int kc = min(k0, nq - 1);
+    // all path-cost words first (ndir x Q loads in flight), clamped into the window
+    uint32_t w[8][Q];
+#pragma unroll
+    for (int d = 0; d < 8; ++d)
+#pragma unroll
+        for (int t = 0; t < Q; ++t)
+            w[d][t] = d < ndir ? __ldg(pd + d * dstride + pm.qo + min(kc + t, nq - 1)) : 0u;
+    uint32_t best = 0xffffffffu;  // (S << 16) | level, first minimum
 #pragma unroll
     for (int t = 0; t < Q; ++t) {
-        sA[t] = sB[t] = 0u;
-        const int k = k0 + t;
-        if (!(pix && k < nq)) continue;
-        for (int d = 0; d < ndir; ++d) {
-            const uint32_t w = __ldg(pd + d * dstride + pm.qo + k);
-            sA[t] = __vadd2(sA[t], __byte_perm(w, 0u, 0x4140u));
-            sB[t] = __vadd2(sB[t], __byte_perm(w, 0u, 0x4342u));
+        // levels (0,2) and (1,3) as u16x2: byte pairs via PRMT (ALU), sums via
+        // IMAD (FMA pipe); u16 lanes never carry (S <= 8 * 255)
+        uint32_t se = 0u, so = 0u;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            se += __byte_perm(w[d][t], 0u, 0x4240u);
+            so += __byte_perm(w[d][t], 0u, 0x4341u);
         }
-        const int d0 = 4 * (q0 + k);
-        const uint32_t v[4] = {sA[t] & 0xffffu, sA[t] >> 16, sB[t] & 0xffffu, sB[t] >> 16};
+        const uint32_t sA = __byte_perm(se, so, 0x5410u);  // S(d0),   S(d0+1)
+        const uint32_t sB = __byte_perm(se, so, 0x7632u);  // S(d0+2), S(d0+3)
+        const int d0 = 4 * (q0 + k0 + t);
+        const bool act = pix && k0 + t < nq;
+        const uint32_t v[4] = {sA & 0xffffu, sA >> 16, sB & 0xffffu, sB >> 16};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int lv = d0 + u;
-            if (lv < lo || lv > hi) continue;
-            if (write_s) agg[pm.cell + (lv - lo)] = static_cast<uint16_t>(v[u]);
-            best = min(best, (v[u] << 16) | static_cast<uint32_t>(lv));
+            const bool ok = act && lv >= lo && lv <= hi;
+            if (write_s && ok) agg[pm.cell + (lv - lo)] = static_cast<uint16_t>(v[u]);
+            const uint32_t key = (v[u] << 16) | static_cast<uint32_t>(lv);
+            best = min(best, ok ? key : 0xffffffffu);
         }
     }
     if (G > 1) {
@@ -497,12 +508,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int tasks = sp.task_off[k] * n;
     const size_t smem = static_cast<size_t>(kScanWarps) * 32 * (scan_slot_bytes(b.d_max) + 4);
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
-    if (do_wta) {
-        combine_wta_kernel<<<dim3(b.H, n), 256, 0, L.st>>>(b, k, write_s, 1);
-    } else {
-        const size_t csmem = sizeof(uint32_t) * (3 * b.W + 1);
-        sweep_combine_kernel<<<dim3(b.H, n), 512, csmem, L.st>>>(b, k);
-    }
+    combine_wta_kernel<<<dim3(b.H, n), 256, 0, L.st>>>(b, k, write_s, do_wta);
     *L.counter += 2;
 }
 

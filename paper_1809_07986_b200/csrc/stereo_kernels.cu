@@ -348,6 +348,12 @@ void launch_wta(const Bufs& b, int n, Launch L) {
 // ---------------------------------------------------------------- median (A19)
 // median_refine, sgm.cpp:189-216: lower median of the valid 3x3 neighbours,
 // valid iff at least 5.
+__device__ __forceinline__ void cswap(int64_t& a, int64_t& b) {
+    const int64_t lo = a < b ? a : b, hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+}
+
 __global__ void median_kernel(Bufs b, const int32_t* in_d, const uint8_t* in_v, int32_t* out_d,
                               uint8_t* out_v) {
     const int a = blockIdx.y, s = slot_of(b, a);
@@ -355,35 +361,40 @@ __global__ void median_kernel(Bufs b, const int32_t* in_d, const uint8_t* in_v, 
     if (i >= b.P) return;
     const int x = i % b.W, y = i / b.W;
     const size_t base = static_cast<size_t>(s) * b.P;
-    int32_t v[9];
+    // the 9 neighbours, missing/invalid ones as +inf (sort last)
+    int64_t v[9];
     int n = 0;
 #pragma unroll
     for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
         for (int dx = -1; dx <= 1; ++dx) {
             const int nx = x + dx, ny = y + dy;
-            if (nx < 0 || nx >= b.W || ny < 0 || ny >= b.H) continue;
-            const size_t j = base + static_cast<size_t>(ny) * b.W + nx;
-            if (!in_v[j]) continue;
-            v[n++] = in_d[j];
+            const bool in = nx >= 0 && nx < b.W && ny >= 0 && ny < b.H;
+            const size_t j = base + static_cast<size_t>(in ? ny : y) * b.W + (in ? nx : x);
+            const bool ok = in && in_v[j];
+            v[(dy + 1) * 3 + dx + 1] = ok ? static_cast<int64_t>(in_d[j]) : INT64_MAX;
+            n += ok;
         }
     if (n < 5) {
         out_d[base + i] = 0;
         out_v[base + i] = 0;
         return;
     }
-    // lower median = element of rank (n-1)/2
+    // full 9-element sorting network (25 compare-exchanges)
+    cswap(v[0], v[3]); cswap(v[1], v[7]); cswap(v[2], v[5]); cswap(v[4], v[8]);
+    cswap(v[0], v[7]); cswap(v[2], v[4]); cswap(v[3], v[8]); cswap(v[5], v[6]);
+    cswap(v[0], v[2]); cswap(v[1], v[3]); cswap(v[4], v[5]); cswap(v[7], v[8]);
+    cswap(v[1], v[4]); cswap(v[3], v[6]); cswap(v[5], v[7]);
+    cswap(v[0], v[1]); cswap(v[2], v[4]); cswap(v[3], v[5]); cswap(v[6], v[8]);
+    cswap(v[2], v[3]); cswap(v[4], v[5]); cswap(v[6], v[7]);
+    cswap(v[1], v[2]); cswap(v[3], v[4]); cswap(v[5], v[6]);
+    // lower median of the n valid values = element (n-1)/2 of the sorted list
     const int k = (n - 1) / 2;
-    int32_t med = 0;
-    for (int p = 0; p < n; ++p) {
-        int less = 0, leq = 0;
-        for (int q = 0; q < n; ++q) {
-            less += v[q] < v[p];
-            leq += v[q] <= v[p];
-        }
-        if (less <= k && k < leq) med = v[p];
-    }
-    out_d[base + i] = med;
+    int64_t med = v[0];
+#pragma unroll
+    for (int j = 1; j < 5; ++j)
+        if (j == k) med = v[j];
+    out_d[base + i] = static_cast<int32_t>(med);
     out_v[base + i] = 1;
 }
 

@@ -122,57 +122,74 @@ void launch_predict_finalize(const Bufs& b, int n, double q, int apply_phi, Laun
 // ---------------------------------------------------------------- reject + fill (A8, A9)
 // reject_discontinuities (temporal_filter.cpp:51-74) decided on its input,
 // then fill_zoom_holes (:76-106) decided on reject's output, fused: a pixel's
-// fill needs reject's verdict at its 4 neighbours, each recomputed from the
-// input (radius-2 dependence, read through L1).
-__device__ __forceinline__ bool rejected(const double* d, const uint8_t* v, int x, int y, int W,
-                                         int H, double thr) {
-    const int i = y * W + x;
-    if (!v[i]) return false;
-    const double di = d[i];
-    // neighbour order (1,0), (-1,0), (0,1), (0,-1) as kDx/kDy at :52-53
-    if (x + 1 < W && v[i + 1] && fabs(di - d[i + 1]) > thr) return true;
-    if (x - 1 >= 0 && v[i - 1] && fabs(di - d[i - 1]) > thr) return true;
-    if (y + 1 < H && v[i + W] && fabs(di - d[i + W]) > thr) return true;
-    if (y - 1 >= 0 && v[i - W] && fabs(di - d[i - W]) > thr) return true;
-    return false;
-}
+// fill needs reject's verdict at its 4 neighbours (radius-2 dependence).
+// Tiled: the (32+4) x (8+4) input tile is staged in shared memory, the
+// rejection verdict is computed once for the (32+2) x (8+2) ring the fill
+// needs, then the 32 x 8 outputs.
+constexpr int kRfW = 32, kRfH = 8;
 
 __global__ void reject_fill_kernel(Bufs b, const double* in_d, const double* in_p,
                                    const uint8_t* in_v, double* out_d, double* out_p,
                                    uint8_t* out_v, double thr, int do_reject, int do_fill) {
-    const int a = blockIdx.y, s = slot_of(b, a);
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= b.P) return;
+    __shared__ double td[kRfH + 4][kRfW + 4];
+    __shared__ double tp[kRfH + 4][kRfW + 4];
+    __shared__ uint8_t tv[kRfH + 4][kRfW + 4];
+    __shared__ uint8_t rv[kRfH + 2][kRfW + 2];  // validity after rejection
+    const int a = blockIdx.z, s = slot_of(b, a);
     const size_t base = static_cast<size_t>(s) * b.P;
-    const double* d = in_d + base;
-    const double* p = in_p + base;
-    const uint8_t* v = in_v + base;
-    const int W = b.W, H = b.H, x = i % W, y = i / W;
-    // validity after rejection
-    auto rv = [&](int xx, int yy) -> bool {
-        const int j = yy * W + xx;
-        return v[j] && !(do_reject && rejected(d, v, xx, yy, W, H, thr));
-    };
-    double od = d[i], op = p[i];
-    uint8_t ov = v[i];
-    if (v[i] && do_reject && rejected(d, v, x, y, W, H, thr)) {
+    const int W = b.W, H = b.H;
+    const int x0 = blockIdx.x * kRfW - 2, y0 = blockIdx.y * kRfH - 2;
+    const int tid = threadIdx.y * kRfW + threadIdx.x;
+    for (int k = tid; k < (kRfH + 4) * (kRfW + 4); k += kRfW * kRfH) {
+        const int ty = k / (kRfW + 4), tx = k % (kRfW + 4);
+        const int gx = x0 + tx, gy = y0 + ty;
+        const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+        const size_t g = base + static_cast<size_t>(in ? gy : 0) * W + (in ? gx : 0);
+        td[ty][tx] = in ? in_d[g] : 0.0;
+        tp[ty][tx] = in ? in_p[g] : 0.0;
+        tv[ty][tx] = in ? in_v[g] : 0;
+    }
+    __syncthreads();
+    // verdicts for the ring: tile coords (ty, tx) in [1, kRfH+3) x [1, kRfW+3)
+    for (int k = tid; k < (kRfH + 2) * (kRfW + 2); k += kRfW * kRfH) {
+        const int ry = k / (kRfW + 2), rx = k % (kRfW + 2);
+        const int ty = ry + 1, tx = rx + 1;
+        const int gx = x0 + tx, gy = y0 + ty;
+        bool v = tv[ty][tx] != 0;
+        if (v && do_reject) {
+            // neighbour order (1,0), (-1,0), (0,1), (0,-1) as kDx/kDy at :52-53
+            const double di = td[ty][tx];
+            if (gx + 1 < W && tv[ty][tx + 1] && fabs(di - td[ty][tx + 1]) > thr) v = false;
+            else if (gx - 1 >= 0 && tv[ty][tx - 1] && fabs(di - td[ty][tx - 1]) > thr) v = false;
+            else if (gy + 1 < H && tv[ty + 1][tx] && fabs(di - td[ty + 1][tx]) > thr) v = false;
+            else if (gy - 1 >= 0 && tv[ty - 1][tx] && fabs(di - td[ty - 1][tx]) > thr) v = false;
+        }
+        rv[ry][rx] = v;
+    }
+    __syncthreads();
+    const int x = blockIdx.x * kRfW + threadIdx.x, y = blockIdx.y * kRfH + threadIdx.y;
+    if (x >= W || y >= H) return;
+    const int tx = threadIdx.x + 2, ty = threadIdx.y + 2, rx = threadIdx.x + 1, ry = threadIdx.y + 1;
+    double od = td[ty][tx], op = tp[ty][tx];
+    uint8_t ov = tv[ty][tx];
+    if (ov && !rv[ry][rx]) {
         od = op = 0.0;  // DisparityState::invalidate, geometry.hpp:70-74
         ov = 0;
     }
     if (do_fill && !ov) {
-        const bool horiz = x - 1 >= 0 && x + 1 < W && rv(x - 1, y) && rv(x + 1, y);
-        const bool vert = y - 1 >= 0 && y + 1 < H && rv(x, y - 1) && rv(x, y + 1);
+        const bool horiz = x - 1 >= 0 && x + 1 < W && rv[ry][rx - 1] && rv[ry][rx + 1];
+        const bool vert = y - 1 >= 0 && y + 1 < H && rv[ry - 1][rx] && rv[ry + 1][rx];
         if (horiz || vert) {
             double ds = 0.0, ps = 0.0;
             int nn = 0;
             if (horiz) {
-                ds = __dadd_rn(ds, __dadd_rn(d[i - 1], d[i + 1]));
-                ps = __dadd_rn(ps, __dadd_rn(p[i - 1], p[i + 1]));
+                ds = __dadd_rn(ds, __dadd_rn(td[ty][tx - 1], td[ty][tx + 1]));
+                ps = __dadd_rn(ps, __dadd_rn(tp[ty][tx - 1], tp[ty][tx + 1]));
                 nn += 2;
             }
             if (vert) {
-                ds = __dadd_rn(ds, __dadd_rn(d[i - W], d[i + W]));
-                ps = __dadd_rn(ps, __dadd_rn(p[i - W], p[i + W]));
+                ds = __dadd_rn(ds, __dadd_rn(td[ty - 1][tx], td[ty + 1][tx]));
+                ps = __dadd_rn(ps, __dadd_rn(tp[ty - 1][tx], tp[ty + 1][tx]));
                 nn += 2;
             }
             od = ds / nn;
@@ -180,18 +197,21 @@ __global__ void reject_fill_kernel(Bufs b, const double* in_d, const double* in_
             ov = 1;
         }
     }
-    out_d[base + i] = od;
-    out_p[base + i] = op;
-    out_v[base + i] = ov;
+    const size_t g = base + static_cast<size_t>(y) * W + x;
+    out_d[g] = od;
+    out_p[g] = op;
+    out_v[g] = ov;
 }
 
 void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* in_p,
                         const uint8_t* in_v, double* out_d, double* out_p, uint8_t* out_v,
                         double disc_thresh, int do_reject, int do_fill, Launch L) {
-    reject_fill_kernel<<<dim3((b.P + 255) / 256, n), 256, 0, L.st>>>(
-        b, in_d, in_p, in_v, out_d, out_p, out_v, disc_thresh, do_reject, do_fill);
+    dim3 grid((b.W + kRfW - 1) / kRfW, (b.H + kRfH - 1) / kRfH, n);
+    reject_fill_kernel<<<grid, dim3(kRfW, kRfH), 0, L.st>>>(b, in_d, in_p, in_v, out_d, out_p,
+                                                           out_v, disc_thresh, do_reject, do_fill);
     ++*L.counter;
 }
+
 
 // ---------------------------------------------------------------- correct (A16-A18, A21)
 // correct (temporal_filter.cpp:145-170), the diff map (:223-229), the
