@@ -317,171 +317,81 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
     }
 }
 
-// S = sum of the per-direction path costs, written in the reference's ragged
-// layout. One CTA per (row, slot); one thread per QUAD of the row's quad
-// layout: 8 coalesced u32 loads (4 u8 path costs each), u16x2 sums, and the
-// valid levels stored as u16 at their ragged cell positions.
-__global__ void sweep_combine_kernel(Bufs b, int ndir) {
-    extern __shared__ uint32_t sm[];
-    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x, W = b.W;
-    uint32_t* qo = sm;               // W+1 in-row quad offsets (relative)
-    uint32_t* cl = qo + W + 1;       // W cell offsets (absolute, per slot)
-    uint32_t* lh = cl + W;           // W lo | hi << 16
-    const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
-    const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
-    const uint32_t q_row0 = b.qoff[obase];
-    for (int x = threadIdx.x; x < W; x += blockDim.x) {
-        qo[x] = b.qoff[obase + x] - q_row0;
-        cl[x] = b.off[obase + x];
-        lh[x] = b.lohi[pbase + x];
-    }
-    if (threadIdx.x == 0) qo[W] = b.qoff[obase + W] - q_row0;
-    __syncthreads();
-    const uint32_t nq = qo[W];
-    const size_t dstride = static_cast<size_t>(b.max_slots) * b.quad_cap;  // in u32 quads
-    const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) +
-                         static_cast<size_t>(s) * b.quad_cap + q_row0;
-    uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap;
-    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
-        int l = 0, r = W;  // pixel of quad q
-        while (r - l > 1) {
-            const int m = (l + r) >> 1;
-            if (qo[m] <= q) l = m; else r = m;
-        }
-        uint32_t sa = 0u, sb = 0u;
-        for (int d = 0; d < ndir; ++d) {
-            const uint32_t w = __ldg(pd + d * dstride + q);
-            sa = __vadd2(sa, __byte_perm(w, 0u, 0x4140u));
-            sb = __vadd2(sb, __byte_perm(w, 0u, 0x4342u));
-        }
-        const int lo = static_cast<int>(lh[l] & 0xffffu), hi = static_cast<int>(lh[l] >> 16);
-        const int d0 = 4 * ((lo >> 2) + static_cast<int>(q - qo[l]));
-        uint16_t* dst = agg + cl[l] + (d0 - lo);
-        const uint32_t v[4] = {sa & 0xffffu, sa >> 16, sb & 0xffffu, sb >> 16};
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (d0 + t >= lo && d0 + t <= hi) dst[t] = static_cast<uint16_t>(v[t]);
-    }
-}
+// Fused combine + winner_takes_all (sgm.cpp:163-187) for the production step,
+// also the standalone combine (S only). One CTA per (row, slot), the row taken
+// in chunks of kCwPix pixels: phase 1 runs one thread per QUAD of the chunk
+// (coalesced u32 loads of every direction's path costs, u16x2 sums, S stored
+// when requested, the quad's first (S, level) minimum kept in shared memory);
+// phase 2 reduces each pixel's quads to its first argmin.
+constexpr int kCwThreads = 512;
+constexpr int kCwPix = 128;
 
-// Fused combine + winner_takes_all (sgm.cpp:163-187) for the production step:
-// S of each pixel is summed from the per-direction path costs in registers and
-// reduced to its first argmin; S is written to the ragged volume only when
-// requested (kept volumes / standalone C->S). One CTA per (row, slot); a lane
-// per window of <= 4 quads, 8 lanes x 4 quads per wider window.
-template <int G>
-__device__ __forceinline__ void wta_pixel(bool pix, int x, int y, const PixMeta& pm, int ndir,
-                                          const uint32_t* pd, size_t dstride, uint16_t* agg,
-                                          int32_t* md, uint8_t* mv, int W, int H, bool write_s,
-                                          bool do_wta) {
-    constexpr int Q = 4;
-    const int lg = static_cast<int>(threadIdx.x & (G - 1));
-    const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
-    const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
-    const int k0 = lg * Q;
-    const int kc = min(k0, nq - 1);
-    // all path-cost words first (ndir x Q loads in flight), clamped into the window
-    uint32_t w[8][Q];
-#pragma unroll
-    for (int d = 0; d < 8; ++d)
-#pragma unroll
-        for (int t = 0; t < Q; ++t)
-            w[d][t] = d < ndir ? __ldg(pd + d * dstride + pm.qo + min(kc + t, nq - 1)) : 0u;
-    uint32_t best = 0xffffffffu;  // (S << 16) | level, first minimum
-#pragma unroll
-    for (int t = 0; t < Q; ++t) {
-        // levels (0,2) and (1,3) as u16x2: byte pairs via PRMT (ALU), sums via
-        // IMAD (FMA pipe); u16 lanes never carry (S <= 8 * 255)
-        uint32_t se = 0u, so = 0u;
-#pragma unroll
-        for (int d = 0; d < 8; ++d) {
-            se += __byte_perm(w[d][t], 0u, 0x4240u);
-            so += __byte_perm(w[d][t], 0u, 0x4341u);
-        }
-        const uint32_t sA = __byte_perm(se, so, 0x5410u);  // S(d0),   S(d0+1)
-        const uint32_t sB = __byte_perm(se, so, 0x7632u);  // S(d0+2), S(d0+3)
-        const int d0 = 4 * (q0 + k0 + t);
-        const bool act = pix && k0 + t < nq;
-        const uint32_t v[4] = {sA & 0xffffu, sA >> 16, sB & 0xffffu, sB >> 16};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int lv = d0 + u;
-            const bool ok = act && lv >= lo && lv <= hi;
-            if (write_s && ok) agg[pm.cell + (lv - lo)] = static_cast<uint16_t>(v[u]);
-            const uint32_t key = (v[u] << 16) | static_cast<uint32_t>(lv);
-            best = min(best, ok ? key : 0xffffffffu);
-        }
-    }
-    if (G > 1) {
-#pragma unroll
-        for (int o = 1; o < G; o <<= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-    }
-    if (do_wta && pix && lg == 0) {
-        const bool def = x >= kCensusRadius && x < W - kCensusRadius && y >= kCensusRadius &&
-                         y < H - kCensusRadius;
-        md[0] = def ? static_cast<int32_t>(best & 0xffffu) : 0;
-        mv[0] = def ? 1 : 0;
-    }
-}
-
-__global__ void __launch_bounds__(256) combine_wta_kernel(Bufs b, int ndir, int write_s,
-                                                          int do_wta) {
-    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x, W = b.W;
-    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+__global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndir, int write_s,
+                                                                 int do_wta) {
+    extern __shared__ uint32_t cw[];
+    const int W = b.W, H = b.H;
+    const int qmax = (b.d_max - 1) / 4 + 1;
+    uint32_t* qo = cw;                     // kCwPix + 1 chunk-relative quad offsets
+    uint32_t* lh = qo + kCwPix + 1;        // kCwPix lo | hi << 16
+    uint32_t* cl = lh + kCwPix;            // kCwPix cell offsets
+    uint32_t* key = cl + kCwPix;           // kCwPix * qmax per-quad minima
+    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
     const size_t dstride = static_cast<size_t>(b.max_slots) * b.quad_cap;
     const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) + static_cast<size_t>(s) * b.quad_cap;
     uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap;
-    for (int x0 = warp * 32; x0 < W; x0 += 32 * (blockDim.x >> 5)) {
-        const int x = x0 + lane;
-        const bool active = x < W;
-        PixMeta m{0u, 0u, 0u};
-        if (active) {
-            m.lohi = b.lohi[pbase + x];
-            m.cell = b.off[obase + x];
-            m.qo = b.qoff[obase + x];
+    for (int x0 = 0; x0 < W; x0 += kCwPix) {
+        const int np = min(kCwPix, W - x0);
+        const uint32_t qbase = b.qoff[obase + x0];
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+            qo[i] = b.qoff[obase + x0 + i] - qbase;
+            lh[i] = b.lohi[pbase + x0 + i];
+            cl[i] = b.off[obase + x0 + i];
         }
-        const int nq = static_cast<int>(m.lohi >> 18) - static_cast<int>((m.lohi & 0xffffu) >> 2) + 1;
-        const bool narrow = active && nq <= 4;
-        wta_pixel<1>(narrow, x, y, m, ndir, pd, dstride, agg, b.md + pbase + x, b.mv + pbase + x,
-                     W, b.H, write_s, do_wta);
-        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow && nq <= 32);
-        while (bw) {
-            const int gi = lane >> 3;
-            const int cntw = __popc(bw);
-            unsigned mk = bw;
+        if (threadIdx.x == 0) qo[np] = b.qoff[obase + x0 + np] - qbase;
+        __syncthreads();
+        const uint32_t nq = qo[np];
+        for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+            int l = 0, r = np;  // pixel of quad q
+            while (r - l > 1) {
+                const int m = (l + r) >> 1;
+                if (qo[m] <= q) l = m; else r = m;
+            }
+            uint32_t se = 0u, so = 0u;
+            for (int d = 0; d < ndir; ++d) {
+                const uint32_t w = __ldg(pd + d * dstride + qbase + q);
+                se += __byte_perm(w, 0u, 0x4240u);  // levels 0, 2 (u16 lanes never carry)
+                so += __byte_perm(w, 0u, 0x4341u);  // levels 1, 3
+            }
+            const int lo = static_cast<int>(lh[l] & 0xffffu), hi = static_cast<int>(lh[l] >> 16);
+            const int k = static_cast<int>(q - qo[l]);
+            const int d0 = 4 * ((lo >> 2) + k);
+            const uint32_t v[4] = {se & 0xffffu, so & 0xffffu, se >> 16, so >> 16};
+            uint32_t best = 0xffffffffu;
 #pragma unroll
-            for (int t = 0; t < 3; ++t)
-                if (t < gi) mk &= mk - 1;
-            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
-            PixMeta pw;
-            pw.lohi = __shfl_sync(0xffffffffu, m.lohi, src);
-            pw.cell = __shfl_sync(0xffffffffu, m.cell, src);
-            pw.qo = __shfl_sync(0xffffffffu, m.qo, src);
-            const int xw = x0 + src;
-            wta_pixel<8>(gi < cntw, xw, y, pw, ndir, pd, dstride, agg, b.md + pbase + xw,
-                         b.mv + pbase + xw, W, b.H, write_s, do_wta);
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (bw) bw &= bw - 1;
+            for (int u = 0; u < 4; ++u) {
+                const int lv = d0 + u;
+                const bool ok = lv >= lo && lv <= hi;
+                if (write_s && ok) agg[cl[l] + (lv - lo)] = static_cast<uint16_t>(v[u]);
+                best = min(best, ok ? ((v[u] << 16) | static_cast<uint32_t>(lv)) : 0xffffffffu);
+            }
+            key[l * qmax + k] = best;
         }
-        unsigned bx = __ballot_sync(0xffffffffu, active && nq > 32);
-        while (bx) {
-            const int gi = lane >> 4;
-            const int cntw = __popc(bx);
-            const unsigned mk = gi ? (bx & (bx - 1)) : bx;
-            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
-            PixMeta pw;
-            pw.lohi = __shfl_sync(0xffffffffu, m.lohi, src);
-            pw.cell = __shfl_sync(0xffffffffu, m.cell, src);
-            pw.qo = __shfl_sync(0xffffffffu, m.qo, src);
-            const int xw = x0 + src;
-            wta_pixel<16>(gi < cntw, xw, y, pw, ndir, pd, dstride, agg, b.md + pbase + xw,
-                          b.mv + pbase + xw, W, b.H, write_s, do_wta);
-            if (bx) bx &= bx - 1;
-            if (bx) bx &= bx - 1;
+        __syncthreads();
+        if (do_wta) {
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+                const int n = static_cast<int>(qo[i + 1] - qo[i]);
+                uint32_t best = 0xffffffffu;
+                for (int k = 0; k < n; ++k) best = min(best, key[i * qmax + k]);
+                const int x = x0 + i;
+                const bool def = x >= kCensusRadius && x < W - kCensusRadius &&
+                                 y >= kCensusRadius && y < H - kCensusRadius;
+                b.md[pbase + x] = def ? static_cast<int32_t>(best & 0xffffu) : 0;
+                b.mv[pbase + x] = def ? 1 : 0;
+            }
         }
+        __syncthreads();
     }
 }
 
@@ -508,7 +418,9 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int tasks = sp.task_off[k] * n;
     const size_t smem = static_cast<size_t>(kScanWarps) * 32 * (scan_slot_bytes(b.d_max) + 4);
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
-    combine_wta_kernel<<<dim3(b.H, n), 256, 0, L.st>>>(b, k, write_s, do_wta);
+    const size_t cwsmem = sizeof(uint32_t) *
+                          (3 * kCwPix + 1 + static_cast<size_t>(kCwPix) * ((b.d_max - 1) / 4 + 1));
+    combine_wta_kernel<<<dim3(b.H, n), kCwThreads, cwsmem, L.st>>>(b, k, write_s, do_wta);
     *L.counter += 2;
 }
 

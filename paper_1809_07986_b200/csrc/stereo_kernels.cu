@@ -230,77 +230,61 @@ void launch_offsets(const Bufs& b, int n, Launch L) {
 
 // ---------------------------------------------------------------- cost (A13)
 // build_cost_volume, matching_cost.cpp:88-117. One CTA per (row, slot); the
-// row's signatures, lo and in-row offsets are staged in shared memory. Each
-// thread produces one ALIGNED group of 4 cells of the ragged volume (one
-// binary search for its first cell, then a walk), stored as one u32; the two
-// groups a row shares with its neighbours are stored byte by byte.
-__global__ void cost_kernel(Bufs b) {
+// row's census signatures are staged in shared memory. Warps take 32-pixel
+// chunks: a window of <= 16 levels is written by its own lane, a wider window
+// by the whole warp (lanes across its levels, coalesced byte stores).
+__device__ __forceinline__ uint8_t cell_cost(const uint32_t* sl, const uint32_t* sr, int x, int d,
+                                             int W, bool row_def) {
+    const int xr = x - d;
+    const bool ok = row_def && x >= kCensusRadius && x < W - kCensusRadius &&
+                    xr >= kCensusRadius && xr < W - kCensusRadius;
+    return ok ? static_cast<uint8_t>(__popc(sl[x] ^ sr[xr])) : static_cast<uint8_t>(kMaxCost);
+}
+
+__global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
     extern __shared__ uint32_t sm[];
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const int W = b.W;
     uint32_t* sl = sm;
     uint32_t* sr = sl + W;
-    uint32_t* o = sr + W;            // W+1 in-row offsets
-    uint16_t* lo = reinterpret_cast<uint16_t*>(o + W + 1);
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
-    const uint32_t row0 = off[0];
     for (int x = threadIdx.x; x < W; x += blockDim.x) {
         sl[x] = b.sigl[pbase + x];
         sr[x] = b.sigr[pbase + x];
-        o[x] = off[x] - row0;
-        lo[x] = b.lo[pbase + x];
     }
-    if (threadIdx.x == 0) o[W] = off[W] - row0;  // next row's first offset (or total)
     __syncthreads();
-    const uint32_t n = o[W];
-    if (n == 0) return;
     uint8_t* base = b.cost + static_cast<size_t>(s) * b.vol_cap;
-    const uintptr_t abs0 = reinterpret_cast<uintptr_t>(base) + row0;  // address of cell 0
-    const uintptr_t g0 = abs0 & ~static_cast<uintptr_t>(3);
-    const uint32_t ngroups = static_cast<uint32_t>(((abs0 + n + 3) & ~static_cast<uintptr_t>(3)) - g0) / 4;
-    const int lead = static_cast<int>(abs0 - g0);  // cells of group 0 before this row
     const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
-    for (uint32_t gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
-        const int c0 = static_cast<int>(4 * gi) - lead;  // relative cell of byte 0
-        const int cf = max(c0, 0);
-        int l = 0, r = W;  // pixel of the first valid cell
-        while (r - l > 1) {
-            const int m = (l + r) >> 1;
-            if (static_cast<int>(o[m]) <= cf) l = m; else r = m;
+    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+    const int nwarps = static_cast<int>(blockDim.x >> 5);
+    for (int x0 = warp * 32; x0 < W; x0 += 32 * nwarps) {
+        const int x = x0 + lane;
+        const bool active = x < W;
+        const uint32_t lh = active ? b.lohi[pbase + x] : 0u;
+        const uint32_t o = active ? off[x] : 0u;
+        const int lo = static_cast<int>(lh & 0xffffu), n = static_cast<int>(lh >> 16) - lo + 1;
+        const bool narrow = active && n <= 16;
+        if (narrow) {
+            uint8_t* dst = base + o;
+            for (int j = 0; j < n; ++j) dst[j] = cell_cost(sl, sr, x, lo + j, W, row_def);
         }
-        int x = l;
-        uint32_t word = 0u;
-        bool full = true;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int c = c0 + t;
-            if (c < 0 || c >= static_cast<int>(n)) {
-                full = false;
-                continue;
-            }
-            while (x + 1 < W && static_cast<int>(o[x + 1]) <= c) ++x;
-            const int xr = x - (static_cast<int>(lo[x]) + (c - static_cast<int>(o[x])));
-            const bool ok = row_def && x >= kCensusRadius && x < W - kCensusRadius &&
-                            xr >= kCensusRadius && xr < W - kCensusRadius;
-            const uint32_t cv = ok ? static_cast<uint32_t>(__popc(sl[x] ^ sr[xr])) : kMaxCost;
-            word |= cv << (8 * t);
-        }
-        uint8_t* gptr = reinterpret_cast<uint8_t*>(g0 + 4 * static_cast<uintptr_t>(gi));
-        if (full) {
-            *reinterpret_cast<uint32_t*>(gptr) = word;
-        } else {
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const int c = c0 + t;
-                if (c >= 0 && c < static_cast<int>(n)) gptr[t] = static_cast<uint8_t>(word >> (8 * t));
-            }
+        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
+        while (bw) {
+            const int src = __ffs(bw) - 1;
+            bw &= bw - 1;
+            const int xw = x0 + src;
+            const int lo_w = __shfl_sync(0xffffffffu, lo, src);
+            const int n_w = __shfl_sync(0xffffffffu, n, src);
+            const uint32_t o_w = __shfl_sync(0xffffffffu, o, src);
+            uint8_t* dst = base + o_w;
+            for (int j = lane; j < n_w; j += 32) dst[j] = cell_cost(sl, sr, xw, lo_w + j, W, row_def);
         }
     }
 }
 
 void launch_cost(const Bufs& b, int n, Launch L) {
-    const size_t smem = sizeof(uint32_t) * (3 * b.W + 1) + sizeof(uint16_t) * b.W;
+    const size_t smem = sizeof(uint32_t) * 2 * b.W;
     cost_kernel<<<dim3(b.H, n), 512, smem, L.st>>>(b);
     ++*L.counter;
 }
