@@ -52,6 +52,16 @@ struct ScanParams {
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     return __byte_perm(a, b, s);
 }
+// Cost of a level outside the window: L = C + min(...) stays < 2^16 and
+// L - min L >= kPoison - 255 > P2, so it never wins a min and normalises to P2.
+constexpr uint32_t kPoison2 = 0x3f003f00u;
+
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -129,8 +139,8 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
-            CA[t] = prmt(cq, 0u, 0x4140u);
-            CB[t] = prmt(cq, 0u, 0x4342u);
+            CA[t] = prmt(cq, 0u, 0x4140u) | (ivA[t] & kPoison2);
+            CB[t] = prmt(cq, 0u, 0x4342u) | (ivB[t] & kPoison2);
             act[t] = pix && k0 + t < nq;
         }
     }
@@ -145,17 +155,20 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         const bool in = static_cast<uint32_t>(a0 - 1 + u - pq0) <= span;
         w[u] = has_pred ? (in ? raw : P2x4) : 0u;
     }
+    // levels outside the window carry a poisoned cost (kPoison): they lose every
+    // min and normalise to exactly P2 below, so no masking is needed
     uint32_t mn = 0xffffffffu;
-    uint32_t mma = prmt(w[0] >> 24, prmt(w[1], 0u, 0x4140u), 0x5410u);  // M(d0-1), M(d0)
+    uint32_t mma = prmt(w[0], prmt(w[1], 0u, 0x4140u), 0x5453u);  // M(d0-1), M(d0)
 #pragma unroll
     for (int t = 0; t < Q; ++t) {
         const uint32_t e0 = prmt(w[t + 1], 0u, 0x4140u);   // M(d0),   M(d0+1)
         const uint32_t e1 = prmt(w[t + 1], 0u, 0x4342u);   // M(d0+2), M(d0+3)
         const uint32_t mpa = prmt(w[t + 1], 0u, 0x4241u);  // M(d0+1), M(d0+2)
-        const uint32_t mpb = prmt(e1, w[t + 2] & 0xffu, 0x5432u);  // M(d0+3), M(d0+4)
-        LA[t] = __vadd2(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), CA[t]);
-        LB[t] = __vadd2(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), CB[t]);
-        mn = __vminu2(mn, __vminu2(LA[t] | ivA[t], LB[t] | ivB[t]));
+        const uint32_t mpb = prmt(e1, w[t + 2], 0x1432u);  // M(d0+3), M(d0+4)
+        // u16 lanes never carry here, so the adds go to the FMA pipe (IMAD)
+        LA[t] = mad_u32(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), 1u, CA[t]);
+        LB[t] = mad_u32(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), 1u, CB[t]);
+        mn = __vimin3_u16x2(mn, LA[t], LB[t]);
         mma = mpb;
     }
     const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
@@ -164,8 +177,8 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
 #pragma unroll
     for (int t = 0; t < Q; ++t) {
         if (!act[t]) continue;
-        const uint32_t ma = __vmaxu2(__viaddmin_u16x2(LA[t], neg, P2x2), ivA[t] & P2x2);
-        const uint32_t mb = __vmaxu2(__viaddmin_u16x2(LB[t], neg, P2x2), ivB[t] & P2x2);
+        const uint32_t ma = __viaddmin_u16x2(LA[t], neg, P2x2);
+        const uint32_t mb = __viaddmin_u16x2(LB[t], neg, P2x2);
         sts32(sb + 4u + 4u * static_cast<uint32_t>(a0 + t), prmt(ma, mb, 0x6420u));
         out[pm.qo + static_cast<uint32_t>(k0 + t)] = prmt(LA[t], LB[t], 0x6420u);
     }
