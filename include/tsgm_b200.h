@@ -64,6 +64,10 @@ typedef struct tsgm_ctx tsgm_ctx;
 
 #define TSGM_KEEP_VOLUMES 1u /* materialise C (u8) and S (u16) per slot for fetch */
 #define TSGM_FORCE_SCANLINE_AGG 2u /* use the per-direction scanline aggregation kernels */
+/* Extension A22 (NOT in the reference, a declared non-goal: SPEC.md:231):
+ * sub-pixel disparity by a parabola through S(d-1), S(d), S(d+1) around the
+ * WTA minimum, f32, exported only (never fed back into the Kalman state). */
+#define TSGM_SUBPIXEL 4u
 
 typedef struct {
     int32_t width, height;     /* image size (must equal calib.width/height) */
@@ -122,6 +126,7 @@ enum {
     TSGM_OUT_OFFSETS = 14,  /* u32 W*H+1              */
     TSGM_OUT_COST = 15,     /* u8 N   (TSGM_KEEP_VOLUMES) */
     TSGM_OUT_AGG = 16,      /* u16 N  (TSGM_KEEP_VOLUMES) */
+    TSGM_OUT_SUBPIXEL = 17, /* f32 sub-pixel WTA disparity (TSGM_SUBPIXEL), 0 where invalid */
     TSGM_OUT_COUNT
 };
 /* Copies output `what` of `slot` into host memory `dst` (bytes >= size). */

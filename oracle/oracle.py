@@ -507,6 +507,17 @@ class Port(_Lib):
                          C.c_double(tau), _p(out))
         return out
 
+    def subpixel(self, agg, lo, hi, d, valid):
+        lo = np.ascontiguousarray(lo, np.uint16)
+        hi = np.ascontiguousarray(hi, np.uint16)
+        hh, w = lo.shape
+        off = self.offsets(lo, hi)
+        agg = np.ascontiguousarray(agg, np.uint16)
+        out = np.zeros((hh, w), np.float32)
+        self.lib.or_subpixel(_p(agg), _p(lo), _p(hi), _p(off), _p(np.ascontiguousarray(d, np.int32)),
+                             _p(_u8(valid)), w, hh, _p(out))
+        return out
+
     def render(self, d, valid):
         d, valid = _f64(d), _u8(valid)
         h, w = d.shape

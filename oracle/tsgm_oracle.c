@@ -611,6 +611,31 @@ void or_render(const double* d, const uint8_t* valid, int w, int h, int32_t* od,
     }
 }
 
+/* Extension A22 (tsgm_oracle.h). */
+void or_subpixel(const uint16_t* agg, const uint16_t* lo, const uint16_t* hi,
+                 const uint32_t* offsets, const int32_t* d, const uint8_t* valid, int w, int h,
+                 float* out) {
+    const size_t np = (size_t)w * h;
+    for (size_t i = 0; i < np; ++i) {
+        out[i] = 0.0f;
+        if (!valid[i]) continue;
+        const int dd = d[i], l = lo[i], u = hi[i];
+        const uint16_t* s = agg + offsets[i];
+        if (dd - 1 < l || dd + 1 > u) {
+            out[i] = (float)dd;
+            continue;
+        }
+        const int sm1 = s[dd - 1 - l], s0 = s[dd - l], sp1 = s[dd + 1 - l];
+        const int den = sm1 - 2 * s0 + sp1;
+        if (den <= 0) {
+            out[i] = (float)dd;
+            continue;
+        }
+        const float off = (float)(sm1 - sp1) / (2.0f * (float)den);
+        out[i] = (float)dd + off;
+    }
+}
+
 /* step, src/temporal_filter.cpp:195-232 */
 int or_step(const double* sd, const double* sp, const uint8_t* sv, int state_w, int state_h,
             const uint8_t* left, const uint8_t* right, int w, int h, const double* r9,

@@ -13,9 +13,11 @@ TSGM_OK, TSGM_INVALID_ARGUMENT, TSGM_RUNTIME_ERROR = 0, 1, 2
 OUT = dict(
     state_d=0, state_p=1, state_valid=2, export_d=3, export_valid=4, diff=5, mask=6,
     pred_d=7, pred_p=8, pred_valid=9, lo=10, hi=11, meas_d=12, meas_valid=13, offsets=14,
-    cost=15, agg=16,
+    cost=15, agg=16, subpixel=17,
 )
 TSGM_KEEP_VOLUMES = 1
+TSGM_FORCE_SCANLINE_AGG = 2
+TSGM_SUBPIXEL = 4
 
 
 class SgmParamsC(C.Structure):

@@ -339,8 +339,18 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
 constexpr int kCwThreads = 512;
 constexpr int kCwPix = 128;
 
+// Sub-pixel extension (A22, not in the reference): parabola vertex through
+// S(d-1), S(d), S(d+1) of the WTA level d when both neighbours are in the
+// window and the curvature is positive; else d. f32, IEEE ops in this order.
+__device__ __forceinline__ float subpixel_of(int d, int sm1, int s0, int sp1, bool have) {
+    const int den = sm1 - 2 * s0 + sp1;
+    if (!have || den <= 0) return static_cast<float>(d);
+    const float off = __fdiv_rn(static_cast<float>(sm1 - sp1), __fmul_rn(2.0f, static_cast<float>(den)));
+    return __fadd_rn(static_cast<float>(d), off);
+}
+
 __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndir, int write_s,
-                                                                 int do_wta) {
+                                                                 int do_wta, int subpix) {
     extern __shared__ uint32_t cw[];
     const int W = b.W, H = b.H;
     const int qmax = (b.d_max - 1) / 4 + 1;
@@ -348,6 +358,7 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
     uint32_t* lh = qo + kCwPix + 1;        // kCwPix lo | hi << 16
     uint32_t* cl = lh + kCwPix;            // kCwPix cell offsets
     uint32_t* key = cl + kCwPix;           // kCwPix * qmax per-quad minima
+    uint2* qsum = reinterpret_cast<uint2*>(key + kCwPix * qmax);  // (subpix) S of every quad
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
@@ -390,6 +401,8 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
                 best = min(best, ok ? ((v[u] << 16) | static_cast<uint32_t>(lv)) : 0xffffffffu);
             }
             key[l * qmax + k] = best;
+            if (subpix)
+                qsum[l * qmax + k] = make_uint2((se & 0xffffu) | (so << 16), (se >> 16) | (so & 0xffff0000u));
         }
         __syncthreads();
         if (do_wta) {
@@ -402,6 +415,19 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
                                  y >= kCensusRadius && y < H - kCensusRadius;
                 b.md[pbase + x] = def ? static_cast<int32_t>(best & 0xffffu) : 0;
                 b.mv[pbase + x] = def ? 1 : 0;
+                if (subpix) {
+                    const int lo = static_cast<int>(lh[i] & 0xffffu), hi = static_cast<int>(lh[i] >> 16);
+                    const int d = static_cast<int>(best & 0xffffu);
+                    auto s_at = [&](int lv) -> int {
+                        const uint2 qq = qsum[i * qmax + (lv >> 2) - (lo >> 2)];
+                        const uint32_t wv = (lv & 2) ? qq.y : qq.x;
+                        return static_cast<int>((lv & 1) ? (wv >> 16) : (wv & 0xffffu));
+                    };
+                    const bool have = d - 1 >= lo && d + 1 <= hi;
+                    const float sp = subpixel_of(d, have ? s_at(d - 1) : 0, static_cast<int>(best >> 16),
+                                                 have ? s_at(d + 1) : 0, have);
+                    b.sub[pbase + x] = def ? sp : 0.0f;
+                }
             }
         }
         __syncthreads();
@@ -409,7 +435,7 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
 }
 
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
-                            int write_s, int do_wta, Launch L) {
+                            int write_s, int do_wta, Launch L, int subpix) {
     ScanParams sp{};
     sp.p1 = p1;
     sp.p2 = p2;
@@ -431,9 +457,13 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int tasks = sp.task_off[k] * n;
     const size_t smem = static_cast<size_t>(kScanWarps) * 32 * (scan_slot_bytes(b.d_max) + 4);
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
-    const size_t cwsmem = sizeof(uint32_t) *
-                          (3 * kCwPix + 1 + static_cast<size_t>(kCwPix) * ((b.d_max - 1) / 4 + 1));
-    combine_wta_kernel<<<dim3(b.H, n), kCwThreads, cwsmem, L.st>>>(b, k, write_s, do_wta);
+    const size_t qm = static_cast<size_t>((b.d_max - 1) / 4 + 1);
+    const size_t cwsmem = sizeof(uint32_t) * (3 * kCwPix + 1 + kCwPix * qm) +
+                          (subpix ? sizeof(uint2) * kCwPix * qm + 8 : 0);
+    cudaFuncSetAttribute(combine_wta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(cwsmem));
+    combine_wta_kernel<<<dim3(b.H, n), kCwThreads, cwsmem, L.st>>>(b, k, write_s, do_wta,
+                                                                   subpix);
     *L.counter += 2;
 }
 

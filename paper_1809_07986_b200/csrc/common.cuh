@@ -55,9 +55,10 @@ struct Bufs {
     // WTA, render, export (A15, A18, A19)
     int32_t *md, *rd, *ed;
     uint8_t *mv, *rv, *ev;
-    // diff, mask (A17, A21)
+    // diff, mask (A17, A21); optional sub-pixel WTA (A22 extension)
     double* diff;
     uint8_t* mask;
+    float* sub;
     // per active index: 4x4 homography (row-major), A4
     const double* H16;
 };
@@ -135,6 +136,6 @@ bool sweep_supported(int W, int H, int d_max, int p2);
 // write_s: store S in the ragged volume; do_wta: fuse winner_takes_all
 // (writes md/mv). At least one of the two must be set.
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
-                            int write_s, int do_wta, Launch L);
+                            int write_s, int do_wta, Launch L, int subpix = 0);
 
 }  // namespace tsgm

@@ -325,6 +325,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.ev = ctx->dalloc<uint8_t>(S * P);
     b.diff = ctx->dalloc<double>(S * P);
     b.mask = ctx->dalloc<uint8_t>(S * P);
+    b.sub = (c.flags & TSGM_SUBPIXEL) ? ctx->dalloc<float>(S * P) : nullptr;
     ctx->d_slots = ctx->dalloc<int>(S);
     ctx->d_left = ctx->dalloc<const uint8_t*>(S);
     ctx->d_right = ctx->dalloc<const uint8_t*>(S);
@@ -389,9 +390,11 @@ bool aggregate(tsgm_ctx* ctx, int n, Launch L, bool fuse_wta = false, bool keep_
     const tsgm_config& c = ctx->cfg;
     if (ctx->use_sweep && sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2)) {
         launch_aggregate_sweep(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
-                               (keep_s || !fuse_wta) ? 1 : 0, fuse_wta ? 1 : 0, L);
+                               (keep_s || !fuse_wta) ? 1 : 0, fuse_wta ? 1 : 0, L,
+                               (fuse_wta && ctx->b.sub) ? 1 : 0);
         return fuse_wta;
     }
+    if (ctx->b.sub) bad("TSGM_SUBPIXEL needs the scan aggregation (P2 + 24 <= 255, d_max <= 256)");
     launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
     return false;
 }
@@ -462,6 +465,9 @@ OutDesc out_desc(tsgm_ctx* ctx, int what) {
         case TSGM_OUT_OFFSETS: return {b.off, 4, P + 1};
         case TSGM_OUT_COST: return {b.cost, 1, ctx->vol_cap};
         case TSGM_OUT_AGG: return {b.agg, 2, ctx->vol_cap};
+        case TSGM_OUT_SUBPIXEL:
+            if (!b.sub) bad("tsgm_fetch: context created without TSGM_SUBPIXEL");
+            return {b.sub, 4, P};
         default: bad("tsgm_fetch: unknown output");
     }
 }

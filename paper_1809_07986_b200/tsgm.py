@@ -296,7 +296,7 @@ _OUT_DTYPES = dict(state_d=np.float64, state_p=np.float64, state_valid=np.uint8,
                    export_d=np.int32, export_valid=np.uint8, diff=np.float64, mask=np.uint8,
                    pred_d=np.float64, pred_p=np.float64, pred_valid=np.uint8, lo=np.uint16,
                    hi=np.uint16, meas_d=np.int32, meas_valid=np.uint8, offsets=np.uint32,
-                   cost=np.uint8, agg=np.uint16)
+                   cost=np.uint8, agg=np.uint16, subpixel=np.float32)
 
 
 @dataclass
@@ -308,6 +308,7 @@ class EngineConfig:
     device: int = 0
     mask_tau: float = 3.0
     keep_volumes: bool = True
+    subpixel: bool = False  # A22 extension: export-only sub-pixel WTA (f32)
 
 
 class Engine:
@@ -318,7 +319,8 @@ class Engine:
         cal = _as(cfg.calib, StereoCalib)
         c = ConfigC(cal.width, cal.height, cfg.max_slots, cfg.device, cal._c(),
                     _as(cfg.sgm, SgmParams)._c(), _as(cfg.filter, FilterConfig)._c(),
-                    cfg.mask_tau, _lib.TSGM_KEEP_VOLUMES if cfg.keep_volumes else 0)
+                    cfg.mask_tau, (_lib.TSGM_KEEP_VOLUMES if cfg.keep_volumes else 0) |
+                    (_lib.TSGM_SUBPIXEL if cfg.subpixel else 0))
         self._lib = _lib.load()
         h = C.c_void_p()
         check(self._lib.tsgm_create(C.byref(c), C.byref(h)))

@@ -152,3 +152,32 @@ def test_config4_gain_and_occluders(port):
                                         cy=127.5, seed=s) for s in (1, 2)]
     run_parity(port, cfgs, 4, tsgm.SgmParams(10, 120, 8, 0, 256),
                tsgm.FilterConfig(p_init=16384.0, range_use_stddev=True, range_stddev_gain=3.0))
+
+
+def test_subpixel_extension(port):
+    """A22 extension (opt-in, export only): the f32 parabola refinement of the
+    WTA level, bit-exact against the oracle's definition; the integer outputs
+    and the Kalman state are unchanged by it."""
+    cfg = SceneConfig.baseline_config(1, width=320, height=120, focal=200.0, cx=159.5, cy=59.5,
+                                      d_max=64, seed=8, n_movers=2)
+    L, R, P, _ = render(cfg, 0, 3)
+    calib = tsgm.StereoCalib(cfg.focal, cfg.cx, cfg.cy, cfg.baseline, 320, 120, 64)
+    params = tsgm.SgmParams(10, 120, 8, 0, 64)
+    filt = tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=3.0)
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=1, subpixel=True))
+    state = None
+    for k in range(3):
+        m = (np.eye(3), np.zeros(3)) if k == 0 else tsgm.relative_motion(P[k - 1], P[k])
+        eng.step([0], [L[k]], [R[k]], [m])
+        ref = port.step(state, L[k], R[k], m[0], m[1], calib, params, filt, debug=True)
+        np.testing.assert_array_equal(eng.fetch(0, "meas_d"), ref["meas_d"])
+        np.testing.assert_array_equal(eng.fetch(0, "state_p"), ref["p"])
+        _, cost = port.cost_volume(L[k], R[k], ref["lo"], ref["hi"])
+        agg = port.aggregate(cost, ref["lo"], ref["hi"], params)
+        want = port.subpixel(agg, ref["lo"], ref["hi"], ref["meas_d"], ref["meas_valid"])
+        got = eng.fetch(0, "subpixel")
+        np.testing.assert_array_equal(got, want)
+        v = ref["meas_valid"] > 0
+        assert (np.abs(got[v] - ref["meas_d"][v]) <= 0.5).all()
+        state = (ref["d"], ref["p"], ref["valid"])
+    eng.close()
