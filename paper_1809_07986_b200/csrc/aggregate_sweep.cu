@@ -29,7 +29,7 @@
 
 namespace tsgm {
 
-constexpr int kScanWarps = 4;  // warps per CTA (one task each)
+constexpr int kScanWarps = 2;  // warps per CTA (one task each)
 
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
 __host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
@@ -206,10 +206,12 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
     const int task = blockIdx.x * kScanWarps + warp;
     const int per_slot = sp.task_off[sp.ndir];
     if (task >= per_slot * sp.n) return;
-    const int a = task / per_slot, r = task % per_slot;
+    // direction-major over all slots: the long horizontal tasks start first
     int d = 0;
-    while (r >= sp.task_off[d + 1]) ++d;
-    const int g = r - sp.task_off[d];
+    while (task >= sp.task_off[d + 1] * sp.n) ++d;
+    const int r = task - sp.task_off[d] * sp.n;
+    const int groups = sp.task_off[d + 1] - sp.task_off[d];
+    const int a = r / groups, g = r % groups;
     const int s = slot_of(b, a);
     const int W = b.W, H = b.H;
     const int dx = sp.dx[d], dy = sp.dy[d];
@@ -358,7 +360,8 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
     uint32_t* lh = qo + kCwPix + 1;        // kCwPix lo | hi << 16
     uint32_t* cl = lh + kCwPix;            // kCwPix cell offsets
     uint32_t* key = cl + kCwPix;           // kCwPix * qmax per-quad minima
-    uint2* qsum = reinterpret_cast<uint2*>(key + kCwPix * qmax);  // (subpix) S of every quad
+    uint2* qsum = reinterpret_cast<uint2*>(  // (subpix) S of every quad, 8-byte aligned
+        (reinterpret_cast<uintptr_t>(key + kCwPix * qmax) + 7) & ~static_cast<uintptr_t>(7));
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
