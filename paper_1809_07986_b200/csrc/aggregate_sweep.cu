@@ -103,11 +103,32 @@ struct PixMeta {
 // quads [lg*Q, lg*Q + Q) of the window. All lanes of the warp call it (pix =
 // false: no pixel for this group; everything masked, nothing stored). `sb` /
 // `rp` are the shared addresses of the scanline's slot and quad range.
+// Cost words of a lane's Q quads (Q + 1 aligned words + funnel shift).
+template <int Q>
+struct CostWords {
+    uint32_t c[Q + 1];
+    uint32_t sh;
+};
+
 template <int G, int Q>
+__device__ __forceinline__ void load_costs(const PixMeta& pm, const uint8_t* cost, CostWords<Q>& cw) {
+    const int lg = static_cast<int>(threadIdx.x & (G - 1));
+    const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
+    const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
+    const int a0 = q0 + min(lg * Q, nq - 1);
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
+    const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+    cw.sh = 8u * static_cast<uint32_t>(addr & 3);
+#pragma unroll
+    for (int t = 0; t <= Q; ++t) cw.c[t] = __ldg(aw + t);
+}
+
+template <int G, int Q, bool kPreloaded = false>
 __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has_pred,
                                            uint32_t sb, uint32_t rp, const uint8_t* cost,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
-                                           uint32_t P2x4, const uint8_t* mask_tab) {
+                                           uint32_t P2x4, const uint8_t* mask_tab,
+                                           const CostWords<Q>* pre = nullptr) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
@@ -118,12 +139,11 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     bool act[Q];
     {
         // matching costs of levels 4*a0 .. 4*a0 + 4Q - 1 (bytes outside the window masked)
-        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
-        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-        const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
-        uint32_t c[Q + 1];
-#pragma unroll
-        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
+        CostWords<Q> cwl;
+        if (kPreloaded) cwl = *pre;
+        else load_costs<G, Q>(pm, cost, cwl);
+        const uint32_t* c = cwl.c;
+        const uint32_t sh = cwl.sh;
         // invalid-level masks of the lane's 16 levels from the table:
         // row = levels below lo in the first quad, col = last valid level + 1
         const int start = 4 * (q0 + k0);  // unclamped first level of the lane
@@ -265,6 +285,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
     bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
     PixMeta m2{0u, 0u, 0u};
     if (act2) load_meta(p_tmp, m2);
+    CostWords<4> cw_nxt;
+    if (act1) load_costs<1, 4>(m1, cost, cw_nxt);
     for (int k = 0; k < nsteps; ++k) {
         const bool active = act1;
         const PixMeta mc = m1;
@@ -278,15 +300,17 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
+        const CostWords<4> cw_cur = cw_nxt;  // this step's narrow costs
+        if (act1) load_costs<1, 4>(m1, cost, cw_nxt);
         if (__ballot_sync(0xffffffffu, active) == 0u) {
             prev_active = false;
             continue;
         }
         const int nq = static_cast<int>(mc.lohi >> 18) - static_cast<int>((mc.lohi & 0xffffu) >> 2) + 1;
         const bool narrow = active && nq <= 4;
-        // windows of <= 4 quads: the lane itself
-        scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                         mask_tab);
+        // windows of <= 4 quads: the lane itself, costs loaded a step ahead
+        scan_pixel<1, 4, true>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                               mask_tab, &cw_cur);
         // wider windows: 8 lanes x 4 quads (<= 128 levels), 4 windows per pass
         unsigned bw = __ballot_sync(0xffffffffu, active && !narrow && nq <= 32);
         while (bw) {
