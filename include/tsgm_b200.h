@@ -77,7 +77,15 @@ typedef struct {
     tsgm_sgm_params sgm;
     tsgm_filter_config filter;
     double mask_tau;           /* A21 extension: Mahalanobis gate, 3.0 */
-    uint32_t flags;            /* TSGM_KEEP_VOLUMES */
+    uint32_t flags;            /* TSGM_KEEP_VOLUMES | TSGM_FORCE_SCANLINE_AGG | TSGM_SUBPIXEL */
+    /* Volume working set: how many sequences' per-frame volumes (C, S and the
+     * per-direction path costs, up to ~9 B per cell of W*H*d_max) are resident
+     * at once. The Kalman state and per-pixel outputs are always resident for
+     * all max_slots; a step over more sequences than vol_slots runs the
+     * matching stages in balanced chunks. 0 = auto: max_slots, capped to what
+     * fits the device's free memory (config 4: 2048x1024, D=256, 32 sequences
+     * needs ~6 GB of volumes per sequence). */
+    int32_t vol_slots;
 } tsgm_config;
 
 const char* tsgm_last_error(void);
@@ -124,8 +132,8 @@ enum {
     TSGM_OUT_MEAS_D = 12,   /* i32 WTA (sgm_match)    */
     TSGM_OUT_MEAS_VALID = 13,
     TSGM_OUT_OFFSETS = 14,  /* u32 W*H+1              */
-    TSGM_OUT_COST = 15,     /* u8 N   (TSGM_KEEP_VOLUMES) */
-    TSGM_OUT_AGG = 16,      /* u16 N  (TSGM_KEEP_VOLUMES) */
+    TSGM_OUT_COST = 15,     /* u8 N   (TSGM_KEEP_VOLUMES; slot in the last volume chunk) */
+    TSGM_OUT_AGG = 16,      /* u16 N  (TSGM_KEEP_VOLUMES; slot in the last volume chunk) */
     TSGM_OUT_SUBPIXEL = 17, /* f32 sub-pixel WTA disparity (TSGM_SUBPIXEL), 0 where invalid */
     TSGM_OUT_COUNT
 };
@@ -148,6 +156,8 @@ int tsgm_timer_begin(tsgm_ctx* ctx);
 int tsgm_timer_end(tsgm_ctx* ctx, float* ms);
 int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t reps,
                          float* ms_per_launch, uint64_t* cells);
+/* Volume working set chosen at creation (see tsgm_config.vol_slots). */
+int tsgm_volume_slots(tsgm_ctx* ctx, int32_t* vol_slots);
 /* Kernel launches issued by the context since creation (all stages). */
 uint64_t tsgm_launch_count(tsgm_ctx* ctx);
 

@@ -182,7 +182,8 @@ inline DisparityState correct(const DisparityState& pred, const DisparityMap& me
 class Engine {
 public:
     Engine(const StereoCalib& calib, const SgmParams& params, const FilterConfig& cfg,
-           int max_slots, int device = 0, double mask_tau = 3.0, unsigned flags = 0) {
+           int max_slots, int device = 0, double mask_tau = 3.0, unsigned flags = 0,
+           int vol_slots = 0) {
         tsgm_config c{};
         c.width = calib.width;
         c.height = calib.height;
@@ -193,6 +194,7 @@ public:
         c.filter = detail::to_c(cfg);
         c.mask_tau = mask_tau;
         c.flags = flags;
+        c.vol_slots = vol_slots;
         detail::check(tsgm_create(&c, &ctx_));
         w_ = calib.width;
         h_ = calib.height;

@@ -40,7 +40,8 @@ class StereoCalibC(C.Structure):
 class ConfigC(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("max_slots", C.c_int32),
                 ("device", C.c_int32), ("calib", StereoCalibC), ("sgm", SgmParamsC),
-                ("filter", FilterConfigC), ("mask_tau", C.c_double), ("flags", C.c_uint32)]
+                ("filter", FilterConfigC), ("mask_tau", C.c_double), ("flags", C.c_uint32),
+                ("vol_slots", C.c_int32)]
 
 
 _lib = None
@@ -49,7 +50,7 @@ _lib = None
 EXPORTS = [
     "tsgm_last_error", "tsgm_create", "tsgm_destroy", "tsgm_reset", "tsgm_set_state",
     "tsgm_step", "tsgm_step_device", "tsgm_fetch", "tsgm_fetch_batch", "tsgm_cells", "tsgm_sync",
-    "tsgm_timer_begin", "tsgm_timer_end", "tsgm_bench_aggregate", "tsgm_launch_count",
+    "tsgm_timer_begin", "tsgm_timer_end", "tsgm_bench_aggregate", "tsgm_volume_slots", "tsgm_launch_count",
     "tsgm_census_transform", "tsgm_build_cost_volume", "tsgm_aggregate_paths",
     "tsgm_winner_takes_all", "tsgm_median_refine", "tsgm_sgm_match", "tsgm_relative_motion",
     "tsgm_disparity_homography", "tsgm_warp_state_ex", "tsgm_predict",
@@ -83,6 +84,7 @@ def load():
                                          C.c_size_t]
         lib.tsgm_cells.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64)]
         lib.tsgm_sync.argtypes = [C.c_void_p]
+        lib.tsgm_volume_slots.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         lib.tsgm_timer_begin.argtypes = [C.c_void_p]
         lib.tsgm_timer_end.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
         lib.tsgm_bench_aggregate.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,

@@ -103,32 +103,11 @@ struct PixMeta {
 // quads [lg*Q, lg*Q + Q) of the window. All lanes of the warp call it (pix =
 // false: no pixel for this group; everything masked, nothing stored). `sb` /
 // `rp` are the shared addresses of the scanline's slot and quad range.
-// Cost words of a lane's Q quads (Q + 1 aligned words + funnel shift).
-template <int Q>
-struct CostWords {
-    uint32_t c[Q + 1];
-    uint32_t sh;
-};
-
 template <int G, int Q>
-__device__ __forceinline__ void load_costs(const PixMeta& pm, const uint8_t* cost, CostWords<Q>& cw) {
-    const int lg = static_cast<int>(threadIdx.x & (G - 1));
-    const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
-    const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
-    const int a0 = q0 + min(lg * Q, nq - 1);
-    const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
-    const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-    cw.sh = 8u * static_cast<uint32_t>(addr & 3);
-#pragma unroll
-    for (int t = 0; t <= Q; ++t) cw.c[t] = __ldg(aw + t);
-}
-
-template <int G, int Q, bool kPreloaded = false>
 __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has_pred,
                                            uint32_t sb, uint32_t rp, const uint8_t* cost,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
-                                           uint32_t P2x4, const uint8_t* mask_tab,
-                                           const CostWords<Q>* pre = nullptr) {
+                                           uint32_t P2x4, const uint8_t* mask_tab) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
@@ -139,11 +118,12 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     bool act[Q];
     {
         // matching costs of levels 4*a0 .. 4*a0 + 4Q - 1 (bytes outside the window masked)
-        CostWords<Q> cwl;
-        if (kPreloaded) cwl = *pre;
-        else load_costs<G, Q>(pm, cost, cwl);
-        const uint32_t* c = cwl.c;
-        const uint32_t sh = cwl.sh;
+        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+        const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
+        uint32_t c[Q + 1];
+#pragma unroll
+        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
         // invalid-level masks of the lane's 16 levels from the table:
         // row = levels below lo in the first quad, col = last valid level + 1
         const int start = 4 * (q0 + k0);  // unclamped first level of the lane
@@ -248,9 +228,9 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
     const uint32_t* lohi = b.lohi + static_cast<size_t>(s) * b.P;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
     const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1);
-    const uint8_t* cost = b.cost + static_cast<size_t>(s) * b.vol_cap;
+    const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
     uint32_t* out = reinterpret_cast<uint32_t*>(
-        b.pdir + (static_cast<size_t>(d) * b.max_slots + s) * b.quad_cap * 4);
+        b.pdir + (static_cast<size_t>(d) * b.vol_slots + a) * b.quad_cap * 4);
 
     // line geometry: horizontal directions sweep x with lane = row; the others
     // sweep y with lane = line c, pixel x = c + sl*y (sl = dx*dy)
@@ -285,8 +265,6 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
     bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
     PixMeta m2{0u, 0u, 0u};
     if (act2) load_meta(p_tmp, m2);
-    CostWords<4> cw_nxt;
-    if (act1) load_costs<1, 4>(m1, cost, cw_nxt);
     for (int k = 0; k < nsteps; ++k) {
         const bool active = act1;
         const PixMeta mc = m1;
@@ -300,17 +278,15 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
-        const CostWords<4> cw_cur = cw_nxt;  // this step's narrow costs
-        if (act1) load_costs<1, 4>(m1, cost, cw_nxt);
         if (__ballot_sync(0xffffffffu, active) == 0u) {
             prev_active = false;
             continue;
         }
         const int nq = static_cast<int>(mc.lohi >> 18) - static_cast<int>((mc.lohi & 0xffffu) >> 2) + 1;
         const bool narrow = active && nq <= 4;
-        // windows of <= 4 quads: the lane itself, costs loaded a step ahead
-        scan_pixel<1, 4, true>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                               mask_tab, &cw_cur);
+        // windows of <= 4 quads: the lane itself
+        scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                         mask_tab);
         // wider windows: 8 lanes x 4 quads (<= 128 levels), 4 windows per pass
         unsigned bw = __ballot_sync(0xffffffffu, active && !narrow && nq <= 32);
         while (bw) {
@@ -389,9 +365,9 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
-    const size_t dstride = static_cast<size_t>(b.max_slots) * b.quad_cap;
-    const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) + static_cast<size_t>(s) * b.quad_cap;
-    uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap;
+    const size_t dstride = static_cast<size_t>(b.vol_slots) * b.quad_cap;
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) + static_cast<size_t>(a) * b.quad_cap;
+    uint16_t* agg = b.agg + static_cast<size_t>(a) * b.vol_cap;
     for (int x0 = 0; x0 < W; x0 += kCwPix) {
         const int np = min(kCwPix, W - x0);
         const uint32_t qbase = b.qoff[obase + x0];

@@ -1,11 +1,12 @@
 // Shared device-side definitions for the tsgm sm_100a kernels.
 //
 // Batched layout in HBM: every per-pixel map is slot-major, [max_slots][W*H]
-// (offsets: [max_slots][W*H+1]); ragged cost volumes are [max_slots][cap]
+// (offsets: [max_slots][W*H+1]); ragged cost volumes are [vol_slots][cap]
 // with cap = W*H*d_max cells, cell (x, y, lo+j) at off[y*W+x] + j exactly as in
 // the reference's CostVolume (include/tsgm/matching_cost.hpp:50-73). A launch
 // covers `n` active slots; blockIdx.{y,z} selects the active index a, and
-// slots[a] the slot.
+// slots[a] the slot. Per-pixel maps are indexed by the slot, volumes by a
+// (the volume stages run in chunks of at most vol_slots sequences).
 #pragma once
 
 #include <cstdint>
@@ -18,7 +19,11 @@ constexpr int kMaxCost = 24;      // matching_cost.hpp:13
 
 struct Bufs {
     int W, H, P, d_max;
-    size_t vol_cap;  // cells per slot in cost/agg
+    size_t vol_cap;  // cells per volume position in cost/agg
+    // cost, agg and pdir are indexed by the position a of the slot in the
+    // launch's batch (a volume chunk of at most vol_slots sequences), not by
+    // the slot: only the per-pixel state and outputs are slot-resident
+    int vol_slots;
     const int* slots;  // device [n] slot ids of the active batch
     // posterior state (A2)
     double *sd, *sp;
@@ -44,12 +49,12 @@ struct Bufs {
     uint32_t *sigl, *sigr;
     const uint8_t* const* left;   // device [n] image pointers
     const uint8_t* const* right;
-    uint8_t* cost;   // 16 bytes of padding before slot 0 and after the last slot
-    uint16_t* agg;
+    uint8_t* cost;   // [vol pos][vol_cap]; 16 bytes of padding on both ends
+    uint16_t* agg;   // [vol pos][vol_cap]
     // scanline-group aggregation: per-direction path costs (u8) in the quad
-    // layout (qoff), [dir][slot][quad_cap][4]
+    // layout (qoff), [dir][vol pos][quad_cap][4]
     uint8_t* pdir;
-    size_t quad_cap;  // quads per slot
+    size_t quad_cap;  // quads per volume position
     int max_slots;
     int* work;
     // WTA, render, export (A15, A18, A19)

@@ -179,6 +179,9 @@ struct tsgm_ctx {
     tsgm_config cfg{};
     int W = 0, H = 0, P = 0, d_max = 0, max_slots = 0;
     size_t vol_cap = 0;
+    int vol_slots = 0;            // volume working set (positions of cost/agg/pdir)
+    std::vector<int> vol_owner;   // slot whose volumes sit at each position (-1: none)
+    std::vector<int> h_slots;     // host copy of the current batch's slots
     int device = 0;
     int num_sms = 148;
     bool use_sweep = false;  // line-sweep aggregation (else per-direction scanline kernel)
@@ -304,17 +307,12 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.overflow = ctx->dalloc<int>(S);
     b.sigl = ctx->dalloc<uint32_t>(S * P);
     b.sigr = ctx->dalloc<uint32_t>(S * P);
-    // 16 bytes of padding on both sides: the sweep reads aligned words around
-    // each window
-    b.cost = ctx->dalloc<uint8_t>(S * ctx->vol_cap + 32) + 16;
-    b.agg = ctx->dalloc<uint16_t>(S * ctx->vol_cap);
     const char* force = std::getenv("TSGM_FORCE_SCANLINE_AGG");
     const bool force_scan = (c.flags & TSGM_FORCE_SCANLINE_AGG) || (force && force[0] == '1');
     ctx->use_sweep = !force_scan &&
                      sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2);
     b.quad_cap = P * static_cast<size_t>((ctx->d_max - 1) / 4 + 1);
     b.max_slots = c.max_slots;
-    if (ctx->use_sweep) b.pdir = ctx->dalloc<uint8_t>(8 * S * b.quad_cap * 4);
     b.work = ctx->dalloc<int>(1);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device));
     b.md = ctx->dalloc<int32_t>(S * P);
@@ -331,6 +329,27 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     ctx->d_right = ctx->dalloc<const uint8_t*>(S);
     ctx->d_H = ctx->dalloc<double>(S * 16);
     ctx->d_img = ctx->dalloc<uint8_t>(S * 2 * P);
+    // the per-frame volumes last: C (u8), S (u16) and, for the scan
+    // aggregation, 8 directions of u8 path costs per cell, for vol_slots
+    // sequences at a time (the rest of the batch runs in further chunks)
+    const size_t vol_bytes = 3 * ctx->vol_cap + (ctx->use_sweep ? 8 * b.quad_cap * 4 : 0);
+    int vs = c.vol_slots > 0 ? std::min(c.vol_slots, c.max_slots) : c.max_slots;
+    if (c.vol_slots <= 0) {
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const size_t reserve = size_t(1) << 30;  // headroom for the runtime and fetches
+        const size_t fit = free_b > reserve ? (free_b - reserve) / vol_bytes : 0;
+        vs = static_cast<int>(std::min<size_t>(vs, fit));
+        if (vs < 1) throw std::runtime_error("tsgm_create: device memory too small for one frame's volumes");
+    }
+    ctx->vol_slots = vs;
+    ctx->vol_owner.assign(vs, -1);
+    b.vol_slots = vs;
+    // 16 bytes of padding on both sides: the sweep reads aligned words around
+    // each window
+    b.cost = ctx->dalloc<uint8_t>(vs * ctx->vol_cap + 32) + 16;
+    b.agg = ctx->dalloc<uint16_t>(vs * ctx->vol_cap);
+    if (ctx->use_sweep) b.pdir = ctx->dalloc<uint8_t>(8 * vs * b.quad_cap * 4);
     b.slots = ctx->d_slots;
     b.left = ctx->d_left;
     b.right = ctx->d_right;
@@ -361,6 +380,7 @@ void upload_step(tsgm_ctx* ctx, int n, const int32_t* slots, const uint8_t* cons
     ctx->ring_i = (ctx->ring_i + 1) % kRing;
     if (r.used) CK(cudaEventSynchronize(r.done));
     std::memcpy(r.slots, slots, sizeof(int) * n);
+    ctx->h_slots.assign(slots, slots + n);
     std::memcpy(r.left, dl, sizeof(void*) * n);
     std::memcpy(r.right, dr, sizeof(void*) * n);
     std::memcpy(r.H, H, sizeof(double) * 16 * n);
@@ -386,17 +406,35 @@ void check_slots(tsgm_ctx* ctx, int n, const int32_t* slots) {
 // configuration fits it, else the per-direction scanline kernels. With
 // fuse_wta, winner_takes_all is fused into the combine (S is then written
 // only if keep_s) and the caller skips launch_wta.
-bool aggregate(tsgm_ctx* ctx, int n, Launch L, bool fuse_wta = false, bool keep_s = true) {
+bool aggregate(tsgm_ctx* ctx, const Bufs& b, int n, Launch L, bool fuse_wta = false,
+               bool keep_s = true) {
     const tsgm_config& c = ctx->cfg;
     if (ctx->use_sweep && sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2)) {
-        launch_aggregate_sweep(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
+        launch_aggregate_sweep(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
                                (keep_s || !fuse_wta) ? 1 : 0, fuse_wta ? 1 : 0, L,
-                               (fuse_wta && ctx->b.sub) ? 1 : 0);
+                               (fuse_wta && b.sub) ? 1 : 0);
         return fuse_wta;
     }
-    if (ctx->b.sub) bad("TSGM_SUBPIXEL needs the scan aggregation (P2 + 24 <= 255, d_max <= 256)");
-    launch_aggregate(ctx->b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+    if (b.sub) bad("TSGM_SUBPIXEL needs the scan aggregation (P2 + 24 <= 255, d_max <= 256)");
+    launch_aggregate(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
     return false;
+}
+
+// The batch arrays of a volume chunk starting at batch position c0.
+Bufs chunk_bufs(const Bufs& b, int c0) {
+    Bufs bc = b;
+    bc.slots = b.slots + c0;
+    bc.left = b.left + c0;
+    bc.right = b.right + c0;
+    bc.H16 = b.H16 + 16 * static_cast<size_t>(c0);
+    return bc;
+}
+
+// Volume position of a slot whose volumes are still resident (last chunk).
+int vol_pos(tsgm_ctx* ctx, int slot) {
+    for (int a = 0; a < ctx->vol_slots; ++a)
+        if (ctx->vol_owner[a] == slot) return a;
+    bad("tsgm_fetch: the volumes of this slot are not resident (not in the last volume chunk)");
 }
 
 // The per-frame pipeline of step() (temporal_filter.cpp:195-232) for n slots.
@@ -414,9 +452,18 @@ void run_step(tsgm_ctx* ctx, int n) {
     launch_offsets(b, n, L);
     // sgm_match (A12-A15)
     launch_census(b, n, L);
-    launch_cost(b, n, L);
-    if (!aggregate(ctx, n, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0))
-        launch_wta(b, n, L);
+    // the volume stages in balanced chunks of at most vol_slots sequences;
+    // cost, agg and pdir are indexed by the position within the chunk
+    const int chunks = (n + ctx->vol_slots - 1) / ctx->vol_slots;
+    for (int k = 0, c0 = 0; k < chunks; ++k) {
+        const int m = (n - c0) / (chunks - k);
+        const Bufs bc = chunk_bufs(b, c0);
+        launch_cost(bc, m, L);
+        if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0))
+            launch_wta(bc, m, L);
+        for (int a = 0; a < m; ++a) ctx->vol_owner[a] = ctx->h_slots[c0 + a];
+        c0 += m;
+    }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
     if (ctx->copy_pending) {  // the previous frame's outputs are still being copied out
         CK(cudaStreamWaitEvent(ctx->st, ctx->ev_copied, 0));
@@ -609,9 +656,13 @@ int tsgm_fetch(tsgm_ctx* ctx, int32_t slot, int32_t what, void* dst, size_t byte
         CK(cudaSetDevice(ctx->device));
         const OutDesc o = out_desc(ctx, what);
         size_t count = o.stride;
-        if (what == TSGM_OUT_COST || what == TSGM_OUT_AGG) count = cells_of(ctx, slot);
+        size_t pos = static_cast<size_t>(slot);
+        if (what == TSGM_OUT_COST || what == TSGM_OUT_AGG) {
+            count = cells_of(ctx, slot);
+            pos = static_cast<size_t>(vol_pos(ctx, slot));
+        }
         if (bytes < count * o.elem) bad("tsgm_fetch: destination too small");
-        const char* src = static_cast<const char*>(o.base) + static_cast<size_t>(slot) * o.stride * o.elem;
+        const char* src = static_cast<const char*>(o.base) + pos * o.stride * o.elem;
         CK(cudaMemcpyAsync(dst, src, count * o.elem, cudaMemcpyDeviceToHost, ctx->st));
         sync(ctx);
     });
@@ -669,6 +720,10 @@ int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t
                          float* ms_per_launch, uint64_t* cells) {
     return guarded([&] {
         check_slots(ctx, n, slots);
+        if (n > ctx->vol_slots) bad("tsgm_bench_aggregate: more slots than the volume working set");
+        for (int i = 0; i < n; ++i)
+            if (ctx->vol_owner[i] != slots[i])
+                bad("tsgm_bench_aggregate: slots must be the last volume chunk, in step order");
         CK(cudaSetDevice(ctx->device));
         std::vector<const uint8_t*> dl(n, ctx->d_img), dr(n, ctx->d_img);
         std::vector<double> H(16 * static_cast<size_t>(n), 0.0);
@@ -676,9 +731,9 @@ int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t
         const tsgm_config& c = ctx->cfg;
         Launch L = ctx->L();
         (void)c;
-        aggregate(ctx, n, L);  // warm
+        aggregate(ctx, ctx->b, n, L);  // warm
         CK(cudaEventRecord(ctx->ev0, ctx->st));
-        for (int r = 0; r < reps; ++r) aggregate(ctx, n, L);
+        for (int r = 0; r < reps; ++r) aggregate(ctx, ctx->b, n, L);
         CK(cudaEventRecord(ctx->ev1, ctx->st));
         CK(cudaEventSynchronize(ctx->ev1));
         float ms = 0.f;
@@ -687,6 +742,13 @@ int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t
         unsigned long long total = 0;
         for (int i = 0; i < n; ++i) total += cells_of(ctx, slots[i]);
         *cells = total;
+    });
+}
+
+int tsgm_volume_slots(tsgm_ctx* ctx, int32_t* vol_slots) {
+    return guarded([&] {
+        if (!ctx || !vol_slots) bad("tsgm_volume_slots: null argument");
+        *vol_slots = ctx->vol_slots;
     });
 }
 
@@ -745,7 +807,7 @@ int tsgm_aggregate_paths(const uint8_t* cost, const uint16_t* lo, const uint16_t
         launch_ranges_given(c->b, 1, c->L());
         launch_offsets(c->b, 1, c->L());
         c->cfg.sgm = *params;
-        aggregate(c, 1, c->L());
+        aggregate(c, c->b, 1, c->L());
         d2h(c, agg, c->b.agg, total);
         sync(c);
     });
@@ -806,7 +868,7 @@ int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t
         launch_census(c->b, 1, c->L());
         launch_cost(c->b, 1, c->L());
         c->cfg.sgm = *params;
-        aggregate(c, 1, c->L());
+        aggregate(c, c->b, 1, c->L());
         launch_wta(c->b, 1, c->L());
         d2h(c, d, c->b.md, P);
         d2h(c, valid, c->b.mv, P);

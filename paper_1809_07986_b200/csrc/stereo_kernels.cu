@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
         sr[x] = b.sigr[pbase + x];
     }
     __syncthreads();
-    uint8_t* base = b.cost + static_cast<size_t>(s) * b.vol_cap;
+    uint8_t* base = b.cost + static_cast<size_t>(a) * b.vol_cap;
     const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
     const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
     const int nwarps = static_cast<int>(blockDim.x >> 5);
@@ -298,7 +298,7 @@ __global__ void wta_kernel(Bufs b) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
-    const uint16_t* agg = b.agg + static_cast<size_t>(s) * b.vol_cap;
+    const uint16_t* agg = b.agg + static_cast<size_t>(a) * b.vol_cap;
     for (int i = warp; i < b.P; i += nwarps) {
         const int x = i % b.W, y = i / b.W;
         const size_t pi = static_cast<size_t>(s) * b.P + i;

@@ -309,6 +309,7 @@ class EngineConfig:
     mask_tau: float = 3.0
     keep_volumes: bool = True
     subpixel: bool = False  # A22 extension: export-only sub-pixel WTA (f32)
+    vol_slots: int = 0  # volume working set (0 = auto: max_slots, capped to free memory)
 
 
 class Engine:
@@ -320,7 +321,7 @@ class Engine:
         c = ConfigC(cal.width, cal.height, cfg.max_slots, cfg.device, cal._c(),
                     _as(cfg.sgm, SgmParams)._c(), _as(cfg.filter, FilterConfig)._c(),
                     cfg.mask_tau, (_lib.TSGM_KEEP_VOLUMES if cfg.keep_volumes else 0) |
-                    (_lib.TSGM_SUBPIXEL if cfg.subpixel else 0))
+                    (_lib.TSGM_SUBPIXEL if cfg.subpixel else 0), cfg.vol_slots)
         self._lib = _lib.load()
         h = C.c_void_p()
         check(self._lib.tsgm_create(C.byref(c), C.byref(h)))
@@ -410,6 +411,13 @@ class Engine:
         ms = C.c_float()
         check(self._lib.tsgm_timer_end(self._h, C.byref(ms)))
         return float(ms.value)
+
+    @property
+    def vol_slots(self) -> int:
+        """Sequences whose per-frame volumes are resident at once."""
+        v = C.c_int32()
+        check(self._lib.tsgm_volume_slots(self._h, C.byref(v)))
+        return int(v.value)
 
     def bench_aggregate(self, slots, reps=10):
         """Standalone C -> S aggregation over the slots' current volumes:

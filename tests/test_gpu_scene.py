@@ -18,11 +18,14 @@ OUTS = [("d", "state_d"), ("p", "state_p"), ("valid", "state_valid"),
         ("mask", "mask")]
 
 
-def run_parity(port, cfgs, frames, params, filt, check_volumes=False):
+def run_parity(port, cfgs, frames, params, filt, check_volumes=False, vol_slots=0):
     calib = tsgm.StereoCalib(cfgs[0].focal, cfgs[0].cx, cfgs[0].cy, cfgs[0].baseline,
                              cfgs[0].width, cfgs[0].height, cfgs[0].d_max)
     seqs = [render(c, 0, frames) for c in cfgs]
-    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=len(cfgs) + 1))
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=len(cfgs) + 1,
+                                        vol_slots=vol_slots))
+    if vol_slots:
+        assert eng.vol_slots == vol_slots
     # use non-contiguous slots to exercise the slot indirection
     slots = [i + 1 for i in range(len(cfgs))][::-1]
     states = [None] * len(cfgs)
@@ -54,6 +57,36 @@ def test_config0_full_size(port):
     run_parity(port, [cfg], 8, tsgm.SgmParams(10, 120, 8, 0, 128),
                tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=3.0),
                check_volumes=True)
+
+
+@pytest.mark.parametrize("vol_slots", [1, 2])
+def test_volume_chunks(port, vol_slots):
+    """A batch larger than the volume working set runs the matching stages in
+    chunks (config 4's memory plan): every output still bit-exact."""
+    cfgs = [SceneConfig.baseline_config(1, width=256, height=96, focal=160.0, cx=127.5,
+                                        cy=47.5, d_max=48, seed=s, n_movers=2) for s in range(5)]
+    run_parity(port, cfgs, 4, tsgm.SgmParams(10, 120, 8, 0, 48),
+               tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=3.0),
+               vol_slots=vol_slots)
+
+
+def test_volume_fetch_needs_last_chunk(port):
+    """C/S of a slot are fetchable while its volumes are resident (the last
+    chunk); older chunks' volumes were recycled and the fetch says so."""
+    cfg = SceneConfig.baseline_config(0, width=128, height=64, focal=100.0, cx=63.5, cy=31.5,
+                                      d_max=32, seed=4)
+    L, R, _, _ = render(cfg, 0, 1)
+    calib = tsgm.StereoCalib(cfg.focal, cfg.cx, cfg.cy, cfg.baseline, 128, 64, 32)
+    params, filt = tsgm.SgmParams(10, 120, 8, 0, 32), tsgm.FilterConfig()
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=3, vol_slots=1))
+    eye = (np.eye(3), np.zeros(3))
+    eng.step([0, 1, 2], [L[0]] * 3, [R[0]] * 3, [eye] * 3)
+    ref = port.step(None, L[0], R[0], eye[0], eye[1], calib, params, filt, debug=True)
+    _, cost = port.cost_volume(L[0], R[0], ref["lo"], ref["hi"])
+    np.testing.assert_array_equal(eng.fetch(2, "cost"), cost)
+    with pytest.raises(ValueError, match="not resident"):
+        eng.fetch(0, "cost")
+    eng.close()
 
 
 def test_config1_movers_batched(port):
