@@ -8,8 +8,9 @@
 // diagonal directions: x = c + sl*y, sweeping y) or of one column
 // (horizontal: sweeping x), which keeps the metadata and cost loads
 // coalesced. A pixel whose window spans <= 4 aligned quads of levels is
-// computed by its own lane (4 consecutive quads); wider windows are computed
-// cooperatively, 8 lanes x 4 quads per window, 4 windows per pass. Arithmetic
+// computed by its own lane (Q = 2..4 consecutive quads, the warp's widest);
+// wider windows are computed cooperatively by groups of G = 2, 4, 8 or 16
+// lanes x 4 quads (5-8, 9-16, 17-32, 33-64 quads), 32/G windows per pass. Arithmetic
 // is u16x2 SIMD (VIADDMNMX / VIMNMX .U16x2), two levels per instruction.
 //
 // State. Each scanline keeps its last pixel's normalised path cost
@@ -27,12 +28,16 @@
 // (SgmParams::validate, sgm.cpp:21-22), so the grouping is exact.
 #include "common.cuh"
 
+#include <type_traits>
+
 namespace tsgm {
 
 constexpr int kScanWarps = 2;  // warps per CTA (one task each)
 
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
 __host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
+// shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group sources
+__host__ __device__ inline int scan_warp_bytes(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 64; }
 
 bool sweep_supported(int W, int H, int d_max, int p2) {
     // u8 path costs need 24 + P2 <= 255; a window is <= 16 lanes x 4 quads
@@ -185,7 +190,7 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     if (pix && lg == 0) sts32(rp, static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16));
 }
 
-__global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParams sp) {
+__global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
     // invalid-level masks: entry (lrel, hrel) covers 16 levels = 4 quads x
     // (ivA, ivB); level j is invalid iff j < lrel or j > hrel (hrel in -1..16)
@@ -217,10 +222,11 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
     const int dx = sp.dx[d], dy = sp.dy[d];
     const int SB = scan_slot_bytes(b.d_max);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
-                           static_cast<uint32_t>(warp) * 32u * static_cast<uint32_t>(SB + 4);
+                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(scan_warp_bytes(b.d_max));
     const uint32_t my_sb = wbase + static_cast<uint32_t>(lane) * SB;
     const uint32_t rbase = wbase + 32u * static_cast<uint32_t>(SB);
     const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(lane);
+    const uint32_t srcbase = rbase + 128u;  // 16 group source lanes
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
@@ -284,58 +290,59 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_kernel(Bufs b, ScanParam
         }
         const int nq = static_cast<int>(mc.lohi >> 18) - static_cast<int>((mc.lohi & 0xffffu) >> 2) + 1;
         const bool narrow = active && nq <= 4;
-        // windows of <= 4 quads: the lane itself
-        scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                         mask_tab);
-        // wider windows: 8 lanes x 4 quads (<= 128 levels), 4 windows per pass
-        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow && nq <= 32);
-        while (bw) {
-            const int gi = lane >> 3;
-            const int cntw = __popc(bw);
-            // lane of the gi-th remaining wide window
-            unsigned mk = bw;
-#pragma unroll
-            for (int t = 0; t < 3; ++t)
-                if (t < gi) mk &= mk - 1;
-            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
-            PixMeta pw;
-            pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
-            pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
-            pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
-            const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
-            scan_pixel<8, 4>(gi < cntw, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
-                             rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2, P2x4,
+        // windows of <= 4 quads: the lane itself, Q = the warp's widest such window
+        const int qn = __reduce_max_sync(0xffffffffu, narrow ? nq : 0);
+        if (qn > 3)
+            scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
                              mask_tab);
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (bw) bw &= bw - 1;
-        }
-        // extra-wide windows (<= 256 levels): 16 lanes x 4 quads, 2 per pass
-        unsigned bx = __ballot_sync(0xffffffffu, active && nq > 32);
-        while (bx) {
-            const int gi = lane >> 4;
-            const int cntw = __popc(bx);
-            const unsigned mk = gi ? (bx & (bx - 1)) : bx;
-            const int src = gi < cntw ? __ffs(mk) - 1 : lane;
-            PixMeta pw;
-            pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
-            pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
-            pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
-            const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
-            scan_pixel<16, 4>(gi < cntw, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
-                              rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2,
-                              P2x4, mask_tab);
-            if (bx) bx &= bx - 1;
-            if (bx) bx &= bx - 1;
-        }
+        else if (qn == 3)
+            scan_pixel<1, 3>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                             mask_tab);
+        else if (qn > 0)
+            scan_pixel<1, 2>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                             mask_tab);
+        // wider windows: groups of G lanes x 4 quads, 32/G windows per pass
+        const auto wide = [&](auto gtag, unsigned bw) {
+            constexpr int G = decltype(gtag)::value;
+            constexpr int PER = 32 / G;
+            const int gi = lane / G;
+            while (bw) {
+                const bool mine = (bw >> lane) & 1u;
+                const int rank = __popc(bw & ((1u << lane) - 1u));
+                const bool go = mine && rank < PER;
+                if (go) sts32(srcbase + 4u * static_cast<uint32_t>(rank), static_cast<uint32_t>(lane));
+                const unsigned done = __ballot_sync(0xffffffffu, go);
+                const int cnt = __popc(done);
+                const int src = gi < cnt ? static_cast<int>(lds32(srcbase + 4u * static_cast<uint32_t>(gi))) : lane;
+                __syncwarp();
+                PixMeta pw;
+                pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
+                pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
+                pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
+                const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
+                scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
+                                 rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2,
+                                 P2x4, mask_tab);
+                bw &= ~done;
+            }
+        };
+        const unsigned b2 = __ballot_sync(0xffffffffu, active && nq > 4 && nq <= 8);
+        if (b2) wide(std::integral_constant<int, 2>{}, b2);
+        const unsigned b4 = __ballot_sync(0xffffffffu, active && nq > 8 && nq <= 16);
+        if (b4) wide(std::integral_constant<int, 4>{}, b4);
+        const unsigned b8 = __ballot_sync(0xffffffffu, active && nq > 16 && nq <= 32);
+        if (b8) wide(std::integral_constant<int, 8>{}, b8);
+        const unsigned b16 = __ballot_sync(0xffffffffu, active && nq > 32);
+        if (b16) wide(std::integral_constant<int, 16>{}, b16);
         prev_active = active;
     }
 }
 
 // Fused combine + winner_takes_all (sgm.cpp:163-187) for the production step,
 // also the standalone combine (S only). One CTA per (row, slot), the row taken
-// in chunks of kCwPix pixels: phase 1 runs one thread per QUAD of the chunk
-// (coalesced u32 loads of every direction's path costs, u16x2 sums, S stored
+// in chunks of kCwPix pixels: a shared-memory owner map gives each quad its
+// pixel; phase 1 runs one thread per QUAD of the chunk (coalesced u32 loads of
+// every direction's path costs, all issued up front, u16x2 sums, S stored
 // when requested, the quad's first (S, level) minimum kept in shared memory);
 // phase 2 reduces each pixel's quads to its first argmin.
 constexpr int kCwThreads = 512;
@@ -351,8 +358,9 @@ __device__ __forceinline__ float subpixel_of(int d, int sm1, int s0, int sp1, bo
     return __fadd_rn(static_cast<float>(d), off);
 }
 
-__global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndir, int write_s,
-                                                                 int do_wta, int subpix) {
+template <int NDIR>
+__global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int write_s, int do_wta,
+                                                                 int subpix) {
     extern __shared__ uint32_t cw[];
     const int W = b.W, H = b.H;
     const int qmax = (b.d_max - 1) / 4 + 1;
@@ -360,8 +368,9 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
     uint32_t* lh = qo + kCwPix + 1;        // kCwPix lo | hi << 16
     uint32_t* cl = lh + kCwPix;            // kCwPix cell offsets
     uint32_t* key = cl + kCwPix;           // kCwPix * qmax per-quad minima
+    uint8_t* own = reinterpret_cast<uint8_t*>(key + kCwPix * qmax);  // pixel of each quad
     uint2* qsum = reinterpret_cast<uint2*>(  // (subpix) S of every quad, 8-byte aligned
-        (reinterpret_cast<uintptr_t>(key + kCwPix * qmax) + 7) & ~static_cast<uintptr_t>(7));
+        (reinterpret_cast<uintptr_t>(own + kCwPix * qmax) + 7) & ~static_cast<uintptr_t>(7));
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
@@ -378,18 +387,20 @@ __global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int ndi
         }
         if (threadIdx.x == 0) qo[np] = b.qoff[obase + x0 + np] - qbase;
         __syncthreads();
+        for (int i = threadIdx.x; i < np; i += blockDim.x)
+            for (uint32_t q = qo[i]; q < qo[i + 1]; ++q) own[q] = static_cast<uint8_t>(i);
+        __syncthreads();
         const uint32_t nq = qo[np];
         for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
-            int l = 0, r = np;  // pixel of quad q
-            while (r - l > 1) {
-                const int m = (l + r) >> 1;
-                if (qo[m] <= q) l = m; else r = m;
-            }
+            uint32_t w[NDIR];
+#pragma unroll
+            for (int d = 0; d < NDIR; ++d) w[d] = __ldg(pd + d * dstride + qbase + q);
+            const int l = own[q];
             uint32_t se = 0u, so = 0u;
-            for (int d = 0; d < ndir; ++d) {
-                const uint32_t w = __ldg(pd + d * dstride + qbase + q);
-                se += __byte_perm(w, 0u, 0x4240u);  // levels 0, 2 (u16 lanes never carry)
-                so += __byte_perm(w, 0u, 0x4341u);  // levels 1, 3
+#pragma unroll
+            for (int d = 0; d < NDIR; ++d) {
+                se += __byte_perm(w[d], 0u, 0x4240u);  // levels 0, 2 (u16 lanes never carry)
+                so += __byte_perm(w[d], 0u, 0x4341u);  // levels 1, 3
             }
             const int lo = static_cast<int>(lh[l] & 0xffffu), hi = static_cast<int>(lh[l] >> 16);
             const int k = static_cast<int>(q - qo[l]);
@@ -458,15 +469,15 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         sp.task_off[i + 1] = sp.task_off[i] + (lines + 31) / 32;
     }
     const int tasks = sp.task_off[k] * n;
-    const size_t smem = static_cast<size_t>(kScanWarps) * 32 * (scan_slot_bytes(b.d_max) + 4);
+    const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max);
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
     const size_t qm = static_cast<size_t>((b.d_max - 1) / 4 + 1);
-    const size_t cwsmem = sizeof(uint32_t) * (3 * kCwPix + 1 + kCwPix * qm) +
+    const size_t cwsmem = sizeof(uint32_t) * (3 * kCwPix + 1 + kCwPix * qm) + kCwPix * qm +
                           (subpix ? sizeof(uint2) * kCwPix * qm + 8 : 0);
-    cudaFuncSetAttribute(combine_wta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = k == 8 ? combine_wta_kernel<8> : combine_wta_kernel<4>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(cwsmem));
-    combine_wta_kernel<<<dim3(b.H, n), kCwThreads, cwsmem, L.st>>>(b, k, write_s, do_wta,
-                                                                   subpix);
+    kern<<<dim3(b.H, n), kCwThreads, cwsmem, L.st>>>(b, write_s, do_wta, subpix);
     *L.counter += 2;
 }
 
