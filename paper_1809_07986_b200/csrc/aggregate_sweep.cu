@@ -339,14 +339,25 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
 }
 
 // Fused combine + winner_takes_all (sgm.cpp:163-187) for the production step,
-// also the standalone combine (S only). One CTA per (row, slot), the row taken
-// in chunks of kCwPix pixels: a shared-memory owner map gives each quad its
-// pixel; phase 1 runs one thread per QUAD of the chunk (coalesced u32 loads of
-// every direction's path costs, all issued up front, u16x2 sums, S stored
-// when requested, the quad's first (S, level) minimum kept in shared memory);
-// phase 2 reduces each pixel's quads to its first argmin.
-constexpr int kCwThreads = 512;
-constexpr int kCwPix = 128;
+// also the standalone combine (S only). ONE WARP per 32-pixel chunk of a row,
+// independent of every other warp (no block barriers): a shared-memory owner
+// map gives each quad of the chunk its pixel; lanes stride the chunk's quads,
+// two at a time, with every direction's u32 path-cost word loaded up front
+// (coalesced), u16x2 sums, S stored when requested and the quad's first
+// (S, level) minimum kept in shared memory; then lane = pixel reduces its
+// quads to the first argmin.
+constexpr int kCwWarps = 8;
+
+// per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
+// key[32*qmax] (u32), qsum[32*qmax] (uint2, sub-pixel only)
+__host__ __device__ inline size_t cw_warp_bytes(int d_max, int subpix) {
+    const size_t qm = static_cast<size_t>((d_max - 1) / 4 + 1);
+    size_t bytes = 4 * 100 + 32 * qm;       // qo, lh, cl + own
+    bytes = (bytes + 7) & ~static_cast<size_t>(7);
+    bytes += 4 * 32 * qm;                    // key
+    if (subpix) bytes += 8 * 32 * qm;        // qsum (8-byte aligned)
+    return bytes;
+}
 
 // Sub-pixel extension (A22, not in the reference): parabola vertex through
 // S(d-1), S(d), S(d+1) of the WTA level d when both neighbours are in the
@@ -359,92 +370,116 @@ __device__ __forceinline__ float subpixel_of(int d, int sm1, int s0, int sp1, bo
 }
 
 template <int NDIR>
-__global__ void __launch_bounds__(kCwThreads) combine_wta_kernel(Bufs b, int write_s, int do_wta,
-                                                                 int subpix) {
-    extern __shared__ uint32_t cw[];
+__global__ void __launch_bounds__(32 * kCwWarps) combine_wta_kernel(Bufs b, int n, int write_s,
+                                                                    int do_wta, int subpix) {
+    extern __shared__ __align__(16) uint8_t cwm[];
     const int W = b.W, H = b.H;
     const int qmax = (b.d_max - 1) / 4 + 1;
-    uint32_t* qo = cw;                     // kCwPix + 1 chunk-relative quad offsets
-    uint32_t* lh = qo + kCwPix + 1;        // kCwPix lo | hi << 16
-    uint32_t* cl = lh + kCwPix;            // kCwPix cell offsets
-    uint32_t* key = cl + kCwPix;           // kCwPix * qmax per-quad minima
-    uint8_t* own = reinterpret_cast<uint8_t*>(key + kCwPix * qmax);  // pixel of each quad
-    uint2* qsum = reinterpret_cast<uint2*>(  // (subpix) S of every quad, 8-byte aligned
-        (reinterpret_cast<uintptr_t>(own + kCwPix * qmax) + 7) & ~static_cast<uintptr_t>(7));
-    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
-    const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
-    const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
+    const int lane = static_cast<int>(threadIdx.x & 31), wib = static_cast<int>(threadIdx.x >> 5);
+    const int chunks = (W + 31) / 32;
+    const long long task = static_cast<long long>(blockIdx.x) * kCwWarps + wib;
+    if (task >= static_cast<long long>(chunks) * H * n) return;
+    const int a = static_cast<int>(task / (static_cast<long long>(chunks) * H));
+    const int rem = static_cast<int>(task % (static_cast<long long>(chunks) * H));
+    const int y = rem / chunks, x0 = (rem % chunks) * 32;
+    const int s = slot_of(b, a);
+    uint8_t* wsm = cwm + static_cast<size_t>(wib) * cw_warp_bytes(b.d_max, subpix);
+    uint32_t* qo = reinterpret_cast<uint32_t*>(wsm);  // 33 chunk-relative quad offsets
+    uint32_t* lh = qo + 36;                             // lo | hi << 16
+    uint32_t* cl = lh + 32;                             // cell offsets
+    uint8_t* own = reinterpret_cast<uint8_t*>(cl + 32); // pixel of each quad
+    uint32_t* key = reinterpret_cast<uint32_t*>(
+        (reinterpret_cast<uintptr_t>(own + 32 * qmax) + 7) & ~static_cast<uintptr_t>(7));
+    uint2* qsum = reinterpret_cast<uint2*>(key + 32 * qmax);  // 8-byte aligned (qmax*128 bytes)
+
+    const int np = min(32, W - x0);
+    const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W + x0;
+    const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W + x0;
     const size_t dstride = static_cast<size_t>(b.vol_slots) * b.quad_cap;
     const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) + static_cast<size_t>(a) * b.quad_cap;
     uint16_t* agg = b.agg + static_cast<size_t>(a) * b.vol_cap;
-    for (int x0 = 0; x0 < W; x0 += kCwPix) {
-        const int np = min(kCwPix, W - x0);
-        const uint32_t qbase = b.qoff[obase + x0];
-        for (int i = threadIdx.x; i < np; i += blockDim.x) {
-            qo[i] = b.qoff[obase + x0 + i] - qbase;
-            lh[i] = b.lohi[pbase + x0 + i];
-            cl[i] = b.off[obase + x0 + i];
-        }
-        if (threadIdx.x == 0) qo[np] = b.qoff[obase + x0 + np] - qbase;
-        __syncthreads();
-        for (int i = threadIdx.x; i < np; i += blockDim.x)
-            for (uint32_t q = qo[i]; q < qo[i + 1]; ++q) own[q] = static_cast<uint8_t>(i);
-        __syncthreads();
-        const uint32_t nq = qo[np];
-        for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
-            uint32_t w[NDIR];
+
+    uint32_t my_q = 0, my_lh = 0;
+    if (lane < np) {
+        my_q = __ldg(b.qoff + obase + lane);
+        my_lh = __ldg(b.lohi + pbase + lane);
+        cl[lane] = __ldg(b.off + obase + lane);
+    }
+    const uint32_t qbase = __shfl_sync(0xffffffffu, my_q, 0);
+    const int my_nq = lane < np ? static_cast<int>(my_lh >> 18) - static_cast<int>((my_lh & 0xffffu) >> 2) + 1 : 0;
+    const uint32_t rq = my_q - qbase;
+    if (lane < np) {
+        qo[lane] = rq;
+        lh[lane] = my_lh;
+        for (int k = 0; k < my_nq; ++k) own[rq + k] = static_cast<uint8_t>(lane);
+    }
+    const uint32_t nq = __shfl_sync(0xffffffffu, rq + static_cast<uint32_t>(my_nq), np - 1);
+    __syncwarp();
+
+    auto finish = [&](uint32_t q, const uint32_t (&w)[NDIR]) {
+        uint32_t se = 0u, so = 0u;
 #pragma unroll
-            for (int d = 0; d < NDIR; ++d) w[d] = __ldg(pd + d * dstride + qbase + q);
-            const int l = own[q];
-            uint32_t se = 0u, so = 0u;
-#pragma unroll
-            for (int d = 0; d < NDIR; ++d) {
-                se += __byte_perm(w[d], 0u, 0x4240u);  // levels 0, 2 (u16 lanes never carry)
-                so += __byte_perm(w[d], 0u, 0x4341u);  // levels 1, 3
-            }
-            const int lo = static_cast<int>(lh[l] & 0xffffu), hi = static_cast<int>(lh[l] >> 16);
-            const int k = static_cast<int>(q - qo[l]);
-            const int d0 = 4 * ((lo >> 2) + k);
-            const uint32_t v[4] = {se & 0xffffu, so & 0xffffu, se >> 16, so >> 16};
-            uint32_t best = 0xffffffffu;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int lv = d0 + u;
-                const bool ok = lv >= lo && lv <= hi;
-                if (write_s && ok) agg[cl[l] + (lv - lo)] = static_cast<uint16_t>(v[u]);
-                best = min(best, ok ? ((v[u] << 16) | static_cast<uint32_t>(lv)) : 0xffffffffu);
-            }
-            key[l * qmax + k] = best;
-            if (subpix)
-                qsum[l * qmax + k] = make_uint2((se & 0xffffu) | (so << 16), (se >> 16) | (so & 0xffff0000u));
+        for (int d = 0; d < NDIR; ++d) {
+            se += __byte_perm(w[d], 0u, 0x4240u);  // levels 0, 2 (u16 lanes never carry)
+            so += __byte_perm(w[d], 0u, 0x4341u);  // levels 1, 3
         }
-        __syncthreads();
-        if (do_wta) {
-            for (int i = threadIdx.x; i < np; i += blockDim.x) {
-                const int n = static_cast<int>(qo[i + 1] - qo[i]);
-                uint32_t best = 0xffffffffu;
-                for (int k = 0; k < n; ++k) best = min(best, key[i * qmax + k]);
-                const int x = x0 + i;
-                const bool def = x >= kCensusRadius && x < W - kCensusRadius &&
-                                 y >= kCensusRadius && y < H - kCensusRadius;
-                b.md[pbase + x] = def ? static_cast<int32_t>(best & 0xffffu) : 0;
-                b.mv[pbase + x] = def ? 1 : 0;
-                if (subpix) {
-                    const int lo = static_cast<int>(lh[i] & 0xffffu), hi = static_cast<int>(lh[i] >> 16);
-                    const int d = static_cast<int>(best & 0xffffu);
-                    auto s_at = [&](int lv) -> int {
-                        const uint2 qq = qsum[i * qmax + (lv >> 2) - (lo >> 2)];
-                        const uint32_t wv = (lv & 2) ? qq.y : qq.x;
-                        return static_cast<int>((lv & 1) ? (wv >> 16) : (wv & 0xffffu));
-                    };
-                    const bool have = d - 1 >= lo && d + 1 <= hi;
-                    const float sp = subpixel_of(d, have ? s_at(d - 1) : 0, static_cast<int>(best >> 16),
-                                                 have ? s_at(d + 1) : 0, have);
-                    b.sub[pbase + x] = def ? sp : 0.0f;
-                }
-            }
+        const int l = own[q];
+        const uint32_t plh = lh[l];
+        const int lo = static_cast<int>(plh & 0xffffu), hi = static_cast<int>(plh >> 16);
+        const int k = static_cast<int>(q - qo[l]);
+        const int d0 = 4 * ((lo >> 2) + k);
+        const uint32_t v[4] = {se & 0xffffu, so & 0xffffu, se >> 16, so >> 16};
+        uint32_t best = 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int lv = d0 + u;
+            const bool ok = lv >= lo && lv <= hi;
+            if (write_s && ok) agg[cl[l] + (lv - lo)] = static_cast<uint16_t>(v[u]);
+            best = min(best, ok ? ((v[u] << 16) | static_cast<uint32_t>(lv)) : 0xffffffffu);
         }
-        __syncthreads();
+        key[l * qmax + k] = best;
+        if (subpix)
+            qsum[l * qmax + k] = make_uint2((se & 0xffffu) | (so << 16), (se >> 16) | (so & 0xffff0000u));
+    };
+    uint32_t q = static_cast<uint32_t>(lane);
+    for (; q + 32 < nq; q += 64) {
+        uint32_t w0[NDIR], w1[NDIR];
+#pragma unroll
+        for (int d = 0; d < NDIR; ++d) {
+            w0[d] = __ldg(pd + d * dstride + qbase + q);
+            w1[d] = __ldg(pd + d * dstride + qbase + q + 32);
+        }
+        finish(q, w0);
+        finish(q + 32, w1);
+    }
+    if (q < nq) {
+        uint32_t w0[NDIR];
+#pragma unroll
+        for (int d = 0; d < NDIR; ++d) w0[d] = __ldg(pd + d * dstride + qbase + q);
+        finish(q, w0);
+    }
+    __syncwarp();
+    if (do_wta && lane < np) {
+        uint32_t best = 0xffffffffu;
+        for (int k = 0; k < my_nq; ++k) best = min(best, key[lane * qmax + k]);
+        const int x = x0 + lane;
+        const bool def = x >= kCensusRadius && x < W - kCensusRadius &&
+                         y >= kCensusRadius && y < H - kCensusRadius;
+        b.md[pbase + lane] = def ? static_cast<int32_t>(best & 0xffffu) : 0;
+        b.mv[pbase + lane] = def ? 1 : 0;
+        if (subpix) {
+            const int lo = static_cast<int>(my_lh & 0xffffu), hi = static_cast<int>(my_lh >> 16);
+            const int d = static_cast<int>(best & 0xffffu);
+            auto s_at = [&](int lv) -> int {
+                const uint2 qq = qsum[lane * qmax + (lv >> 2) - (lo >> 2)];
+                const uint32_t wv = (lv & 2) ? qq.y : qq.x;
+                return static_cast<int>((lv & 1) ? (wv >> 16) : (wv & 0xffffu));
+            };
+            const bool have = d - 1 >= lo && d + 1 <= hi;
+            const float sp = subpixel_of(d, have ? s_at(d - 1) : 0, static_cast<int>(best >> 16),
+                                         have ? s_at(d + 1) : 0, have);
+            b.sub[pbase + lane] = def ? sp : 0.0f;
+        }
     }
 }
 
@@ -471,13 +506,13 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int tasks = sp.task_off[k] * n;
     const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max);
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
-    const size_t qm = static_cast<size_t>((b.d_max - 1) / 4 + 1);
-    const size_t cwsmem = sizeof(uint32_t) * (3 * kCwPix + 1 + kCwPix * qm) + kCwPix * qm +
-                          (subpix ? sizeof(uint2) * kCwPix * qm + 8 : 0);
+    const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
     auto kern = k == 8 ? combine_wta_kernel<8> : combine_wta_kernel<4>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(cwsmem));
-    kern<<<dim3(b.H, n), kCwThreads, cwsmem, L.st>>>(b, write_s, do_wta, subpix);
+    const long long warps = static_cast<long long>((b.W + 31) / 32) * b.H * n;
+    kern<<<static_cast<unsigned>((warps + kCwWarps - 1) / kCwWarps), 32 * kCwWarps, cwsmem, L.st>>>(
+        b, n, write_s, do_wta, subpix);
     *L.counter += 2;
 }
 

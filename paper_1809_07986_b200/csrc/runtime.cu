@@ -206,12 +206,24 @@ struct tsgm_ctx {
     int ring_i = 0;
     uint8_t* d_img = nullptr;  // [max_slots][2][P] staging for host-image steps
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // output copies overlap the next frame: a copy stream that starts after
-    // the frame's kernels; the next frame waits for it only before the
-    // kernels that overwrite the outputs (correct, median)
+    // Host-image steps upload on their own stream into two alternating
+    // staging buffers, so frame k+1's images cross PCIe while frame k
+    // computes; a buffer is reused once the census that read it has run.
+    cudaStream_t up_st = nullptr;
+    uint8_t* d_img_alt = nullptr;
+    int img_buf = 0;
+    int img_pending_free = -1;  // buffer the current step reads (free after census)
+    cudaEvent_t ev_img_ready[2]{}, ev_img_free[2]{};
+    bool img_free_recorded[2]{};
+    // Batched fetches: a device-to-device snapshot on the compute stream, then
+    // the device-to-host copy from the snapshot on the copy stream, so the
+    // next frame never waits for PCIe; a kind's snapshot is rewritten only
+    // after its previous copy-out finished (a frame later).
     cudaStream_t copy_st = nullptr;
-    cudaEvent_t ev_frame = nullptr, ev_copied = nullptr;
-    bool copy_pending = false;
+    cudaEvent_t ev_frame = nullptr;
+    void* snap[TSGM_OUT_COUNT]{};
+    cudaEvent_t ev_snap_copied[TSGM_OUT_COUNT]{};
+    bool snap_pending[TSGM_OUT_COUNT]{};
 
     template <typename T>
     T* dalloc(size_t count) {
@@ -234,9 +246,16 @@ struct tsgm_ctx {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (copy_st) cudaStreamSynchronize(copy_st);
+        if (up_st) cudaStreamSynchronize(up_st);
         if (ev_frame) cudaEventDestroy(ev_frame);
-        if (ev_copied) cudaEventDestroy(ev_copied);
+        for (auto e : ev_snap_copied)
+            if (e) cudaEventDestroy(e);
+        for (int i = 0; i < 2; ++i) {
+            if (ev_img_ready[i]) cudaEventDestroy(ev_img_ready[i]);
+            if (ev_img_free[i]) cudaEventDestroy(ev_img_free[i]);
+        }
         if (copy_st) cudaStreamDestroy(copy_st);
+        if (up_st) cudaStreamDestroy(up_st);
         if (st) cudaStreamDestroy(st);
     }
     Launch L() { return Launch{st, &launches}; }
@@ -271,8 +290,13 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     CK(cudaSetDevice(c.device));
     CK(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->up_st, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_frame, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ctx->ev_copied, cudaEventDisableTiming));
+    for (auto& e : ctx->ev_snap_copied) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&ctx->ev_img_ready[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_img_free[i], cudaEventDisableTiming));
+    }
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
     const size_t S = c.max_slots, P = ctx->P;
@@ -329,6 +353,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     ctx->d_right = ctx->dalloc<const uint8_t*>(S);
     ctx->d_H = ctx->dalloc<double>(S * 16);
     ctx->d_img = ctx->dalloc<uint8_t>(S * 2 * P);
+    ctx->d_img_alt = ctx->dalloc<uint8_t>(S * 2 * P);
     // the per-frame volumes last: C (u8), S (u16) and, for the scan
     // aggregation, 8 directions of u8 path costs per cell, for vol_slots
     // sequences at a time (the rest of the batch runs in further chunks)
@@ -337,7 +362,8 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     if (c.vol_slots <= 0) {
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
-        const size_t reserve = size_t(1) << 30;  // headroom for the runtime and fetches
+        // headroom: the runtime, plus fetch_batch snapshots of every per-pixel output
+        const size_t reserve = (size_t(1) << 30) + S * P * 16;
         const size_t fit = free_b > reserve ? (free_b - reserve) / vol_bytes : 0;
         vs = static_cast<int>(std::min<size_t>(vs, fit));
         if (vs < 1) throw std::runtime_error("tsgm_create: device memory too small for one frame's volumes");
@@ -452,6 +478,11 @@ void run_step(tsgm_ctx* ctx, int n) {
     launch_offsets(b, n, L);
     // sgm_match (A12-A15)
     launch_census(b, n, L);
+    if (ctx->img_pending_free >= 0) {  // the staging buffer may take the next upload
+        CK(cudaEventRecord(ctx->ev_img_free[ctx->img_pending_free], ctx->st));
+        ctx->img_free_recorded[ctx->img_pending_free] = true;
+        ctx->img_pending_free = -1;
+    }
     // the volume stages in balanced chunks of at most vol_slots sequences;
     // cost, agg and pdir are indexed by the position within the chunk
     const int chunks = (n + ctx->vol_slots - 1) / ctx->vol_slots;
@@ -465,10 +496,6 @@ void run_step(tsgm_ctx* ctx, int n) {
         c0 += m;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
-    if (ctx->copy_pending) {  // the previous frame's outputs are still being copied out
-        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_copied, 0));
-        ctx->copy_pending = false;
-    }
     launch_correct(b, n, c.filter.r, c.mask_tau, L);
     launch_median(b, n, b.rd, b.rv, b.ed, b.ev, L);
     CK(cudaGetLastError());
@@ -560,6 +587,7 @@ void sync(tsgm_ctx* ctx) {
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->st));
     if (ctx->copy_st) CK(cudaStreamSynchronize(ctx->copy_st));
+    if (ctx->up_st) CK(cudaStreamSynchronize(ctx->up_st));
 }
 
 // Host-side window bookkeeping for caller-provided ranges (make_cost_volume,
@@ -630,13 +658,20 @@ int tsgm_step(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const uint8_t* con
         CK(cudaSetDevice(ctx->device));
         std::vector<const uint8_t*> dl(n), dr(n);
         const size_t P = ctx->P;
+        const int bi = ctx->img_buf;
+        ctx->img_buf ^= 1;
+        uint8_t* img = bi ? ctx->d_img_alt : ctx->d_img;
+        if (ctx->img_free_recorded[bi]) CK(cudaStreamWaitEvent(ctx->up_st, ctx->ev_img_free[bi], 0));
         for (int i = 0; i < n; ++i) {
-            uint8_t* base = ctx->d_img + static_cast<size_t>(slots[i]) * 2 * P;
-            h2d(ctx, base, left[i], P);
-            h2d(ctx, base + P, right[i], P);
+            uint8_t* base = img + static_cast<size_t>(slots[i]) * 2 * P;
+            CK(cudaMemcpyAsync(base, left[i], P, cudaMemcpyHostToDevice, ctx->up_st));
+            CK(cudaMemcpyAsync(base + P, right[i], P, cudaMemcpyHostToDevice, ctx->up_st));
             dl[i] = base;
             dr[i] = base + P;
         }
+        CK(cudaEventRecord(ctx->ev_img_ready[bi], ctx->up_st));
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_img_ready[bi], 0));
+        ctx->img_pending_free = bi;
         step_impl(ctx, n, slots, dl.data(), dr.data(), motion);
     });
 }
@@ -675,17 +710,41 @@ int tsgm_fetch_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t wha
         CK(cudaSetDevice(ctx->device));
         const OutDesc o = out_desc(ctx, what);
         if (bytes_each < o.stride * o.elem) bad("tsgm_fetch_batch: destination too small");
-        // after the last frame's kernels, on the copy engine
+        for (int i = 0; i < n; ++i)
+            if (slots[i] < 0 || slots[i] >= ctx->max_slots) bad("tsgm_fetch_batch: slot out of range");
+        const size_t bytes = o.stride * o.elem;
+        if (!ctx->snap[what]) ctx->snap[what] = ctx->dalloc<char>(bytes * ctx->max_slots);
+        // the kind's previous copy-out must have left the snapshot
+        if (ctx->snap_pending[what]) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_snap_copied[what], 0));
+        // runs of consecutive slots with contiguous destinations: one copy each
+        std::vector<std::pair<int, int>> runs;  // (first batch index, length)
+        for (int i = 0; i < n; ++i) {
+            if (!runs.empty()) {
+                auto& r = runs.back();
+                const int j = r.first + r.second - 1;
+                if (slots[i] == slots[j] + 1 &&
+                    static_cast<char*>(dsts[i]) == static_cast<char*>(dsts[j]) + bytes) {
+                    ++r.second;
+                    continue;
+                }
+            }
+            runs.push_back({i, 1});
+        }
+        char* snap = static_cast<char*>(ctx->snap[what]);
+        for (auto& r : runs) {
+            const size_t at = static_cast<size_t>(slots[r.first]) * bytes;
+            CK(cudaMemcpyAsync(snap + at, static_cast<const char*>(o.base) + at, bytes * r.second,
+                               cudaMemcpyDeviceToDevice, ctx->st));
+        }
         CK(cudaEventRecord(ctx->ev_frame, ctx->st));
         CK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_frame, 0));
-        for (int i = 0; i < n; ++i) {
-            if (slots[i] < 0 || slots[i] >= ctx->max_slots) bad("tsgm_fetch_batch: slot out of range");
-            const char* src = static_cast<const char*>(o.base) +
-                              static_cast<size_t>(slots[i]) * o.stride * o.elem;
-            CK(cudaMemcpyAsync(dsts[i], src, o.stride * o.elem, cudaMemcpyDeviceToHost, ctx->copy_st));
+        for (auto& r : runs) {
+            const size_t at = static_cast<size_t>(slots[r.first]) * bytes;
+            CK(cudaMemcpyAsync(dsts[r.first], snap + at, bytes * r.second, cudaMemcpyDeviceToHost,
+                               ctx->copy_st));
         }
-        CK(cudaEventRecord(ctx->ev_copied, ctx->copy_st));
-        ctx->copy_pending = true;
+        CK(cudaEventRecord(ctx->ev_snap_copied[what], ctx->copy_st));
+        ctx->snap_pending[what] = true;
     });
 }
 

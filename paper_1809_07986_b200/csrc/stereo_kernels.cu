@@ -331,40 +331,55 @@ void launch_wta(const Bufs& b, int n, Launch L) {
 
 // ---------------------------------------------------------------- median (A19)
 // median_refine, sgm.cpp:189-216: lower median of the valid 3x3 neighbours,
-// valid iff at least 5.
-__device__ __forceinline__ void cswap(int64_t& a, int64_t& b) {
-    const int64_t lo = a < b ? a : b, hi = a < b ? b : a;
+// valid iff at least 5. One thread per pixel of a 32x8 tile; keys (d, or
+// INT32_MAX for an invalid or missing neighbour) and validity staged in shared
+// memory with a 1-px halo. Invalid keys sort after every valid value (ties
+// with a valid INT32_MAX leave the k-th smallest unchanged), so element
+// (n-1)/2 of the sorted 9 is the lower median of the n valid ones.
+constexpr int kMdW = 32, kMdH = 8;
+
+__device__ __forceinline__ void cswap(int32_t& a, int32_t& b) {
+    const int32_t lo = min(a, b), hi = max(a, b);
     a = lo;
     b = hi;
 }
 
 __global__ void median_kernel(Bufs b, const int32_t* in_d, const uint8_t* in_v, int32_t* out_d,
                               uint8_t* out_v) {
-    const int a = blockIdx.y, s = slot_of(b, a);
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= b.P) return;
-    const int x = i % b.W, y = i / b.W;
+    __shared__ int32_t key[kMdH + 2][kMdW + 2];
+    __shared__ uint8_t ok[kMdH + 2][kMdW + 2];
+    const int a = blockIdx.z, s = slot_of(b, a);
     const size_t base = static_cast<size_t>(s) * b.P;
-    // the 9 neighbours, missing/invalid ones as +inf (sort last)
-    int64_t v[9];
+    const int x0 = blockIdx.x * kMdW - 1, y0 = blockIdx.y * kMdH - 1;
+    for (int t = threadIdx.y * kMdW + threadIdx.x; t < (kMdH + 2) * (kMdW + 2); t += kMdW * kMdH) {
+        const int ty = t / (kMdW + 2), tx = t % (kMdW + 2);
+        const int gx = x0 + tx, gy = y0 + ty;
+        const bool in = gx >= 0 && gx < b.W && gy >= 0 && gy < b.H;
+        const size_t j = base + static_cast<size_t>(in ? gy : 0) * b.W + (in ? gx : 0);
+        const bool v = in && in_v[j];
+        key[ty][tx] = v ? in_d[j] : INT32_MAX;
+        ok[ty][tx] = v ? 1 : 0;
+    }
+    __syncthreads();
+    const int x = blockIdx.x * kMdW + threadIdx.x, y = blockIdx.y * kMdH + threadIdx.y;
+    if (x >= b.W || y >= b.H) return;
+    int32_t v[9];
     int n = 0;
 #pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
+    for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-        for (int dx = -1; dx <= 1; ++dx) {
-            const int nx = x + dx, ny = y + dy;
-            const bool in = nx >= 0 && nx < b.W && ny >= 0 && ny < b.H;
-            const size_t j = base + static_cast<size_t>(in ? ny : y) * b.W + (in ? nx : x);
-            const bool ok = in && in_v[j];
-            v[(dy + 1) * 3 + dx + 1] = ok ? static_cast<int64_t>(in_d[j]) : INT64_MAX;
-            n += ok;
+        for (int dx = 0; dx < 3; ++dx) {
+            v[dy * 3 + dx] = key[threadIdx.y + dy][threadIdx.x + dx];
+            n += ok[threadIdx.y + dy][threadIdx.x + dx];
         }
+    const size_t i = base + static_cast<size_t>(y) * b.W + x;
     if (n < 5) {
-        out_d[base + i] = 0;
-        out_v[base + i] = 0;
+        out_d[i] = 0;
+        out_v[i] = 0;
         return;
     }
-    // full 9-element sorting network (25 compare-exchanges)
+    // 9-element sorting network (25 compare-exchanges; the ones that cannot
+    // reach elements 2..4 are dead code)
     cswap(v[0], v[3]); cswap(v[1], v[7]); cswap(v[2], v[5]); cswap(v[4], v[8]);
     cswap(v[0], v[7]); cswap(v[2], v[4]); cswap(v[3], v[8]); cswap(v[5], v[6]);
     cswap(v[0], v[2]); cswap(v[1], v[3]); cswap(v[4], v[5]); cswap(v[7], v[8]);
@@ -372,19 +387,15 @@ __global__ void median_kernel(Bufs b, const int32_t* in_d, const uint8_t* in_v, 
     cswap(v[0], v[1]); cswap(v[2], v[4]); cswap(v[3], v[5]); cswap(v[6], v[8]);
     cswap(v[2], v[3]); cswap(v[4], v[5]); cswap(v[6], v[7]);
     cswap(v[1], v[2]); cswap(v[3], v[4]); cswap(v[5], v[6]);
-    // lower median of the n valid values = element (n-1)/2 of the sorted list
-    const int k = (n - 1) / 2;
-    int64_t med = v[0];
-#pragma unroll
-    for (int j = 1; j < 5; ++j)
-        if (j == k) med = v[j];
-    out_d[base + i] = static_cast<int32_t>(med);
-    out_v[base + i] = 1;
+    const int k = (n - 1) / 2;  // 2, 3 or 4
+    out_d[i] = k == 2 ? v[2] : (k == 3 ? v[3] : v[4]);
+    out_v[i] = 1;
 }
 
 void launch_median(const Bufs& b, int n, const int32_t* in_d, const uint8_t* in_v,
                    int32_t* out_d, uint8_t* out_v, Launch L) {
-    median_kernel<<<dim3((b.P + 255) / 256, n), 256, 0, L.st>>>(b, in_d, in_v, out_d, out_v);
+    dim3 grid((b.W + kMdW - 1) / kMdW, (b.H + kMdH - 1) / kMdH, n);
+    median_kernel<<<grid, dim3(kMdW, kMdH), 0, L.st>>>(b, in_d, in_v, out_d, out_v);
     ++*L.counter;
 }
 

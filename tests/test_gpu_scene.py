@@ -158,6 +158,43 @@ def test_overlapped_fetch_captures_each_frame(port):
     eng.close()
 
 
+def test_interleaved_batches(port):
+    """Sequences stepping at different rates share one engine: slot 0 every
+    call, slot 2 every other call, slot 1 never; the host-image uploads
+    alternate staging buffers on their own stream. Each sequence matches the
+    oracle run on its own frames."""
+    cfgs = [SceneConfig.baseline_config(1, width=192, height=80, focal=120.0, cx=95.5, cy=39.5,
+                                        d_max=40, seed=s, n_movers=1) for s in (6, 7)]
+    calib = tsgm.StereoCalib(120.0, 95.5, 39.5, cfgs[0].baseline, 192, 80, 40)
+    params, filt = tsgm.SgmParams(10, 120, 8, 0, 40), tsgm.FilterConfig(range_use_stddev=True,
+                                                                        range_stddev_gain=3.0)
+    seqs = [render(c, 0, 6) for c in cfgs]
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=3, keep_volumes=False))
+    nxt = [0, 0]
+    states = [None, None]
+
+    def mot(i, k):
+        P = seqs[i][2]
+        return (np.eye(3), np.zeros(3)) if k == 0 else tsgm.relative_motion(P[k - 1], P[k])
+
+    for call in range(6):
+        active = [0] + ([1] if call % 2 == 1 else [])
+        slots = [0 if i == 0 else 2 for i in active]
+        eng.step(slots, [seqs[i][0][nxt[i]] for i in active],
+                 [seqs[i][1][nxt[i]] for i in active], [mot(i, nxt[i]) for i in active])
+        for i, sl in zip(active, slots):
+            k = nxt[i]
+            m = mot(i, k)
+            ref = port.step(states[i], seqs[i][0][k], seqs[i][1][k], m[0], m[1], calib, params,
+                            filt)
+            np.testing.assert_array_equal(eng.fetch(sl, "export_d"), ref["export_d"])
+            np.testing.assert_array_equal(eng.fetch(sl, "state_p"), ref["p"])
+            states[i] = (ref["d"], ref["p"], ref["valid"])
+            nxt[i] += 1
+    assert not eng.fetch(1, "state_valid").any()
+    eng.close()
+
+
 @pytest.mark.parametrize("half", [2, 4, 8, 16])
 def test_config3_fixed_window_sweep(port, half):
     """Config 3: reduced windows of exactly 2h+1 levels (stddev ranges with a
