@@ -29,7 +29,10 @@ struct Bufs {
     double *sd, *sp;
     uint8_t* sv;
     // warp keys (A6) and warp output (pre reject/fill)
-    unsigned long long *kd, *kp, *ks;
+    unsigned long long* kd;  // [slot][P] winning d' key (atomicMax)
+    ulonglong2* kps;         // [slot][P] (p key, source-d key), lexicographic min (128-bit CAS)
+    int* wtgt;               // [slot][P] pass-1 target pixel of each source (-1: dropped)
+    unsigned long long* wdk; // [slot][P] pass-1 d' key of each source
     double *wd, *wp, *wsrc;
     uint8_t* wv;
     // prediction (predict() output)

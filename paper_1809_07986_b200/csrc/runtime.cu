@@ -310,8 +310,9 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.sp = ctx->dalloc<double>(S * P);
     b.sv = ctx->dalloc<uint8_t>(S * P);
     b.kd = ctx->dalloc<unsigned long long>(S * P);
-    b.kp = ctx->dalloc<unsigned long long>(S * P);
-    b.ks = ctx->dalloc<unsigned long long>(S * P);
+    b.kps = ctx->dalloc<ulonglong2>(S * P);
+    b.wtgt = ctx->dalloc<int>(S * P);
+    b.wdk = ctx->dalloc<unsigned long long>(S * P);
     b.wd = ctx->dalloc<double>(S * P);
     b.wp = ctx->dalloc<double>(S * P);
     b.wsrc = ctx->dalloc<double>(S * P);
@@ -385,8 +386,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     CK(cudaMemsetAsync(b.sp, 0, sizeof(double) * S * P, ctx->st));
     CK(cudaMemsetAsync(b.sv, 0, S * P, ctx->st));
     CK(cudaMemsetAsync(b.kd, 0, sizeof(unsigned long long) * S * P, ctx->st));
-    CK(cudaMemsetAsync(b.kp, 0xff, sizeof(unsigned long long) * S * P, ctx->st));
-    CK(cudaMemsetAsync(b.ks, 0xff, sizeof(unsigned long long) * S * P, ctx->st));
+    CK(cudaMemsetAsync(b.kps, 0xff, sizeof(ulonglong2) * S * P, ctx->st));
     CK(cudaMemsetAsync(b.ncells, 0, sizeof(unsigned long long) * S, ctx->st));
     for (auto& r : ctx->ring) {
         CK(cudaMallocHost(&r.slots, sizeof(int) * S));

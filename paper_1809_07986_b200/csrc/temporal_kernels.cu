@@ -11,10 +11,12 @@ namespace tsgm {
 // ---------------------------------------------------------------- warp (A5, A6)
 // warp_state_ex, geometry.cpp:127-156. A colliding target keeps the
 // lexicographic maximum of (d' up, p down, source d down) (replaces(),
-// geometry.cpp:116-123): pass 1 atomicMax on d', pass 2 atomicMin on p among
-// sources whose d' equals the winner, pass 3 atomicMin on the source d among
-// sources matching both. Keys are order-preserving u64 images of the doubles,
-// so the result is exact and independent of thread order.
+// geometry.cpp:116-123). Pass 1 maps every source once (DispHomography::apply
+// and the target rounding), caches (target, d' key) and atomicMax-es the d'
+// key; pass 2, for sources whose d' equals the winner, takes the
+// lexicographic minimum of (p key, source-d key) with a 128-bit CAS loop.
+// Keys are order-preserving u64 images of the doubles, so the result is exact
+// and independent of thread order.
 struct Mapped {
     int t;  // target pixel index, -1 if dropped
     double dp;
@@ -40,48 +42,77 @@ __device__ __forceinline__ Mapped map_source(const double* H, int x, int y, doub
     return m;
 }
 
-template <int kPass>
-__global__ void warp_pass_kernel(Bufs b, const double* src_d, const double* src_p,
-                                 const uint8_t* src_v, int d_max) {
+__global__ void warp_map_kernel(Bufs b, const double* src_d, const uint8_t* src_v, int d_max) {
     const int a = blockIdx.y, s = slot_of(b, a);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= b.P) return;
     const size_t base = static_cast<size_t>(s) * b.P;
-    if (!src_v[base + i]) return;
-    __shared__ double H[16];
-    (void)H;
-    const double* Hg = b.H16 + 16 * a;
-    const double ds = src_d[base + i];
-    const Mapped m = map_source(Hg, i % b.W, i / b.W, ds, b.W, b.H, d_max);
-    if (m.t < 0) return;
-    const size_t t = base + m.t;
-    const unsigned long long kd = ord_key(m.dp);
-    if (kPass == 1) {
-        atomicMax(&b.kd[t], kd);
-    } else if (kPass == 2) {
-        if (b.kd[t] == kd) atomicMin(&b.kp[t], ord_key(src_p[base + i]));
-    } else {
-        if (b.kd[t] == kd && b.kp[t] == ord_key(src_p[base + i])) atomicMin(&b.ks[t], ord_key(ds));
+    int tgt = -1;
+    unsigned long long kd = 0ull;
+    if (src_v[base + i]) {
+        const Mapped m = map_source(b.H16 + 16 * a, i % b.W, i / b.W, src_d[base + i], b.W, b.H,
+                                    d_max);
+        if (m.t >= 0) {
+            tgt = m.t;
+            kd = ord_key(m.dp);
+            atomicMax(&b.kd[base + m.t], kd);
+        }
+    }
+    b.wtgt[base + i] = tgt;
+    b.wdk[base + i] = kd;
+}
+
+__device__ __forceinline__ ulonglong2 cas128(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val) {
+    ulonglong2 old;
+    asm volatile(
+        "{\n\t.reg .b128 d, c, v;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 v, {%4, %5};\n\t"
+        "atom.global.cas.b128 d, [%6], c, v;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(old.x), "=l"(old.y)
+        : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(addr)
+        : "memory");
+    return old;
+}
+
+__device__ __forceinline__ bool lex_less(ulonglong2 a, ulonglong2 b) {
+    return a.x < b.x || (a.x == b.x && a.y < b.y);
+}
+
+__global__ void warp_tiebreak_kernel(Bufs b, const double* src_d, const double* src_p) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.P) return;
+    const size_t base = static_cast<size_t>(s) * b.P;
+    const int tgt = b.wtgt[base + i];
+    if (tgt < 0) return;
+    const size_t t = base + tgt;
+    if (b.kd[t] != b.wdk[base + i]) return;
+    const ulonglong2 mine = make_ulonglong2(ord_key(src_p[base + i]), ord_key(src_d[base + i]));
+    ulonglong2* addr = b.kps + t;
+    // start from the armed value: only the CAS reads the pair atomically (a
+    // plain 16-byte load may tear and hide a smaller pair)
+    ulonglong2 cur = make_ulonglong2(~0ull, ~0ull);
+    while (lex_less(mine, cur)) {
+        const ulonglong2 prev = cas128(addr, cur, mine);
+        if (prev.x == cur.x && prev.y == cur.y) break;
+        cur = prev;
     }
 }
 
 void launch_warp(const Bufs& b, int n, const double* src_d, const double* src_p,
                  const uint8_t* src_v, int d_max, Launch L) {
-    const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(b.P);
-    // keys of the active slots only: slots are not contiguous in general, so
-    // clear per slot (n is small; these are memset nodes, not kernels)
     dim3 grid((b.P + 255) / 256, n);
-    (void)bytes;
-    warp_pass_kernel<1><<<grid, 256, 0, L.st>>>(b, src_d, src_p, src_v, d_max);
-    warp_pass_kernel<2><<<grid, 256, 0, L.st>>>(b, src_d, src_p, src_v, d_max);
-    warp_pass_kernel<3><<<grid, 256, 0, L.st>>>(b, src_d, src_p, src_v, d_max);
-    *L.counter += 3;
+    warp_map_kernel<<<grid, 256, 0, L.st>>>(b, src_d, src_v, d_max);
+    warp_tiebreak_kernel<<<grid, 256, 0, L.st>>>(b, src_d, src_p);
+    *L.counter += 2;
 }
 
 // Decode the winners (warp_state_ex output) and apply predict's variance step,
 // temporal_filter.cpp:35-47: invalidate if the source disparity is not
 // positive, phi = d'/d_src, p = (phi*phi)*p + q. Also re-arms the keys for the
-// next frame (kd = 0, kp = ks = ~0).
+// next frame (kd = 0, (kp, ks) = ~0).
 __global__ void predict_finalize_kernel(Bufs b, double q, int apply_phi) {
     const int a = blockIdx.y, s = slot_of(b, a);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -91,9 +122,10 @@ __global__ void predict_finalize_kernel(Bufs b, double q, int apply_phi) {
     double d = 0.0, p = 0.0, src = 0.0;
     uint8_t v = 0;
     if (kd != 0ull) {
+        const ulonglong2 k2 = b.kps[t];
         d = key_double(kd);
-        p = key_double(b.kp[t]);
-        src = key_double(b.ks[t]);
+        p = key_double(k2.x);
+        src = key_double(k2.y);
         v = 1;
         if (apply_phi) {
             if (!(src > 0.0)) {
@@ -104,14 +136,13 @@ __global__ void predict_finalize_kernel(Bufs b, double q, int apply_phi) {
                 p = __dadd_rn(__dmul_rn(__dmul_rn(phi, phi), p), q);
             }
         }
+        b.kps[t] = make_ulonglong2(~0ull, ~0ull);
     }
     b.wd[t] = d;
     b.wp[t] = p;
     b.wv[t] = v;
     if (b.wsrc) b.wsrc[t] = kd != 0ull ? src : 0.0;
     b.kd[t] = 0ull;
-    b.kp[t] = ~0ull;
-    b.ks[t] = ~0ull;
 }
 
 void launch_predict_finalize(const Bufs& b, int n, double q, int apply_phi, Launch L) {
