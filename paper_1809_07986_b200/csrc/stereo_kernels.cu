@@ -230,32 +230,23 @@ void launch_offsets(const Bufs& b, int n, Launch L) {
 
 // ---------------------------------------------------------------- cost (A13)
 // build_cost_volume, matching_cost.cpp:88-117. One CTA per (row, slot); the
-// row's census signatures are staged in shared memory. A warp takes a chunk of
-// 32 pixels, whose cells are one contiguous range of the ragged layout, and
-// writes it in aligned 32-bit words, lane-strided (a warp store covers 128
-// contiguous bytes); the owner pixel of a word's first cell comes from a
-// binary search over the chunk's 33 offsets (shared memory), the next cells
-// advance from it. Partial words at the range ends are written bytewise.
-constexpr int kCostThreads = 512;
-
-__device__ __forceinline__ uint32_t cell_cost(const uint32_t* sl, const uint32_t* sr, int x, int d,
-                                              int W, bool row_def) {
+// row's census signatures are staged in shared memory. Warps take 32-pixel
+// chunks: a window of <= 16 levels is written by its own lane, a wider window
+// by the whole warp (lanes across its levels, coalesced byte stores).
+__device__ __forceinline__ uint8_t cell_cost(const uint32_t* sl, const uint32_t* sr, int x, int d,
+                                             int W, bool row_def) {
     const int xr = x - d;
     const bool ok = row_def && x >= kCensusRadius && x < W - kCensusRadius &&
                     xr >= kCensusRadius && xr < W - kCensusRadius;
-    return ok ? static_cast<uint32_t>(__popc(sl[x] ^ sr[xr])) : static_cast<uint32_t>(kMaxCost);
+    return ok ? static_cast<uint8_t>(__popc(sl[x] ^ sr[xr])) : static_cast<uint8_t>(kMaxCost);
 }
 
-__global__ void __launch_bounds__(kCostThreads) cost_kernel(Bufs b) {
+__global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
     extern __shared__ uint32_t sm[];
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const int W = b.W;
-    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
-    const int nwarps = static_cast<int>(blockDim.x >> 5);
     uint32_t* sl = sm;
     uint32_t* sr = sl + W;
-    uint32_t* wo = sr + W + warp * 68;  // per warp: offsets[33] (chunk-relative), lo[32]
-    uint32_t* wl = wo + 36;
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
     for (int x = threadIdx.x; x < W; x += blockDim.x) {
@@ -265,53 +256,36 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(Bufs b) {
     __syncthreads();
     uint8_t* base = b.cost + static_cast<size_t>(a) * b.vol_cap;
     const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
+    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+    const int nwarps = static_cast<int>(blockDim.x >> 5);
     for (int x0 = warp * 32; x0 < W; x0 += 32 * nwarps) {
-        const int np = min(32, W - x0);
-        const bool active = lane < np;
-        const uint32_t lh = active ? b.lohi[pbase + x0 + lane] : 0u;
-        const uint32_t o = active ? off[x0 + lane] : 0u;
-        const uint32_t n = active ? (lh >> 16) - (lh & 0xffffu) + 1u : 0u;
-        const uint32_t c0 = __shfl_sync(0xffffffffu, o, 0);
-        const uint32_t len = __shfl_sync(0xffffffffu, o + n, np - 1) - c0;
-        wo[lane] = active ? o - c0 : len;  // inactive lanes sort past the end
-        wl[lane] = lh & 0xffffu;
-        if (lane == 0) wo[32] = len;
-        __syncwarp();
-        // aligned words of [c0, c0 + len) in absolute addresses
-        const uintptr_t A0 = reinterpret_cast<uintptr_t>(base + c0);
-        const uintptr_t W0 = A0 & ~static_cast<uintptr_t>(3);
-        const uint32_t nwords = static_cast<uint32_t>((A0 + len + 3 - W0) >> 2);
-        const int rel0 = static_cast<int>(W0 - A0);  // chunk-relative cell of word 0's byte 0 (<= 0)
-        for (uint32_t w = lane; w < nwords; w += 32) {
-            const int r = rel0 + 4 * static_cast<int>(w);
-            // owner of the first in-range cell of the word
-            const uint32_t rs = static_cast<uint32_t>(max(r, 0));
-            int p = 0;
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1)
-                if (wo[p + step] <= rs) p += step;
-            uint32_t word = 0u;
-            const bool full = r >= 0 && static_cast<uint32_t>(r) + 4u <= len;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int rc = r + k;
-                if (rc < 0 || static_cast<uint32_t>(rc) >= len) continue;
-                while (wo[p + 1] <= static_cast<uint32_t>(rc)) ++p;
-                const uint32_t v = cell_cost(sl, sr, x0 + p,
-                                             static_cast<int>(wl[p] + (static_cast<uint32_t>(rc) - wo[p])),
-                                             W, row_def);
-                if (full) word |= v << (8 * k);
-                else base[c0 + static_cast<uint32_t>(rc)] = static_cast<uint8_t>(v);
-            }
-            if (full) *reinterpret_cast<uint32_t*>(base + c0 + static_cast<uint32_t>(r)) = word;
+        const int x = x0 + lane;
+        const bool active = x < W;
+        const uint32_t lh = active ? b.lohi[pbase + x] : 0u;
+        const uint32_t o = active ? off[x] : 0u;
+        const int lo = static_cast<int>(lh & 0xffffu), n = static_cast<int>(lh >> 16) - lo + 1;
+        const bool narrow = active && n <= 16;
+        if (narrow) {
+            uint8_t* dst = base + o;
+            for (int j = 0; j < n; ++j) dst[j] = cell_cost(sl, sr, x, lo + j, W, row_def);
         }
-        __syncwarp();
+        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
+        while (bw) {
+            const int src = __ffs(bw) - 1;
+            bw &= bw - 1;
+            const int xw = x0 + src;
+            const int lo_w = __shfl_sync(0xffffffffu, lo, src);
+            const int n_w = __shfl_sync(0xffffffffu, n, src);
+            const uint32_t o_w = __shfl_sync(0xffffffffu, o, src);
+            uint8_t* dst = base + o_w;
+            for (int j = lane; j < n_w; j += 32) dst[j] = cell_cost(sl, sr, xw, lo_w + j, W, row_def);
+        }
     }
 }
 
 void launch_cost(const Bufs& b, int n, Launch L) {
-    const size_t smem = sizeof(uint32_t) * (2 * b.W + 68 * (kCostThreads / 32));
-    cost_kernel<<<dim3(b.H, n), kCostThreads, smem, L.st>>>(b);
+    const size_t smem = sizeof(uint32_t) * 2 * b.W;
+    cost_kernel<<<dim3(b.H, n), 512, smem, L.st>>>(b);
     ++*L.counter;
 }
 
