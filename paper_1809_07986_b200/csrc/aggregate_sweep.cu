@@ -36,16 +36,8 @@ constexpr int kScanWarps = 2;  // warps per CTA (one task each)
 
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
 __host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
-// shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group sources,
-// then the narrow lanes' staged cost words (2 buffers x 32 lanes x 5 words)
-__host__ __device__ inline int scan_stage_off(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 64; }
-__host__ __device__ inline int scan_warp_bytes(int d_max) { return scan_stage_off(d_max) + 2 * 32 * 5 * 4; }
-
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group sources
+__host__ __device__ inline int scan_warp_bytes(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 64; }
 
 bool sweep_supported(int W, int H, int d_max, int p2) {
     // u8 path costs need 24 + P2 <= 255; a window is <= 16 lanes x 4 quads
@@ -116,14 +108,11 @@ struct PixMeta {
 // quads [lg*Q, lg*Q + Q) of the window. All lanes of the warp call it (pix =
 // false: no pixel for this group; everything masked, nothing stored). `sb` /
 // `rp` are the shared addresses of the scanline's slot and quad range.
-// `staged` (narrow lanes, G = 1): shared address of the Q+1 cost words the
-// previous step copied in with cp.async; 0: load them from global memory.
 template <int G, int Q>
 __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has_pred,
                                            uint32_t sb, uint32_t rp, const uint8_t* cost,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
-                                           uint32_t P2x4, const uint8_t* mask_tab,
-                                           uint32_t staged = 0u) {
+                                           uint32_t P2x4, const uint8_t* mask_tab) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
@@ -138,13 +127,8 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
         const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
         uint32_t c[Q + 1];
-        if (G == 1 && staged) {
 #pragma unroll
-            for (int t = 0; t <= Q; ++t) c[t] = lds32(staged + 4u * t);
-        } else {
-#pragma unroll
-            for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
-        }
+        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
         // invalid-level masks of the lane's 16 levels from the table:
         // row = levels below lo in the first quad, col = last valid level + 1
         const int start = 4 * (q0 + k0);  // unclamped first level of the lane
@@ -253,20 +237,6 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.vol_slots + a) * b.quad_cap * 4);
-    const uint32_t stage0 = wbase + static_cast<uint32_t>(scan_stage_off(b.d_max)) + 20u * lane;
-    // copy a narrow window's 5 aligned cost words (quads q0 .. q0+3 plus the
-    // spill word) into staging buffer `buf` of this lane
-    auto stage_costs = [&](const PixMeta& m, int buf) {
-        const int lo = static_cast<int>(m.lohi & 0xffffu);
-        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + m.cell + (4 * (lo >> 2) - lo);
-        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-        const uint32_t dst = stage0 + 640u * static_cast<uint32_t>(buf);
-#pragma unroll
-        for (int t = 0; t < 5; ++t) cp_async4(dst + 4u * t, aw + t);
-    };
-    auto is_narrow = [](const PixMeta& m) {
-        return static_cast<int>(m.lohi >> 18) - static_cast<int>((m.lohi & 0xffffu) >> 2) < 4;
-    };
 
     // line geometry: horizontal directions sweep x with lane = row; the others
     // sweep y with lane = line c, pixel x = c + sl*y (sl = dx*dy)
@@ -301,25 +271,17 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
     PixMeta m2{0u, 0u, 0u};
     if (act2) load_meta(p_tmp, m2);
-    if (act1 && is_narrow(m1)) stage_costs(m1, 0);
-    cp_async_commit();
     for (int k = 0; k < nsteps; ++k) {
         const bool active = act1;
         const PixMeta mc = m1;
         act1 = act2;
         m1 = m2;
-        if (act1) {  // step k+1: narrow costs staged into shared memory, wide ones towards L1
-            if (is_narrow(m1)) {
-                stage_costs(m1, (k + 1) & 1);
-            } else {
-                const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
-                const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
-                const uint8_t* c0 = cost + m1.cell;
-                for (int o = 0; o < n_n + 4; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + o));
-            }
+        if (act1) {  // step k+1's window towards L1 (its metadata arrived a step ago)
+            const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
+            const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
+            const uint8_t* c0 = cost + m1.cell;
+            for (int o = 0; o < n_n + 4; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + o));
         }
-        cp_async_commit();
-        cp_async_wait1();  // step k's copies have landed
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
         if (__ballot_sync(0xffffffffu, active) == 0u) {
@@ -332,13 +294,13 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         const int qn = __reduce_max_sync(0xffffffffu, narrow ? nq : 0);
         if (qn > 3)
             scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                             mask_tab, stage0 + 640u * static_cast<uint32_t>(k & 1));
+                             mask_tab);
         else if (qn == 3)
             scan_pixel<1, 3>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                             mask_tab, stage0 + 640u * static_cast<uint32_t>(k & 1));
+                             mask_tab);
         else if (qn > 0)
             scan_pixel<1, 2>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                             mask_tab, stage0 + 640u * static_cast<uint32_t>(k & 1));
+                             mask_tab);
         // wider windows: groups of G lanes x 4 quads, 32/G windows per pass
         const auto wide = [&](auto gtag, unsigned bw) {
             constexpr int G = decltype(gtag)::value;
