@@ -67,6 +67,12 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
     return d;
 }
 
+__device__ __forceinline__ uint32_t ld_na(const uint32_t* p) {
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -119,16 +125,18 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     const int k0 = lg * Q;                  // first window quad of this lane
     const int a0 = q0 + min(k0, nq - 1);    // absolute quad (clamped into the window)
 
-    uint32_t CA[Q], CB[Q], ivA[Q], ivB[Q], LA[Q], LB[Q];
+    uint32_t ivA[Q], ivB[Q], LA[Q], LB[Q];
     bool act[Q];
-    {
-        // matching costs of levels 4*a0 .. 4*a0 + 4Q - 1 (bytes outside the window masked)
-        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
-        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-        const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
-        uint32_t c[Q + 1];
+    // matching costs of levels 4*a0 .. 4*a0 + 4Q - 1 (bytes outside the window
+    // masked): the raw words are loaded first and consumed last, after the
+    // predecessor terms, to cover their latency
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
+    const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+    const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
+    uint32_t c[Q + 1];
 #pragma unroll
-        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
+    for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
+    {
         // invalid-level masks of the lane's 16 levels from the table:
         // row = levels below lo in the first quad, col = last valid level + 1
         const int start = 4 * (q0 + k0);  // unclamped first level of the lane
@@ -142,12 +150,7 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         if (Q > 2) { ivA[2] = m1.x; ivB[2] = m1.y; }
         if (Q > 3) { ivA[3] = m1.z; ivB[3] = m1.w; }
 #pragma unroll
-        for (int t = 0; t < Q; ++t) {
-            const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
-            CA[t] = prmt(cq, 0u, 0x4140u) | (ivA[t] & kPoison2);
-            CB[t] = prmt(cq, 0u, 0x4342u) | (ivB[t] & kPoison2);
-            act[t] = pix && k0 + t < nq;
-        }
+        for (int t = 0; t < Q; ++t) act[t] = pix && k0 + t < nq;
     }
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
     const uint32_t prng = lds32(rp);
@@ -170,11 +173,19 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         const uint32_t e1 = prmt(w[t + 1], 0u, 0x4342u);   // M(d0+2), M(d0+3)
         const uint32_t mpa = prmt(w[t + 1], 0u, 0x4241u);  // M(d0+1), M(d0+2)
         const uint32_t mpb = prmt(e1, w[t + 2], 0x1432u);  // M(d0+3), M(d0+4)
-        // u16 lanes never carry here, so the adds go to the FMA pipe (IMAD)
-        LA[t] = mad_u32(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), 1u, CA[t]);
-        LB[t] = mad_u32(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), 1u, CB[t]);
-        mn = __vimin3_u16x2(mn, LA[t], LB[t]);
+        LA[t] = __viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0);
+        LB[t] = __viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1);
         mma = mpb;
+    }
+#pragma unroll
+    for (int t = 0; t < Q; ++t) {
+        const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
+        const uint32_t CA = prmt(cq, 0u, 0x4140u) | (ivA[t] & kPoison2);
+        const uint32_t CB = prmt(cq, 0u, 0x4342u) | (ivB[t] & kPoison2);
+        // u16 lanes never carry here, so the adds go to the FMA pipe (IMAD)
+        LA[t] = mad_u32(LA[t], 1u, CA);
+        LB[t] = mad_u32(LB[t], 1u, CB);
+        mn = __vimin3_u16x2(mn, LA[t], LB[t]);
     }
     const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
     const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
@@ -257,10 +268,10 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         p = y * W + x;
         return x >= 0 && x < W;
     };
-    auto load_meta = [&](int p, PixMeta& m) {
-        m.lohi = __ldg(lohi + p);
-        m.cell = __ldg(off + p);
-        m.qo = __ldg(qoff + p);
+    auto load_meta = [&](int p, PixMeta& m) {  // used from registers: keep L1 for the costs
+        m.lohi = ld_na(lohi + p);
+        m.cell = ld_na(off + p);
+        m.qo = ld_na(qoff + p);
     };
 
     // metadata two steps ahead, costs of the next step prefetched into L1

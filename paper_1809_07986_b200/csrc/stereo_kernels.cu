@@ -230,14 +230,9 @@ void launch_offsets(const Bufs& b, int n, Launch L) {
 
 // ---------------------------------------------------------------- cost (A13)
 // build_cost_volume, matching_cost.cpp:88-117. One CTA per (row, slot); the
-// row's census signatures are staged in shared memory. A warp takes a chunk of
-// 32 pixels, whose cells are one contiguous range of the ragged layout: a
-// window of <= 16 levels is computed by its own lane, a wider one by the whole
-// warp, into a per-warp shared staging buffer laid out so that its 16-byte
-// blocks map onto aligned 16-byte blocks of the volume; the warp then writes
-// the range with 16-byte stores (bytewise only in the two end blocks).
-constexpr int kCostThreads = 512;
-
+// row's census signatures are staged in shared memory. Warps take 32-pixel
+// chunks: a window of <= 16 levels is written by its own lane, a wider window
+// by the whole warp (lanes across its levels, coalesced byte stores).
 __device__ __forceinline__ uint8_t cell_cost(const uint32_t* sl, const uint32_t* sr, int x, int d,
                                              int W, bool row_def) {
     const int xr = x - d;
@@ -246,18 +241,12 @@ __device__ __forceinline__ uint8_t cell_cost(const uint32_t* sl, const uint32_t*
     return ok ? static_cast<uint8_t>(__popc(sl[x] ^ sr[xr])) : static_cast<uint8_t>(kMaxCost);
 }
 
-__host__ __device__ inline int cost_stage_bytes(int d_max) { return 32 * d_max + 32; }
-
-__global__ void __launch_bounds__(kCostThreads) cost_kernel(Bufs b) {
-    extern __shared__ __align__(16) uint32_t sm[];
+__global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
+    extern __shared__ uint32_t sm[];
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
     const int W = b.W;
-    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
-    const int nwarps = static_cast<int>(blockDim.x >> 5);
     uint32_t* sl = sm;
     uint32_t* sr = sl + W;
-    uint8_t* stg = reinterpret_cast<uint8_t*>(sm + ((2 * W + 3) & ~3)) +
-                   static_cast<size_t>(warp) * cost_stage_bytes(b.d_max);
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
     for (int x = threadIdx.x; x < W; x += blockDim.x) {
@@ -267,52 +256,36 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(Bufs b) {
     __syncthreads();
     uint8_t* base = b.cost + static_cast<size_t>(a) * b.vol_cap;
     const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
+    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+    const int nwarps = static_cast<int>(blockDim.x >> 5);
     for (int x0 = warp * 32; x0 < W; x0 += 32 * nwarps) {
-        const int np = min(32, W - x0);
         const int x = x0 + lane;
-        const bool active = lane < np;
+        const bool active = x < W;
         const uint32_t lh = active ? b.lohi[pbase + x] : 0u;
         const uint32_t o = active ? off[x] : 0u;
-        const int lo = static_cast<int>(lh & 0xffffu), n = active ? static_cast<int>(lh >> 16) - lo + 1 : 0;
-        const uint32_t c0 = __shfl_sync(0xffffffffu, o, 0);
-        const uint32_t len = __shfl_sync(0xffffffffu, o + static_cast<uint32_t>(n), np - 1) - c0;
-        const uint32_t shift = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(base + c0) & 15u);
-        uint8_t* st = stg + shift - c0;  // st[c] stages cell c of the chunk
+        const int lo = static_cast<int>(lh & 0xffffu), n = static_cast<int>(lh >> 16) - lo + 1;
         const bool narrow = active && n <= 16;
-        if (narrow)
-            for (int j = 0; j < n; ++j) st[o + j] = cell_cost(sl, sr, x, lo + j, W, row_def);
+        if (narrow) {
+            uint8_t* dst = base + o;
+            for (int j = 0; j < n; ++j) dst[j] = cell_cost(sl, sr, x, lo + j, W, row_def);
+        }
         unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
         while (bw) {
             const int src = __ffs(bw) - 1;
             bw &= bw - 1;
+            const int xw = x0 + src;
             const int lo_w = __shfl_sync(0xffffffffu, lo, src);
             const int n_w = __shfl_sync(0xffffffffu, n, src);
             const uint32_t o_w = __shfl_sync(0xffffffffu, o, src);
-            for (int j = lane; j < n_w; j += 32) st[o_w + j] = cell_cost(sl, sr, x0 + src, lo_w + j, W, row_def);
+            uint8_t* dst = base + o_w;
+            for (int j = lane; j < n_w; j += 32) dst[j] = cell_cost(sl, sr, xw, lo_w + j, W, row_def);
         }
-        __syncwarp();
-        // copy out: block k covers staging bytes [16k, 16k + 16) = volume
-        // bytes from the aligned address (base + c0 - shift) + 16k
-        const uint32_t total = shift + len;
-        uint8_t* g = base + c0 - shift;
-        for (uint32_t k = lane; 16u * k < total; k += 32) {
-            const uint32_t b0 = 16u * k, b1 = b0 + 16u;
-            if (b0 >= shift && b1 <= total) {
-                *reinterpret_cast<uint4*>(g + b0) = *reinterpret_cast<const uint4*>(stg + b0);
-            } else {
-                for (uint32_t j = max(b0, shift); j < min(b1, total); ++j) g[j] = stg[j];
-            }
-        }
-        __syncwarp();
     }
 }
 
 void launch_cost(const Bufs& b, int n, Launch L) {
-    const size_t smem = sizeof(uint32_t) * ((2 * b.W + 3) & ~3) +
-                        static_cast<size_t>(kCostThreads / 32) * cost_stage_bytes(b.d_max);
-    cudaFuncSetAttribute(cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cost_kernel<<<dim3(b.H, n), kCostThreads, smem, L.st>>>(b);
+    const size_t smem = sizeof(uint32_t) * 2 * b.W;
+    cost_kernel<<<dim3(b.H, n), 512, smem, L.st>>>(b);
     ++*L.counter;
 }
 
