@@ -36,8 +36,9 @@ constexpr int kScanWarps = 2;  // warps per CTA (one task each)
 
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
 __host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
-// shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group sources
-__host__ __device__ inline int scan_warp_bytes(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 64; }
+// shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group source
+// records (lohi, cell, qo, lane << 1 | has_pred)
+__host__ __device__ inline int scan_warp_bytes(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 256; }
 
 bool sweep_supported(int W, int H, int d_max, int p2) {
     // u8 path costs need 24 + P2 <= 255; a window is <= 16 lanes x 4 quads
@@ -67,16 +68,19 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
     return d;
 }
 
-__device__ __forceinline__ uint32_t ld_na(const uint32_t* p) {
-    uint32_t v;
-    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void lds128(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(addr));
 }
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const uint32_t my_sb = wbase + static_cast<uint32_t>(lane) * SB;
     const uint32_t rbase = wbase + 32u * static_cast<uint32_t>(SB);
     const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(lane);
-    const uint32_t srcbase = rbase + 128u;  // 16 group source lanes
+    const uint32_t srcbase = rbase + 128u;  // 16 group source records (16-byte aligned)
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
@@ -268,10 +272,10 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         p = y * W + x;
         return x >= 0 && x < W;
     };
-    auto load_meta = [&](int p, PixMeta& m) {  // used from registers: keep L1 for the costs
-        m.lohi = ld_na(lohi + p);
-        m.cell = ld_na(off + p);
-        m.qo = ld_na(qoff + p);
+    auto load_meta = [&](int p, PixMeta& m) {  // L1-allocating: a line serves 32 steps of a row
+        m.lohi = __ldg(lohi + p);
+        m.cell = __ldg(off + p);
+        m.qo = __ldg(qoff + p);
     };
 
     // metadata two steps ahead, costs of the next step prefetched into L1
@@ -321,16 +325,17 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
                 const bool mine = (bw >> lane) & 1u;
                 const int rank = __popc(bw & ((1u << lane) - 1u));
                 const bool go = mine && rank < PER;
-                if (go) sts32(srcbase + 4u * static_cast<uint32_t>(rank), static_cast<uint32_t>(lane));
+                if (go)
+                    sts128(srcbase + 16u * static_cast<uint32_t>(rank), mc.lohi, mc.cell, mc.qo,
+                           (static_cast<uint32_t>(lane) << 1) | (prev_active ? 1u : 0u));
                 const unsigned done = __ballot_sync(0xffffffffu, go);
                 const int cnt = __popc(done);
-                const int src = gi < cnt ? static_cast<int>(lds32(srcbase + 4u * static_cast<uint32_t>(gi))) : lane;
+                PixMeta pw{0u, 0u, 0u};
+                uint32_t sw = static_cast<uint32_t>(lane) << 1;
+                if (gi < cnt) lds128(srcbase + 16u * static_cast<uint32_t>(gi), pw.lohi, pw.cell, pw.qo, sw);
                 __syncwarp();
-                PixMeta pw;
-                pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
-                pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
-                pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
-                const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
+                const int src = static_cast<int>(sw >> 1);
+                const bool hp = (sw & 1u) != 0u;
                 scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
                                  rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2,
                                  P2x4, mask_tab);
