@@ -36,9 +36,8 @@ constexpr int kScanWarps = 2;  // warps per CTA (one task each)
 
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
 __host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
-// shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group source
-// records (lohi, cell, qo, lane << 1 | has_pred)
-__host__ __device__ inline int scan_warp_bytes(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 256; }
+// shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group sources
+__host__ __device__ inline int scan_warp_bytes(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 64; }
 
 bool sweep_supported(int W, int H, int d_max, int p2) {
     // u8 path costs need 24 + P2 <= 255; a window is <= 16 lanes x 4 quads
@@ -72,15 +71,6 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
-}
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
-                 : "memory");
-}
-__device__ __forceinline__ void lds128(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
-                 : "r"(addr));
 }
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -129,18 +119,16 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     const int k0 = lg * Q;                  // first window quad of this lane
     const int a0 = q0 + min(k0, nq - 1);    // absolute quad (clamped into the window)
 
-    uint32_t ivA[Q], ivB[Q], LA[Q], LB[Q];
+    uint32_t CA[Q], CB[Q], ivA[Q], ivB[Q], LA[Q], LB[Q];
     bool act[Q];
-    // matching costs of levels 4*a0 .. 4*a0 + 4Q - 1 (bytes outside the window
-    // masked): the raw words are loaded first and consumed last, after the
-    // predecessor terms, to cover their latency
-    const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
-    const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-    const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
-    uint32_t c[Q + 1];
-#pragma unroll
-    for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
     {
+        // matching costs of levels 4*a0 .. 4*a0 + 4Q - 1 (bytes outside the window masked)
+        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+        const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
+        uint32_t c[Q + 1];
+#pragma unroll
+        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
         // invalid-level masks of the lane's 16 levels from the table:
         // row = levels below lo in the first quad, col = last valid level + 1
         const int start = 4 * (q0 + k0);  // unclamped first level of the lane
@@ -154,7 +142,12 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         if (Q > 2) { ivA[2] = m1.x; ivB[2] = m1.y; }
         if (Q > 3) { ivA[3] = m1.z; ivB[3] = m1.w; }
 #pragma unroll
-        for (int t = 0; t < Q; ++t) act[t] = pix && k0 + t < nq;
+        for (int t = 0; t < Q; ++t) {
+            const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
+            CA[t] = prmt(cq, 0u, 0x4140u) | (ivA[t] & kPoison2);
+            CB[t] = prmt(cq, 0u, 0x4342u) | (ivB[t] & kPoison2);
+            act[t] = pix && k0 + t < nq;
+        }
     }
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
     const uint32_t prng = lds32(rp);
@@ -177,19 +170,11 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         const uint32_t e1 = prmt(w[t + 1], 0u, 0x4342u);   // M(d0+2), M(d0+3)
         const uint32_t mpa = prmt(w[t + 1], 0u, 0x4241u);  // M(d0+1), M(d0+2)
         const uint32_t mpb = prmt(e1, w[t + 2], 0x1432u);  // M(d0+3), M(d0+4)
-        LA[t] = __viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0);
-        LB[t] = __viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1);
-        mma = mpb;
-    }
-#pragma unroll
-    for (int t = 0; t < Q; ++t) {
-        const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
-        const uint32_t CA = prmt(cq, 0u, 0x4140u) | (ivA[t] & kPoison2);
-        const uint32_t CB = prmt(cq, 0u, 0x4342u) | (ivB[t] & kPoison2);
         // u16 lanes never carry here, so the adds go to the FMA pipe (IMAD)
-        LA[t] = mad_u32(LA[t], 1u, CA);
-        LB[t] = mad_u32(LB[t], 1u, CB);
+        LA[t] = mad_u32(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), 1u, CA[t]);
+        LB[t] = mad_u32(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), 1u, CB[t]);
         mn = __vimin3_u16x2(mn, LA[t], LB[t]);
+        mma = mpb;
     }
     const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
     const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
@@ -241,7 +226,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const uint32_t my_sb = wbase + static_cast<uint32_t>(lane) * SB;
     const uint32_t rbase = wbase + 32u * static_cast<uint32_t>(SB);
     const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(lane);
-    const uint32_t srcbase = rbase + 128u;  // 16 group source records (16-byte aligned)
+    const uint32_t srcbase = rbase + 128u;  // 16 group source lanes
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
@@ -261,10 +246,11 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const int c = horiz ? 32 * g + lane : (sl == 1 ? -(H - 1) : 0) + 32 * g + lane;
     bool prev_active = false;
 
+    // p: the metadata index of step k (column-major for horizontal lines)
     auto pixel_at = [&](int k, int& p) -> bool {
         if (horiz) {
             const int x = dx < 0 ? k : W - 1 - k;
-            p = c * W + x;
+            p = x * H + c;
             return c < H;
         }
         const int y = dy < 0 ? k : H - 1 - k;
@@ -272,10 +258,18 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         p = y * W + x;
         return x >= 0 && x < W;
     };
-    auto load_meta = [&](int p, PixMeta& m) {  // L1-allocating: a line serves 32 steps of a row
-        m.lohi = __ldg(lohi + p);
-        m.cell = __ldg(off + p);
-        m.qo = __ldg(qoff + p);
+    const uint4* tmeta = b.tmeta + static_cast<size_t>(s) * b.P;
+    auto load_meta = [&](int p, PixMeta& m) {
+        if (horiz) {  // lanes = consecutive rows: one coalesced 16-byte record each
+            const uint4 v = __ldg(tmeta + p);
+            m.lohi = v.x;
+            m.cell = v.y;
+            m.qo = v.z;
+        } else {
+            m.lohi = __ldg(lohi + p);
+            m.cell = __ldg(off + p);
+            m.qo = __ldg(qoff + p);
+        }
     };
 
     // metadata two steps ahead, costs of the next step prefetched into L1
@@ -325,17 +319,16 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
                 const bool mine = (bw >> lane) & 1u;
                 const int rank = __popc(bw & ((1u << lane) - 1u));
                 const bool go = mine && rank < PER;
-                if (go)
-                    sts128(srcbase + 16u * static_cast<uint32_t>(rank), mc.lohi, mc.cell, mc.qo,
-                           (static_cast<uint32_t>(lane) << 1) | (prev_active ? 1u : 0u));
+                if (go) sts32(srcbase + 4u * static_cast<uint32_t>(rank), static_cast<uint32_t>(lane));
                 const unsigned done = __ballot_sync(0xffffffffu, go);
                 const int cnt = __popc(done);
-                PixMeta pw{0u, 0u, 0u};
-                uint32_t sw = static_cast<uint32_t>(lane) << 1;
-                if (gi < cnt) lds128(srcbase + 16u * static_cast<uint32_t>(gi), pw.lohi, pw.cell, pw.qo, sw);
+                const int src = gi < cnt ? static_cast<int>(lds32(srcbase + 4u * static_cast<uint32_t>(gi))) : lane;
                 __syncwarp();
-                const int src = static_cast<int>(sw >> 1);
-                const bool hp = (sw & 1u) != 0u;
+                PixMeta pw;
+                pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
+                pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
+                pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
+                const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
                 scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
                                  rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2,
                                  P2x4, mask_tab);

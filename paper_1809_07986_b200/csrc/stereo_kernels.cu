@@ -211,20 +211,37 @@ __global__ void row_scan_kernel(Bufs b) {
     }
 }
 
+// Adds the row bases to the in-row offsets, and writes the column-major
+// packed copy {lohi, off, qoff} that horizontal scanlines read coalesced
+// (lanes = consecutive rows). 32x32 tiles through shared memory.
 __global__ void offsets_finalize_kernel(Bufs b) {
-    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
-    const uint32_t rb = b.row_sum[static_cast<size_t>(s) * b.H + y];
-    const uint32_t qb = b.qrow_sum[static_cast<size_t>(s) * b.H + y];
-    const size_t orow = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * b.W;
-    for (int x = threadIdx.x; x < b.W; x += blockDim.x) {
-        b.off[orow + x] += rb;
-        b.qoff[orow + x] += qb;
+    __shared__ uint4 tile[32][33];
+    const int a = blockIdx.z, s = slot_of(b, a);
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const size_t obase = static_cast<size_t>(s) * (b.P + 1), pbase = static_cast<size_t>(s) * b.P;
+    for (int j = ty; j < 32; j += 8) {
+        const int y = y0 + j, x = x0 + tx;
+        if (y < b.H && x < b.W) {
+            const uint32_t rb = b.row_sum[static_cast<size_t>(s) * b.H + y];
+            const uint32_t qb = b.qrow_sum[static_cast<size_t>(s) * b.H + y];
+            const size_t o = obase + static_cast<size_t>(y) * b.W + x;
+            const uint32_t off = b.off[o] + rb, qo = b.qoff[o] + qb;
+            b.off[o] = off;
+            b.qoff[o] = qo;
+            tile[j][tx] = make_uint4(b.lohi[pbase + static_cast<size_t>(y) * b.W + x], off, qo, 0u);
+        }
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+        const int x = x0 + j, y = y0 + tx;
+        if (y < b.H && x < b.W) b.tmeta[pbase + static_cast<size_t>(x) * b.H + y] = tile[tx][j];
     }
 }
 
 void launch_offsets(const Bufs& b, int n, Launch L) {
     row_scan_kernel<<<dim3(n, 2), 1024, 0, L.st>>>(b);
-    offsets_finalize_kernel<<<dim3(b.H, n), kRowThreads, 0, L.st>>>(b);
+    offsets_finalize_kernel<<<dim3((b.W + 31) / 32, (b.H + 31) / 32, n), dim3(32, 8), 0, L.st>>>(b);
     *L.counter += 2;
 }
 
