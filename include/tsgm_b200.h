@@ -224,6 +224,50 @@ int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_
                    const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov,
                    int32_t* ed, uint8_t* ev, double* diff);
 
+/* ------------------------------------------------------------------------
+ * Moving-object box detector on the diff map (
+ * include/tsgm/motion_detect.hpp, src/motion_detect.cpp). The summed-area
+ * table and the candidate-window scoring run on the GPU; the greedy merge runs
+ * on the host (exact, incremental). Results equal the reference's.
+ * ------------------------------------------------------------------------ */
+/* DetectionBox (motion_detect.hpp:24-34): half-open [x0,x1) x [y0,y1), score =
+ * mean |disparity difference| inside. */
+typedef struct {
+    int32_t x0, y0, x1, y1;
+    double score;
+} tsgm_box;
+
+/* DetectConfig (motion_detect.hpp:36-44): window_wh holds n_windows (w, h)
+ * pairs (at most 16); defaults {20,20},{30,30},{40,40},{50,50},{50,75}, 2.0,
+ * 0.2, 400. Validated like DetectConfig::validate (motion_detect.cpp:11-23). */
+typedef struct {
+    const int32_t* window_wh;
+    int32_t n_windows;
+    double score_thresh;
+    double merge_stop_iou;
+    int64_t min_box_area;
+} tsgm_detect_config;
+
+/* integral_image (motion_detect.hpp:46, motion_detect.cpp:25-42): sat holds
+ * (h+1) x (w+1) doubles, zero first row and column. */
+int tsgm_integral_image(const double* map, int32_t w, int32_t h, double* sat);
+/* detect_candidate_windows (motion_detect.hpp:56-57): writes min(cap, count)
+ * boxes in (size, row, column) order; *n_out = count. */
+int tsgm_detect_candidate_windows(const double* diff, int32_t w, int32_t h,
+                                  const tsgm_detect_config* cfg, tsgm_box* out, int64_t cap,
+                                  int64_t* n_out);
+/* greedy_merge (motion_detect.hpp:63): in place on the host; *n_out = survivors. */
+int tsgm_greedy_merge(tsgm_box* boxes, int64_t n, const tsgm_detect_config* cfg, int64_t* n_out);
+/* detect_moving_objects (motion_detect.hpp:68-69) = merge(candidates). */
+int tsgm_detect_moving_objects(const double* diff, int32_t w, int32_t h,
+                               const tsgm_detect_config* cfg, tsgm_box* out, int64_t cap,
+                               int64_t* n_out);
+/* Batched: detect_moving_objects on the diff maps of the context's last step
+ * for n slots; slot i's boxes go to out[i*cap_each ..], their count (which
+ * may exceed cap_each: then only cap_each are written) to n_each[i]. */
+int tsgm_detect(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const tsgm_detect_config* cfg,
+                tsgm_box* out, int64_t cap_each, int64_t* n_each);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@
 // one batched launch sequence per frame.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -22,6 +23,7 @@
 
 #include "tsgm/geometry.hpp"
 #include "tsgm/matching_cost.hpp"
+#include "tsgm/motion_detect.hpp"
 #include "tsgm/sgm.hpp"
 #include "tsgm/temporal_filter.hpp"
 #include "tsgm_b200.h"
@@ -178,6 +180,83 @@ inline DisparityState correct(const DisparityState& pred, const DisparityMap& me
     return out;
 }
 
+// ---- box detector (motion_detect.hpp:46-72): SAT + scoring on the GPU,
+// greedy merge on the host; results equal the reference's.
+namespace detail {
+struct DetectC {
+    std::vector<std::int32_t> wh;
+    tsgm_detect_config c{};
+    explicit DetectC(const DetectConfig& cfg) {
+        for (const auto& [w, h] : cfg.window_sizes) {
+            wh.push_back(w);
+            wh.push_back(h);
+        }
+        c.window_wh = wh.data();
+        c.n_windows = static_cast<std::int32_t>(cfg.window_sizes.size());
+        c.score_thresh = cfg.score_thresh;
+        c.merge_stop_iou = cfg.merge_stop_iou;
+        c.min_box_area = cfg.min_box_area;
+    }
+};
+inline std::vector<DetectionBox> to_boxes(const std::vector<tsgm_box>& v, std::int64_t n) {
+    std::vector<DetectionBox> out;
+    for (std::int64_t i = 0; i < n; ++i)
+        out.push_back(DetectionBox{v[i].x0, v[i].y0, v[i].x1, v[i].y1, v[i].score});
+    return out;
+}
+template <typename Fn>
+std::vector<DetectionBox> boxes_call(Fn fn) {
+    std::vector<tsgm_box> buf(4096);
+    std::int64_t n = 0;
+    check(fn(buf.data(), static_cast<std::int64_t>(buf.size()), &n));
+    if (n > static_cast<std::int64_t>(buf.size())) {
+        buf.resize(static_cast<size_t>(n));
+        check(fn(buf.data(), n, &n));
+    }
+    return to_boxes(buf, n);
+}
+}  // namespace detail
+
+inline SummedAreaTable integral_image(const Image<double>& map) {
+    SummedAreaTable sat;
+    sat.width = map.width();
+    sat.height = map.height();
+    sat.sum.assign(static_cast<size_t>(sat.height + 1) * (sat.width + 1), 0.0);
+    detail::check(tsgm_integral_image(map.data(), map.width(), map.height(), sat.sum.data()));
+    return sat;
+}
+
+inline std::vector<DetectionBox> detect_candidate_windows(const Image<double>& diff,
+                                                          const DetectConfig& cfg,
+                                                          int threads = 1) {
+    (void)threads;
+    const detail::DetectC c(cfg);
+    return detail::boxes_call([&](tsgm_box* out, std::int64_t cap, std::int64_t* n) {
+        return tsgm_detect_candidate_windows(diff.data(), diff.width(), diff.height(), &c.c, out,
+                                             cap, n);
+    });
+}
+
+inline std::vector<DetectionBox> greedy_merge(std::vector<DetectionBox> boxes,
+                                              const DetectConfig& cfg) {
+    const detail::DetectC c(cfg);
+    std::vector<tsgm_box> v;
+    for (const DetectionBox& b : boxes) v.push_back(tsgm_box{b.x0, b.y0, b.x1, b.y1, b.score});
+    std::int64_t n = 0;
+    detail::check(tsgm_greedy_merge(v.data(), static_cast<std::int64_t>(v.size()), &c.c, &n));
+    return detail::to_boxes(v, n);
+}
+
+inline std::vector<DetectionBox> detect_moving_objects(const Image<double>& diff,
+                                                       const DetectConfig& cfg, int threads = 1) {
+    (void)threads;
+    const detail::DetectC c(cfg);
+    return detail::boxes_call([&](tsgm_box* out, std::int64_t cap, std::int64_t* n) {
+        return tsgm_detect_moving_objects(diff.data(), diff.width(), diff.height(), &c.c, out,
+                                          cap, n);
+    });
+}
+
 // Batched, device-resident production path.
 class Engine {
 public:
@@ -233,6 +312,30 @@ public:
         fetch(slot, TSGM_OUT_EXPORT_VALID, res.export_map.valid.data(), 1);
         fetch(slot, TSGM_OUT_DIFF, res.diff.data(), 8);
         return res;
+    }
+
+    // detect_moving_objects on the diff maps of the slots' last frame.
+    std::vector<std::vector<DetectionBox>> detect(const std::vector<int>& slots,
+                                                  const DetectConfig& cfg) const {
+        const detail::DetectC c(cfg);
+        const int n = static_cast<int>(slots.size());
+        std::int64_t cap = 1024;
+        std::vector<std::int64_t> cnt(n);
+        std::vector<tsgm_box> buf;
+        for (;;) {
+            buf.assign(static_cast<size_t>(cap) * n, tsgm_box{});
+            detail::check(tsgm_detect(ctx_, n, slots.data(), &c.c, buf.data(), cap, cnt.data()));
+            std::int64_t mx = 0;
+            for (std::int64_t v : cnt) mx = std::max(mx, v);
+            if (mx <= cap) break;
+            cap = mx;
+        }
+        std::vector<std::vector<DetectionBox>> out(n);
+        for (int i = 0; i < n; ++i)
+            out[i] = detail::to_boxes(std::vector<tsgm_box>(buf.begin() + i * cap,
+                                                            buf.begin() + i * cap + cnt[i]),
+                                      cnt[i]);
+        return out;
     }
 
     // A21 moving-object mask of a slot's last frame.

@@ -5,6 +5,7 @@
 // facade must throw the reference's exception types. Built by
 // `make -C oracle facade` into oracle/_ref/facade_parity; run on the GPU box by
 // tests/test_gpu_facade.py. Exit 0 = parity.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -136,6 +137,46 @@ int main() {
                    "Engine vs step");
             s = one.state;
         }
+    }
+    // box detector (motion_detect.hpp): reference vs facade on the step's diff
+    {
+        std::mt19937 rng(5);
+        Image<double> diff(w, h, 0.0);
+        std::uniform_int_distribution<int> bx(0, w - 60), by(h / 3, h - 40);
+        std::uniform_real_distribution<double> val(1.0, 8.0);
+        for (int k = 0; k < 5; ++k) {
+            const int x0 = bx(rng), y0 = by(rng);
+            const double v = val(rng);
+            for (int y = y0; y < std::min(h, y0 + 35); ++y)
+                for (int x = x0; x < x0 + 55; ++x) diff(x, y) = v + 0.05 * ((x + 2 * y) % 7);
+        }
+        DetectConfig dc;
+        EXPECT(integral_image(diff).sum == tsgm::gpu::integral_image(diff).sum, "integral_image");
+        const auto cr = detect_candidate_windows(diff, dc, 4);
+        EXPECT(cr == tsgm::gpu::detect_candidate_windows(diff, dc), "detect_candidate_windows");
+        EXPECT(greedy_merge(cr, dc) == tsgm::gpu::greedy_merge(cr, dc), "greedy_merge");
+        const auto dr = detect_moving_objects(diff, dc);
+        EXPECT(!dr.empty() && dr == tsgm::gpu::detect_moving_objects(diff, dc),
+               "detect_moving_objects");
+        try {
+            DetectConfig bad;
+            bad.merge_stop_iou = 1.0;
+            tsgm::gpu::detect_moving_objects(diff, bad);
+            EXPECT(false, "invalid DetectConfig did not throw");
+        } catch (const std::invalid_argument&) {
+        }
+        // batched engine: detection on the slot's own diff map
+        tsgm::gpu::Engine eng(calib, params, cfg, 1);
+        GrayImage left(w, h), right(w, h);
+        std::copy(L.begin(), L.begin() + static_cast<long>(w) * h, left.data());
+        std::copy(R.begin(), R.begin() + static_cast<long>(w) * h, right.data());
+        eng.step({0}, {&left}, {&right}, {RigidMotion{}});
+        eng.step({0}, {&left}, {&right}, {yaw(0.01)});
+        DetectConfig loose;
+        loose.score_thresh = 0.5;
+        const auto got = eng.detect({0}, loose);
+        EXPECT(got.size() == 1 && got[0] == detect_moving_objects(eng.result(0).diff, loose),
+               "Engine::detect");
     }
     std::printf("facade parity: %s (%d failures)\n", fails ? "FAIL" : "ok", fails);
     return fails ? 1 : 0;

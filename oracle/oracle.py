@@ -54,6 +54,24 @@ class FilterConfig:
     range_stddev_gain: float = 2.0
 
 
+@dataclass
+class DetectConfig:
+    """DetectConfig (motion_detect.hpp:36-44)."""
+    window_sizes: tuple = ((20, 20), (30, 30), (40, 40), (50, 50), (50, 75))
+    score_thresh: float = 2.0
+    merge_stop_iou: float = 0.2
+    min_box_area: int = 400
+
+
+def _wh(cfg):
+    return np.ascontiguousarray(np.array(cfg.window_sizes, dtype=np.int32).reshape(-1))
+
+
+def _boxes_arr(boxes):
+    """Boxes as float64 [n, 5] = x0, y0, x1, y1, score."""
+    return np.ascontiguousarray(np.asarray(boxes, dtype=np.float64).reshape(-1, 5))
+
+
 def build(reference: bool = True) -> None:
     """Compile the checkers (``make -C oracle``); the reference only when its
     sources are present (this container, not the GPU box)."""
@@ -288,6 +306,46 @@ class Reference(_Lib):
                                   _p(R), _p(t), _p(c4), calib.d_max, _p(sp), _p(fa), threads,
                                   _p(od), _p(op), _p(ov), _p(ed), _p(ev), _p(diff)))
         return dict(d=od, p=op, valid=ov, export_d=ed, export_valid=ev, diff=diff)
+
+
+    # ---- box detector (motion_detect.cpp) ----
+    def integral_image(self, m):
+        m = _f64(m)
+        h, w = m.shape
+        sat = np.zeros((h + 1, w + 1))
+        self._c(self.lib.ref_integral_image(_p(m), w, h, _p(sat)))
+        return sat
+
+    def _detect_args(self, cfg):
+        wh = _wh(cfg)
+        return wh, [_p(wh), len(cfg.window_sizes), C.c_double(cfg.score_thresh),
+                    C.c_double(cfg.merge_stop_iou), C.c_longlong(cfg.min_box_area)]
+
+    def candidates(self, diff, cfg, threads=1):
+        diff = _f64(diff)
+        h, w = diff.shape
+        wh, args = self._detect_args(cfg)
+        n = C.c_longlong()
+        cap = 1 << 16
+        while True:
+            out = np.zeros((cap, 5))
+            self._c(self.lib.ref_candidates(_p(diff), w, h, *args, threads, _p(out),
+                                            C.c_longlong(cap), C.byref(n)))
+            if n.value <= cap:
+                return out[:n.value]
+            cap = n.value
+
+    def greedy_merge(self, boxes, cfg):
+        b = _boxes_arr(boxes)
+        wh, args = self._detect_args(cfg)
+        out = np.zeros_like(b)
+        n = C.c_longlong()
+        self._c(self.lib.ref_greedy_merge(_p(b), C.c_longlong(len(b)), *args, _p(out),
+                                          C.byref(n)))
+        return out[:n.value]
+
+    def detect(self, diff, cfg, threads=1):
+        return self.greedy_merge(self.candidates(diff, cfg, threads), cfg)
 
 
 class _OrCalib(C.Structure):
@@ -557,6 +615,68 @@ class Port(_Lib):
                                  _p(out["export_d"]), _p(out["export_valid"]), _p(out["diff"]),
                                  C.byref(dbg) if dbg is not None else None))
         return out
+
+
+
+class _OrBox(C.Structure):
+    _fields_ = [("x0", C.c_int), ("y0", C.c_int), ("x1", C.c_int), ("y1", C.c_int),
+                ("score", C.c_double)]
+
+
+class _OrDetect(C.Structure):
+    _fields_ = [("window_wh", C.c_void_p), ("n_windows", C.c_int), ("score_thresh", C.c_double),
+                ("merge_stop_iou", C.c_double), ("min_box_area", C.c_longlong)]
+
+
+def _port_detect_methods(cls):
+    def _dc(self, cfg):
+        wh = _wh(cfg)
+        return wh, _OrDetect(wh.ctypes.data, len(cfg.window_sizes), cfg.score_thresh,
+                             cfg.merge_stop_iou, cfg.min_box_area)
+
+    def integral_image(self, m):
+        m = _f64(m)
+        h, w = m.shape
+        sat = np.zeros((h + 1, w + 1))
+        self.lib.or_integral_image(_p(m), w, h, _p(sat))
+        return sat
+
+    def candidates(self, diff, cfg, threads=1):
+        diff = _f64(diff)
+        h, w = diff.shape
+        wh, dc = _dc(self, cfg)
+        self.lib.or_candidates.restype = C.c_longlong
+        cap = 1 << 16
+        while True:
+            out = (_OrBox * cap)()
+            n = self.lib.or_candidates(_p(diff), w, h, C.byref(dc), out, C.c_longlong(cap))
+            if n < 0:
+                self._c(1)
+            if n <= cap:
+                return np.array([[b.x0, b.y0, b.x1, b.y1, b.score] for b in out[:n]],
+                                dtype=np.float64).reshape(-1, 5)
+            cap = n
+
+    def greedy_merge(self, boxes, cfg):
+        b = _boxes_arr(boxes)
+        wh, dc = _dc(self, cfg)
+        self._c(self.lib.or_detect_validate(C.byref(dc)))
+        arr = (_OrBox * max(1, len(b)))(*[_OrBox(int(r[0]), int(r[1]), int(r[2]), int(r[3]), r[4])
+                                         for r in b])
+        self.lib.or_greedy_merge.restype = C.c_longlong
+        n = self.lib.or_greedy_merge(arr, C.c_longlong(len(b)), C.byref(dc))
+        return np.array([[x.x0, x.y0, x.x1, x.y1, x.score] for x in arr[:n]],
+                        dtype=np.float64).reshape(-1, 5)
+
+    def detect(self, diff, cfg, threads=1):
+        return greedy_merge(self, candidates(self, diff, cfg), cfg)
+
+    for f in (integral_image, candidates, greedy_merge, detect):
+        setattr(cls, f.__name__, f)
+    return cls
+
+
+_port_detect_methods(Port)
 
 
 _port = None

@@ -320,4 +320,82 @@ int ref_filter_validate(const double* filter, int d_max) {
     return guarded([&] { make_filter(filter).validate(d_max); });
 }
 
+
+// ---- box detector (motion_detect.cpp), SURVEY §8(f) row 1. Boxes are
+// exchanged as 5 doubles each: x0, y0, x1, y1, score.
+}  // extern "C"
+
+namespace {
+DetectConfig make_detect(const int* wh, int n_windows, double thresh, double stop_iou,
+                         long long min_area) {
+    DetectConfig c;
+    c.window_sizes.clear();
+    for (int i = 0; i < n_windows; ++i) c.window_sizes.emplace_back(wh[2 * i], wh[2 * i + 1]);
+    c.score_thresh = thresh;
+    c.merge_stop_iou = stop_iou;
+    c.min_box_area = min_area;
+    return c;
+}
+long long put_boxes(const std::vector<DetectionBox>& v, double* out, long long cap) {
+    for (size_t i = 0; i < v.size() && static_cast<long long>(i) < cap; ++i) {
+        out[5 * i + 0] = v[i].x0;
+        out[5 * i + 1] = v[i].y0;
+        out[5 * i + 2] = v[i].x1;
+        out[5 * i + 3] = v[i].y1;
+        out[5 * i + 4] = v[i].score;
+    }
+    return static_cast<long long>(v.size());
+}
+std::vector<DetectionBox> get_boxes(const double* in, long long n) {
+    std::vector<DetectionBox> v(static_cast<size_t>(n));
+    for (long long i = 0; i < n; ++i)
+        v[i] = DetectionBox{static_cast<int>(in[5 * i]), static_cast<int>(in[5 * i + 1]),
+                            static_cast<int>(in[5 * i + 2]), static_cast<int>(in[5 * i + 3]),
+                            in[5 * i + 4]};
+    return v;
+}
+}  // namespace
+
+extern "C" {
+
+int ref_integral_image(const double* map, int w, int h, double* sat) {
+    return guarded([&] {
+        const SummedAreaTable t = integral_image(to_image(map, w, h));
+        std::memcpy(sat, t.sum.data(), sizeof(double) * t.sum.size());
+    });
+}
+
+int ref_candidates(const double* diff, int w, int h, const int* wh, int n_windows, double thresh,
+                   double stop_iou, long long min_area, int threads, double* out, long long cap,
+                   long long* n_out) {
+    return guarded([&] {
+        *n_out = put_boxes(detect_candidate_windows(to_image(diff, w, h),
+                                                    make_detect(wh, n_windows, thresh, stop_iou,
+                                                                min_area),
+                                                    threads),
+                           out, cap);
+    });
+}
+
+int ref_greedy_merge(const double* in, long long n, const int* wh, int n_windows, double thresh,
+                     double stop_iou, long long min_area, double* out, long long* n_out) {
+    return guarded([&] {
+        *n_out = put_boxes(greedy_merge(get_boxes(in, n),
+                                        make_detect(wh, n_windows, thresh, stop_iou, min_area)),
+                           out, n);
+    });
+}
+
+int ref_detect(const double* diff, int w, int h, const int* wh, int n_windows, double thresh,
+               double stop_iou, long long min_area, int threads, double* out, long long cap,
+               long long* n_out) {
+    return guarded([&] {
+        *n_out = put_boxes(detect_moving_objects(to_image(diff, w, h),
+                                                 make_detect(wh, n_windows, thresh, stop_iou,
+                                                             min_area),
+                                                 threads),
+                           out, cap);
+    });
+}
+
 }  // extern "C"

@@ -693,3 +693,128 @@ int or_step(const double* sd, const double* sp, const uint8_t* sv, int state_w, 
     free(zd); free(zp); free(zv);
     return rc;
 }
+
+
+/* ======================================================= box detector (§8(f) row 1) */
+int or_detect_validate(const or_detect_cfg* c) {
+    /* DetectConfig::validate, motion_detect.cpp:11-23 */
+    if (c->n_windows < 1) return fail("DetectConfig: no window sizes");
+    for (int i = 0; i < c->n_windows; ++i)
+        if (c->window_wh[2 * i] < 1 || c->window_wh[2 * i + 1] < 1)
+            return fail("DetectConfig: non-positive window size");
+    if (!(c->score_thresh > 0.0)) return fail("DetectConfig: score_thresh must be positive");
+    if (!(c->merge_stop_iou > 0.0 && c->merge_stop_iou < 1.0))
+        return fail("DetectConfig: merge_stop_iou must lie in (0, 1)");
+    if (c->min_box_area < 0) return fail("DetectConfig: negative min_box_area");
+    return 0;
+}
+
+void or_integral_image(const double* map, int w, int h, double* sat) {
+    /* integral_image, motion_detect.cpp:25-42: row accumulator left to right,
+     * cur = above + row_acc */
+    const size_t sw = (size_t)w + 1;
+    for (size_t i = 0; i < sw; ++i) sat[i] = 0.0;
+    for (int y = 0; y < h; ++y) {
+        double acc = 0.0;
+        double* cur = sat + (size_t)(y + 1) * sw;
+        const double* above = sat + (size_t)y * sw;
+        cur[0] = 0.0;
+        for (int x = 0; x < w; ++x) {
+            acc += map[(size_t)y * w + x];
+            cur[x + 1] = above[x + 1] + acc;
+        }
+    }
+}
+
+static double sat_at(const double* sat, int w, int row, int col) {
+    return sat[(size_t)row * ((size_t)w + 1) + col];
+}
+
+int or_box_sum(const double* sat, int w, int h, const or_box* b, double* out) {
+    /* box_sum, motion_detect.cpp:44-50: ((a - b) - c) + d */
+    if (b->x0 < 0 || b->y0 < 0 || b->x1 > w || b->y1 > h || b->x0 >= b->x1 || b->y0 >= b->y1)
+        return fail("box_sum: box out of bounds");
+    *out = sat_at(sat, w, b->y1, b->x1) - sat_at(sat, w, b->y0, b->x1) -
+           sat_at(sat, w, b->y1, b->x0) + sat_at(sat, w, b->y0, b->x0);
+    return 0;
+}
+
+static long long box_area(const or_box* b) { return (long long)(b->x1 - b->x0) * (b->y1 - b->y0); }
+
+double or_iou(const or_box* a, const or_box* b) {
+    /* iou, motion_detect.cpp:52-62 */
+    const int ix0 = a->x0 > b->x0 ? a->x0 : b->x0;
+    const int iy0 = a->y0 > b->y0 ? a->y0 : b->y0;
+    const int ix1 = a->x1 < b->x1 ? a->x1 : b->x1;
+    const int iy1 = a->y1 < b->y1 ? a->y1 : b->y1;
+    if (ix0 >= ix1 || iy0 >= iy1) return 0.0;
+    const double inter = (double)(ix1 - ix0) * (iy1 - iy0);
+    const double uni = (double)box_area(a) + (double)box_area(b) - inter;
+    return inter / uni;
+}
+
+long long or_candidates(const double* diff, int w, int h, const or_detect_cfg* c, or_box* out,
+                        long long cap) {
+    /* detect_candidate_windows, motion_detect.cpp:64-99: sizes in order, rows
+     * top to bottom, columns left to right */
+    if (or_detect_validate(c)) return -1;
+    double* sat = (double*)malloc(sizeof(double) * ((size_t)w + 1) * ((size_t)h + 1));
+    or_integral_image(diff, w, h, sat);
+    const int region_top = h / 3;
+    long long n = 0;
+    for (int k = 0; k < c->n_windows; ++k) {
+        const int ww = c->window_wh[2 * k], wh = c->window_wh[2 * k + 1];
+        if (ww > w || region_top + wh > h) continue;
+        const int sx = ww / 4 > 1 ? ww / 4 : 1, sy = wh / 4 > 1 ? wh / 4 : 1;
+        const int n_rows = (h - wh - region_top) / sy + 1;
+        for (int row = 0; row < n_rows; ++row) {
+            const int y0 = region_top + row * sy;
+            for (int x0 = 0; x0 + ww <= w; x0 += sx) {
+                or_box b = {x0, y0, x0 + ww, y0 + wh, 0.0};
+                double sum;
+                or_box_sum(sat, w, h, &b, &sum);
+                const double mean = sum / (double)box_area(&b);
+                if (mean > c->score_thresh) {
+                    b.score = mean;
+                    if (n < cap) out[n] = b;
+                    ++n;
+                }
+            }
+        }
+    }
+    free(sat);
+    return n;
+}
+
+long long or_greedy_merge(or_box* boxes, long long n, const or_detect_cfg* c) {
+    /* greedy_merge, motion_detect.cpp:101-129: the best pair (first on ties)
+     * by exhaustive search, merged into the earlier box; then the area filter */
+    while (n > 1) {
+        double best = 0.0;
+        long long bi = 0, bj = 0;
+        for (long long i = 0; i + 1 < n; ++i)
+            for (long long j = i + 1; j < n; ++j) {
+                const double v = or_iou(&boxes[i], &boxes[j]);
+                if (v > best) {
+                    best = v;
+                    bi = i;
+                    bj = j;
+                }
+            }
+        if (best < c->merge_stop_iou) break;
+        or_box* a = &boxes[bi];
+        const or_box* b = &boxes[bj];
+        const double aa = (double)box_area(a), ab = (double)box_area(b);
+        a->score = (a->score * aa + b->score * ab) / (aa + ab);
+        if (b->x0 < a->x0) a->x0 = b->x0;
+        if (b->y0 < a->y0) a->y0 = b->y0;
+        if (b->x1 > a->x1) a->x1 = b->x1;
+        if (b->y1 > a->y1) a->y1 = b->y1;
+        memmove(&boxes[bj], &boxes[bj + 1], sizeof(or_box) * (size_t)(n - bj - 1));
+        --n;
+    }
+    long long m = 0;
+    for (long long i = 0; i < n; ++i)
+        if (box_area(&boxes[i]) >= c->min_box_area) boxes[m++] = boxes[i];
+    return m;
+}

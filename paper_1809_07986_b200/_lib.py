@@ -56,7 +56,22 @@ EXPORTS = [
     "tsgm_disparity_homography", "tsgm_warp_state_ex", "tsgm_predict",
     "tsgm_reject_discontinuities", "tsgm_fill_zoom_holes", "tsgm_derive_search_ranges",
     "tsgm_correct", "tsgm_step_once",
+    "tsgm_integral_image", "tsgm_detect_candidate_windows", "tsgm_greedy_merge",
+    "tsgm_detect_moving_objects", "tsgm_detect",
 ]
+
+
+class BoxC(C.Structure):
+    """tsgm_box (DetectionBox, motion_detect.hpp:24-34)."""
+    _fields_ = [("x0", C.c_int32), ("y0", C.c_int32), ("x1", C.c_int32), ("y1", C.c_int32),
+                ("score", C.c_double)]
+
+
+class DetectConfigC(C.Structure):
+    """tsgm_detect_config (DetectConfig, motion_detect.hpp:36-44)."""
+    _fields_ = [("window_wh", C.c_void_p), ("n_windows", C.c_int32),
+                ("score_thresh", C.c_double), ("merge_stop_iou", C.c_double),
+                ("min_box_area", C.c_int64)]
 
 
 def load():
@@ -89,6 +104,14 @@ def load():
         lib.tsgm_timer_end.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
         lib.tsgm_bench_aggregate.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                              C.POINTER(C.c_float), C.POINTER(C.c_uint64)]
+        dc = C.POINTER(DetectConfigC)
+        lib.tsgm_integral_image.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        for name in ("tsgm_detect_candidate_windows", "tsgm_detect_moving_objects"):
+            getattr(lib, name).argtypes = [C.c_void_p, C.c_int32, C.c_int32, dc, C.c_void_p,
+                                           C.c_int64, C.POINTER(C.c_int64)]
+        lib.tsgm_greedy_merge.argtypes = [C.c_void_p, C.c_int64, dc, C.POINTER(C.c_int64)]
+        lib.tsgm_detect.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, dc, C.c_void_p, C.c_int64,
+                                    C.c_void_p]
         _lib = lib
     return _lib
 

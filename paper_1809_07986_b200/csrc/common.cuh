@@ -12,6 +12,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/tsgm_b200.h"
+
 namespace tsgm {
 
 constexpr int kCensusRadius = 2;  // matching_cost.hpp:11
@@ -146,5 +148,25 @@ bool sweep_supported(int W, int H, int d_max, int p2);
 // (writes md/mv). At least one of the two must be set.
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
                             int write_s, int do_wta, Launch L, int subpix = 0);
+
+// Box detector (detect.cu), SURVEY §8(f) row 1.
+constexpr int kMaxDetectWindows = 16;
+struct DetectWindows {
+    int n;
+    int ww[kMaxDetectWindows], wh[kMaxDetectWindows];
+    int cols[kMaxDetectWindows], rows[kMaxDetectWindows];  // positions per size
+    long long base[kMaxDetectWindows + 1];                  // prefix of positions per size
+    int region_top;
+    double thresh;
+};
+// Window positions of the sizes that fit (motion_detect.cpp:68-76).
+void detect_windows(const tsgm_detect_config& c, int W, int H, DetectWindows& dw);
+// SAT of n maps (map + slots[a] * map_stride, or + a * map_stride when slots
+// is null) into sat + a * sat_stride, (H+1) x (W+1) each.
+void launch_sat(const double* map, size_t map_stride, double* sat, size_t sat_stride, int W, int H,
+                int n, const int* slots, Launch L);
+void launch_candidates(const double* sat, size_t sat_stride, int W, const DetectWindows& dw, int n,
+                       tsgm_box* out, long long cap, long long* counts, Launch L);
+long long greedy_merge_host(tsgm_box* boxes, long long n, const tsgm_detect_config& c);
 
 }  // namespace tsgm

@@ -13,6 +13,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -224,6 +225,11 @@ struct tsgm_ctx {
     void* snap[TSGM_OUT_COUNT]{};
     cudaEvent_t ev_snap_copied[TSGM_OUT_COUNT]{};
     bool snap_pending[TSGM_OUT_COUNT]{};
+    // box detector (tsgm_detect): per-slot SAT, candidate boxes and counts
+    double* det_sat = nullptr;
+    tsgm_box* det_boxes = nullptr;
+    long long* det_counts = nullptr;
+    long long det_cap = 0;  // candidate capacity per slot
 
     template <typename T>
     T* dalloc(size_t count) {
@@ -1124,6 +1130,204 @@ int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_
         d2h(x, ev, x->b.ev, P);
         d2h(x, diff, x->b.diff, P);
         sync(x);
+    });
+}
+
+
+// ---------------------------------------------------------------- box detector
+}  // extern "C"
+
+namespace {
+
+// DetectConfig::validate (motion_detect.cpp:11-23), same messages.
+void detect_validate(const tsgm_detect_config* c) {
+    if (!c) bad("DetectConfig: null configuration");
+    if (c->n_windows < 1 || !c->window_wh) bad("DetectConfig: no window sizes");
+    if (c->n_windows > kMaxDetectWindows) bad("DetectConfig: at most 16 window sizes");
+    for (int i = 0; i < c->n_windows; ++i)
+        if (c->window_wh[2 * i] < 1 || c->window_wh[2 * i + 1] < 1)
+            bad("DetectConfig: non-positive window size");
+    if (!(c->score_thresh > 0.0)) bad("DetectConfig: score_thresh must be positive");
+    if (!(c->merge_stop_iou > 0.0 && c->merge_stop_iou < 1.0))
+        bad("DetectConfig: merge_stop_iou must lie in (0, 1)");
+    if (c->min_box_area < 0) bad("DetectConfig: negative min_box_area");
+}
+
+// Device scratch for the stateless detector calls.
+struct DevScratch {
+    std::vector<void*> p;
+    cudaStream_t st = nullptr;
+    unsigned long long launches = 0;
+    DevScratch() { CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); }
+    ~DevScratch() {
+        if (st) cudaStreamSynchronize(st);
+        for (void* q : p) cudaFree(q);
+        if (st) cudaStreamDestroy(st);
+    }
+    template <typename T>
+    T* alloc(size_t n) {
+        void* q = nullptr;
+        CK(cudaMalloc(&q, sizeof(T) * std::max<size_t>(n, 1)));
+        p.push_back(q);
+        return static_cast<T*>(q);
+    }
+    Launch L() { return Launch{st, &launches}; }
+};
+
+// SAT + candidates of one host map on the GPU; returns the full count and
+// fills `boxes` with all of them.
+long long candidates_one(const double* diff, int w, int h, const tsgm_detect_config& c,
+                         std::vector<tsgm_box>& boxes) {
+    boxes.clear();
+    DetectWindows dw;
+    detect_windows(c, w, h, dw);
+    const long long total = dw.base[dw.n];
+    if (total == 0) return 0;
+    DevScratch d;
+    const size_t P = static_cast<size_t>(w) * h, SP = static_cast<size_t>(w + 1) * (h + 1);
+    double* m = d.alloc<double>(P);
+    double* sat = d.alloc<double>(SP);
+    tsgm_box* out = d.alloc<tsgm_box>(static_cast<size_t>(total));
+    long long* cnt = d.alloc<long long>(1);
+    CK(cudaMemcpyAsync(m, diff, sizeof(double) * P, cudaMemcpyHostToDevice, d.st));
+    launch_sat(m, P, sat, SP, w, h, 1, nullptr, d.L());
+    launch_candidates(sat, SP, w, dw, 1, out, total, cnt, d.L());
+    CK(cudaGetLastError());
+    long long n = 0;
+    CK(cudaMemcpyAsync(&n, cnt, sizeof n, cudaMemcpyDeviceToHost, d.st));
+    CK(cudaStreamSynchronize(d.st));
+    boxes.resize(static_cast<size_t>(n));
+    if (n) CK(cudaMemcpy(boxes.data(), out, sizeof(tsgm_box) * n, cudaMemcpyDeviceToHost));
+    return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsgm_integral_image(const double* map, int32_t w, int32_t h, double* sat) {
+    return guarded([&] {
+        if (!sat || (w > 0 && h > 0 && !map)) bad("integral_image: null argument");
+        if (w < 0 || h < 0) bad("integral_image: negative size");
+        const size_t SP = static_cast<size_t>(w + 1) * (h + 1);
+        if (w == 0 || h == 0) {
+            std::memset(sat, 0, sizeof(double) * SP);
+            return;
+        }
+        DevScratch d;
+        const size_t P = static_cast<size_t>(w) * h;
+        double* m = d.alloc<double>(P);
+        double* s = d.alloc<double>(SP);
+        CK(cudaMemcpyAsync(m, map, sizeof(double) * P, cudaMemcpyHostToDevice, d.st));
+        launch_sat(m, P, s, SP, w, h, 1, nullptr, d.L());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(sat, s, sizeof(double) * SP, cudaMemcpyDeviceToHost, d.st));
+        CK(cudaStreamSynchronize(d.st));
+    });
+}
+
+int tsgm_detect_candidate_windows(const double* diff, int32_t w, int32_t h,
+                                  const tsgm_detect_config* cfg, tsgm_box* out, int64_t cap,
+                                  int64_t* n_out) {
+    return guarded([&] {
+        detect_validate(cfg);
+        if (!n_out || (cap > 0 && !out)) bad("detect_candidate_windows: null argument");
+        if (w < 1 || h < 1 || !diff) bad("detect_candidate_windows: empty map");
+        std::vector<tsgm_box> boxes;
+        const long long n = candidates_one(diff, w, h, *cfg, boxes);
+        std::memcpy(out, boxes.data(), sizeof(tsgm_box) * static_cast<size_t>(std::min<long long>(n, cap)));
+        *n_out = n;
+    });
+}
+
+int tsgm_greedy_merge(tsgm_box* boxes, int64_t n, const tsgm_detect_config* cfg, int64_t* n_out) {
+    return guarded([&] {
+        detect_validate(cfg);
+        if (!n_out || (n > 0 && !boxes) || n < 0) bad("greedy_merge: bad arguments");
+        *n_out = greedy_merge_host(boxes, n, *cfg);
+    });
+}
+
+int tsgm_detect_moving_objects(const double* diff, int32_t w, int32_t h,
+                               const tsgm_detect_config* cfg, tsgm_box* out, int64_t cap,
+                               int64_t* n_out) {
+    return guarded([&] {
+        detect_validate(cfg);
+        if (!n_out || (cap > 0 && !out)) bad("detect_moving_objects: null argument");
+        if (w < 1 || h < 1 || !diff) bad("detect_moving_objects: empty map");
+        std::vector<tsgm_box> boxes;
+        const long long n = candidates_one(diff, w, h, *cfg, boxes);
+        const long long m = greedy_merge_host(boxes.data(), n, *cfg);
+        std::memcpy(out, boxes.data(), sizeof(tsgm_box) * static_cast<size_t>(std::min<long long>(m, cap)));
+        *n_out = m;
+    });
+}
+
+int tsgm_detect(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const tsgm_detect_config* cfg,
+                tsgm_box* out, int64_t cap_each, int64_t* n_each) {
+    return guarded([&] {
+        detect_validate(cfg);
+        if (!ctx || !slots || !n_each || (cap_each > 0 && !out)) bad("tsgm_detect: null argument");
+        check_slots(ctx, n, slots);
+        CK(cudaSetDevice(ctx->device));
+        DetectWindows dw;
+        detect_windows(*cfg, ctx->W, ctx->H, dw);
+        const long long total = dw.base[dw.n];
+        if (total == 0) {
+            for (int i = 0; i < n; ++i) n_each[i] = 0;
+            return;
+        }
+        const size_t SP = static_cast<size_t>(ctx->W + 1) * (ctx->H + 1);
+        if (!ctx->det_sat) {
+            ctx->det_sat = ctx->dalloc<double>(SP * ctx->max_slots);
+            ctx->det_counts = ctx->dalloc<long long>(ctx->max_slots);
+        }
+        if (total > ctx->det_cap) {
+            if (ctx->det_boxes) {
+                CK(cudaStreamSynchronize(ctx->st));
+                CK(cudaFree(ctx->det_boxes));
+                ctx->allocs.erase(std::find(ctx->allocs.begin(), ctx->allocs.end(),
+                                            static_cast<void*>(ctx->det_boxes)));
+            }
+            ctx->det_boxes = ctx->dalloc<tsgm_box>(static_cast<size_t>(total) * ctx->max_slots);
+            ctx->det_cap = total;
+        }
+        // this call's slot list (it may differ from the last step's)
+        std::vector<const uint8_t*> dl(n, ctx->d_img), dr(n, ctx->d_img);
+        std::vector<double> Hm(16 * static_cast<size_t>(n), 0.0);
+        upload_step(ctx, n, slots, dl.data(), dr.data(), Hm.data());
+        Launch L = ctx->L();
+        launch_sat(ctx->b.diff, ctx->P, ctx->det_sat, SP, ctx->W, ctx->H, n, ctx->d_slots, L);
+        launch_candidates(ctx->det_sat, SP, ctx->W, dw, n, ctx->det_boxes, ctx->det_cap,
+                          ctx->det_counts, L);
+        CK(cudaGetLastError());
+        std::vector<long long> cnt(n);
+        CK(cudaMemcpyAsync(cnt.data(), ctx->det_counts, sizeof(long long) * n,
+                           cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        std::vector<std::vector<tsgm_box>> boxes(n);
+        for (int i = 0; i < n; ++i) {
+            boxes[i].resize(static_cast<size_t>(cnt[i]));
+            if (cnt[i])
+                CK(cudaMemcpyAsync(boxes[i].data(), ctx->det_boxes + static_cast<size_t>(i) * ctx->det_cap,
+                                   sizeof(tsgm_box) * cnt[i], cudaMemcpyDeviceToHost, ctx->st));
+        }
+        CK(cudaStreamSynchronize(ctx->st));
+        // host merges, one sequence per worker thread
+        const int nt = std::max(1, std::min<int>(n, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<std::thread> pool;
+        std::vector<long long> kept(n, 0);
+        for (int t = 0; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                for (int i = t; i < n; i += nt)
+                    kept[i] = greedy_merge_host(boxes[i].data(), cnt[i], *cfg);
+            });
+        for (auto& th : pool) th.join();
+        for (int i = 0; i < n; ++i) {
+            n_each[i] = kept[i];
+            std::memcpy(out + static_cast<size_t>(i) * cap_each, boxes[i].data(),
+                        sizeof(tsgm_box) * static_cast<size_t>(std::min<long long>(kept[i], cap_each)));
+        }
     });
 }
 

@@ -85,3 +85,16 @@ class GpuBackend:
         finally:
             eng.close()
         return out
+
+    # ---- box detector (motion_detect.cpp) ----
+    def integral_image(self, m):
+        return tsgm.integral_image(m)
+
+    def candidates(self, diff, cfg, threads=1):
+        return tsgm.detect_candidate_windows(diff, cfg)
+
+    def greedy_merge(self, boxes, cfg):
+        return tsgm.greedy_merge(boxes, cfg)
+
+    def detect(self, diff, cfg, threads=1):
+        return tsgm.detect_moving_objects(diff, cfg)

@@ -291,6 +291,79 @@ def step(state, left, right, R, t, calib, params, cfg):
     return out
 
 
+# --------------------------------------------------------------------- detector
+@dataclass
+class DetectConfig:  # motion_detect.hpp:36-44
+    window_sizes: tuple = ((20, 20), (30, 30), (40, 40), (50, 50), (50, 75))
+    score_thresh: float = 2.0
+    merge_stop_iou: float = 0.2
+    min_box_area: int = 400
+
+    def _c(self):
+        wh = np.ascontiguousarray(np.asarray(self.window_sizes, np.int32).reshape(-1))
+        return wh, _lib.DetectConfigC(wh.ctypes.data, len(self.window_sizes), self.score_thresh,
+                                      self.merge_stop_iou, int(self.min_box_area))
+
+
+def _box_array(n):
+    return np.zeros(max(1, n), dtype=[("x0", np.int32), ("y0", np.int32), ("x1", np.int32),
+                                      ("y1", np.int32), ("score", np.float64)])
+
+
+def _boxes_out(arr, n):
+    """Boxes as float64 [n, 5] = x0, y0, x1, y1, score (DetectionBox fields)."""
+    a = arr[:n]
+    return np.stack([a["x0"], a["y0"], a["x1"], a["y1"], a["score"]], axis=1).astype(np.float64) \
+        if n else np.zeros((0, 5))
+
+
+def integral_image(m):
+    """integral_image (motion_detect.cpp:25-42): (h+1) x (w+1) f64, on the GPU."""
+    m = _f64(m)
+    h, w = m.shape
+    sat = np.zeros((h + 1, w + 1))
+    check(_lib.load().tsgm_integral_image(ptr(m), w, h, ptr(sat)))
+    return sat
+
+
+def _detect_call(fn, diff, cfg):
+    diff = _f64(diff)
+    h, w = diff.shape
+    wh, c = _as(cfg, DetectConfig)._c()
+    n = C.c_int64()
+    cap = 4096
+    while True:
+        out = _box_array(cap)
+        check(fn(ptr(diff), w, h, C.byref(c), ptr(out), cap, C.byref(n)))
+        if n.value <= cap:
+            return _boxes_out(out, n.value)
+        cap = n.value
+
+
+def detect_candidate_windows(diff, cfg=None):
+    """detect_candidate_windows (motion_detect.cpp:64-99), SAT and scoring on
+    the GPU; boxes in (size, row, column) order."""
+    return _detect_call(_lib.load().tsgm_detect_candidate_windows, diff, cfg or DetectConfig())
+
+
+def greedy_merge(boxes, cfg=None):
+    """greedy_merge (motion_detect.cpp:101-129), host, exact."""
+    b = np.asarray(boxes, np.float64).reshape(-1, 5)
+    arr = _box_array(len(b))
+    for k, f in enumerate(("x0", "y0", "x1", "y1")):
+        arr[f][:len(b)] = b[:, k].astype(np.int32)
+    arr["score"][:len(b)] = b[:, 4]
+    wh, c = _as(cfg or DetectConfig(), DetectConfig)._c()
+    n = C.c_int64()
+    check(_lib.load().tsgm_greedy_merge(ptr(arr), len(b), C.byref(c), C.byref(n)))
+    return _boxes_out(arr, n.value)
+
+
+def detect_moving_objects(diff, cfg=None):
+    """detect_moving_objects (motion_detect.cpp:142-145)."""
+    return _detect_call(_lib.load().tsgm_detect_moving_objects, diff, cfg or DetectConfig())
+
+
 # --------------------------------------------------------------------- engine
 _OUT_DTYPES = dict(state_d=np.float64, state_p=np.float64, state_valid=np.uint8,
                    export_d=np.int32, export_valid=np.uint8, diff=np.float64, mask=np.uint8,
@@ -411,6 +484,21 @@ class Engine:
         ms = C.c_float()
         check(self._lib.tsgm_timer_end(self._h, C.byref(ms)))
         return float(ms.value)
+
+    def detect(self, slots, cfg=None, cap_each=1024):
+        """detect_moving_objects on each slot's diff map of the last step
+        (SAT + scoring on the GPU, merges on host threads); list of [n, 5]."""
+        sl = np.asarray(slots, np.int32)
+        wh, c = _as(cfg or DetectConfig(), DetectConfig)._c()
+        while True:
+            out = _box_array(cap_each * len(sl))
+            n_each = np.zeros(len(sl), np.int64)
+            check(self._lib.tsgm_detect(self._h, len(sl), ptr(sl), C.byref(c), ptr(out), cap_each,
+                                        ptr(n_each)))
+            if n_each.max(initial=0) <= cap_each:
+                return [_boxes_out(out[i * cap_each:(i + 1) * cap_each], int(n_each[i]))
+                        for i in range(len(sl))]
+            cap_each = int(n_each.max())
 
     @property
     def vol_slots(self) -> int:

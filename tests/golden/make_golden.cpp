@@ -412,6 +412,92 @@ int main(int argc, char** argv) {
             st = res.state;
         }
     }
+    // ---- box detector (test_motion_detect.cpp), SURVEY §8(f) row 1 ----
+    auto put_boxes = [](const std::string& n, const std::vector<DetectionBox>& v) {
+        std::vector<double> f;
+        for (const DetectionBox& b : v) {
+            f.push_back(b.x0);
+            f.push_back(b.y0);
+            f.push_back(b.x1);
+            f.push_back(b.y1);
+            f.push_back(b.score);
+        }
+        put(n, "f8", {static_cast<long>(v.size()), 5}, f.data(), sizeof(double) * f.size());
+    };
+    {   // test_motion_detect.cpp:60-69 — SAT of a random integer map, seed 61
+        std::mt19937 rng(61);
+        Image<double> m(100, 100);
+        std::uniform_int_distribution<int> dist(0, 20);
+        for (int y = 0; y < 100; ++y)
+            for (int x = 0; x < 100; ++x) m(x, y) = dist(rng);
+        const SummedAreaTable sat = integral_image(m);
+        put_img("det_sat/map", m);
+        put("det_sat/sat", "f8", {101, 101}, sat.sum.data(), sizeof(double) * sat.sum.size());
+    }
+    {   // :86-133 — candidate windows on the test maps
+        DetectConfig cfg;
+        Image<double> hot(120, 120, 0.0);
+        for (int y = 60; y < 100; ++y)
+            for (int x = 40; x < 80; ++x) hot(x, y) = 10.0;
+        put_img("det_cand/hot", hot);
+        put_boxes("det_cand/hot_boxes", detect_candidate_windows(hot, cfg));
+        std::mt19937 rng(62);
+        Image<double> rnd(150, 150, 0.0);
+        std::uniform_real_distribution<double> v(0.0, 6.0);
+        for (int y = 0; y < 150; ++y)
+            for (int x = 0; x < 150; ++x) rnd(x, y) = v(rng);
+        put_img("det_cand/rand", rnd);
+        put_boxes("det_cand/rand_boxes", detect_candidate_windows(rnd, cfg));
+        Image<double> flat(200, 90, 5.0);
+        put_img("det_cand/flat", flat);
+        put_boxes("det_cand/flat_boxes", detect_candidate_windows(flat, cfg));
+    }
+    {   // :165-195 — greedy merging of random box sets, seeds 63 and 64
+        for (int seed : {63, 64}) {
+            std::mt19937 rng(seed);
+            std::uniform_int_distribution<int> c(0, seed == 63 ? 60 : 50);
+            std::uniform_int_distribution<int> sz(seed == 63 ? 20 : 21, seed == 63 ? 40 : 35);
+            std::vector<DetectionBox> in;
+            for (int i = 0; i < (seed == 63 ? 40 : 25); ++i) {
+                const int x0 = c(rng), y0 = c(rng);
+                in.push_back({x0, y0, x0 + sz(rng), y0 + sz(rng), 1.0});
+            }
+            DetectConfig loose;
+            loose.min_box_area = 0;
+            const std::string n = "det_merge/s" + std::to_string(seed);
+            put_boxes(n + "/in", in);
+            put_boxes(n + "/out_default", greedy_merge(in, DetectConfig{}));
+            put_boxes(n + "/out_loose", greedy_merge(in, loose));
+        }
+    }
+    {   // :221-257 — end-to-end detection, plus a KITTI-sized sparse map
+        Image<double> blk(160, 160, 0.0);
+        for (int y = 90; y < 130; ++y)
+            for (int x = 60; x < 100; ++x) blk(x, y) = 3.0;
+        DetectConfig cfg;
+        cfg.merge_stop_iou = 0.12;
+        put_img("det_e2e/block", blk);
+        put_boxes("det_e2e/block_boxes", detect_moving_objects(blk, cfg));
+        Image<double> three(160, 160, 0.0);
+        for (auto [bx, by] : {std::pair{20, 60}, {90, 100}, {40, 120}})
+            for (int y = by; y < by + 25; ++y)
+                for (int x = bx; x < bx + 25; ++x) three(x, y) = 6.0;
+        put_img("det_e2e/three", three);
+        put_boxes("det_e2e/three_boxes", detect_moving_objects(three, DetectConfig{}));
+        std::mt19937 rng(65);
+        Image<double> big(1242, 375, 0.0);
+        std::uniform_int_distribution<int> bxd(0, 1100), byd(100, 300), bsz(20, 120);
+        std::uniform_real_distribution<double> val(1.0, 9.0);
+        for (int k = 0; k < 8; ++k) {
+            const int x0 = bxd(rng), y0 = byd(rng), w = bsz(rng), h = bsz(rng) / 2 + 10;
+            const double v0 = val(rng);
+            for (int y = y0; y < std::min(375, y0 + h); ++y)
+                for (int x = x0; x < std::min(1242, x0 + w); ++x) big(x, y) = v0 + 0.01 * ((x * 7 + y * 3) % 11);
+        }
+        put_img("det_e2e/kitti", big);
+        put_boxes("det_e2e/kitti_cands", detect_candidate_windows(big, DetectConfig{}));
+        put_boxes("det_e2e/kitti_boxes", detect_moving_objects(big, DetectConfig{}));
+    }
     std::fclose(g_out);
     return 0;
 }
