@@ -231,9 +231,6 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
 
-    const uint32_t* lohi = b.lohi + static_cast<size_t>(s) * b.P;
-    const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
-    const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1);
     const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.vol_slots + a) * b.quad_cap * 4);
@@ -259,16 +256,18 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         return x >= 0 && x < W;
     };
     const uint4* tmeta = b.tmeta + static_cast<size_t>(s) * b.P;
+    const uint4* rmeta = b.rmeta + static_cast<size_t>(s) * b.P;
     auto load_meta = [&](int p, PixMeta& m) {
         if (horiz) {  // lanes = consecutive rows: one coalesced 16-byte record each
             const uint4 v = __ldg(tmeta + p);
             m.lohi = v.x;
             m.cell = v.y;
             m.qo = v.z;
-        } else {
-            m.lohi = __ldg(lohi + p);
-            m.cell = __ldg(off + p);
-            m.qo = __ldg(qoff + p);
+        } else {  // lanes = adjacent pixels of a row
+            const uint4 v = __ldg(rmeta + p);
+            m.lohi = v.x;
+            m.cell = v.y;
+            m.qo = v.z;
         }
     };
 

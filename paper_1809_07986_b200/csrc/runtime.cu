@@ -333,6 +333,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.row_sum = ctx->dalloc<uint32_t>(S * ctx->H);
     b.qoff = ctx->dalloc<uint32_t>(S * (P + 1));
     b.tmeta = ctx->dalloc<uint4>(S * P);
+    b.rmeta = ctx->dalloc<uint4>(S * P);
     b.qrow_sum = ctx->dalloc<uint32_t>(S * ctx->H);
     b.nquads = ctx->dalloc<unsigned long long>(S);
     b.ncells = ctx->dalloc<unsigned long long>(S);

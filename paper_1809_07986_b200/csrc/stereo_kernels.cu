@@ -211,9 +211,10 @@ __global__ void row_scan_kernel(Bufs b) {
     }
 }
 
-// Adds the row bases to the in-row offsets, and writes the column-major
-// packed copy {lohi, off, qoff} that horizontal scanlines read coalesced
-// (lanes = consecutive rows). 32x32 tiles through shared memory.
+// Adds the row bases to the in-row offsets, and writes the packed records
+// {lohi, off, qoff} the scan kernel loads with one 16-byte access: row-major
+// (lanes = adjacent pixels of a row) and column-major (horizontal scanlines,
+// lanes = consecutive rows). 32x32 tiles through shared memory.
 __global__ void offsets_finalize_kernel(Bufs b) {
     __shared__ uint4 tile[32][33];
     const int a = blockIdx.z, s = slot_of(b, a);
@@ -229,7 +230,9 @@ __global__ void offsets_finalize_kernel(Bufs b) {
             const uint32_t off = b.off[o] + rb, qo = b.qoff[o] + qb;
             b.off[o] = off;
             b.qoff[o] = qo;
-            tile[j][tx] = make_uint4(b.lohi[pbase + static_cast<size_t>(y) * b.W + x], off, qo, 0u);
+            const uint4 rec = make_uint4(b.lohi[pbase + static_cast<size_t>(y) * b.W + x], off, qo, 0u);
+            b.rmeta[pbase + static_cast<size_t>(y) * b.W + x] = rec;
+            tile[j][tx] = rec;
         }
     }
     __syncthreads();
