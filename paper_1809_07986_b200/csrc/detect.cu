@@ -161,6 +161,29 @@ double iou_of(const tsgm_box& a, const tsgm_box& b) {
     return inter / uni;
 }
 
+// IoU as the exact fraction inter / union (both integers, union < 2^53): the
+// reference's double division rounds it correctly, and distinct fractions with
+// denominators below 2^26 differ by more than an ulp, so comparing fractions
+// by cross-multiplication orders (and ties) pairs exactly like comparing the
+// reference's doubles. Only a row's winner is divided.
+struct Frac {
+    long long num = 0, den = 1;
+};
+Frac iou_frac(const tsgm_box& a, const tsgm_box& b) {
+    const int ix0 = std::max(a.x0, b.x0), iy0 = std::max(a.y0, b.y0);
+    const int ix1 = std::min(a.x1, b.x1), iy1 = std::min(a.y1, b.y1);
+    if (ix0 >= ix1 || iy0 >= iy1) return Frac{};
+    const long long inter = static_cast<long long>(ix1 - ix0) * (iy1 - iy0);
+    return Frac{inter, area_of(a) + area_of(b) - inter};
+}
+int frac_cmp(const Frac& a, const Frac& b) {
+    const __int128 l = static_cast<__int128>(a.num) * b.den, r = static_cast<__int128>(b.num) * a.den;
+    return l < r ? -1 : (l > r ? 1 : 0);
+}
+double frac_value(const Frac& f) {  // = iou_of(): inter / (area_a + area_b - inter) in double
+    return f.num ? static_cast<double>(f.num) / static_cast<double>(f.den) : 0.0;
+}
+
 }  // namespace
 
 void detect_windows(const tsgm_detect_config& c, int W, int H, DetectWindows& dw) {
@@ -200,41 +223,163 @@ void launch_candidates(const double* sat, size_t sat_stride, int W, const Detect
 // reference rescans all pairs per merge and takes the first pair (in list
 // order) of maximal IoU > 0. Here every live row i keeps its best (value,
 // first j) over live j > i; the global choice is the first row of maximal
-// value, i.e. the same pair. A merge changes box bi and removes bj, so only
-// row bi, rows whose best was bi or bj, and the entries (k, bi) of earlier
-// rows can change; list order of the survivors is untouched by erase().
-long long greedy_merge_host(tsgm_box* boxes, long long n, const tsgm_detect_config& c) {
-    std::vector<char> alive(static_cast<size_t>(n), 1);
-    std::vector<double> bv(static_cast<size_t>(n), 0.0);
-    std::vector<long long> bj(static_cast<size_t>(n), -1);
-    auto recompute = [&](long long i) {
-        double best = 0.0;
-        long long j_best = -1;
-        for (long long j = i + 1; j < n; ++j)
-            if (alive[j]) {
-                const double v = iou_of(boxes[i], boxes[j]);
-                if (v > best) {
-                    best = v;
-                    j_best = j;
+// value (a segment tree over rows), i.e. the same pair. Only overlapping boxes
+// can have IoU > 0, so each row scans a neighbour list (built with a uniform
+// grid and extended when a merged box grows). A merge changes box bi and
+// removes bj: rows whose partner was bi or bj are rescanned, earlier rows
+// overlapping the new bi compare against it, and row bi is rescanned; list
+// order of the survivors is untouched by erase().
+namespace {
+
+bool overlaps(const tsgm_box& a, const tsgm_box& b) {
+    return std::max(a.x0, b.x0) < std::min(a.x1, b.x1) && std::max(a.y0, b.y0) < std::min(a.y1, b.y1);
+}
+
+struct BestTree {  // max value, then smallest row index
+    int n = 1;
+    std::vector<double> v;
+    std::vector<int> id;
+    explicit BestTree(int rows) {
+        while (n < rows) n <<= 1;
+        v.assign(2 * n, -1.0);
+        id.assign(2 * n, -1);
+    }
+    void set(int i, double val) {
+        int k = i + n;
+        v[k] = val;
+        id[k] = val > 0.0 ? i : -1;
+        for (k >>= 1; k >= 1; k >>= 1) {
+            const int l = 2 * k, r = 2 * k + 1;
+            const bool left = v[l] >= v[r];  // ties: the left (smaller index) wins
+            v[k] = left ? v[l] : v[r];
+            id[k] = left ? id[l] : id[r];
+        }
+    }
+};
+
+}  // namespace
+
+long long greedy_merge_host(tsgm_box* boxes, long long n_ll, const tsgm_detect_config& c) {
+    const int n = static_cast<int>(n_ll);
+    if (n <= 1) {
+        long long m = 0;
+        for (int i = 0; i < n; ++i)
+            if (area_of(boxes[i]) >= c.min_box_area) boxes[m++] = boxes[i];
+        return m;
+    }
+    // uniform grid over the boxes' extent for the neighbour lists
+    int gx0 = boxes[0].x0, gy0 = boxes[0].y0, gx1 = boxes[0].x1, gy1 = boxes[0].y1;
+    for (int i = 1; i < n; ++i) {
+        gx0 = std::min(gx0, boxes[i].x0);
+        gy0 = std::min(gy0, boxes[i].y0);
+        gx1 = std::max(gx1, boxes[i].x1);
+        gy1 = std::max(gy1, boxes[i].y1);
+    }
+    const int cell = 32;
+    const int gw = (gx1 - gx0) / cell + 1, gh = (gy1 - gy0) / cell + 1;
+    std::vector<std::vector<int>> grid(static_cast<size_t>(gw) * gh);
+    auto cells = [&](const tsgm_box& b, auto&& fn) {
+        const int cx0 = (b.x0 - gx0) / cell, cx1 = (std::max(b.x1 - 1, b.x0) - gx0) / cell;
+        const int cy0 = (b.y0 - gy0) / cell, cy1 = (std::max(b.y1 - 1, b.y0) - gy0) / cell;
+        for (int cy = std::max(0, cy0); cy <= std::min(gh - 1, cy1); ++cy)
+            for (int cx = std::max(0, cx0); cx <= std::min(gw - 1, cx1); ++cx) fn(cy * gw + cx);
+    };
+    for (int i = 0; i < n; ++i) cells(boxes[i], [&](int g) { grid[g].push_back(i); });
+    std::vector<char> alive(n, 1);
+    std::vector<int> stamp(n, -1);
+    int now = 0;
+    auto cell_inside = [&](int g, const tsgm_box& b) {  // cell g entirely within box b
+        const int cx = g % gw, cy = g / gw;
+        const int x0 = gx0 + cx * cell, y0 = gy0 + cy * cell;
+        return b.x0 <= x0 && x0 + cell <= b.x1 && b.y0 <= y0 && y0 + cell <= b.y1;
+    };
+    // adjacency: every overlapping pair once (lists hold live overlapping boxes)
+    std::vector<std::vector<int>> adj(n);
+    for (int i = 0; i < n; ++i) {
+        ++now;
+        cells(boxes[i], [&](int g) {
+            for (int j : grid[g])
+                if (j > i && stamp[j] != now) {
+                    stamp[j] = now;
+                    if (overlaps(boxes[i], boxes[j])) {
+                        adj[i].push_back(j);
+                        adj[j].push_back(i);
+                    }
+                }
+        });
+    }
+    // live boxes overlapping the merged box `self` (grown from old_a and
+    // old_b): the parts' neighbours, plus a grid scan of the cells not inside
+    // either part (a box meeting a cell inside a part overlaps that part, so
+    // it is already in the part's list)
+    auto merged_neighbours = [&](int self, int other, const tsgm_box& old_a, const tsgm_box& old_b,
+                                 std::vector<int>& out) {
+        out.clear();
+        ++now;
+        stamp[self] = now;
+        stamp[other] = now;
+        for (const std::vector<int>* l : {&adj[self], &adj[other]})
+            for (int j : *l)
+                if (alive[j] && stamp[j] != now) {
+                    stamp[j] = now;
+                    if (overlaps(boxes[self], boxes[j])) out.push_back(j);
+                }
+        cells(boxes[self], [&](int g) {
+            if (cell_inside(g, old_a) || cell_inside(g, old_b)) return;
+            std::vector<int>& cl = grid[g];
+            size_t w = 0;
+            for (size_t t = 0; t < cl.size(); ++t) {
+                const int j = cl[t];
+                if (!alive[j]) continue;  // drop merged-away boxes from the cell
+                cl[w++] = j;
+                if (stamp[j] != now) {
+                    stamp[j] = now;
+                    if (overlaps(boxes[self], boxes[j])) out.push_back(j);
                 }
             }
-        bv[i] = best;
-        bj[i] = j_best;
+            cl.resize(w);
+        });
     };
-    for (long long i = 0; i < n; ++i) recompute(i);
-    long long live = n;
-    while (live > 1) {
-        double best = 0.0;
-        long long bi = -1;
-        for (long long i = 0; i < n; ++i)
-            if (alive[i] && bv[i] > best) {
-                best = bv[i];
-                bi = i;
+    std::vector<double> bv(n, 0.0);
+    std::vector<Frac> bf(n);
+    std::vector<int> bj(n, -1);
+    BestTree tree(n);
+    auto rescan = [&](int i) {
+        Frac best;
+        int jb = -1;
+        std::vector<int>& a = adj[i];
+        size_t w = 0;
+        ++now;
+        for (size_t t = 0; t < a.size(); ++t) {
+            const int j = a[t];
+            if (!alive[j] || stamp[j] == now) continue;  // prune dead and duplicate entries
+            stamp[j] = now;
+            a[w++] = j;
+            if (j <= i) continue;
+            const Frac v = iou_frac(boxes[i], boxes[j]);
+            if (v.num == 0) continue;
+            const int cmp = jb < 0 ? 1 : frac_cmp(v, best);
+            if (cmp > 0 || (cmp == 0 && j < jb)) {
+                best = v;
+                jb = j;
             }
-        if (bi < 0 || best < c.merge_stop_iou) break;  // best = 0 with no pair also stops
-        const long long j = bj[bi];
+        }
+        a.resize(w);
+        bf[i] = best;
+        bv[i] = jb >= 0 ? frac_value(best) : 0.0;
+        bj[i] = jb;
+        tree.set(i, bv[i]);
+    };
+    for (int i = 0; i < n; ++i) rescan(i);
+    std::vector<int> touched, fresh;
+    int live = n;
+    while (live > 1) {
+        const int bi = tree.id[1];
+        if (bi < 0 || tree.v[1] < c.merge_stop_iou) break;  // no pair with IoU > 0 also stops
+        const int j = bj[bi];
         tsgm_box& a = boxes[bi];
-        const tsgm_box& b = boxes[j];
+        const tsgm_box b = boxes[j];
+        const tsgm_box old_a = a;
         const double aa = static_cast<double>(area_of(a)), ab = static_cast<double>(area_of(b));
         a.score = (a.score * aa + b.score * ab) / (aa + ab);
         a.x0 = std::min(a.x0, b.x0);
@@ -243,22 +388,50 @@ long long greedy_merge_host(tsgm_box* boxes, long long n, const tsgm_detect_conf
         a.y1 = std::max(a.y1, b.y1);
         alive[j] = 0;
         --live;
-        for (long long k = 0; k < n; ++k) {
-            if (!alive[k] || k == bi) continue;
+        tree.set(j, 0.0);
+        // rows that may change: neighbours of the old bi / bj and of the new bi
+        touched.clear();
+        for (int k : adj[bi]) touched.push_back(k);
+        for (int k : adj[j]) touched.push_back(k);
+        {  // a box only grows: register bi in the cells outside its old extent
+            const int ox0 = (old_a.x0 - gx0) / cell, ox1 = (std::max(old_a.x1 - 1, old_a.x0) - gx0) / cell;
+            const int oy0 = (old_a.y0 - gy0) / cell, oy1 = (std::max(old_a.y1 - 1, old_a.y0) - gy0) / cell;
+            cells(a, [&](int g) {
+                const int cx = g % gw, cy = g / gw;
+                if (cx < ox0 || cx > ox1 || cy < oy0 || cy > oy1) grid[g].push_back(bi);
+            });
+        }
+        merged_neighbours(bi, j, old_a, b, fresh);
+        for (int k : fresh) {
+            touched.push_back(k);
+            adj[k].push_back(bi);
+        }
+        adj[bi] = fresh;
+        ++now;
+        const int mark = now;
+        for (int k : touched) {
+            if (!alive[k] || k == bi || stamp[k] == mark) continue;
+            stamp[k] = mark;
             if (bj[k] == j || bj[k] == bi) {
-                recompute(k);
-            } else if (k < bi) {
-                const double v = iou_of(boxes[k], a);
-                if (v > bv[k] || (v == bv[k] && v > 0.0 && bi < bj[k])) {
-                    bv[k] = v;
+                rescan(k);
+                ++now;  // rescan used its own stamp; keep this pass's marks distinct
+                // (re-mark k so a later duplicate entry is skipped)
+                stamp[k] = mark;
+            } else if (k < bi && overlaps(boxes[k], a)) {
+                const Frac v = iou_frac(boxes[k], a);
+                const int cmp = bj[k] < 0 ? 1 : frac_cmp(v, bf[k]);
+                if (cmp > 0 || (cmp == 0 && bi < bj[k])) {
+                    bf[k] = v;
+                    bv[k] = frac_value(v);
                     bj[k] = bi;
+                    tree.set(k, bv[k]);
                 }
             }
         }
-        recompute(bi);
+        rescan(bi);
     }
     long long m = 0;
-    for (long long i = 0; i < n; ++i)
+    for (int i = 0; i < n; ++i)
         if (alive[i] && area_of(boxes[i]) >= c.min_box_area) boxes[m++] = boxes[i];
     return m;
 }
