@@ -267,6 +267,20 @@ def run_ours(args):
     e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
     e2e_s = max_over_ranks(e2e_s)
 
+    # accuracy (outside every timed region): KITTI-style outliers of the last
+    # frame's export maps against the synthetic ground truth (eval.cpp:59-85,
+    # 3 px and 5%), pooled over sequences, and the export density
+    gts = []
+    for s in my:
+        _, _, _, g = render(scene_cfg(s, args.frames), args.frames - 1, args.frames,
+                            threads=nthreads, gt=True)
+        gts.append(g[0].astype(np.float64))
+    ev, out = eng.count_outliers(slots, gts, "export_d")
+    n_valid = float(sum(int(eng.fetch(s, "export_valid").sum()) for s in slots))
+    acc_ev = sum_over_ranks(float(ev.sum()))
+    acc_out = sum_over_ranks(float(out.sum()))
+    acc_valid = sum_over_ranks(n_valid)
+
     result = None
     if rank == 0:
         value = frames_total / (ms_per_step * 1e-3)
@@ -307,6 +321,11 @@ def run_ours(args):
                          "cells": int(agg_cells)},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
+            "accuracy": {"frame": "last (29)", "outlier_rule": "|e| > 3 px and |e|/gt > 5%",
+                         "pooled_outlier_pct": round(100.0 * acc_out / max(acc_ev, 1.0), 3),
+                         "evaluated_px": int(acc_ev),
+                         "density_pct": round(100.0 * acc_valid / (args.seqs * W_ * H_), 2),
+                         "counted_on": "GPU (tsgm_count_outliers_batch)"},
         }
         if cpu is not None:
             result["cpu_baseline"] = cpu

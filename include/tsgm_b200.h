@@ -268,6 +268,28 @@ int tsgm_detect_moving_objects(const double* diff, int32_t w, int32_t h,
 int tsgm_detect(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const tsgm_detect_config* cfg,
                 tsgm_box* out, int64_t cap_each, int64_t* n_each);
 
+/* ------------------------------------------------------------------------
+ * KITTI-style outlier count of a disparity map against ground truth
+ * (include/tsgm/eval.hpp:13-42, src/eval.cpp:59-93).
+ * ------------------------------------------------------------------------ */
+/* OutlierOptions (eval.hpp:13-19); defaults 3.0, 0.05, 0. */
+typedef struct {
+    double abs_thresh_px;
+    double rel_thresh;
+    int32_t strict_density;
+} tsgm_outlier_options;
+
+/* count_outliers (eval.cpp:59-85) on the GPU: GT valid iff gt > 0; outlier iff
+ * |d - gt| > abs AND |d - gt| / gt > rel. */
+int tsgm_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt, int32_t w,
+                        int32_t h, const tsgm_outlier_options* opts, int64_t* evaluated,
+                        int64_t* outliers);
+/* Batched on the context's last step: output `what` (TSGM_OUT_EXPORT_D or
+ * TSGM_OUT_MEAS_D, with its validity) of n slots against host GT maps gt[i]. */
+int tsgm_count_outliers_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t what,
+                              const double* const* gt, const tsgm_outlier_options* opts,
+                              int64_t* evaluated, int64_t* outliers);
+
 #ifdef __cplusplus
 }
 #endif

@@ -348,6 +348,16 @@ class Reference(_Lib):
         return self.greedy_merge(self.candidates(diff, cfg, threads), cfg)
 
 
+    def count_outliers(self, d, valid, gt, abs_thresh=3.0, rel_thresh=0.05, strict=False):
+        d, valid, gt = np.ascontiguousarray(d, np.int32), _u8(valid), _f64(gt)
+        h, w = gt.shape
+        ev, out = C.c_longlong(), C.c_longlong()
+        self._c(self.lib.ref_count_outliers(_p(d), _p(valid), _p(gt), w, h, C.c_double(abs_thresh),
+                                            C.c_double(rel_thresh), int(strict), C.byref(ev),
+                                            C.byref(out)))
+        return ev.value, out.value
+
+
 class _OrCalib(C.Structure):
     _fields_ = [("focal_px", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
                 ("baseline_m", C.c_double), ("width", C.c_int), ("height", C.c_int),
@@ -677,6 +687,18 @@ def _port_detect_methods(cls):
 
 
 _port_detect_methods(Port)
+
+
+def _port_count_outliers(self, d, valid, gt, abs_thresh=3.0, rel_thresh=0.05, strict=False):
+    d, valid, gt = np.ascontiguousarray(d, np.int32), _u8(valid), _f64(gt)
+    h, w = gt.shape
+    ev, out = C.c_longlong(), C.c_longlong()
+    self.lib.or_count_outliers(_p(d), _p(valid), _p(gt), w, h, C.c_double(abs_thresh),
+                               C.c_double(rel_thresh), int(strict), C.byref(ev), C.byref(out))
+    return ev.value, out.value
+
+
+Port.count_outliers = _port_count_outliers
 
 
 _port = None

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "tsgm/eval.hpp"
 #include "tsgm/geometry.hpp"
 #include "tsgm/matching_cost.hpp"
 #include "tsgm/motion_detect.hpp"
@@ -395,6 +396,23 @@ int ref_detect(const double* diff, int w, int h, const int* wh, int n_windows, d
                                                              min_area),
                                                  threads),
                            out, cap);
+    });
+}
+
+int ref_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt, int w, int h,
+                       double abs_thresh, double rel_thresh, int strict, long long* evaluated,
+                       long long* outliers) {
+    return guarded([&] {
+        DisparityMap est;
+        est.d = to_image(d, w, h);
+        est.valid = to_image(valid, w, h);
+        OutlierOptions o;
+        o.abs_thresh_px = abs_thresh;
+        o.rel_thresh = rel_thresh;
+        o.strict_density = strict != 0;
+        const OutlierStats s = count_outliers(est, to_image(gt, w, h), o);
+        *evaluated = s.evaluated;
+        *outliers = s.outliers;
     });
 }
 

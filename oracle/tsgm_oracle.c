@@ -818,3 +818,27 @@ long long or_greedy_merge(or_box* boxes, long long n, const or_detect_cfg* c) {
         if (box_area(&boxes[i]) >= c->min_box_area) boxes[m++] = boxes[i];
     return m;
 }
+
+
+/* ======================================================= outlier metric (§8(f) row 3) */
+void or_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt, int w, int h,
+                       double abs_thresh, double rel_thresh, int strict_density,
+                       long long* evaluated, long long* outliers) {
+    /* count_outliers, eval.cpp:59-85: GT valid iff gt > 0; an estimate is an
+     * outlier iff |e| > abs AND |e| / gt > rel; strict density counts missing
+     * estimates as evaluated outliers */
+    long long ev = 0, out = 0;
+    for (size_t i = 0; i < (size_t)w * h; ++i) {
+        const double g = gt[i];
+        if (!(g > 0.0)) continue;
+        if (!valid[i]) {
+            if (strict_density) { ++ev; ++out; }
+            continue;
+        }
+        ++ev;
+        const double e = fabs((double)d[i] - g);
+        if (e > abs_thresh && e / g > rel_thresh) ++out;
+    }
+    *evaluated = ev;
+    *outliers = out;
+}

@@ -6,7 +6,8 @@ The product is the CUDA library ``lib/libtsgm_b200.so`` behind the C-ABI in
 ``tsgm::`` API (see :mod:`.tsgm`)."""
 from .tsgm import (  # noqa: F401
     DIAGONAL, NONDIAGONAL, DetectConfig, Engine, EngineConfig, FilterConfig, SgmParams,
-    StereoCalib, detect_candidate_windows, detect_moving_objects, greedy_merge, integral_image,
+    OutlierOptions, StereoCalib, count_outliers, detect_candidate_windows, detect_moving_objects,
+    greedy_merge, integral_image, outlier_rate,
     aggregate_paths, build_cost_volume, census_transform, correct, derive_search_ranges,
     disparity_homography, fill_zoom_holes, median_refine, predict, reject_discontinuities,
     relative_motion, sgm_match, step, warp_state_ex, winner_takes_all,

@@ -57,8 +57,15 @@ EXPORTS = [
     "tsgm_reject_discontinuities", "tsgm_fill_zoom_holes", "tsgm_derive_search_ranges",
     "tsgm_correct", "tsgm_step_once",
     "tsgm_integral_image", "tsgm_detect_candidate_windows", "tsgm_greedy_merge",
-    "tsgm_detect_moving_objects", "tsgm_detect",
+    "tsgm_detect_moving_objects", "tsgm_detect", "tsgm_count_outliers",
+    "tsgm_count_outliers_batch",
 ]
+
+
+class OutlierOptionsC(C.Structure):
+    """tsgm_outlier_options (OutlierOptions, eval.hpp:13-19)."""
+    _fields_ = [("abs_thresh_px", C.c_double), ("rel_thresh", C.c_double),
+                ("strict_density", C.c_int32)]
 
 
 class BoxC(C.Structure):
@@ -112,6 +119,12 @@ def load():
         lib.tsgm_greedy_merge.argtypes = [C.c_void_p, C.c_int64, dc, C.POINTER(C.c_int64)]
         lib.tsgm_detect.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, dc, C.c_void_p, C.c_int64,
                                     C.c_void_p]
+        oc = C.POINTER(OutlierOptionsC)
+        lib.tsgm_count_outliers.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                            C.c_int32, oc, C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_int64)]
+        lib.tsgm_count_outliers_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                                  C.c_void_p, oc, C.c_void_p, C.c_void_p]
         _lib = lib
     return _lib
 

@@ -170,4 +170,11 @@ void launch_candidates(const double* sat, size_t sat_stride, int W, const Detect
                        tsgm_box* out, long long cap, long long* counts, Launch L);
 long long greedy_merge_host(tsgm_box* boxes, long long n, const tsgm_detect_config& c);
 
+// Outlier count (detect.cu): n maps, d/valid/gt at
+// base + (slots ? slots[a] : a) * P for d/valid and gt + a * P; counts[2a],
+// counts[2a+1] = evaluated, outliers (zeroed by the launcher).
+void launch_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt, size_t P,
+                           int n, const int* slots, double abs_thresh, double rel_thresh,
+                           int strict, unsigned long long* counts, Launch L);
+
 }  // namespace tsgm

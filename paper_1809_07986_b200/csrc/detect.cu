@@ -151,15 +151,6 @@ namespace {
 
 long long area_of(const tsgm_box& b) { return static_cast<long long>(b.x1 - b.x0) * (b.y1 - b.y0); }
 
-// iou, motion_detect.cpp:52-62
-double iou_of(const tsgm_box& a, const tsgm_box& b) {
-    const int ix0 = std::max(a.x0, b.x0), iy0 = std::max(a.y0, b.y0);
-    const int ix1 = std::min(a.x1, b.x1), iy1 = std::min(a.y1, b.y1);
-    if (ix0 >= ix1 || iy0 >= iy1) return 0.0;
-    const double inter = static_cast<double>(ix1 - ix0) * (iy1 - iy0);
-    const double uni = static_cast<double>(area_of(a)) + static_cast<double>(area_of(b)) - inter;
-    return inter / uni;
-}
 
 // IoU as the exact fraction inter / union (both integers, union < 2^53): the
 // reference's double division rounds it correctly, and distinct fractions with
@@ -180,7 +171,7 @@ int frac_cmp(const Frac& a, const Frac& b) {
     const __int128 l = static_cast<__int128>(a.num) * b.den, r = static_cast<__int128>(b.num) * a.den;
     return l < r ? -1 : (l > r ? 1 : 0);
 }
-double frac_value(const Frac& f) {  // = iou_of(): inter / (area_a + area_b - inter) in double
+double frac_value(const Frac& f) {  // = iou(), motion_detect.cpp:52-62, in double
     return f.num ? static_cast<double>(f.num) / static_cast<double>(f.den) : 0.0;
 }
 
@@ -434,6 +425,51 @@ long long greedy_merge_host(tsgm_box* boxes, long long n_ll, const tsgm_detect_c
     for (int i = 0; i < n; ++i)
         if (alive[i] && area_of(boxes[i]) >= c.min_box_area) boxes[m++] = boxes[i];
     return m;
+}
+
+// ---------------------------------------------------------------- outliers
+// count_outliers (eval.cpp:59-85): the same per-pixel FP64 test, integer
+// counts reduced per block and added atomically (exact, order-free).
+__global__ void count_outliers_kernel(const int32_t* __restrict__ d, const uint8_t* __restrict__ valid,
+                                      const double* __restrict__ gt, size_t P, const int* slots,
+                                      double abs_thresh, double rel_thresh, int strict,
+                                      unsigned long long* counts) {
+    const int a = blockIdx.y, s = slots ? slots[a] : a;
+    const size_t base = static_cast<size_t>(s) * P, gbase = static_cast<size_t>(a) * P;
+    unsigned long long ev = 0, out = 0;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double g = gt[gbase + i];
+        if (!(g > 0.0)) continue;
+        if (!valid[base + i]) {
+            if (strict) {
+                ++ev;
+                ++out;
+            }
+            continue;
+        }
+        ++ev;
+        const double e = fabs(__dsub_rn(static_cast<double>(d[base + i]), g));
+        if (e > abs_thresh && e / g > rel_thresh) ++out;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ev += __shfl_down_sync(0xffffffffu, ev, o);
+        out += __shfl_down_sync(0xffffffffu, out, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (ev || out)) {
+        atomicAdd(counts + 2 * a, ev);
+        atomicAdd(counts + 2 * a + 1, out);
+    }
+}
+
+void launch_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt, size_t P,
+                           int n, const int* slots, double abs_thresh, double rel_thresh,
+                           int strict, unsigned long long* counts, Launch L) {
+    cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * 2 * n, L.st);
+    const unsigned blocks = static_cast<unsigned>(std::min<size_t>((P + 255) / 256, 148 * 4));
+    count_outliers_kernel<<<dim3(blocks, n), 256, 0, L.st>>>(d, valid, gt, P, slots, abs_thresh,
+                                                             rel_thresh, strict, counts);
+    ++*L.counter;
 }
 
 }  // namespace tsgm

@@ -230,6 +230,9 @@ struct tsgm_ctx {
     tsgm_box* det_boxes = nullptr;
     long long* det_counts = nullptr;
     long long det_cap = 0;  // candidate capacity per slot
+    // outlier metric (tsgm_count_outliers_batch): uploaded GT maps and counts
+    double* eval_gt = nullptr;
+    unsigned long long* eval_counts = nullptr;
 
     template <typename T>
     T* dalloc(size_t count) {
@@ -1328,6 +1331,87 @@ int tsgm_detect(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const tsgm_detec
             n_each[i] = kept[i];
             std::memcpy(out + static_cast<size_t>(i) * cap_each, boxes[i].data(),
                         sizeof(tsgm_box) * static_cast<size_t>(std::min<long long>(kept[i], cap_each)));
+        }
+    });
+}
+
+// ---------------------------------------------------------------- outliers
+}  // extern "C"
+
+namespace {
+void outlier_validate(const tsgm_outlier_options* o) {
+    if (!o) bad("count_outliers: null options");
+}
+}  // namespace
+
+extern "C" {
+
+int tsgm_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt, int32_t w,
+                        int32_t h, const tsgm_outlier_options* opts, int64_t* evaluated,
+                        int64_t* outliers) {
+    return guarded([&] {
+        outlier_validate(opts);
+        if (!evaluated || !outliers || w < 0 || h < 0) bad("count_outliers: bad arguments");
+        const size_t P = static_cast<size_t>(w) * h;
+        if (P == 0) {
+            *evaluated = *outliers = 0;
+            return;
+        }
+        if (!d || !valid || !gt) bad("count_outliers: null argument");
+        DevScratch s;
+        int32_t* dd = s.alloc<int32_t>(P);
+        uint8_t* dv = s.alloc<uint8_t>(P);
+        double* dg = s.alloc<double>(P);
+        unsigned long long* cnt = s.alloc<unsigned long long>(2);
+        CK(cudaMemcpyAsync(dd, d, 4 * P, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(dv, valid, P, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(dg, gt, 8 * P, cudaMemcpyHostToDevice, s.st));
+        launch_count_outliers(dd, dv, dg, P, 1, nullptr, opts->abs_thresh_px, opts->rel_thresh,
+                              opts->strict_density, cnt, s.L());
+        CK(cudaGetLastError());
+        unsigned long long h2[2];
+        CK(cudaMemcpyAsync(h2, cnt, sizeof h2, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        *evaluated = static_cast<int64_t>(h2[0]);
+        *outliers = static_cast<int64_t>(h2[1]);
+    });
+}
+
+int tsgm_count_outliers_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t what,
+                              const double* const* gt, const tsgm_outlier_options* opts,
+                              int64_t* evaluated, int64_t* outliers) {
+    return guarded([&] {
+        outlier_validate(opts);
+        if (!ctx || !slots || !gt || !evaluated || !outliers) bad("count_outliers_batch: null argument");
+        if (what != TSGM_OUT_EXPORT_D && what != TSGM_OUT_MEAS_D)
+            bad("count_outliers_batch: what must be TSGM_OUT_EXPORT_D or TSGM_OUT_MEAS_D");
+        check_slots(ctx, n, slots);
+        CK(cudaSetDevice(ctx->device));
+        const size_t P = ctx->P;
+        if (!ctx->eval_gt) {
+            ctx->eval_gt = ctx->dalloc<double>(P * ctx->max_slots);
+            ctx->eval_counts = ctx->dalloc<unsigned long long>(2 * static_cast<size_t>(ctx->max_slots));
+        }
+        for (int i = 0; i < n; ++i) {
+            if (!gt[i]) bad("count_outliers_batch: null GT map");
+            CK(cudaMemcpyAsync(ctx->eval_gt + i * P, gt[i], 8 * P, cudaMemcpyHostToDevice, ctx->st));
+        }
+        std::vector<const uint8_t*> dl(n, ctx->d_img), dr(n, ctx->d_img);
+        std::vector<double> Hm(16 * static_cast<size_t>(n), 0.0);
+        upload_step(ctx, n, slots, dl.data(), dr.data(), Hm.data());
+        const Bufs& b = ctx->b;
+        launch_count_outliers(what == TSGM_OUT_EXPORT_D ? b.ed : b.md,
+                              what == TSGM_OUT_EXPORT_D ? b.ev : b.mv, ctx->eval_gt, P, n,
+                              ctx->d_slots, opts->abs_thresh_px, opts->rel_thresh,
+                              opts->strict_density, ctx->eval_counts, ctx->L());
+        CK(cudaGetLastError());
+        std::vector<unsigned long long> c(2 * static_cast<size_t>(n));
+        CK(cudaMemcpyAsync(c.data(), ctx->eval_counts, sizeof(unsigned long long) * 2 * n,
+                           cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        for (int i = 0; i < n; ++i) {
+            evaluated[i] = static_cast<int64_t>(c[2 * i]);
+            outliers[i] = static_cast<int64_t>(c[2 * i + 1]);
         }
     });
 }

@@ -98,3 +98,7 @@ class GpuBackend:
 
     def detect(self, diff, cfg, threads=1):
         return tsgm.detect_moving_objects(diff, cfg)
+
+    # ---- outlier metric (eval.cpp) ----
+    def count_outliers(self, d, valid, gt, abs_thresh=3.0, rel_thresh=0.05, strict=False):
+        return tsgm.count_outliers(d, valid, gt, tsgm.OutlierOptions(abs_thresh, rel_thresh, strict))

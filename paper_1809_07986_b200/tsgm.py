@@ -364,6 +364,40 @@ def detect_moving_objects(diff, cfg=None):
     return _detect_call(_lib.load().tsgm_detect_moving_objects, diff, cfg or DetectConfig())
 
 
+# --------------------------------------------------------------------- outliers
+@dataclass
+class OutlierOptions:  # eval.hpp:13-19
+    abs_thresh_px: float = 3.0
+    rel_thresh: float = 0.05
+    strict_density: bool = False
+
+    def _c(self):
+        return _lib.OutlierOptionsC(self.abs_thresh_px, self.rel_thresh,
+                                    1 if self.strict_density else 0)
+
+
+def count_outliers(d, valid, gt, opts=None):
+    """count_outliers (eval.cpp:59-85) on the GPU -> (evaluated, outliers)."""
+    d, valid, gt = _i32(d), _u8(valid), _f64(gt)
+    if d.shape != gt.shape or valid.shape != gt.shape:
+        raise ValueError("count_outliers: est/gt dimension mismatch")
+    w, h = _hw(gt)
+    o = _as(opts or OutlierOptions(), OutlierOptions)._c()
+    ev, out = C.c_int64(), C.c_int64()
+    check(_lib.load().tsgm_count_outliers(ptr(d), ptr(valid), ptr(gt), w, h, C.byref(o),
+                                         C.byref(ev), C.byref(out)))
+    return int(ev.value), int(out.value)
+
+
+def outlier_rate(d, valid, gt, opts=None):
+    """outlier_rate (eval.cpp:87-93): percentage; no evaluated pixel is a
+    runtime error."""
+    ev, out = count_outliers(d, valid, gt, opts)
+    if ev == 0:
+        raise RuntimeError("outlier_rate: no mutually valid pixels")
+    return 100.0 * out / ev
+
+
 # --------------------------------------------------------------------- engine
 _OUT_DTYPES = dict(state_d=np.float64, state_p=np.float64, state_valid=np.uint8,
                    export_d=np.int32, export_valid=np.uint8, diff=np.float64, mask=np.uint8,
@@ -499,6 +533,19 @@ class Engine:
                 return [_boxes_out(out[i * cap_each:(i + 1) * cap_each], int(n_each[i]))
                         for i in range(len(sl))]
             cap_each = int(n_each.max())
+
+    def count_outliers(self, slots, gts, what="export_d", opts=None):
+        """count_outliers of each slot's last export map (or WTA map) against
+        host GT maps -> (evaluated[n], outliers[n])."""
+        sl = np.asarray(slots, np.int32)
+        gs = [_f64(g) for g in gts]
+        gp = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+        o = _as(opts or OutlierOptions(), OutlierOptions)._c()
+        ev = np.zeros(len(sl), np.int64)
+        out = np.zeros(len(sl), np.int64)
+        check(self._lib.tsgm_count_outliers_batch(self._h, len(sl), ptr(sl), OUT[what], gp,
+                                                  C.byref(o), ptr(ev), ptr(out)))
+        return ev, out
 
     @property
     def vol_slots(self) -> int:

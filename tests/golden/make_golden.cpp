@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "oracles.hpp"
+#include "tsgm/eval.hpp"
 #include "tsgm/geometry.hpp"
 #include "tsgm/matching_cost.hpp"
 #include "tsgm/motion_detect.hpp"
@@ -497,6 +498,34 @@ int main(int argc, char** argv) {
         put_img("det_e2e/kitti", big);
         put_boxes("det_e2e/kitti_cands", detect_candidate_windows(big, DetectConfig{}));
         put_boxes("det_e2e/kitti_boxes", detect_moving_objects(big, DetectConfig{}));
+    }
+    {   // eval.cpp:59-85 / test_eval.cpp — outlier counts on random maps
+        std::mt19937 rng(66);
+        for (int t = 0; t < 4; ++t) {
+            const int w = 40 + 30 * t, h = 20 + 10 * t;
+            DisparityMap est(w, h);
+            Image<double> gt(w, h, 0.0);
+            std::uniform_int_distribution<int> dd(0, 90), vv(0, 4);
+            std::uniform_real_distribution<double> gg(-5.0, 90.0);
+            for (int y = 0; y < h; ++y)
+                for (int x = 0; x < w; ++x) {
+                    est.d(x, y) = dd(rng);
+                    est.valid(x, y) = vv(rng) != 0;
+                    const double g = gg(rng);
+                    gt(x, y) = g < 0.0 ? 0.0 : (t == 3 ? std::round(g) : g);
+                }
+            const std::string n = "eval_outliers/" + std::to_string(t);
+            put_img(n + "/d", est.d);
+            put_img(n + "/valid", est.valid);
+            put_img(n + "/gt", gt);
+            for (int strict = 0; strict < 2; ++strict) {
+                OutlierOptions o;
+                o.strict_density = strict != 0;
+                const OutlierStats s = count_outliers(est, gt, o);
+                const std::vector<int64_t> c = {s.evaluated, s.outliers};
+                put_vec(n + "/counts_strict" + std::to_string(strict), c);
+            }
+        }
     }
     std::fclose(g_out);
     return 0;

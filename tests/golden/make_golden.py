@@ -23,7 +23,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 REF = "/root/reference/proj"
 SRCS = ["matching_cost.cpp", "sgm.cpp", "geometry.cpp", "temporal_filter.cpp",
-        "motion_detect.cpp"]
+        "motion_detect.cpp", "eval.cpp"]
 
 
 def build_and_run(tmp: str) -> str:
