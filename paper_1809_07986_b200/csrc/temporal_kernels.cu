@@ -141,8 +141,9 @@ __global__ void predict_finalize_kernel(Bufs b, double q, int apply_phi) {
     b.wd[t] = d;
     b.wp[t] = p;
     b.wv[t] = v;
-    if (b.wsrc) b.wsrc[t] = kd != 0ull ? src : 0.0;
-    b.kd[t] = 0ull;
+    // source_d is an output of warp_state_ex only (the stage API, apply_phi = 0)
+    if (!apply_phi) b.wsrc[t] = kd != 0ull ? src : 0.0;
+    if (kd != 0ull) b.kd[t] = 0ull;  // untouched keys are still armed
 }
 
 void launch_predict_finalize(const Bufs& b, int n, double q, int apply_phi, Launch L) {
