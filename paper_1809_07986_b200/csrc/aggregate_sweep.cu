@@ -100,8 +100,12 @@ __device__ __forceinline__ uint32_t group_min(uint32_t v) {
     return v;
 }
 
+// lohi = lo | hi << 16, cell / qo = cell and quad offsets, nq = quads of the
+// window. The packed records carry nq in their 4th word so that all four
+// loaded registers stay live (a dead one gets reused while the load is still
+// in flight, and its next writer then waits for the load).
 struct PixMeta {
-    uint32_t lohi, cell, qo;
+    uint32_t lohi, cell, qo, nq;
 };
 
 // One pixel, processed by a group of G lanes; lane lg owns the Q consecutive
@@ -263,21 +267,23 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
             m.lohi = v.x;
             m.cell = v.y;
             m.qo = v.z;
+            m.nq = v.w;
         } else {  // lanes = adjacent pixels of a row
             const uint4 v = __ldg(rmeta + p);
             m.lohi = v.x;
             m.cell = v.y;
             m.qo = v.z;
+            m.nq = v.w;
         }
     };
 
     // metadata two steps ahead, costs of the next step prefetched into L1
     int p_tmp = 0;
     bool act1 = pixel_at(0, p_tmp);
-    PixMeta m1{0u, 0u, 0u};
+    PixMeta m1{0u, 0u, 0u, 0u};
     if (act1) load_meta(p_tmp, m1);
     bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
-    PixMeta m2{0u, 0u, 0u};
+    PixMeta m2{0u, 0u, 0u, 0u};
     if (act2) load_meta(p_tmp, m2);
     for (int k = 0; k < nsteps; ++k) {
         const bool active = act1;
@@ -296,7 +302,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
             prev_active = false;
             continue;
         }
-        const int nq = static_cast<int>(mc.lohi >> 18) - static_cast<int>((mc.lohi & 0xffffu) >> 2) + 1;
+        const int nq = static_cast<int>(mc.nq);
         const bool narrow = active && nq <= 4;
         // windows of <= 4 quads: the lane itself, Q = the warp's widest such window
         const int qn = __reduce_max_sync(0xffffffffu, narrow ? nq : 0);
@@ -324,6 +330,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
                 const int src = gi < cnt ? static_cast<int>(lds32(srcbase + 4u * static_cast<uint32_t>(gi))) : lane;
                 __syncwarp();
                 PixMeta pw;
+                pw.nq = 0u;  // unused by scan_pixel
                 pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
                 pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);

@@ -46,8 +46,8 @@ struct Bufs {
     uint32_t* off;       // [slot][P+1]
     uint32_t* row_sum;   // [slot][H]
     uint32_t* qoff;      // [slot][P+1] quad-aligned offsets (aggregation partials)
-    uint4* tmeta;        // [slot][W][H] column-major {lohi, off, qoff, 0} (horizontal scanlines)
-    uint4* rmeta;        // [slot][H][W] row-major {lohi, off, qoff, 0} (the other scanlines)
+    uint4* tmeta;        // [slot][W][H] column-major {lohi, off, qoff, quads} (horizontal scanlines)
+    uint4* rmeta;        // [slot][H][W] row-major {lohi, off, qoff, quads} (the other scanlines)
     uint32_t* qrow_sum;  // [slot][H]
     unsigned long long* ncells;  // [slot]
     unsigned long long* nquads;  // [slot]

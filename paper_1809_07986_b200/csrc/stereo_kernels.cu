@@ -212,7 +212,7 @@ __global__ void row_scan_kernel(Bufs b) {
 }
 
 // Adds the row bases to the in-row offsets, and writes the packed records
-// {lohi, off, qoff} the scan kernel loads with one 16-byte access: row-major
+// {lohi, off, qoff, quads} the scan kernel loads with one 16-byte access: row-major
 // (lanes = adjacent pixels of a row) and column-major (horizontal scanlines,
 // lanes = consecutive rows). 32x32 tiles through shared memory.
 __global__ void offsets_finalize_kernel(Bufs b) {
@@ -230,7 +230,9 @@ __global__ void offsets_finalize_kernel(Bufs b) {
             const uint32_t off = b.off[o] + rb, qo = b.qoff[o] + qb;
             b.off[o] = off;
             b.qoff[o] = qo;
-            const uint4 rec = make_uint4(b.lohi[pbase + static_cast<size_t>(y) * b.W + x], off, qo, 0u);
+            const uint32_t lh = b.lohi[pbase + static_cast<size_t>(y) * b.W + x];
+            const uint32_t nq = (lh >> 18) - ((lh & 0xffffu) >> 2) + 1u;  // quads of the window
+            const uint4 rec = make_uint4(lh, off, qo, nq);
             b.rmeta[pbase + static_cast<size_t>(y) * b.W + x] = rec;
             tile[j][tx] = rec;
         }
