@@ -356,8 +356,8 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
 // Fused combine + winner_takes_all (sgm.cpp:163-187) for the production step,
 // also the standalone combine (S only). ONE WARP per 32-pixel chunk of a row,
 // independent of every other warp (no block barriers): a shared-memory owner
-// map gives each quad of the chunk its pixel; lanes stride aligned groups of
-// 4 quads, each direction's 4 path-cost words read with one 16-byte load
+// map gives each quad of the chunk its pixel; lanes stride the chunk's quads,
+// two at a time, with every direction's u32 path-cost word loaded up front
 // (coalesced), u16x2 sums, S stored when requested and the quad's first
 // (S, level) minimum kept in shared memory; then lane = pixel reduces its
 // quads to the first argmin.
@@ -385,7 +385,7 @@ __device__ __forceinline__ float subpixel_of(int d, int sm1, int s0, int sp1, bo
 }
 
 template <int NDIR>
-__global__ void __launch_bounds__(32 * kCwWarps, 6) combine_wta_kernel(Bufs b, int n, int write_s,
+__global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, int n, int write_s,
                                                                     int do_wta, int subpix) {
     extern __shared__ __align__(16) uint8_t cwm[];
     const int W = b.W, H = b.H;
@@ -456,24 +456,22 @@ __global__ void __launch_bounds__(32 * kCwWarps, 6) combine_wta_kernel(Bufs b, i
         if (subpix)
             qsum[l * qmax + k] = make_uint2((se & 0xffffu) | (so << 16), (se >> 16) | (so & 0xffff0000u));
     };
-    // aligned groups of 4 quads: one 16-byte load per direction per lane
-    const uint32_t ga = qbase & ~3u;
-    const uint32_t ngroups = (qbase + nq - ga + 3) / 4;
-    for (uint32_t g = static_cast<uint32_t>(lane); g < ngroups; g += 32) {
-        uint4 w4[NDIR];
+    uint32_t q = static_cast<uint32_t>(lane);
+    for (; q + 32 < nq; q += 64) {
+        uint32_t w0[NDIR], w1[NDIR];
 #pragma unroll
-        for (int d = 0; d < NDIR; ++d)
-            w4[d] = __ldg(reinterpret_cast<const uint4*>(pd + d * dstride + ga) + g);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int rq = static_cast<int>(ga + 4 * g + t) - static_cast<int>(qbase);
-            if (rq < 0 || rq >= static_cast<int>(nq)) continue;
-            uint32_t w[NDIR];
-#pragma unroll
-            for (int d = 0; d < NDIR; ++d)
-                w[d] = t == 0 ? w4[d].x : (t == 1 ? w4[d].y : (t == 2 ? w4[d].z : w4[d].w));
-            finish(static_cast<uint32_t>(rq), w);
+        for (int d = 0; d < NDIR; ++d) {
+            w0[d] = __ldg(pd + d * dstride + qbase + q);
+            w1[d] = __ldg(pd + d * dstride + qbase + q + 32);
         }
+        finish(q, w0);
+        finish(q + 32, w1);
+    }
+    if (q < nq) {
+        uint32_t w0[NDIR];
+#pragma unroll
+        for (int d = 0; d < NDIR; ++d) w0[d] = __ldg(pd + d * dstride + qbase + q);
+        finish(q, w0);
     }
     __syncwarp();
     if (do_wta && lane < np) {
