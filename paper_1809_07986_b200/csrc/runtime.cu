@@ -488,24 +488,23 @@ void run_step(tsgm_ctx* ctx, int n) {
     launch_ranges_from_pred(b, n, c.filter.min_range_halfwidth, c.filter.range_use_stddev,
                             c.filter.range_stddev_gain, L);
     launch_offsets(b, n, L);
-    // sgm_match (A12-A15)
-    launch_census(b, n, L);
-    if (ctx->img_pending_free >= 0) {  // the staging buffer may take the next upload
-        CK(cudaEventRecord(ctx->ev_img_free[ctx->img_pending_free], ctx->st));
-        ctx->img_free_recorded[ctx->img_pending_free] = true;
-        ctx->img_pending_free = -1;
-    }
+    // sgm_match (A12-A15); the census is computed inside the cost kernel
     // the volume stages in balanced chunks of at most vol_slots sequences;
     // cost, agg and pdir are indexed by the position within the chunk
     const int chunks = (n + ctx->vol_slots - 1) / ctx->vol_slots;
     for (int k = 0, c0 = 0; k < chunks; ++k) {
         const int m = (n - c0) / (chunks - k);
         const Bufs bc = chunk_bufs(b, c0);
-        launch_cost(bc, m, L);
+        launch_cost(bc, m, L, /*fused_census=*/true);
         if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0))
             launch_wta(bc, m, L);
         for (int a = 0; a < m; ++a) ctx->vol_owner[a] = ctx->h_slots[c0 + a];
         c0 += m;
+    }
+    if (ctx->img_pending_free >= 0) {  // the images are read: the buffer may take the next upload
+        CK(cudaEventRecord(ctx->ev_img_free[ctx->img_pending_free], ctx->st));
+        ctx->img_free_recorded[ctx->img_pending_free] = true;
+        ctx->img_pending_free = -1;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
     launch_correct(b, n, c.filter.r, c.mask_tau, L);
