@@ -141,6 +141,8 @@ void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* 
                         const uint8_t* in_v, double* out_d, double* out_p, uint8_t* out_v,
                         double disc_thresh, int do_reject, int do_fill, Launch L);
 void launch_correct(const Bufs& b, int n, double r, double mask_tau, Launch L);
+// correct + render + export median fused (the step's path)
+void launch_correct_median(const Bufs& b, int n, double r, double mask_tau, Launch L);
 
 void launch_aggregate(const Bufs& b, int n, int p1, int p2, int paths, int path_set, Launch L);
 // Line-sweep aggregation (aggregate_sweep.cu): returns false when the

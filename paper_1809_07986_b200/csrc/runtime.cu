@@ -507,8 +507,7 @@ void run_step(tsgm_ctx* ctx, int n) {
         ctx->img_pending_free = -1;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
-    launch_correct(b, n, c.filter.r, c.mask_tau, L);
-    launch_median(b, n, b.rd, b.rv, b.ed, b.ev, L);
+    launch_correct_median(b, n, c.filter.r, c.mask_tau, L);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev_frame, ctx->st));
 }

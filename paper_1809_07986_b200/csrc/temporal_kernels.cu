@@ -248,11 +248,12 @@ void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* 
 // ---------------------------------------------------------------- correct (A16-A18, A21)
 // correct (temporal_filter.cpp:145-170), the diff map (:223-229), the
 // Mahalanobis mask extension (A21) and render_integer (:178-191), fused.
-__global__ void correct_kernel(Bufs b, double r, double tau) {
-    const int a = blockIdx.y, s = slot_of(b, a);
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= b.P) return;
-    const size_t t = static_cast<size_t>(s) * b.P + i;
+struct Corrected {
+    double d, p, diff;
+    uint8_t v, mask;
+};
+
+__device__ __forceinline__ Corrected correct_px(const Bufs& b, size_t t, double r, double tau) {
     const bool hp = b.pv[t] != 0, hm = b.mv[t] != 0;
     const double pdv = b.pd[t], ppv = b.pp[t];
     const double dz = static_cast<double>(b.md[t]);
@@ -273,22 +274,109 @@ __global__ void correct_kernel(Bufs b, double r, double tau) {
         p = ppv;
         v = 1;
     }
-    b.sd[t] = d;
-    b.sp[t] = p;
-    b.sv[t] = v;
-    b.diff[t] = (hp && hm) ? fabs(__dsub_rn(pdv, dz)) : 0.0;
     uint8_t mk = 0;
     if (hp && hm) {
         const double e = __dsub_rn(dz, pdv);
         mk = __dmul_rn(e, e) > __dmul_rn(__dmul_rn(tau, tau), __dadd_rn(ppv, r)) ? 1 : 0;
     }
-    b.mask[t] = mk;
-    b.rd[t] = v ? x86_lround_int(d) : 0;
-    b.rv[t] = v;
+    return Corrected{d, p, (hp && hm) ? fabs(__dsub_rn(pdv, dz)) : 0.0, v, mk};
+}
+
+__device__ __forceinline__ void store_corrected(const Bufs& b, size_t t, const Corrected& c) {
+    b.sd[t] = c.d;
+    b.sp[t] = c.p;
+    b.sv[t] = c.v;
+    b.diff[t] = c.diff;
+    b.mask[t] = c.mask;
+}
+
+__global__ void correct_kernel(Bufs b, double r, double tau) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.P) return;
+    const size_t t = static_cast<size_t>(s) * b.P + i;
+    const Corrected c = correct_px(b, t, r, tau);
+    store_corrected(b, t, c);
+    b.rd[t] = c.v ? x86_lround_int(c.d) : 0;
+    b.rv[t] = c.v;
 }
 
 void launch_correct(const Bufs& b, int n, double r, double mask_tau, Launch L) {
     correct_kernel<<<dim3((b.P + 255) / 256, n), 256, 0, L.st>>>(b, r, mask_tau);
+    ++*L.counter;
+}
+
+// correct + render_integer + median_refine fused for the step (A16-A19, A21):
+// a 32x8 tile computes correct and render for its 34x10 footprint (the 1-px
+// halo recomputed from the same inputs), writes the state, diff and mask of
+// its own pixels, and takes the 3x3 lower median of the rendered map from
+// shared memory (median_kernel's keys: INT32_MAX for invalid or missing) —
+// the rendered map never goes to HBM.
+constexpr int kCmW = 32, kCmH = 8;
+
+__device__ __forceinline__ void cm_swap(int32_t& a, int32_t& b) {
+    const int32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+__global__ void correct_median_kernel(Bufs b, double r, double tau) {
+    __shared__ int32_t key[kCmH + 2][kCmW + 2];
+    __shared__ uint8_t okv[kCmH + 2][kCmW + 2];
+    const int a = blockIdx.z, s = slot_of(b, a);
+    const size_t base = static_cast<size_t>(s) * b.P;
+    const int W = b.W, H = b.H;
+    const int x0 = blockIdx.x * kCmW - 1, y0 = blockIdx.y * kCmH - 1;
+    for (int k = threadIdx.y * kCmW + threadIdx.x; k < (kCmH + 2) * (kCmW + 2); k += kCmW * kCmH) {
+        const int ty = k / (kCmW + 2), tx = k % (kCmW + 2);
+        const int gx = x0 + tx, gy = y0 + ty;
+        int32_t kv = INT32_MAX;
+        uint8_t ov = 0;
+        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+            const size_t t = base + static_cast<size_t>(gy) * W + gx;
+            const Corrected c = correct_px(b, t, r, tau);
+            if (ty >= 1 && ty <= kCmH && tx >= 1 && tx <= kCmW) store_corrected(b, t, c);
+            if (c.v) {
+                kv = x86_lround_int(c.d);  // render_integer, temporal_filter.cpp:178-191
+                ov = 1;
+            }
+        }
+        key[ty][tx] = kv;
+        okv[ty][tx] = ov;
+    }
+    __syncthreads();
+    const int x = blockIdx.x * kCmW + threadIdx.x, y = blockIdx.y * kCmH + threadIdx.y;
+    if (x >= W || y >= H) return;
+    int32_t v[9];
+    int nv = 0;
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+            v[dy * 3 + dx] = key[threadIdx.y + dy][threadIdx.x + dx];
+            nv += okv[threadIdx.y + dy][threadIdx.x + dx];
+        }
+    const size_t i = base + static_cast<size_t>(y) * W + x;
+    if (nv < 5) {  // median_refine: valid iff at least 5 valid neighbours (sgm.cpp:189-216)
+        b.ed[i] = 0;
+        b.ev[i] = 0;
+        return;
+    }
+    cm_swap(v[0], v[3]); cm_swap(v[1], v[7]); cm_swap(v[2], v[5]); cm_swap(v[4], v[8]);
+    cm_swap(v[0], v[7]); cm_swap(v[2], v[4]); cm_swap(v[3], v[8]); cm_swap(v[5], v[6]);
+    cm_swap(v[0], v[2]); cm_swap(v[1], v[3]); cm_swap(v[4], v[5]); cm_swap(v[7], v[8]);
+    cm_swap(v[1], v[4]); cm_swap(v[3], v[6]); cm_swap(v[5], v[7]);
+    cm_swap(v[0], v[1]); cm_swap(v[2], v[4]); cm_swap(v[3], v[5]); cm_swap(v[6], v[8]);
+    cm_swap(v[2], v[3]); cm_swap(v[4], v[5]); cm_swap(v[6], v[7]);
+    cm_swap(v[1], v[2]); cm_swap(v[3], v[4]); cm_swap(v[5], v[6]);
+    const int k = (nv - 1) / 2;
+    b.ed[i] = k == 2 ? v[2] : (k == 3 ? v[3] : v[4]);
+    b.ev[i] = 1;
+}
+
+void launch_correct_median(const Bufs& b, int n, double r, double mask_tau, Launch L) {
+    dim3 grid((b.W + kCmW - 1) / kCmW, (b.H + kCmH - 1) / kCmH, n);
+    correct_median_kernel<<<grid, dim3(kCmW, kCmH), 0, L.st>>>(b, r, mask_tau);
     ++*L.counter;
 }
 
