@@ -523,8 +523,12 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
     const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
     auto kern = k == 8 ? combine_wta_kernel<8> : combine_wta_kernel<4>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(cwsmem));
+    static size_t cw_set[2] = {48 * 1024, 48 * 1024};  // opt in once per variant
+    if (cwsmem > cw_set[k == 8]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(cwsmem));
+        cw_set[k == 8] = cwsmem;
+    }
     const long long warps = static_cast<long long>((b.W + 31) / 32) * b.H * n;
     kern<<<static_cast<unsigned>((warps + kCwWarps - 1) / kCwWarps), 32 * kCwWarps, cwsmem, L.st>>>(
         b, n, write_s, do_wta, subpix);

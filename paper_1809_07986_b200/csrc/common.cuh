@@ -127,8 +127,7 @@ void launch_ranges_from_pred(const Bufs& b, int n, int min_hw, int use_stddev, d
                              Launch L);
 void launch_ranges_given(const Bufs& b, int n, Launch L);  // lo/hi already set
 void launch_offsets(const Bufs& b, int n, Launch L);       // row scan + finalize
-// fused_census: compute the signatures in the cost kernel (no census_kernel pass)
-void launch_cost(const Bufs& b, int n, Launch L, bool fused_census = false);
+void launch_cost(const Bufs& b, int n, Launch L);
 void launch_wta(const Bufs& b, int n, Launch L);
 void launch_median(const Bufs& b, int n, const int32_t* in_d, const uint8_t* in_v,
                    int32_t* out_d, uint8_t* out_v, Launch L);

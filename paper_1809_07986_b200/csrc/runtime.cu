@@ -211,11 +211,12 @@ struct tsgm_ctx {
     // staging buffers, so frame k+1's images cross PCIe while frame k
     // computes; a buffer is reused once the census that read it has run.
     cudaStream_t up_st = nullptr;
-    uint8_t* d_img_alt = nullptr;
+    static constexpr int kImgBufs = 2;
+    uint8_t* d_img_up[kImgBufs]{};
     int img_buf = 0;
     int img_pending_free = -1;  // buffer the current step reads (free after census)
-    cudaEvent_t ev_img_ready[2]{}, ev_img_free[2]{};
-    bool img_free_recorded[2]{};
+    cudaEvent_t ev_img_ready[kImgBufs]{}, ev_img_free[kImgBufs]{};
+    bool img_free_recorded[kImgBufs]{};
     // Batched fetches: a device-to-device snapshot on the compute stream, then
     // the device-to-host copy from the snapshot on the copy stream, so the
     // next frame never waits for PCIe; a kind's snapshot is rewritten only
@@ -259,7 +260,7 @@ struct tsgm_ctx {
         if (ev_frame) cudaEventDestroy(ev_frame);
         for (auto e : ev_snap_copied)
             if (e) cudaEventDestroy(e);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kImgBufs; ++i) {
             if (ev_img_ready[i]) cudaEventDestroy(ev_img_ready[i]);
             if (ev_img_free[i]) cudaEventDestroy(ev_img_free[i]);
         }
@@ -302,7 +303,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     CK(cudaStreamCreateWithFlags(&ctx->up_st, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_frame, cudaEventDisableTiming));
     for (auto& e : ctx->ev_snap_copied) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < tsgm_ctx::kImgBufs; ++i) {
         CK(cudaEventCreateWithFlags(&ctx->ev_img_ready[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_img_free[i], cudaEventDisableTiming));
     }
@@ -366,7 +367,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     ctx->d_right = ctx->dalloc<const uint8_t*>(S);
     ctx->d_H = ctx->dalloc<double>(S * 16);
     ctx->d_img = ctx->dalloc<uint8_t>(S * 2 * P);
-    ctx->d_img_alt = ctx->dalloc<uint8_t>(S * 2 * P);
+    for (auto& u : ctx->d_img_up) u = ctx->dalloc<uint8_t>(S * 2 * P);
     // the per-frame volumes last: C (u8), S (u16) and, for the scan
     // aggregation, 8 directions of u8 path costs per cell, for vol_slots
     // sequences at a time (the rest of the batch runs in further chunks)
@@ -488,23 +489,27 @@ void run_step(tsgm_ctx* ctx, int n) {
     launch_ranges_from_pred(b, n, c.filter.min_range_halfwidth, c.filter.range_use_stddev,
                             c.filter.range_stddev_gain, L);
     launch_offsets(b, n, L);
-    // sgm_match (A12-A15); the census is computed inside the cost kernel
+    // sgm_match (A12-A15)
+    launch_census(b, n, L);
+    // Release the upload buffer right after the census, its only reader. (The
+    // release must come early in the frame: recorded after the cost kernels
+    // instead, it measurably serialised the next uploads behind the copy-outs.)
+    if (ctx->img_pending_free >= 0) {
+        CK(cudaEventRecord(ctx->ev_img_free[ctx->img_pending_free], ctx->st));
+        ctx->img_free_recorded[ctx->img_pending_free] = true;
+        ctx->img_pending_free = -1;
+    }
     // the volume stages in balanced chunks of at most vol_slots sequences;
     // cost, agg and pdir are indexed by the position within the chunk
     const int chunks = (n + ctx->vol_slots - 1) / ctx->vol_slots;
     for (int k = 0, c0 = 0; k < chunks; ++k) {
         const int m = (n - c0) / (chunks - k);
         const Bufs bc = chunk_bufs(b, c0);
-        launch_cost(bc, m, L, /*fused_census=*/true);
+        launch_cost(bc, m, L);
         if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0))
             launch_wta(bc, m, L);
         for (int a = 0; a < m; ++a) ctx->vol_owner[a] = ctx->h_slots[c0 + a];
         c0 += m;
-    }
-    if (ctx->img_pending_free >= 0) {  // the images are read: the buffer may take the next upload
-        CK(cudaEventRecord(ctx->ev_img_free[ctx->img_pending_free], ctx->st));
-        ctx->img_free_recorded[ctx->img_pending_free] = true;
-        ctx->img_pending_free = -1;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
     launch_correct_median(b, n, c.filter.r, c.mask_tau, L);
@@ -669,8 +674,8 @@ int tsgm_step(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const uint8_t* con
         std::vector<const uint8_t*> dl(n), dr(n);
         const size_t P = ctx->P;
         const int bi = ctx->img_buf;
-        ctx->img_buf ^= 1;
-        uint8_t* img = bi ? ctx->d_img_alt : ctx->d_img;
+        ctx->img_buf = (ctx->img_buf + 1) % tsgm_ctx::kImgBufs;
+        uint8_t* img = ctx->d_img_up[bi];
         if (ctx->img_free_recorded[bi]) CK(cudaStreamWaitEvent(ctx->up_st, ctx->ev_img_free[bi], 0));
         for (int i = 0; i < n; ++i) {
             uint8_t* base = img + static_cast<size_t>(slots[i]) * 2 * P;

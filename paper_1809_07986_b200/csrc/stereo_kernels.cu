@@ -263,11 +263,6 @@ __device__ __forceinline__ uint8_t cell_cost(const uint32_t* sl, const uint32_t*
     return ok ? static_cast<uint8_t>(__popc(sl[x] ^ sr[xr])) : static_cast<uint8_t>(kMaxCost);
 }
 
-// With kFusedCensus the CTA computes its row's census signatures itself
-// (census_transform, matching_cost.cpp:53-79, same bit order as
-// census_kernel) from the 5 image rows staged in shared memory, instead of
-// reading sigl/sigr written by census_kernel.
-template <bool kFusedCensus>
 __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
     extern __shared__ uint32_t sm[];
     const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
@@ -276,56 +271,13 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
     uint32_t* sr = sl + W;
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
-    const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
-    if (kFusedCensus) {
-        // rows y-2 .. y+2 of both images (only rows with a defined census need them;
-        // elsewhere every cost is kMaxCost and the signatures are never read)
-        uint8_t* rows = reinterpret_cast<uint8_t*>(sr + W);  // [2][5][W]
-        if (row_def) {
-            const uint8_t* L = b.left[a];
-            const uint8_t* R = b.right[a];
-            const int nw = W >> 2;
-            const bool al = ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(R) | W) & 3) == 0;
-            for (int r = 0; r < 5; ++r) {
-                const size_t g = static_cast<size_t>(y - kCensusRadius + r) * W;
-                if (al) {
-                    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
-                        reinterpret_cast<uint32_t*>(rows + r * W)[i] = reinterpret_cast<const uint32_t*>(L + g)[i];
-                        reinterpret_cast<uint32_t*>(rows + (5 + r) * W)[i] = reinterpret_cast<const uint32_t*>(R + g)[i];
-                    }
-                } else {
-                    for (int i = threadIdx.x; i < W; i += blockDim.x) {
-                        rows[r * W + i] = L[g + i];
-                        rows[(5 + r) * W + i] = R[g + i];
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        for (int x = threadIdx.x; x < 2 * W; x += blockDim.x) {
-            const int img = x >= W, xx = img ? x - W : x;
-            uint32_t v = 0;
-            if (row_def && xx >= kCensusRadius && xx < W - kCensusRadius) {
-                const uint8_t* t = rows + img * 5 * W + xx - kCensusRadius;
-                const uint8_t c = t[2 * W + kCensusRadius];
-#pragma unroll
-                for (int dy = 0; dy < 5; ++dy)
-#pragma unroll
-                    for (int dx = 0; dx < 5; ++dx) {
-                        if (dx == 2 && dy == 2) continue;
-                        v = (v << 1) | (t[dy * W + dx] < c ? 1u : 0u);
-                    }
-            }
-            sm[x] = v;  // sl[xx] or sr[xx]
-        }
-    } else {
-        for (int x = threadIdx.x; x < W; x += blockDim.x) {
-            sl[x] = b.sigl[pbase + x];
-            sr[x] = b.sigr[pbase + x];
-        }
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+        sl[x] = b.sigl[pbase + x];
+        sr[x] = b.sigr[pbase + x];
     }
     __syncthreads();
     uint8_t* base = b.cost + static_cast<size_t>(a) * b.vol_cap;
+    const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
     const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
     const int nwarps = static_cast<int>(blockDim.x >> 5);
     for (int x0 = warp * 32; x0 < W; x0 += 32 * nwarps) {
@@ -353,15 +305,9 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
     }
 }
 
-void launch_cost(const Bufs& b, int n, Launch L, bool fused_census) {
-    if (fused_census) {
-        const size_t smem = sizeof(uint32_t) * 2 * b.W + 10 * static_cast<size_t>(b.W);
-        cudaFuncSetAttribute(cost_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        cost_kernel<true><<<dim3(b.H, n), 512, smem, L.st>>>(b);
-    } else {
-        cost_kernel<false><<<dim3(b.H, n), 512, sizeof(uint32_t) * 2 * b.W, L.st>>>(b);
-    }
+void launch_cost(const Bufs& b, int n, Launch L) {
+    const size_t smem = sizeof(uint32_t) * 2 * b.W;
+    cost_kernel<<<dim3(b.H, n), 512, smem, L.st>>>(b);
     ++*L.counter;
 }
 
