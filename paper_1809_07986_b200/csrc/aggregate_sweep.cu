@@ -28,6 +28,8 @@
 // (SgmParams::validate, sgm.cpp:21-22), so the grouping is exact.
 #include "common.cuh"
 
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 namespace tsgm {
@@ -194,11 +196,9 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     if (pix && lg == 0) sts32(rp, static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16));
 }
 
-__global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    // invalid-level masks: entry (lrel, hrel) covers 16 levels = 4 quads x
-    // (ivA, ivB); level j is invalid iff j < lrel or j > hrel (hrel in -1..16)
-    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+// invalid-level masks: entry (lrel, hrel) covers 16 levels = 4 quads x
+// (ivA, ivB); level j is invalid iff j < lrel or j > hrel (hrel in -1..16)
+__device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
     for (int e = threadIdx.x; e < 4 * 18 * 8; e += blockDim.x) {
         const int lrel = e / (18 * 8), hrel = (e / 8) % 18 - 1, word = e % 8;
         const int t = word >> 1, half0 = 4 * t + 2 * (word & 1);
@@ -207,8 +207,14 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
             const int j = half0 + h;
             if (j < lrel || j > hrel) m |= 0xffffu << (16 * h);
         }
-        mask_tab_s[e] = m;
+        tab[e] = m;
     }
+}
+
+__global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+    fill_mask_table(mask_tab_s);
     __syncthreads();
     const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
     const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
@@ -349,6 +355,98 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         if (b8) wide(std::integral_constant<int, 8>{}, b8);
         const unsigned b16 = __ballot_sync(0xffffffffu, active && nq > 32);
         if (b16) wide(std::integral_constant<int, 16>{}, b16);
+        prev_active = active;
+    }
+}
+
+// Line-group variant for small batches (latency): a warp owns 32/G
+// scanlines, each with a fixed group of G lanes x 4 quads (every window fits,
+// G = the smallest power of two with 4G >= ceil(d_max/4)), one scan_pixel per
+// step. ~8x more warps than scan_kernel, no per-step window classes: for one
+// or a few sequences the GPU is otherwise nearly idle (scan_kernel has 306
+// warp tasks per sequence).
+template <int G>
+__global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, ScanParams sp) {
+    constexpr int LPW = 32 / G;  // scanlines per warp
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+    fill_mask_table(mask_tab_s);
+    __syncthreads();
+    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
+    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+    const int gi = lane / G;
+    const int task = blockIdx.x * kScanWarps + warp;
+    if (task >= sp.task_off[sp.ndir] * sp.n) return;
+    int d = 0;
+    while (task >= sp.task_off[d + 1] * sp.n) ++d;
+    const int r = task - sp.task_off[d] * sp.n;
+    const int groups = sp.task_off[d + 1] - sp.task_off[d];
+    const int a = r / groups, g = r % groups;
+    const int s = slot_of(b, a);
+    const int W = b.W, H = b.H;
+    const int dx = sp.dx[d], dy = sp.dy[d];
+    const int SB = scan_slot_bytes(b.d_max);
+    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
+                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(LPW * (SB + 4));
+    const uint32_t my_sb = wbase + static_cast<uint32_t>(gi) * SB;
+    const uint32_t my_rp = wbase + static_cast<uint32_t>(LPW * SB) + 4u * static_cast<uint32_t>(gi);
+    const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
+    const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
+    const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
+    const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
+    uint32_t* out = reinterpret_cast<uint32_t*>(
+        b.pdir + (static_cast<size_t>(d) * b.vol_slots + a) * b.quad_cap * 4);
+    const bool horiz = dy == 0;
+    const int nsteps = horiz ? W : H;
+    const int sl = dx * dy;
+    const int c = (horiz ? 0 : (sl == 1 ? -(H - 1) : 0)) + LPW * g + gi;
+    const uint4* meta = (horiz ? b.tmeta : b.rmeta) + static_cast<size_t>(s) * b.P;
+    auto pixel_at = [&](int k, int& p) -> bool {
+        if (horiz) {
+            const int x = dx < 0 ? k : W - 1 - k;
+            p = x * H + c;
+            return c < H;
+        }
+        const int y = dy < 0 ? k : H - 1 - k;
+        const int x = c + sl * y;
+        p = y * W + x;
+        return x >= 0 && x < W;
+    };
+    auto load_meta = [&](int p, PixMeta& m) {
+        const uint4 v = __ldg(meta + p);
+        m.lohi = v.x;
+        m.cell = v.y;
+        m.qo = v.z;
+        m.nq = v.w;
+    };
+    bool prev_active = false;
+    int p_tmp = 0;
+    bool act1 = pixel_at(0, p_tmp);
+    PixMeta m1{0u, 0u, 0u, 0u};
+    if (act1) load_meta(p_tmp, m1);
+    bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
+    PixMeta m2{0u, 0u, 0u, 0u};
+    if (act2) load_meta(p_tmp, m2);
+    const int lg = lane & (G - 1);
+    for (int k = 0; k < nsteps; ++k) {
+        const bool active = act1;
+        const PixMeta mc = m1;
+        act1 = act2;
+        m1 = m2;
+        if (act1) {  // this lane's 16 levels of step k+1 towards L1
+            const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
+            const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
+            if (16 * lg < n_n + 4)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(cost + m1.cell + 16 * lg));
+        }
+        act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
+        if (act2) load_meta(p_tmp, m2);
+        if (__ballot_sync(0xffffffffu, active) == 0u) {
+            prev_active = false;
+            continue;
+        }
+        scan_pixel<G, 4>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                         mask_tab);
         prev_active = active;
     }
 }
@@ -518,9 +616,41 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
         sp.task_off[i + 1] = sp.task_off[i] + (lines + 31) / 32;
     }
-    const int tasks = sp.task_off[k] * n;
-    const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max);
-    scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
+    // small batches: the line-group kernel (latency); else the scanline-group
+    // kernel (throughput). TSGM_SCAN_KERNEL=lines|groups forces one (tests).
+    const int qmax = (b.d_max + 3) / 4;
+    int G = 1;
+    while (4 * G < qmax) G <<= 1;
+    int batched_warps = 0;
+    for (int i = 0; i < k; ++i) {
+        const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
+        batched_warps += (lines + 31) / 32;
+    }
+    batched_warps *= n;
+    const char* force = std::getenv("TSGM_SCAN_KERNEL");
+    const bool lines_mode = force ? std::strcmp(force, "lines") == 0 : batched_warps < 148 * 16;
+    if (lines_mode) {
+        const int lpw = 32 / G;
+        sp.task_off[0] = 0;
+        for (int i = 0; i < k; ++i) {
+            const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
+            sp.task_off[i + 1] = sp.task_off[i] + (lines + lpw - 1) / lpw;
+        }
+        const int tasks = sp.task_off[k] * n;
+        const size_t smem = static_cast<size_t>(kScanWarps) * lpw * (scan_slot_bytes(b.d_max) + 4);
+        const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
+        switch (G) {
+            case 1: scan_lines_kernel<1><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
+            case 2: scan_lines_kernel<2><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
+            case 4: scan_lines_kernel<4><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
+            case 8: scan_lines_kernel<8><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
+            default: scan_lines_kernel<16><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
+        }
+    } else {
+        const int tasks = sp.task_off[k] * n;
+        const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max);
+        scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
+    }
     const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
     auto kern = k == 8 ? combine_wta_kernel<8> : combine_wta_kernel<4>;
     static size_t cw_set[2] = {48 * 1024, 48 * 1024};  // opt in once per variant

@@ -1,7 +1,8 @@
 """aggregate_paths on the GPU vs the oracle on adversarial ragged volumes:
 random narrow/wide/full windows, large window shifts between neighbours,
-odd sizes, d_max not a multiple of 4, every path set, random P1/P2 — for both
-aggregation kernels (line sweep and per-direction scanline). Bit-exact."""
+odd sizes, d_max not a multiple of 4, every path set, random P1/P2 — for all
+three aggregation kernels (scanline groups, line groups, per-direction
+scanline). Bit-exact."""
 import numpy as np
 import pytest
 
@@ -42,11 +43,15 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("kernel", ["sweep", "scanline"])
+@pytest.mark.parametrize("kernel", ["groups", "lines", "scanline"])
 @pytest.mark.parametrize("w,h,d_max,p_full", CASES)
 def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
+    """groups: the scanline-group kernel (batched throughput path); lines: the
+    line-group kernel (small batches); scanline: the per-direction fallback."""
     if kernel == "scanline":
         monkeypatch.setenv("TSGM_FORCE_SCANLINE_AGG", "1")
+    else:
+        monkeypatch.setenv("TSGM_SCAN_KERNEL", kernel)
     rng = np.random.default_rng(w * 1000 + h * 7 + d_max)
     lo, hi = ragged_ranges(rng, w, h, d_max, p_full)
     n = int((hi.astype(np.int64) - lo + 1).sum())
