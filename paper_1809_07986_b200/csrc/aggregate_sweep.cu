@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
 }
 
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
-                            int write_s, int do_wta, Launch L, int subpix) {
+                            int write_s, int do_wta, Launch L, int subpix, bool full_range) {
     ScanParams sp{};
     sp.p1 = p1;
     sp.p2 = p2;
@@ -616,8 +616,9 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
         sp.task_off[i + 1] = sp.task_off[i] + (lines + 31) / 32;
     }
-    // small batches: the line-group kernel (latency); else the scanline-group
-    // kernel (throughput). TSGM_SCAN_KERNEL=lines|groups forces one (tests).
+    // small batches or full-range frames: the line-group kernel; else the
+    // scanline-group kernel (throughput on reduced windows).
+    // TSGM_SCAN_KERNEL=lines|groups forces one (tests).
     const int qmax = (b.d_max + 3) / 4;
     int G = 1;
     while (4 * G < qmax) G <<= 1;
@@ -628,7 +629,8 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     }
     batched_warps *= n;
     const char* force = std::getenv("TSGM_SCAN_KERNEL");
-    const bool lines_mode = force ? std::strcmp(force, "lines") == 0 : batched_warps < 148 * 16;
+    const bool lines_mode =
+        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < 148 * 16);
     if (lines_mode) {
         const int lpw = 32 / G;
         sp.task_off[0] = 0;

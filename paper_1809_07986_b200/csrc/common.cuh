@@ -148,9 +148,11 @@ void launch_aggregate(const Bufs& b, int n, int p1, int p2, int paths, int path_
 // configuration does not fit its shared-memory plan (caller falls back).
 bool sweep_supported(int W, int H, int d_max, int p2);
 // write_s: store S in the ragged volume; do_wta: fuse winner_takes_all
-// (writes md/mv). At least one of the two must be set.
+// (writes md/mv). At least one of the two must be set. full_range: every
+// window spans d_max (frames from an empty state): the line-group scan wins.
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
-                            int write_s, int do_wta, Launch L, int subpix = 0);
+                            int write_s, int do_wta, Launch L, int subpix = 0,
+                            bool full_range = false);
 
 // Box detector (detect.cu), SURVEY §8(f) row 1.
 constexpr int kMaxDetectWindows = 16;

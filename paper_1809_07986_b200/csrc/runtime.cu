@@ -183,6 +183,7 @@ struct tsgm_ctx {
     int vol_slots = 0;            // volume working set (positions of cost/agg/pdir)
     std::vector<int> vol_owner;   // slot whose volumes sit at each position (-1: none)
     std::vector<int> h_slots;     // host copy of the current batch's slots
+    std::vector<char> fresh;      // slot holds the empty state (its next frame is full range)
     int device = 0;
     int num_sms = 148;
     bool use_sweep = false;  // line-sweep aggregation (else per-direction scanline kernel)
@@ -384,6 +385,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     }
     ctx->vol_slots = vs;
     ctx->vol_owner.assign(vs, -1);
+    ctx->fresh.assign(c.max_slots, 1);
     b.vol_slots = vs;
     // 16 bytes of padding on both sides: the sweep reads aligned words around
     // each window
@@ -446,12 +448,12 @@ void check_slots(tsgm_ctx* ctx, int n, const int32_t* slots) {
 // fuse_wta, winner_takes_all is fused into the combine (S is then written
 // only if keep_s) and the caller skips launch_wta.
 bool aggregate(tsgm_ctx* ctx, const Bufs& b, int n, Launch L, bool fuse_wta = false,
-               bool keep_s = true) {
+               bool keep_s = true, bool full_range = false) {
     const tsgm_config& c = ctx->cfg;
     if (ctx->use_sweep && sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2)) {
         launch_aggregate_sweep(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
                                (keep_s || !fuse_wta) ? 1 : 0, fuse_wta ? 1 : 0, L,
-                               (fuse_wta && b.sub) ? 1 : 0);
+                               (fuse_wta && b.sub) ? 1 : 0, full_range);
         return fuse_wta;
     }
     if (b.sub) bad("TSGM_SUBPIXEL needs the scan aggregation (P2 + 24 <= 255, d_max <= 256)");
@@ -505,14 +507,17 @@ void run_step(tsgm_ctx* ctx, int n) {
     for (int k = 0, c0 = 0; k < chunks; ++k) {
         const int m = (n - c0) / (chunks - k);
         const Bufs bc = chunk_bufs(b, c0);
+        bool full = true;  // every sequence of the chunk starts empty: full-range windows
+        for (int a = 0; a < m; ++a) full = full && ctx->fresh[ctx->h_slots[c0 + a]];
         launch_cost(bc, m, L);
-        if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0))
+        if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0, full))
             launch_wta(bc, m, L);
         for (int a = 0; a < m; ++a) ctx->vol_owner[a] = ctx->h_slots[c0 + a];
         c0 += m;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
     launch_correct_median(b, n, c.filter.r, c.mask_tau, L);
+    for (int i = 0; i < n; ++i) ctx->fresh[ctx->h_slots[i]] = 0;
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev_frame, ctx->st));
 }
@@ -646,6 +651,7 @@ int tsgm_reset(tsgm_ctx* ctx, int32_t slot) {
         CK(cudaMemsetAsync(ctx->b.sd + slot * P, 0, 8 * P, ctx->st));
         CK(cudaMemsetAsync(ctx->b.sp + slot * P, 0, 8 * P, ctx->st));
         CK(cudaMemsetAsync(ctx->b.sv + slot * P, 0, P, ctx->st));
+        ctx->fresh[slot] = 1;
     });
 }
 
@@ -654,6 +660,7 @@ int tsgm_set_state(tsgm_ctx* ctx, int32_t slot, const double* d, const double* p
     return guarded([&] {
         if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_set_state: slot out of range");
         CK(cudaSetDevice(ctx->device));
+        ctx->fresh[slot] = 0;  // a caller state may hold valid pixels: reduced windows
         const size_t P = ctx->P;
         if (d) h2d(ctx, ctx->b.sd + slot * P, d, P);
         else CK(cudaMemsetAsync(ctx->b.sd + slot * P, 0, 8 * P, ctx->st));
@@ -1115,6 +1122,7 @@ int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_
         }
         tsgm_ctx* x = cache.get();
         const size_t P = x->P;
+        x->fresh[0] = (empty || !sv) ? 1 : 0;
         if (empty || !sv) {
             CK(cudaMemsetAsync(x->b.sd, 0, 8 * P, x->st));
             CK(cudaMemsetAsync(x->b.sp, 0, 8 * P, x->st));
