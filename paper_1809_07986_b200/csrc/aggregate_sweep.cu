@@ -457,17 +457,18 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
 // map gives each quad of the chunk its pixel; lanes stride the chunk's quads,
 // two at a time, with every direction's u32 path-cost word loaded up front
 // (coalesced), u16x2 sums, S stored when requested and the quad's first
-// (S, level) minimum kept in shared memory; then lane = pixel reduces its
-// quads to the first argmin.
+// (S, level) minimum folded into its pixel's minimum with a shared-memory
+// atomicMin (the key (S << 16 | level) makes the minimum the first argmin);
+// then lane = pixel writes the WTA result.
 constexpr int kCwWarps = 4;
 
 // per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
-// key[32*qmax] (u32), qsum[32*qmax] (uint2, sub-pixel only)
+// best[32] (u32), qsum[32*qmax] (uint2, sub-pixel only)
 __host__ __device__ inline size_t cw_warp_bytes(int d_max, int subpix) {
     const size_t qm = static_cast<size_t>((d_max - 1) / 4 + 1);
     size_t bytes = 4 * 100 + 32 * qm;       // qo, lh, cl + own
     bytes = (bytes + 7) & ~static_cast<size_t>(7);
-    bytes += 4 * 32 * qm;                    // key
+    bytes += 4 * 32;                         // best
     if (subpix) bytes += 8 * 32 * qm;        // qsum (8-byte aligned)
     return bytes;
 }
@@ -501,9 +502,9 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
     uint32_t* lh = qo + 36;                             // lo | hi << 16
     uint32_t* cl = lh + 32;                             // cell offsets
     uint8_t* own = reinterpret_cast<uint8_t*>(cl + 32); // pixel of each quad
-    uint32_t* key = reinterpret_cast<uint32_t*>(
+    uint32_t* best_s = reinterpret_cast<uint32_t*>(
         (reinterpret_cast<uintptr_t>(own + 32 * qmax) + 7) & ~static_cast<uintptr_t>(7));
-    uint2* qsum = reinterpret_cast<uint2*>(key + 32 * qmax);  // 8-byte aligned (qmax*128 bytes)
+    uint2* qsum = reinterpret_cast<uint2*>(best_s + 32);  // 8-byte aligned
 
     const int np = min(32, W - x0);
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W + x0;
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
         my_lh = __ldg(b.lohi + pbase + lane);
         cl[lane] = __ldg(b.off + obase + lane);
     }
+    best_s[lane] = 0xffffffffu;
     const uint32_t qbase = __shfl_sync(0xffffffffu, my_q, 0);
     const int my_nq = lane < np ? static_cast<int>(my_lh >> 18) - static_cast<int>((my_lh & 0xffffu) >> 2) + 1 : 0;
     const uint32_t rq = my_q - qbase;
@@ -550,7 +552,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
             if (write_s && ok) agg[cl[l] + (lv - lo)] = static_cast<uint16_t>(v[u]);
             best = min(best, ok ? ((v[u] << 16) | static_cast<uint32_t>(lv)) : 0xffffffffu);
         }
-        key[l * qmax + k] = best;
+        atomicMin(best_s + l, best);
         if (subpix)
             qsum[l * qmax + k] = make_uint2((se & 0xffffu) | (so << 16), (se >> 16) | (so & 0xffff0000u));
     };
@@ -573,8 +575,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
     }
     __syncwarp();
     if (do_wta && lane < np) {
-        uint32_t best = 0xffffffffu;
-        for (int k = 0; k < my_nq; ++k) best = min(best, key[lane * qmax + k]);
+        const uint32_t best = best_s[lane];
         const int x = x0 + lane;
         const bool def = x >= kCensusRadius && x < W - kCensusRadius &&
                          y >= kCensusRadius && y < H - kCensusRadius;
