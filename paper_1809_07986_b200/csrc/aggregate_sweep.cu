@@ -462,19 +462,15 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
 // then lane = pixel writes the WTA result.
 constexpr int kCwWarps = 4;
 
-// per-warp shared bytes: (write_s) the chunk's S cells staged for 16-byte
-// stores, then qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8), best[32]
-// (u32), qsum[32*qmax] (uint2, sub-pixel only); a multiple of 16
-__host__ __device__ inline size_t cw_stage_bytes(int d_max, int write_s) {
-    return write_s ? ((static_cast<size_t>(2) * 32 * d_max + 16 + 15) & ~static_cast<size_t>(15)) : 0;
-}
-__host__ __device__ inline size_t cw_warp_bytes(int d_max, int subpix, int write_s) {
+// per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
+// best[32] (u32), qsum[32*qmax] (uint2, sub-pixel only)
+__host__ __device__ inline size_t cw_warp_bytes(int d_max, int subpix) {
     const size_t qm = static_cast<size_t>((d_max - 1) / 4 + 1);
     size_t bytes = 4 * 100 + 32 * qm;       // qo, lh, cl + own
     bytes = (bytes + 7) & ~static_cast<size_t>(7);
     bytes += 4 * 32;                         // best
     if (subpix) bytes += 8 * 32 * qm;        // qsum (8-byte aligned)
-    return cw_stage_bytes(d_max, write_s) + ((bytes + 15) & ~static_cast<size_t>(15));
+    return bytes;
 }
 
 // Sub-pixel extension (A22, not in the reference): parabola vertex through
@@ -501,9 +497,8 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
     const int rem = static_cast<int>(task % (static_cast<long long>(chunks) * H));
     const int y = rem / chunks, x0 = (rem % chunks) * 32;
     const int s = slot_of(b, a);
-    uint8_t* wsm = cwm + static_cast<size_t>(wib) * cw_warp_bytes(b.d_max, subpix, write_s);
-    uint16_t* sst = reinterpret_cast<uint16_t*>(wsm);  // (write_s) staged S cells
-    uint32_t* qo = reinterpret_cast<uint32_t*>(wsm + cw_stage_bytes(b.d_max, write_s));  // 33 chunk-relative quad offsets
+    uint8_t* wsm = cwm + static_cast<size_t>(wib) * cw_warp_bytes(b.d_max, subpix);
+    uint32_t* qo = reinterpret_cast<uint32_t*>(wsm);  // 33 chunk-relative quad offsets
     uint32_t* lh = qo + 36;                             // lo | hi << 16
     uint32_t* cl = lh + 32;                             // cell offsets
     uint8_t* own = reinterpret_cast<uint8_t*>(cl + 32); // pixel of each quad
@@ -526,13 +521,6 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
     }
     best_s[lane] = 0xffffffffu;
     const uint32_t qbase = __shfl_sync(0xffffffffu, my_q, 0);
-    // S cells of the chunk: [c0, c0 + clen) of the ragged layout, staged from
-    // element sshift on so that staged 16-byte blocks are aligned in HBM
-    const uint32_t c0 = __shfl_sync(0xffffffffu, lane < np ? cl[lane] : 0u, 0);
-    const uint32_t cend = __shfl_sync(0xffffffffu,
-                                      lane < np ? cl[lane] + (my_lh >> 16) - (my_lh & 0xffffu) + 1u : 0u,
-                                      np - 1);
-    const uint32_t sshift = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(agg + c0) & 15u) >> 1);
     const int my_nq = lane < np ? static_cast<int>(my_lh >> 18) - static_cast<int>((my_lh & 0xffffu) >> 2) + 1 : 0;
     const uint32_t rq = my_q - qbase;
     if (lane < np) {
@@ -561,7 +549,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
         for (int u = 0; u < 4; ++u) {
             const int lv = d0 + u;
             const bool ok = lv >= lo && lv <= hi;
-            if (write_s && ok) sst[sshift + cl[l] - c0 + (lv - lo)] = static_cast<uint16_t>(v[u]);
+            if (write_s && ok) agg[cl[l] + (lv - lo)] = static_cast<uint16_t>(v[u]);
             best = min(best, ok ? ((v[u] << 16) | static_cast<uint32_t>(lv)) : 0xffffffffu);
         }
         atomicMin(best_s + l, best);
@@ -586,18 +574,6 @@ __global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, i
         finish(q, w0);
     }
     __syncwarp();
-    if (write_s) {  // staged S out with 16-byte stores (bytewise only in the end blocks)
-        const uint32_t total = sshift + (cend - c0);
-        uint16_t* g = agg + c0 - sshift;
-        for (uint32_t k = static_cast<uint32_t>(lane); 8u * k < total; k += 32) {
-            const uint32_t e0 = 8u * k, e1 = e0 + 8u;
-            if (e0 >= sshift && e1 <= total) {
-                *reinterpret_cast<uint4*>(g + e0) = *reinterpret_cast<const uint4*>(sst + e0);
-            } else {
-                for (uint32_t e = max(e0, sshift); e < min(e1, total); ++e) g[e] = sst[e];
-            }
-        }
-    }
     if (do_wta && lane < np) {
         const uint32_t best = best_s[lane];
         const int x = x0 + lane;
@@ -678,7 +654,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max);
         scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
     }
-    const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix, write_s);
+    const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
     auto kern = k == 8 ? combine_wta_kernel<8> : combine_wta_kernel<4>;
     static size_t cw_set[2] = {48 * 1024, 48 * 1024};  // opt in once per variant
     if (cwsmem > cw_set[k == 8]) {
