@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
 // (S, level) minimum folded into its pixel's minimum with a shared-memory
 // atomicMin (the key (S << 16 | level) makes the minimum the first argmin);
 // then lane = pixel writes the WTA result.
-constexpr int kCwWarps = 4;
+constexpr int kCwWarps = 2;
 
 // per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
 // best[32] (u32), qsum[32*qmax] (uint2, sub-pixel only)
@@ -484,7 +484,7 @@ __device__ __forceinline__ float subpixel_of(int d, int sm1, int s0, int sp1, bo
 }
 
 template <int NDIR>
-__global__ void __launch_bounds__(32 * kCwWarps, 8) combine_wta_kernel(Bufs b, int n, int write_s,
+__global__ void __launch_bounds__(32 * kCwWarps, 16) combine_wta_kernel(Bufs b, int n, int write_s,
                                                                     int do_wta, int subpix) {
     extern __shared__ __align__(16) uint8_t cwm[];
     const int W = b.W, H = b.H;
