@@ -299,8 +299,35 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
             const int lo_w = __shfl_sync(0xffffffffu, lo, src);
             const int n_w = __shfl_sync(0xffffffffu, n, src);
             const uint32_t o_w = __shfl_sync(0xffffffffu, o, src);
-            uint8_t* dst = base + o_w;
-            for (int j = lane; j < n_w; j += 32) dst[j] = cell_cost(sl, sr, xw, lo_w + j, W, row_def);
+            // aligned 32-bit words over the window's bytes, one per lane and
+            // iteration; only the two end words (shared with the neighbouring
+            // windows) are written bytewise
+            const bool xdef = row_def && xw >= kCensusRadius && xw < W - kCensusRadius;
+            const uint32_t slx = sl[xw];
+            const uintptr_t A0 = reinterpret_cast<uintptr_t>(base + o_w);
+            const uintptr_t W0 = A0 & ~static_cast<uintptr_t>(3);
+            const int head = static_cast<int>(A0 - W0);  // window bytes start inside word 0
+            const int nwords = (head + n_w + 3) >> 2;
+            for (int wi = lane; wi < nwords; wi += 32) {
+                const int j0 = 4 * wi - head;  // window level index of the word's byte 0
+                uint32_t word = 0u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int xr = xw - (lo_w + j0 + k);
+                    const bool ok = xdef && xr >= kCensusRadius && xr < W - kCensusRadius;
+                    const uint32_t v = ok ? static_cast<uint32_t>(__popc(slx ^ sr[ok ? xr : 0]))
+                                          : static_cast<uint32_t>(kMaxCost);
+                    word |= v << (8 * k);
+                }
+                uint8_t* wp = reinterpret_cast<uint8_t*>(W0) + 4 * wi;
+                if (j0 >= 0 && j0 + 4 <= n_w) {
+                    *reinterpret_cast<uint32_t*>(wp) = word;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (j0 + k >= 0 && j0 + k < n_w) wp[k] = static_cast<uint8_t>(word >> (8 * k));
+                }
+            }
         }
     }
 }
