@@ -39,7 +39,9 @@ constexpr int kScanWarps = 2;  // warps per CTA (one task each)
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
 __host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
 // shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group sources
-__host__ __device__ inline int scan_warp_bytes(int d_max) { return 32 * (scan_slot_bytes(d_max) + 4) + 64; }
+__host__ __device__ inline int scan_warp_bytes(int d_max, int spw = 32) {
+    return spw * (scan_slot_bytes(d_max) + 4) + 64;
+}
 
 bool sweep_supported(int W, int H, int d_max, int p2) {
     // u8 path costs need 24 + P2 <= 255; a window is <= 16 lanes x 4 quads
@@ -211,7 +213,12 @@ __device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
     }
 }
 
+// SPW = scanlines per warp (32, 16 or 8): a narrow window (<= 4 quads) is
+// computed by GN = 32/SPW lanes x QN = 4/GN quads of its scanline's group;
+// fewer scanlines per warp give proportionally more warps for small batches.
+template <int SPW>
 __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
+    constexpr int GN = 32 / SPW, QN = 4 / GN;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
     fill_mask_table(mask_tab_s);
@@ -231,12 +238,13 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const int W = b.W, H = b.H;
     const int dx = sp.dx[d], dy = sp.dy[d];
     const int SB = scan_slot_bytes(b.d_max);
+    const int gs = lane / GN, lgs = lane % GN;  // the lane's scanline in the warp, rank in its group
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
-                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(scan_warp_bytes(b.d_max));
-    const uint32_t my_sb = wbase + static_cast<uint32_t>(lane) * SB;
-    const uint32_t rbase = wbase + 32u * static_cast<uint32_t>(SB);
-    const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(lane);
-    const uint32_t srcbase = rbase + 128u;  // 16 group source lanes
+                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(scan_warp_bytes(b.d_max, SPW));
+    const uint32_t my_sb = wbase + static_cast<uint32_t>(gs) * SB;
+    const uint32_t rbase = wbase + static_cast<uint32_t>(SPW * SB);
+    const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(gs);
+    const uint32_t srcbase = rbase + 4u * SPW;  // 16 group source lanes
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const bool horiz = dy == 0;
     const int nsteps = horiz ? W : H;
     const int sl = dx * dy;
-    const int c = horiz ? 32 * g + lane : (sl == 1 ? -(H - 1) : 0) + 32 * g + lane;
+    const int c = (horiz ? 0 : (sl == 1 ? -(H - 1) : 0)) + SPW * g + gs;
     bool prev_active = false;
 
     // p: the metadata index of step k (column-major for horizontal lines)
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         const PixMeta mc = m1;
         act1 = act2;
         m1 = m2;
-        if (act1) {  // step k+1's window towards L1 (its metadata arrived a step ago)
+        if (act1 && lgs == 0) {  // step k+1's window towards L1 (its metadata arrived a step ago)
             const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
             const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
             const uint8_t* c0 = cost + m1.cell;
@@ -310,18 +318,25 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         }
         const int nq = static_cast<int>(mc.nq);
         const bool narrow = active && nq <= 4;
-        // windows of <= 4 quads: the lane itself, Q = the warp's widest such window
-        const int qn = __reduce_max_sync(0xffffffffu, narrow ? nq : 0);
-        if (qn > 3)
-            scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                             mask_tab);
-        else if (qn == 3)
-            scan_pixel<1, 3>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                             mask_tab);
-        else if (qn > 0)
-            scan_pixel<1, 2>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                             mask_tab);
-        // wider windows: groups of G lanes x 4 quads, 32/G windows per pass
+        if (SPW == 32) {
+            // windows of <= 4 quads: the lane itself, Q = the warp's widest such window
+            const int qn = __reduce_max_sync(0xffffffffu, narrow ? nq : 0);
+            if (qn > 3)
+                scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2,
+                                 P2x4, mask_tab);
+            else if (qn == 3)
+                scan_pixel<1, 3>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2,
+                                 P2x4, mask_tab);
+            else if (qn > 0)
+                scan_pixel<1, 2>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2,
+                                 P2x4, mask_tab);
+        } else if (__any_sync(0xffffffffu, narrow)) {
+            // windows of <= 4 quads: the scanline's GN lanes x QN quads
+            scan_pixel<GN, QN>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                               mask_tab);
+        }
+        // wider windows: groups of G lanes x 4 quads, 32/G windows per pass;
+        // a window's owner is the first lane of its scanline's group
         const auto wide = [&](auto gtag, unsigned bw) {
             constexpr int G = decltype(gtag)::value;
             constexpr int PER = 32 / G;
@@ -341,19 +356,20 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
                 pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
                 const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
-                scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + static_cast<uint32_t>(src) * SB,
-                                 rbase + 4u * static_cast<uint32_t>(src), cost, out, P1x2, P2x2,
-                                 P2x4, mask_tab);
+                const uint32_t sline = static_cast<uint32_t>(src / GN);
+                scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, cost, out,
+                                 P1x2, P2x2, P2x4, mask_tab);
                 bw &= ~done;
             }
         };
-        const unsigned b2 = __ballot_sync(0xffffffffu, active && nq > 4 && nq <= 8);
+        const bool owner = active && lgs == 0;
+        const unsigned b2 = __ballot_sync(0xffffffffu, owner && nq > 4 && nq <= 8);
         if (b2) wide(std::integral_constant<int, 2>{}, b2);
-        const unsigned b4 = __ballot_sync(0xffffffffu, active && nq > 8 && nq <= 16);
+        const unsigned b4 = __ballot_sync(0xffffffffu, owner && nq > 8 && nq <= 16);
         if (b4) wide(std::integral_constant<int, 4>{}, b4);
-        const unsigned b8 = __ballot_sync(0xffffffffu, active && nq > 16 && nq <= 32);
+        const unsigned b8 = __ballot_sync(0xffffffffu, owner && nq > 16 && nq <= 32);
         if (b8) wide(std::integral_constant<int, 8>{}, b8);
-        const unsigned b16 = __ballot_sync(0xffffffffu, active && nq > 32);
+        const unsigned b16 = __ballot_sync(0xffffffffu, owner && nq > 32);
         if (b16) wide(std::integral_constant<int, 16>{}, b16);
         prev_active = active;
     }
@@ -631,7 +647,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     batched_warps *= n;
     const char* force = std::getenv("TSGM_SCAN_KERNEL");
     const bool lines_mode =
-        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < 148 * 16);
+        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < 148 * 4);
     if (lines_mode) {
         const int lpw = 32 / G;
         sp.task_off[0] = 0;
@@ -650,9 +666,26 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
             default: scan_lines_kernel<16><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
         }
     } else {
+        // scanlines per warp: enough warps to fill the GPU (148 SMs x 32 warps)
+        const char* fspw = std::getenv("TSGM_SCAN_SPW");
+        int spw = 32;
+        if (fspw) spw = std::atoi(fspw);
+        else if (batched_warps < 148 * 32 / 4) spw = 8;
+        else if (batched_warps < 148 * 32) spw = 16;
+        if (spw != 8 && spw != 16) spw = 32;
+        if (spw != 32) {
+            sp.task_off[0] = 0;
+            for (int i = 0; i < k; ++i) {
+                const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
+                sp.task_off[i + 1] = sp.task_off[i] + (lines + spw - 1) / spw;
+            }
+        }
         const int tasks = sp.task_off[k] * n;
-        const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max);
-        scan_kernel<<<(tasks + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, smem, L.st>>>(b, sp);
+        const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max, spw);
+        const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
+        if (spw == 8) scan_kernel<8><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
+        else if (spw == 16) scan_kernel<16><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
+        else scan_kernel<32><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
     }
     const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
     auto kern = k == 8 ? combine_wta_kernel<8> : combine_wta_kernel<4>;

@@ -43,15 +43,19 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("kernel", ["groups", "lines", "scanline"])
+@pytest.mark.parametrize("kernel", ["groups32", "groups16", "groups8", "lines", "scanline"])
 @pytest.mark.parametrize("w,h,d_max,p_full", CASES)
 def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
-    """groups: the scanline-group kernel (batched throughput path); lines: the
-    line-group kernel (small batches); scanline: the per-direction fallback."""
+    """groupsN: the scanline-group kernel with N scanlines per warp (batched
+    throughput path); lines: the line-group kernel (single sequences,
+    full-range frames); scanline: the per-direction fallback."""
     if kernel == "scanline":
         monkeypatch.setenv("TSGM_FORCE_SCANLINE_AGG", "1")
+    elif kernel == "lines":
+        monkeypatch.setenv("TSGM_SCAN_KERNEL", "lines")
     else:
-        monkeypatch.setenv("TSGM_SCAN_KERNEL", kernel)
+        monkeypatch.setenv("TSGM_SCAN_KERNEL", "groups")
+        monkeypatch.setenv("TSGM_SCAN_SPW", kernel[len("groups"):])
     rng = np.random.default_rng(w * 1000 + h * 7 + d_max)
     lo, hi = ragged_ranges(rng, w, h, d_max, p_full)
     n = int((hi.astype(np.int64) - lo + 1).sum())

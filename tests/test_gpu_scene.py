@@ -89,11 +89,13 @@ def test_volume_fetch_needs_last_chunk(port):
     eng.close()
 
 
-@pytest.mark.parametrize("scan", ["groups", "lines"])
+@pytest.mark.parametrize("scan", ["groups32", "groups16", "groups8", "lines"])
 def test_config1_movers_batched(port, monkeypatch, scan):
     """Config-1 scenes with movers, 3 sequences batched, reduced size, with
     each aggregation scan kernel."""
-    monkeypatch.setenv("TSGM_SCAN_KERNEL", scan)
+    monkeypatch.setenv("TSGM_SCAN_KERNEL", "lines" if scan == "lines" else "groups")
+    if scan != "lines":
+        monkeypatch.setenv("TSGM_SCAN_SPW", scan[len("groups"):])
     cfgs = [SceneConfig.baseline_config(1, width=320, height=120, focal=200.0, cx=159.5,
                                         cy=59.5, d_max=64, seed=s, n_movers=3) for s in range(3)]
     run_parity(port, cfgs, 10, tsgm.SgmParams(10, 120, 8, 0, 64),
@@ -209,10 +211,12 @@ def test_config3_fixed_window_sweep(port, half):
                                  min_range_halfwidth=half), check_volumes=True)
 
 
-@pytest.mark.parametrize("scan", ["groups", "lines"])
+@pytest.mark.parametrize("scan", ["groups32", "groups8", "lines"])
 def test_config3_full_range_d256(port, monkeypatch, scan):
     """Config 3's D=256 full-range baseline (p_init >= d_max^2/4)."""
-    monkeypatch.setenv("TSGM_SCAN_KERNEL", scan)
+    monkeypatch.setenv("TSGM_SCAN_KERNEL", "lines" if scan == "lines" else "groups")
+    if scan != "lines":
+        monkeypatch.setenv("TSGM_SCAN_SPW", scan[len("groups"):])
     cfg = SceneConfig.baseline_config(3, width=384, height=96, focal=240.0, cx=191.5, cy=47.5,
                                       d_max=256, seed=22)
     run_parity(port, [cfg], 2, tsgm.SgmParams(10, 120, 8, 0, 256),
