@@ -666,12 +666,13 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
             default: scan_lines_kernel<16><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
         }
     } else {
-        // scanlines per warp: enough warps to fill the GPU (148 SMs x 32 warps)
+        // scanlines per warp: more, thinner warps while the batch is small
+        // (measured on config 2: 8 up to 16 sequences, 16 at 32, 32 from 48)
         const char* fspw = std::getenv("TSGM_SCAN_SPW");
         int spw = 32;
         if (fspw) spw = std::atoi(fspw);
-        else if (batched_warps < 148 * 32 / 4) spw = 8;
-        else if (batched_warps < 148 * 32) spw = 16;
+        else if (batched_warps < 148 * 40) spw = 8;
+        else if (batched_warps < 148 * 80) spw = 16;
         if (spw != 8 && spw != 16) spw = 32;
         if (spw != 32) {
             sp.task_off[0] = 0;
