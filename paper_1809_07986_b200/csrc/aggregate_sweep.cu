@@ -633,8 +633,8 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
         sp.task_off[i + 1] = sp.task_off[i] + (lines + 31) / 32;
     }
-    // small batches or full-range frames: the line-group kernel; else the
-    // scanline-group kernel (throughput on reduced windows).
+    // up to ~5 sequences or full-range frames: the line-group kernel (measured
+    // crossover vs 8 scanlines per warp); else the scanline-group kernel.
     // TSGM_SCAN_KERNEL=lines|groups forces one (tests).
     const int qmax = (b.d_max + 3) / 4;
     int G = 1;
@@ -647,7 +647,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     batched_warps *= n;
     const char* force = std::getenv("TSGM_SCAN_KERNEL");
     const bool lines_mode =
-        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < 148 * 4);
+        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < 148 * 12);
     if (lines_mode) {
         const int lpw = 32 / G;
         sp.task_off[0] = 0;
