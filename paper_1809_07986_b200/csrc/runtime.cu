@@ -227,6 +227,11 @@ struct tsgm_ctx {
     void* snap[TSGM_OUT_COUNT]{};
     cudaEvent_t ev_snap_copied[TSGM_OUT_COUNT]{};
     bool snap_pending[TSGM_OUT_COUNT]{};
+    // Outputs written only by the frame's last kernel (correct_median: state,
+    // export map, diff, mask) are copied out directly from the live buffers;
+    // the next frame's correct_median waits for those copies instead.
+    cudaEvent_t ev_direct_copied = nullptr;
+    bool direct_pending = false;
     // box detector (tsgm_detect): per-slot SAT, candidate boxes and counts
     double* det_sat = nullptr;
     tsgm_box* det_boxes = nullptr;
@@ -261,6 +266,7 @@ struct tsgm_ctx {
         if (ev_frame) cudaEventDestroy(ev_frame);
         for (auto e : ev_snap_copied)
             if (e) cudaEventDestroy(e);
+        if (ev_direct_copied) cudaEventDestroy(ev_direct_copied);
         for (int i = 0; i < kImgBufs; ++i) {
             if (ev_img_ready[i]) cudaEventDestroy(ev_img_ready[i]);
             if (ev_img_free[i]) cudaEventDestroy(ev_img_free[i]);
@@ -304,6 +310,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     CK(cudaStreamCreateWithFlags(&ctx->up_st, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_frame, cudaEventDisableTiming));
     for (auto& e : ctx->ev_snap_copied) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_direct_copied, cudaEventDisableTiming));
     for (int i = 0; i < tsgm_ctx::kImgBufs; ++i) {
         CK(cudaEventCreateWithFlags(&ctx->ev_img_ready[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_img_free[i], cudaEventDisableTiming));
@@ -433,6 +440,14 @@ void upload_step(tsgm_ctx* ctx, int n, const int32_t* slots, const uint8_t* cons
     r.used = true;
 }
 
+// Before the compute stream overwrites a directly copied output (state,
+// export map, diff, mask), its pending copy-out must have finished.
+void wait_direct_copies(tsgm_ctx* ctx) {
+    if (!ctx->direct_pending) return;
+    CK(cudaStreamWaitEvent(ctx->st, ctx->ev_direct_copied, 0));
+    ctx->direct_pending = false;
+}
+
 void check_slots(tsgm_ctx* ctx, int n, const int32_t* slots) {
     if (n < 1 || n > ctx->max_slots) bad("tsgm_step: n out of range");
     std::vector<char> seen(ctx->max_slots, 0);
@@ -516,6 +531,7 @@ void run_step(tsgm_ctx* ctx, int n) {
         c0 += m;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
+    wait_direct_copies(ctx);  // the previous frame's outputs may still be copying out
     launch_correct_median(b, n, c.filter.r, c.mask_tau, L);
     for (int i = 0; i < n; ++i) ctx->fresh[ctx->h_slots[i]] = 0;
     CK(cudaGetLastError());
@@ -647,6 +663,7 @@ int tsgm_reset(tsgm_ctx* ctx, int32_t slot) {
     return guarded([&] {
         if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_reset: slot out of range");
         CK(cudaSetDevice(ctx->device));
+        wait_direct_copies(ctx);
         const size_t P = ctx->P;
         CK(cudaMemsetAsync(ctx->b.sd + slot * P, 0, 8 * P, ctx->st));
         CK(cudaMemsetAsync(ctx->b.sp + slot * P, 0, 8 * P, ctx->st));
@@ -660,6 +677,7 @@ int tsgm_set_state(tsgm_ctx* ctx, int32_t slot, const double* d, const double* p
     return guarded([&] {
         if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_set_state: slot out of range");
         CK(cudaSetDevice(ctx->device));
+        wait_direct_copies(ctx);
         ctx->fresh[slot] = 0;  // a caller state may hold valid pixels: reduced windows
         const size_t P = ctx->P;
         if (d) h2d(ctx, ctx->b.sd + slot * P, d, P);
@@ -735,9 +753,15 @@ int tsgm_fetch_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t wha
         for (int i = 0; i < n; ++i)
             if (slots[i] < 0 || slots[i] >= ctx->max_slots) bad("tsgm_fetch_batch: slot out of range");
         const size_t bytes = o.stride * o.elem;
-        if (!ctx->snap[what]) ctx->snap[what] = ctx->dalloc<char>(bytes * ctx->max_slots);
-        // the kind's previous copy-out must have left the snapshot
-        if (ctx->snap_pending[what]) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_snap_copied[what], 0));
+        const bool direct = what == TSGM_OUT_STATE_D || what == TSGM_OUT_STATE_P ||
+                            what == TSGM_OUT_STATE_VALID || what == TSGM_OUT_EXPORT_D ||
+                            what == TSGM_OUT_EXPORT_VALID || what == TSGM_OUT_DIFF ||
+                            what == TSGM_OUT_MASK;
+        if (!direct) {
+            if (!ctx->snap[what]) ctx->snap[what] = ctx->dalloc<char>(bytes * ctx->max_slots);
+            // the kind's previous copy-out must have left the snapshot
+            if (ctx->snap_pending[what]) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_snap_copied[what], 0));
+        }
         // runs of consecutive slots with contiguous destinations: one copy each
         std::vector<std::pair<int, int>> runs;  // (first batch index, length)
         for (int i = 0; i < n; ++i) {
@@ -752,21 +776,28 @@ int tsgm_fetch_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t wha
             }
             runs.push_back({i, 1});
         }
-        char* snap = static_cast<char*>(ctx->snap[what]);
-        for (auto& r : runs) {
-            const size_t at = static_cast<size_t>(slots[r.first]) * bytes;
-            CK(cudaMemcpyAsync(snap + at, static_cast<const char*>(o.base) + at, bytes * r.second,
-                               cudaMemcpyDeviceToDevice, ctx->st));
-        }
+        const char* src = direct ? static_cast<const char*>(o.base) : static_cast<char*>(ctx->snap[what]);
+        if (!direct)
+            for (auto& r : runs) {
+                const size_t at = static_cast<size_t>(slots[r.first]) * bytes;
+                CK(cudaMemcpyAsync(ctx->snap[what] ? static_cast<char*>(ctx->snap[what]) + at : nullptr,
+                                   static_cast<const char*>(o.base) + at, bytes * r.second,
+                                   cudaMemcpyDeviceToDevice, ctx->st));
+            }
         CK(cudaEventRecord(ctx->ev_frame, ctx->st));
         CK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_frame, 0));
         for (auto& r : runs) {
             const size_t at = static_cast<size_t>(slots[r.first]) * bytes;
-            CK(cudaMemcpyAsync(dsts[r.first], snap + at, bytes * r.second, cudaMemcpyDeviceToHost,
+            CK(cudaMemcpyAsync(dsts[r.first], src + at, bytes * r.second, cudaMemcpyDeviceToHost,
                                ctx->copy_st));
         }
-        CK(cudaEventRecord(ctx->ev_snap_copied[what], ctx->copy_st));
-        ctx->snap_pending[what] = true;
+        if (direct) {
+            CK(cudaEventRecord(ctx->ev_direct_copied, ctx->copy_st));
+            ctx->direct_pending = true;
+        } else {
+            CK(cudaEventRecord(ctx->ev_snap_copied[what], ctx->copy_st));
+            ctx->snap_pending[what] = true;
+        }
     });
 }
 
