@@ -33,7 +33,6 @@ struct Bufs {
     // warp keys (A6) and warp output (pre reject/fill)
     unsigned long long* kd;  // [slot][P] winning d' key (atomicMax)
     ulonglong2* kps;         // [slot][P] (p key, source-d key), lexicographic min (128-bit CAS)
-    uint8_t* kcol;           // [slot][P] target hit by more than one source this frame
     int* wtgt;               // [slot][P] pass-1 target pixel of each source (-1: dropped)
     unsigned long long* wdk; // [slot][P] pass-1 d' key of each source
     double *wd, *wp, *wsrc;

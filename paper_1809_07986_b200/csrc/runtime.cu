@@ -329,7 +329,6 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.sv = ctx->dalloc<uint8_t>(S * P);
     b.kd = ctx->dalloc<unsigned long long>(S * P);
     b.kps = ctx->dalloc<ulonglong2>(S * P);
-    b.kcol = ctx->dalloc<uint8_t>(S * P);
     b.wtgt = ctx->dalloc<int>(S * P);
     b.wdk = ctx->dalloc<unsigned long long>(S * P);
     b.wd = ctx->dalloc<double>(S * P);
@@ -410,7 +409,6 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     CK(cudaMemsetAsync(b.sv, 0, S * P, ctx->st));
     CK(cudaMemsetAsync(b.kd, 0, sizeof(unsigned long long) * S * P, ctx->st));
     CK(cudaMemsetAsync(b.kps, 0xff, sizeof(ulonglong2) * S * P, ctx->st));
-    CK(cudaMemsetAsync(b.kcol, 0, S * P, ctx->st));
     CK(cudaMemsetAsync(b.ncells, 0, sizeof(unsigned long long) * S, ctx->st));
     for (auto& r : ctx->ring) {
         CK(cudaMallocHost(&r.slots, sizeof(int) * S));

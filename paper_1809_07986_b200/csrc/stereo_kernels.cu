@@ -7,12 +7,9 @@
 namespace tsgm {
 
 // ---------------------------------------------------------------- census (A12)
-// census_transform, matching_cost.cpp:53-79. A 32x8 thread block covers a
-// 64x8 pixel tile, two horizontally adjacent pixels per thread sharing the
-// 5x6 neighbourhood they read; the 68x12 input tile (2-px halo) is staged in
-// shared memory. Bit order: (dy, dx) in raster order, centre skipped, bit 23
-// = (-2,-2).
-constexpr int kCtW = 64, kCtH = 8;
+// census_transform, matching_cost.cpp:53-79. One thread per pixel of a
+// 32x8 tile; the 36x12 input tile (2-px halo) is staged in shared memory.
+constexpr int kCtW = 32, kCtH = 8;
 
 __global__ void census_kernel(Bufs b) {
     __shared__ uint8_t tile[kCtH + 4][kCtW + 4];
@@ -21,38 +18,31 @@ __global__ void census_kernel(Bufs b) {
     const uint8_t* img = which ? b.right[a] : b.left[a];
     uint32_t* sig = (which ? b.sigr : b.sigl) + static_cast<size_t>(s) * b.P;
     const int x0 = blockIdx.x * kCtW - 2, y0 = blockIdx.y * kCtH - 2;
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
-    for (int i = tid; i < (kCtH + 4) * (kCtW + 4); i += nt) {
+    for (int i = threadIdx.y * kCtW + threadIdx.x; i < (kCtH + 4) * (kCtW + 4); i += kCtW * kCtH) {
         const int ty = i / (kCtW + 4), tx = i % (kCtW + 4);
         const int gx = x0 + tx, gy = y0 + ty;
         tile[ty][tx] = (gx >= 0 && gx < b.W && gy >= 0 && gy < b.H) ? img[gy * b.W + gx] : 0;
     }
     __syncthreads();
-    const int lx = 2 * threadIdx.x, x = blockIdx.x * kCtW + lx, y = blockIdx.y * kCtH + threadIdx.y;
+    const int x = blockIdx.x * kCtW + threadIdx.x, y = blockIdx.y * kCtH + threadIdx.y;
     if (x >= b.W || y >= b.H) return;
-    uint8_t w[5][6];
+    uint32_t v = 0;
+    if (census_defined(x, y, b.W, b.H)) {
+        const uint8_t c = tile[threadIdx.y + 2][threadIdx.x + 2];
 #pragma unroll
-    for (int dy = 0; dy < 5; ++dy)
+        for (int dy = 0; dy < 5; ++dy)
 #pragma unroll
-        for (int dx = 0; dx < 6; ++dx) w[dy][dx] = tile[threadIdx.y + dy][lx + dx];
-    uint32_t v0 = 0, v1 = 0;
-    const uint8_t c0 = w[2][2], c1 = w[2][3];
-#pragma unroll
-    for (int dy = 0; dy < 5; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 5; ++dx) {
-            if (dx == 2 && dy == 2) continue;
-            v0 = (v0 << 1) | (w[dy][dx] < c0 ? 1u : 0u);
-            v1 = (v1 << 1) | (w[dy][dx + 1] < c1 ? 1u : 0u);
-        }
-    const size_t o = static_cast<size_t>(y) * b.W + x;
-    sig[o] = census_defined(x, y, b.W, b.H) ? v0 : 0u;
-    if (x + 1 < b.W) sig[o + 1] = census_defined(x + 1, y, b.W, b.H) ? v1 : 0u;
+            for (int dx = 0; dx < 5; ++dx) {
+                if (dx == 2 && dy == 2) continue;
+                v = (v << 1) | (tile[threadIdx.y + dy][threadIdx.x + dx] < c ? 1u : 0u);
+            }
+    }
+    sig[y * b.W + x] = v;
 }
 
 void launch_census(const Bufs& b, int n, Launch L) {
     dim3 grid((b.W + kCtW - 1) / kCtW, (b.H + kCtH - 1) / kCtH, 2 * n);
-    census_kernel<<<grid, dim3(kCtW / 2, kCtH), 0, L.st>>>(b);
+    census_kernel<<<grid, dim3(kCtW, kCtH), 0, L.st>>>(b);
     ++*L.counter;
 }
 

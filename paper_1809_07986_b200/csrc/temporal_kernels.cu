@@ -16,8 +16,7 @@ namespace tsgm {
 // key; pass 2, for sources whose d' equals the winner, takes the
 // lexicographic minimum of (p key, source-d key) with a 128-bit CAS loop.
 // Keys are order-preserving u64 images of the doubles, so the result is exact
-// and independent of thread order. Targets reached by a single source (most
-// of them) skip the CAS: pass 1 flags every target a second source reaches.
+// and independent of thread order.
 struct Mapped {
     int t;  // target pixel index, -1 if dropped
     double dp;
@@ -56,8 +55,7 @@ __global__ void warp_map_kernel(Bufs b, const double* src_d, const uint8_t* src_
         if (m.t >= 0) {
             tgt = m.t;
             kd = ord_key(m.dp);
-            // every source but the first to reach the target sees a non-armed key
-            if (atomicMax(&b.kd[base + m.t], kd) != 0ull) b.kcol[base + m.t] = 1;
+            atomicMax(&b.kd[base + m.t], kd);
         }
     }
     b.wtgt[base + i] = tgt;
@@ -93,10 +91,6 @@ __global__ void warp_tiebreak_kernel(Bufs b, const double* src_d, const double* 
     if (b.kd[t] != b.wdk[base + i]) return;
     const ulonglong2 mine = make_ulonglong2(ord_key(src_p[base + i]), ord_key(src_d[base + i]));
     ulonglong2* addr = b.kps + t;
-    if (!b.kcol[t]) {  // the only source of this target: no competitor, plain store
-        *addr = mine;
-        return;
-    }
     // start from the armed value: only the CAS reads the pair atomically (a
     // plain 16-byte load may tear and hide a smaller pair)
     ulonglong2 cur = make_ulonglong2(~0ull, ~0ull);
@@ -143,7 +137,6 @@ __global__ void predict_finalize_kernel(Bufs b, double q, int apply_phi) {
             }
         }
         b.kps[t] = make_ulonglong2(~0ull, ~0ull);
-        b.kcol[t] = 0;
     }
     b.wd[t] = d;
     b.wp[t] = p;
