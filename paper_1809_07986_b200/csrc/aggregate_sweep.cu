@@ -56,6 +56,9 @@ struct ScanParams {
     int dx[8], dy[8];        // predecessor offsets of the active directions
     int task_off[9];         // prefix of warp tasks per direction (per slot)
     int n;                   // active slots
+    int full_ok;             // ceil(d_max/4) is a power of two >= 8: full windows take scan_pixel_full
+    uint32_t full_lohi;      // lohi of a full-range window: 0 | (d_max - 1) << 16
+    uint32_t full_rng;       // quad range of a full-range window: 0 | (qmax - 1) << 16
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
@@ -198,6 +201,81 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     if (pix && lg == 0) sts32(rp, static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16));
 }
 
+// scan_pixel for a full-range window [0, d_max-1] with 4G = ceil(d_max/4)
+// quads (every lane's 16 levels valid): no masks, no poison, and when the
+// predecessor's window was full range as well its words are used unchecked —
+// the slot's guard words (quads -1 and qmax) hold P2, which is what the masked
+// path reads there. Same arithmetic as scan_pixel<G, 4>.
+template <int G>
+__device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, bool has_pred,
+                                                uint32_t sb, uint32_t rp, const uint8_t* cost,
+                                                uint32_t* out, uint32_t P1x2, uint32_t P2x2,
+                                                uint32_t P2x4, uint32_t full_rng) {
+    constexpr int Q = 4;
+    const int lg = static_cast<int>(threadIdx.x & (G - 1));
+    const int a0 = lg * Q;
+    uint32_t CA[Q], CB[Q], LA[Q], LB[Q];
+    {
+        // (a group without a pixel reads the volume's first window instead: in bounds)
+        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + (pix ? pm.cell : 0u) + 4 * a0;
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+        const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
+        uint32_t c[Q + 1];
+#pragma unroll
+        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
+#pragma unroll
+        for (int t = 0; t < Q; ++t) {
+            const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
+            CA[t] = prmt(cq, 0u, 0x4140u);
+            CB[t] = prmt(cq, 0u, 0x4342u);
+        }
+    }
+    const uint32_t prng = lds32(rp);
+    uint32_t w[Q + 2];
+    if (prng == full_rng) {
+#pragma unroll
+        for (int u = 0; u < Q + 2; ++u) {
+            const uint32_t raw = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
+            w[u] = has_pred ? raw : 0u;
+        }
+    } else {
+        const int pq0 = static_cast<int>(prng & 0xffffu);
+        const uint32_t span = (prng >> 16) - static_cast<uint32_t>(pq0);
+#pragma unroll
+        for (int u = 0; u < Q + 2; ++u) {
+            const uint32_t raw = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
+            const bool in = static_cast<uint32_t>(a0 - 1 + u - pq0) <= span;
+            w[u] = has_pred ? (in ? raw : P2x4) : 0u;
+        }
+    }
+    uint32_t mn = 0xffffffffu;
+    uint32_t mma = prmt(w[0], prmt(w[1], 0u, 0x4140u), 0x5453u);
+#pragma unroll
+    for (int t = 0; t < Q; ++t) {
+        const uint32_t e0 = prmt(w[t + 1], 0u, 0x4140u);
+        const uint32_t e1 = prmt(w[t + 1], 0u, 0x4342u);
+        const uint32_t mpa = prmt(w[t + 1], 0u, 0x4241u);
+        const uint32_t mpb = prmt(e1, w[t + 2], 0x1432u);
+        LA[t] = mad_u32(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, e0), 1u, CA[t]);
+        LB[t] = mad_u32(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, e1), 1u, CB[t]);
+        mn = __vimin3_u16x2(mn, LA[t], LB[t]);
+        mma = mpb;
+    }
+    const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
+    const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
+    if (G > 1) __syncwarp();
+    if (pix) {
+#pragma unroll
+        for (int t = 0; t < Q; ++t) {
+            const uint32_t ma = __viaddmin_u16x2(LA[t], neg, P2x2);
+            const uint32_t mb = __viaddmin_u16x2(LB[t], neg, P2x2);
+            sts32(sb + 4u + 4u * static_cast<uint32_t>(a0 + t), prmt(ma, mb, 0x6420u));
+            out[pm.qo + static_cast<uint32_t>(a0 + t)] = prmt(LA[t], LB[t], 0x6420u);
+        }
+        if (lg == 0) sts32(rp, full_rng);
+    }
+}
+
 // invalid-level masks: entry (lrel, hrel) covers 16 levels = 4 quads x
 // (ivA, ivB); level j is invalid iff j < lrel or j > hrel (hrel in -1..16)
 __device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
@@ -248,6 +326,11 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
+    if (lgs == 0) {  // guard words of the scanline's slot: quads -1 and qmax read as P2
+        const int qmax = (b.d_max + 3) / 4;
+        sts32(my_sb, P2x4);
+        sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
+    }
 
     const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
     uint32_t* out = reinterpret_cast<uint32_t*>(
@@ -337,7 +420,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         }
         // wider windows: groups of G lanes x 4 quads, 32/G windows per pass;
         // a window's owner is the first lane of its scanline's group
-        const auto wide = [&](auto gtag, unsigned bw) {
+        const auto wide = [&](auto gtag, unsigned bw, bool full) {
             constexpr int G = decltype(gtag)::value;
             constexpr int PER = 32 / G;
             const int gi = lane / G;
@@ -357,20 +440,37 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
                 const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
                 const uint32_t sline = static_cast<uint32_t>(src / GN);
-                scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, cost, out,
-                                 P1x2, P2x2, P2x4, mask_tab);
+                if (full)
+                    scan_pixel_full<G>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, cost,
+                                       out, P1x2, P2x2, P2x4, sp.full_rng);
+                else
+                    scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, cost,
+                                     out, P1x2, P2x2, P2x4, mask_tab);
                 bw &= ~done;
             }
         };
+        // full-range windows (when their class covers them exactly) take the
+        // unmasked pass
         const bool owner = active && lgs == 0;
-        const unsigned b2 = __ballot_sync(0xffffffffu, owner && nq > 4 && nq <= 8);
-        if (b2) wide(std::integral_constant<int, 2>{}, b2);
-        const unsigned b4 = __ballot_sync(0xffffffffu, owner && nq > 8 && nq <= 16);
-        if (b4) wide(std::integral_constant<int, 4>{}, b4);
-        const unsigned b8 = __ballot_sync(0xffffffffu, owner && nq > 16 && nq <= 32);
-        if (b8) wide(std::integral_constant<int, 8>{}, b8);
-        const unsigned b16 = __ballot_sync(0xffffffffu, owner && nq > 32);
-        if (b16) wide(std::integral_constant<int, 16>{}, b16);
+        const bool fullw = sp.full_ok && mc.lohi == sp.full_lohi;
+        const unsigned bf = __ballot_sync(0xffffffffu, owner && fullw);
+        const bool part = owner && !fullw;
+        const unsigned b2 = __ballot_sync(0xffffffffu, part && nq > 4 && nq <= 8);
+        if (b2) wide(std::integral_constant<int, 2>{}, b2, false);
+        const unsigned b4 = __ballot_sync(0xffffffffu, part && nq > 8 && nq <= 16);
+        if (b4) wide(std::integral_constant<int, 4>{}, b4, false);
+        const unsigned b8 = __ballot_sync(0xffffffffu, part && nq > 16 && nq <= 32);
+        if (b8) wide(std::integral_constant<int, 8>{}, b8, false);
+        const unsigned b16 = __ballot_sync(0xffffffffu, part && nq > 32);
+        if (b16) wide(std::integral_constant<int, 16>{}, b16, false);
+        if (bf) {
+            switch (sp.full_ok) {  // = 4G of the full window's class
+                case 8: wide(std::integral_constant<int, 2>{}, bf, true); break;
+                case 16: wide(std::integral_constant<int, 4>{}, bf, true); break;
+                case 32: wide(std::integral_constant<int, 8>{}, bf, true); break;
+                default: wide(std::integral_constant<int, 16>{}, bf, true); break;
+            }
+        }
         prev_active = active;
     }
 }
@@ -409,6 +509,11 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
+    if ((lane & (G - 1)) == 0) {  // guard words of the scanline's slot
+        const int qmax = (b.d_max + 3) / 4;
+        sts32(my_sb, P2x4);
+        sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
+    }
     const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.vol_slots + a) * b.quad_cap * 4);
@@ -461,8 +566,15 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
             prev_active = false;
             continue;
         }
-        scan_pixel<G, 4>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                         mask_tab);
+        // the unmasked pass when every active scanline of the warp has a full
+        // window of the class size (frames from an empty state)
+        const bool fullw = sp.full_ok == 4 * G && mc.lohi == sp.full_lohi;
+        if (__all_sync(0xffffffffu, fullw || !active))
+            scan_pixel_full<G>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                               sp.full_rng);
+        else
+            scan_pixel<G, 4>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                             mask_tab);
         prev_active = active;
     }
 }
@@ -628,6 +740,13 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     if (paths == 8 || path_set == 1)
         for (int i = 0; i < 4; ++i, ++k) { sp.dx[k] = diag[i][0]; sp.dy[k] = diag[i][1]; }
     sp.ndir = k;
+    {
+        const int qm = (b.d_max + 3) / 4;
+        const bool pow2 = (qm & (qm - 1)) == 0;
+        sp.full_ok = (b.d_max % 4 == 0 && pow2 && qm >= 8 && qm <= 64) ? qm : 0;
+        sp.full_lohi = static_cast<uint32_t>(b.d_max - 1) << 16;
+        sp.full_rng = static_cast<uint32_t>(qm - 1) << 16;
+    }
     sp.task_off[0] = 0;
     for (int i = 0; i < k; ++i) {
         const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
