@@ -764,9 +764,10 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         batched_warps += (lines + 31) / 32;
     }
     batched_warps *= n;
+    const int sms = b.num_sms > 0 ? b.num_sms : 148;  // thresholds measured on a 148-SM B200
     const char* force = std::getenv("TSGM_SCAN_KERNEL");
     const bool lines_mode =
-        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < 148 * 12);
+        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < sms * 12);
     if (lines_mode) {
         const int lpw = 32 / G;
         sp.task_off[0] = 0;
@@ -790,8 +791,8 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const char* fspw = std::getenv("TSGM_SCAN_SPW");
         int spw = 32;
         if (fspw) spw = std::atoi(fspw);
-        else if (batched_warps < 148 * 40) spw = 8;
-        else if (batched_warps < 148 * 80) spw = 16;
+        else if (batched_warps < sms * 40) spw = 8;
+        else if (batched_warps < sms * 80) spw = 16;
         if (spw != 8 && spw != 16) spw = 32;
         if (spw != 32) {
             sp.task_off[0] = 0;

@@ -63,6 +63,7 @@ struct Bufs {
     uint8_t* pdir;
     size_t quad_cap;  // quads per volume position
     int max_slots;
+    int num_sms;     // of the context's device (kernel-choice thresholds)
     int* work;
     // WTA, render, export (A15, A18, A19)
     int32_t *md, *rd, *ed;

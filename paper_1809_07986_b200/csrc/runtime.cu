@@ -361,6 +361,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.max_slots = c.max_slots;
     b.work = ctx->dalloc<int>(1);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device));
+    b.num_sms = ctx->num_sms;
     b.md = ctx->dalloc<int32_t>(S * P);
     b.rd = ctx->dalloc<int32_t>(S * P);
     b.ed = ctx->dalloc<int32_t>(S * P);
