@@ -589,6 +589,9 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
 // atomicMin (the key (S << 16 | level) makes the minimum the first argmin);
 // then lane = pixel writes the WTA result.
 constexpr int kCwWarps = 2;
+#ifndef CW_LEAN_MINB
+#define CW_LEAN_MINB 20
+#endif
 
 // per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
 // best[32] (u32), qsum[32*qmax] (uint2, sub-pixel only)
@@ -611,9 +614,13 @@ __device__ __forceinline__ float subpixel_of(int d, int sm1, int s0, int sp1, bo
     return __fadd_rn(static_cast<float>(d), off);
 }
 
-template <int NDIR>
-__global__ void __launch_bounds__(32 * kCwWarps, 16) combine_wta_kernel(Bufs b, int n, int write_s,
-                                                                    int do_wta, int subpix) {
+// kLean: the production step's variant (WTA only: no S, no sub-pixel) —
+// compiled without those paths it needs fewer registers and runs more warps.
+template <int NDIR, bool kLean>
+__global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : 16)
+    combine_wta_kernel(Bufs b, int n, int write_s_in, int do_wta_in, int subpix_in) {
+    const int write_s = kLean ? 0 : write_s_in, do_wta = kLean ? 1 : do_wta_in;
+    const int subpix = kLean ? 0 : subpix_in;
     extern __shared__ __align__(16) uint8_t cwm[];
     const int W = b.W, H = b.H;
     const int qmax = (b.d_max - 1) / 4 + 1;
@@ -685,7 +692,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, 16) combine_wta_kernel(Bufs b, 
             qsum[l * qmax + k] = make_uint2((se & 0xffffu) | (so << 16), (se >> 16) | (so & 0xffff0000u));
     };
     uint32_t q = static_cast<uint32_t>(lane);
-    for (; q + 32 < nq; q += 64) {
+    for (; !kLean && q + 32 < nq; q += 64) {
         uint32_t w0[NDIR], w1[NDIR];
 #pragma unroll
         for (int d = 0; d < NDIR; ++d) {
@@ -695,7 +702,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, 16) combine_wta_kernel(Bufs b, 
         finish(q, w0);
         finish(q + 32, w1);
     }
-    if (q < nq) {
+    for (; q < nq; q += 32) {  // (lean: one quad per lane and iteration, fewer registers)
         uint32_t w0[NDIR];
 #pragma unroll
         for (int d = 0; d < NDIR; ++d) w0[d] = __ldg(pd + d * dstride + qbase + q);
@@ -809,12 +816,15 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         else scan_kernel<32><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
     }
     const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
-    auto kern = k == 8 ? combine_wta_kernel<8> : combine_wta_kernel<4>;
-    static size_t cw_set[2] = {48 * 1024, 48 * 1024};  // opt in once per variant
-    if (cwsmem > cw_set[k == 8]) {
+    const bool lean = !write_s && do_wta && !subpix;
+    auto kern = k == 8 ? (lean ? combine_wta_kernel<8, true> : combine_wta_kernel<8, false>)
+                       : (lean ? combine_wta_kernel<4, true> : combine_wta_kernel<4, false>);
+    static size_t cw_set[4] = {48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024};  // opt in once per variant
+    const int vi = (k == 8 ? 2 : 0) + (lean ? 1 : 0);
+    if (cwsmem > cw_set[vi]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(cwsmem));
-        cw_set[k == 8] = cwsmem;
+        cw_set[vi] = cwsmem;
     }
     const long long warps = static_cast<long long>((b.W + 31) / 32) * b.H * n;
     kern<<<static_cast<unsigned>((warps + kCwWarps - 1) / kCwWarps), 32 * kCwWarps, cwsmem, L.st>>>(
