@@ -158,7 +158,7 @@ void launch_predict_finalize(const Bufs& b, int n, double q, int apply_phi, Laun
 // Tiled: the (32+4) x (8+4) input tile is staged in shared memory, the
 // rejection verdict is computed once for the (32+2) x (8+2) ring the fill
 // needs, then the 32 x 8 outputs.
-constexpr int kRfW = 32, kRfH = 16;
+constexpr int kRfW = 32, kRfH = 8;
 
 __global__ void reject_fill_kernel(Bufs b, const double* in_d, const double* in_p,
                                    const uint8_t* in_v, double* out_d, double* out_p,
@@ -312,7 +312,7 @@ void launch_correct(const Bufs& b, int n, double r, double mask_tau, Launch L) {
 // its own pixels, and takes the 3x3 lower median of the rendered map from
 // shared memory (median_kernel's keys: INT32_MAX for invalid or missing) —
 // the rendered map never goes to HBM.
-constexpr int kCmW = 32, kCmH = 16;
+constexpr int kCmW = 32, kCmH = 8;
 
 __device__ __forceinline__ void cm_swap(int32_t& a, int32_t& b) {
     const int32_t lo = min(a, b), hi = max(a, b);
