@@ -85,7 +85,8 @@ def load():
     """The product library; raises if it is not built (no fallback)."""
     global _lib
     if _lib is None:
-        path = lib_path("libtsgm_b200.so")
+        # TSGM_LIB_VARIANT=<suffix> loads libtsgm_b200<suffix>.so (kernel-tuning builds)
+        path = lib_path(f"libtsgm_b200{os.environ.get('TSGM_LIB_VARIANT', '')}.so")
         if not os.path.exists(path):
             raise RuntimeError(
                 f"{path} is missing: the CUDA path is required (run __graft_entry__.build())")
