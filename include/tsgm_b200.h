@@ -290,6 +290,49 @@ int tsgm_count_outliers_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, in
                               const double* const* gt, const tsgm_outlier_options* opts,
                               int64_t* evaluated, int64_t* outliers);
 
+/* ------------------------------------------------------------------------
+ * Noise calibration on the GPU: the reference's
+ * estimate_process_noise / estimate_measurement_noise / accumulate_error_map
+ * (noise_calib.hpp:52-80, noise_calib.cpp:102-182). The reference passes a
+ * std::vector<SequenceFrame> (dataset.hpp:18-25); here n frames are n
+ * contiguous W x H maps (gt f64, gt > 0 = valid; images u8) and n row-major
+ * 3x4 camera-to-world poses (Pose, geometry.hpp:106). Counts are exact; the
+ * gated FP64 moments use a fixed GPU reduction order (deterministic, equal to
+ * the reference's raster-order sums up to FP64 reassociation).
+ * ------------------------------------------------------------------------ */
+/* CalibOptions (noise_calib.hpp:43-49) */
+typedef struct {
+    double outlier_gate_px, bin_width, q_floor;
+} tsgm_calib_options;
+
+/* NoiseEstimate + its ErrorHistogram (noise_calib.hpp:14-41, 51-55). */
+typedef struct {
+    double variance;          /* raw unbiased variance of the gated samples */
+    int64_t samples_used;     /* gated samples */
+    double lo, hi, bin_width; /* histogram layout: [-gate, gate) */
+    int64_t underflow, overflow, within_1px, total;
+    double sum, sum_sq;       /* gated moments */
+    int32_t n_bins;           /* in: capacity of counts; out: number of bins */
+    int64_t* counts;          /* caller buffer of tsgm_calib_bins() entries */
+} tsgm_noise_estimate;
+
+/* Number of histogram bins, ceil(2 * gate / bin_width); validates the options
+ * like CalibOptions::validate (noise_calib.cpp:60-67). */
+int tsgm_calib_bins(const tsgm_calib_options* opts, int32_t* n_bins);
+/* estimate_process_noise (noise_calib.cpp:102-128): n >= 2 frames. */
+int tsgm_estimate_process_noise(int32_t n_frames, int32_t w, int32_t h, const double* gt,
+                                const double* poses12, const tsgm_stereo_calib* calib,
+                                const tsgm_calib_options* opts, tsgm_noise_estimate* out);
+/* estimate_measurement_noise (noise_calib.cpp:130-147): full-range SGM per
+ * frame, every frame matched in isolation (batched on the GPU). */
+int tsgm_estimate_measurement_noise(int32_t n_frames, int32_t w, int32_t h, const uint8_t* left,
+                                    const uint8_t* right, const double* gt,
+                                    const tsgm_sgm_params* params, const tsgm_calib_options* opts,
+                                    tsgm_noise_estimate* out);
+/* accumulate_error_map (noise_calib.cpp:149-182): acc[W*H], bit-exact. */
+int tsgm_accumulate_error_map(int32_t n_frames, int32_t w, int32_t h, const double* gt,
+                              const double* poses12, const tsgm_stereo_calib* calib, double* acc);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,14 @@ class FilterConfig:
 
 
 @dataclass
+class CalibOpts:
+    """CalibOptions (noise_calib.hpp:43-49)."""
+    outlier_gate_px: float = 10.0
+    bin_width: float = 0.25
+    q_floor: float = 0.1
+
+
+@dataclass
 class DetectConfig:
     """DetectConfig (motion_detect.hpp:36-44)."""
     window_sizes: tuple = ((20, 20), (30, 30), (40, 40), (50, 50), (50, 75))
@@ -699,6 +707,166 @@ def _port_count_outliers(self, d, valid, gt, abs_thresh=3.0, rel_thresh=0.05, st
 
 
 Port.count_outliers = _port_count_outliers
+
+
+# ------------------------------------------------ noise calibration (row 4)
+# Results of both checkers: dict(variance, mean, within_1px (fraction),
+# samples_used, total, underflow, overflow, counts).
+def _nbins(opts):
+    import math
+    return int(math.ceil((2.0 * opts.outlier_gate_px) / opts.bin_width))
+
+
+def _opts3(opts):
+    return np.array([opts.outlier_gate_px, opts.bin_width, opts.q_floor], np.float64)
+
+
+def _ref_estimate(self, call, opts):
+    nb = _nbins(opts)
+    mom = np.zeros(3)
+    ints = np.zeros(5, np.int64)
+    counts = np.zeros(nb, np.int64)
+    self._c(call(_p(mom), _p(ints), _p(counts), nb))
+    return dict(variance=mom[0], mean=mom[1], within_1px=mom[2], samples_used=int(ints[0]),
+                total=int(ints[1]), underflow=int(ints[2]), overflow=int(ints[3]), counts=counts)
+
+
+def _ref_process_noise(self, gt, poses, calib, opts):
+    gt = _f64(gt)
+    n, h, w = gt.shape
+    poses = None if poses is None else _f64(poses)
+    c4 = np.array([calib.focal_px, calib.cx, calib.cy, calib.baseline_m])
+    o3 = _opts3(opts)
+    return _ref_estimate(self, lambda m, i, cn, nb: self.lib.ref_process_noise(
+        n, w, h, _p(gt), _p(poses), _p(c4), calib.width, calib.height, calib.d_max,
+        _p(o3), m, i, cn, nb), opts)
+
+
+def _ref_measurement_noise(self, left, right, gt, params, opts, threads=1):
+    left, right, gt = _u8(left), _u8(right), _f64(gt)
+    n, h, w = gt.shape
+    sp = np.array([params.p1, params.p2, params.paths, params.path_set, params.d_max], np.int32)
+    o3 = _opts3(opts)
+    return _ref_estimate(self, lambda m, i, cn, nb: self.lib.ref_measurement_noise(
+        n, w, h, _p(left), _p(right), _p(gt), _p(sp), threads, _p(o3), m, i, cn, nb), opts)
+
+
+def _ref_error_map(self, gt, poses, calib):
+    gt, poses = _f64(gt), _f64(poses)
+    n, h, w = gt.shape
+    c4 = np.array([calib.focal_px, calib.cx, calib.cy, calib.baseline_m])
+    acc = np.zeros((h, w))
+    self._c(self.lib.ref_accumulate_error_map(n, w, h, _p(gt), _p(poses), _p(c4), calib.width,
+                                              calib.height, calib.d_max, _p(acc)))
+    return acc
+
+
+def _ref_calib_report(self, path, left, right, gt, poses, calib, params, opts):
+    """write_calib_report of the reference's own estimates, run in a separate
+    process (oracle/report_driver.c): its iostreams crash inside Python."""
+    import tempfile
+    left, right, gt, poses = _u8(left), _u8(right), _f64(gt), _f64(poses)
+    n, h, w = gt.shape
+    hd = np.array([n, w, h, calib.width, calib.height, calib.d_max, params.p1, params.p2,
+                   params.paths, params.path_set, params.d_max], np.int32)
+    with tempfile.NamedTemporaryFile(suffix=".bin") as f:
+        for a in (hd, np.array([calib.focal_px, calib.cx, calib.cy, calib.baseline_m]),
+                  _opts3(opts), left, right, gt, poses):
+            f.write(np.ascontiguousarray(a).tobytes())
+        f.flush()
+        r = subprocess.run([os.path.join(REF_DIR, "report_driver"), f.name, str(path)],
+                           capture_output=True, text=True)
+    if r.returncode == 1:
+        raise ValueError(r.stderr.strip())
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr.strip() or f"report_driver failed ({r.returncode})")
+
+
+Reference.process_noise = _ref_process_noise
+Reference.measurement_noise = _ref_measurement_noise
+Reference.error_map = _ref_error_map
+Reference.calib_report = _ref_calib_report
+
+
+def _port_hist(self, es, uses, opts):
+    """ErrorHistogram over the (e, use) maps in order (or_error_hist)."""
+    nb = _nbins(opts)
+    counts = np.zeros(nb, np.int64)
+    tal = np.zeros(4, np.int64)
+    sums = np.zeros(2)
+    for e, u in zip(es, uses):
+        e, u = _f64(e), _u8(u)
+        self.lib.or_error_hist(_p(e), _p(u), C.c_size_t(e.size), C.c_double(-opts.outlier_gate_px),
+                               C.c_double(opts.outlier_gate_px), C.c_double(opts.bin_width),
+                               _p(counts), nb, _p(tal), _p(sums))
+    gated = int(tal[3])
+    total = gated + int(tal[0]) + int(tal[1])
+    var = 0.0
+    if gated >= 2:  # ErrorHistogram::variance, noise_calib.cpp:45-52
+        n = float(gated)
+        m = sums[0] / n
+        var = max((sums[1] - n * m * m) / (n - 1.0), 0.0)
+    return dict(variance=var, mean=sums[0] / gated if gated else 0.0,
+                within_1px=int(tal[2]) / total if total else 0.0, samples_used=gated,
+                total=total, underflow=int(tal[0]), overflow=int(tal[1]), counts=counts,
+                sum=sums[0], sum_sq=sums[1])
+
+
+def _port_warped_pairs(self, gt, poses, calib):
+    """state_from_gt of frame k-1 warped by relative_motion(k-1, k)
+    (noise_calib.cpp:71-78, 115-119) -> [(warped d, warped valid, gt k)]."""
+    gt, poses = _f64(gt), _f64(poses)
+    out = []
+    for k in range(1, gt.shape[0]):
+        R, t = self.relative_motion(poses[k - 1], poses[k])
+        H = self.homography(R, t, calib)
+        g = gt[k - 1]
+        v = (g > 0.0).astype(np.uint8)
+        d = np.where(v == 1, g, 0.0)
+        wd, _, wv, _ = self.warp(d, np.zeros_like(d), v, H, calib.d_max)
+        out.append((wd, wv, gt[k]))
+    return out
+
+
+def _port_process_noise(self, gt, poses, calib, opts):
+    pairs = _port_warped_pairs(self, gt, poses, calib)
+    r = _port_hist(self, [wd - g for wd, wv, g in pairs],
+                   [(wv == 1) & (g > 0.0) for wd, wv, g in pairs], opts)
+    if r["total"] == 0:
+        raise RuntimeError("estimate_process_noise: no overlapping valid pixels")
+    return r
+
+
+def _port_measurement_noise(self, left, right, gt, params, opts):
+    es, uses = [], []
+    for k in range(gt.shape[0]):
+        h, w = gt[k].shape
+        lo = np.zeros((h, w), np.uint16)
+        hi = np.full((h, w), params.d_max - 1, np.uint16)
+        d, v = self.sgm_match(left[k], right[k], lo, hi, params)
+        es.append(d.astype(np.float64) - gt[k])
+        uses.append((v == 1) & (gt[k] > 0.0))
+    r = _port_hist(self, es, uses, opts)
+    if r["total"] == 0:
+        raise RuntimeError("estimate_measurement_noise: no overlapping valid pixels")
+    return r
+
+
+def _port_error_map(self, gt, poses, calib):
+    acc = np.zeros(_f64(gt).shape[1:])
+    overlap = 0
+    for wd, wv, g in _port_warped_pairs(self, gt, poses, calib):
+        m = (wv == 1) & (g > 0.0)
+        acc[m] += np.abs(wd[m] - g[m])  # per pixel in pair order, as the reference
+        overlap += int(m.sum())
+    if overlap == 0:
+        raise RuntimeError("accumulate_error_map: no overlapping valid pixels")
+    return acc
+
+
+Port.process_noise = _port_process_noise
+Port.measurement_noise = _port_measurement_noise
+Port.error_map = _port_error_map
 
 
 _port = None

@@ -417,3 +417,107 @@ int ref_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Noise calibration (noise_calib.cpp), SURVEY §8(f) row 4. Frames: n
+// contiguous W x H maps; null image / gt / pose arrays leave the optional
+// fields empty (for the reference's own "missing GT / pose" errors).
+#include "tsgm/noise_calib.hpp"
+
+namespace {
+
+std::vector<SequenceFrame> make_frames(int n, int w, int h, const uint8_t* left,
+                                       const uint8_t* right, const double* gt,
+                                       const double* poses) {
+    const size_t P = static_cast<size_t>(w) * h;
+    std::vector<SequenceFrame> frames(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+        SequenceFrame& f = frames[static_cast<size_t>(k)];
+        f.index = k;
+        if (left) f.left = to_image(left + k * P, w, h);
+        if (right) f.right = to_image(right + k * P, w, h);
+        if (gt) f.gt_disp = to_image(gt + k * P, w, h);
+        if (poses) {
+            Pose p;
+            for (int i = 0; i < 12; ++i) p(i / 4, i % 4) = poses[12 * k + i];
+            f.pose = p;
+        }
+    }
+    return frames;
+}
+
+CalibOptions make_opts(const double* o3) {
+    CalibOptions o;
+    o.outlier_gate_px = o3[0];
+    o.bin_width = o3[1];
+    o.q_floor = o3[2];
+    return o;
+}
+
+// moments: variance, mean, fraction within 1 px; ints: samples_used, total,
+// underflow, overflow; counts: the bins (up to nbins)
+void put_estimate(const NoiseEstimate& e, double* moments, long long* ints, long long* counts,
+                  int nbins) {
+    moments[0] = e.variance;
+    moments[1] = e.hist.mean();
+    moments[2] = e.hist.fraction_within_1px();
+    ints[0] = e.samples_used;
+    ints[1] = e.hist.total();
+    ints[2] = e.hist.underflow;
+    ints[3] = e.hist.overflow;
+    ints[4] = static_cast<long long>(e.hist.counts.size());
+    for (size_t i = 0; i < e.hist.counts.size() && static_cast<int>(i) < nbins; ++i)
+        counts[i] = e.hist.counts[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_process_noise(int n, int w, int h, const double* gt, const double* poses,
+                      const double* calib4, int cw, int ch, int d_max, const double* opts3,
+                      double* moments, long long* ints, long long* counts, int nbins) {
+    return guarded([&] {
+        const NoiseEstimate e = estimate_process_noise(
+            make_frames(n, w, h, nullptr, nullptr, gt, poses), make_calib(calib4, cw, ch, d_max),
+            make_opts(opts3));
+        put_estimate(e, moments, ints, counts, nbins);
+    });
+}
+
+int ref_measurement_noise(int n, int w, int h, const uint8_t* left, const uint8_t* right,
+                          const double* gt, const int* sgm_params, int threads,
+                          const double* opts3, double* moments, long long* ints,
+                          long long* counts, int nbins) {
+    return guarded([&] {
+        const NoiseEstimate e =
+            estimate_measurement_noise(make_frames(n, w, h, left, right, gt, nullptr),
+                                       make_params(sgm_params), threads, make_opts(opts3));
+        put_estimate(e, moments, ints, counts, nbins);
+    });
+}
+
+int ref_accumulate_error_map(int n, int w, int h, const double* gt, const double* poses,
+                             const double* calib4, int cw, int ch, int d_max, double* acc) {
+    return guarded([&] {
+        const Image<double> m = accumulate_error_map(
+            make_frames(n, w, h, nullptr, nullptr, gt, poses), make_calib(calib4, cw, ch, d_max));
+        from_image(m, acc);
+    });
+}
+
+// Both estimates by the reference, then its write_calib_report.
+int ref_calib_report(const char* path, int n, int w, int h, const uint8_t* left,
+                     const uint8_t* right, const double* gt, const double* poses,
+                     const double* calib4, int cw, int ch, int d_max, const int* sgm_params,
+                     const double* opts3) {
+    return guarded([&] {
+        const auto frames = make_frames(n, w, h, left, right, gt, poses);
+        const CalibOptions o = make_opts(opts3);
+        const NoiseEstimate pe = estimate_process_noise(frames, make_calib(calib4, cw, ch, d_max), o);
+        const NoiseEstimate me = estimate_measurement_noise(frames, make_params(sgm_params), 1, o);
+        write_calib_report(path, pe, me, o);
+    });
+}
+
+}  // extern "C"

@@ -842,3 +842,22 @@ void or_count_outliers(const int32_t* d, const uint8_t* valid, const double* gt,
     *evaluated = ev;
     *outliers = out;
 }
+
+void or_error_hist(const double* e, const uint8_t* use, size_t n, double lo, double hi,
+                   double bw, long long* counts, int nbins, long long* tallies, double* sums) {
+    /* ErrorHistogram::add, noise_calib.cpp:16-33, samples in the reference's
+     * order (frames in order, each row-major) */
+    for (size_t i = 0; i < n; ++i) {
+        if (!use[i]) continue;
+        const double v = e[i];
+        if (fabs(v) <= 1.0) ++tallies[2];
+        if (v < lo) { ++tallies[0]; continue; }
+        if (v >= hi) { ++tallies[1]; continue; }
+        size_t bin = (size_t)((v - lo) / bw);
+        if (bin >= (size_t)nbins) bin = (size_t)nbins - 1;
+        ++counts[bin];
+        ++tallies[3];
+        sums[0] += v;
+        sums[1] += v * v;
+    }
+}

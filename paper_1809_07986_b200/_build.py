@@ -27,7 +27,7 @@ CUDA_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-f
               f"-I{INCLUDE}", f"-I{CSRC}"]
 
 CU_SOURCES = ["stereo_kernels.cu", "temporal_kernels.cu", "aggregate_kernels.cu",
-              "aggregate_sweep.cu", "detect.cu", "runtime.cu"]
+              "aggregate_sweep.cu", "detect.cu", "noise.cu", "runtime.cu"]
 
 
 def lib_path(name: str) -> str:

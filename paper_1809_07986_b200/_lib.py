@@ -58,8 +58,24 @@ EXPORTS = [
     "tsgm_correct", "tsgm_step_once",
     "tsgm_integral_image", "tsgm_detect_candidate_windows", "tsgm_greedy_merge",
     "tsgm_detect_moving_objects", "tsgm_detect", "tsgm_count_outliers",
-    "tsgm_count_outliers_batch",
+    "tsgm_count_outliers_batch", "tsgm_calib_bins", "tsgm_estimate_process_noise",
+    "tsgm_estimate_measurement_noise", "tsgm_accumulate_error_map",
 ]
+
+
+class CalibOptionsC(C.Structure):
+    """tsgm_calib_options (CalibOptions, noise_calib.hpp:43-49)."""
+    _fields_ = [("outlier_gate_px", C.c_double), ("bin_width", C.c_double),
+                ("q_floor", C.c_double)]
+
+
+class NoiseEstimateC(C.Structure):
+    """tsgm_noise_estimate (NoiseEstimate + ErrorHistogram, noise_calib.hpp:14-55)."""
+    _fields_ = [("variance", C.c_double), ("samples_used", C.c_int64), ("lo", C.c_double),
+                ("hi", C.c_double), ("bin_width", C.c_double), ("underflow", C.c_int64),
+                ("overflow", C.c_int64), ("within_1px", C.c_int64), ("total", C.c_int64),
+                ("sum", C.c_double), ("sum_sq", C.c_double), ("n_bins", C.c_int32),
+                ("counts", C.c_void_p)]
 
 
 class OutlierOptionsC(C.Structure):
@@ -126,6 +142,15 @@ def load():
                                             C.POINTER(C.c_int64)]
         lib.tsgm_count_outliers_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                                   C.c_void_p, oc, C.c_void_p, C.c_void_p]
+        co, ne = C.POINTER(CalibOptionsC), C.POINTER(NoiseEstimateC)
+        lib.tsgm_calib_bins.argtypes = [co, C.POINTER(C.c_int32)]
+        lib.tsgm_estimate_process_noise.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                                    C.c_void_p, C.POINTER(StereoCalibC), co, ne]
+        lib.tsgm_estimate_measurement_noise.argtypes = [
+            C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+            C.POINTER(SgmParamsC), co, ne]
+        lib.tsgm_accumulate_error_map.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                                  C.c_void_p, C.POINTER(StereoCalibC), C.c_void_p]
         _lib = lib
     return _lib
 

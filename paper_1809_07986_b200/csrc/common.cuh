@@ -155,6 +155,26 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
                             int write_s, int do_wta, Launch L, int subpix = 0,
                             bool full_range = false);
 
+// Noise calibration (noise.cu), SURVEY §8(f) row 4.
+struct HistSpec {
+    double lo, hi, bw;  // ErrorHistogram(lo, hi, bin_width), noise_calib.cpp:9-14
+    int nbins;
+};
+struct HistAcc {                   // device buffers, zeroed by the caller
+    unsigned long long* counts;    // [nbins]
+    unsigned long long* tallies;   // underflow, overflow, within 1 px, gated
+    double* partial;               // [hist_partial_doubles()]
+    double* sums;                  // gated sum, sum of squares (running over batches)
+};
+size_t hist_partial_doubles();
+void launch_gt_state(const Bufs& b, const double* gt, int n, Launch L);
+void launch_error_hist_warped(const Bufs& b, const double* gt, int n, const HistSpec& hs,
+                              const HistAcc& acc, Launch L);
+void launch_error_hist_wta(const Bufs& b, const double* gt, int n, const HistSpec& hs,
+                           const HistAcc& acc, Launch L);
+void launch_error_map(const Bufs& b, const double* gt, int n, double* acc,
+                      unsigned long long* overlap, Launch L);
+
 // Box detector (detect.cu), SURVEY §8(f) row 1.
 constexpr int kMaxDetectWindows = 16;
 struct DetectWindows {

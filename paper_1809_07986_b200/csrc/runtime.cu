@@ -1461,3 +1461,286 @@ int tsgm_count_outliers_batch(tsgm_ctx* ctx, int32_t n, const int32_t* slots, in
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- noise calibration
+// SURVEY §8(f) row 4 (noise_calib.cpp:102-182): the warp and full-range SGM
+// kernels of the step, batched over frames, plus the histogram / error-map
+// kernels of noise.cu.
+namespace {
+
+void calib_options_validate(const tsgm_calib_options* o) {  // noise_calib.cpp:60-67
+    if (!o) bad("CalibOptions: null options");
+    if (!(o->outlier_gate_px > 0.0)) bad("CalibOptions: outlier_gate_px must be positive");
+    if (!(o->bin_width > 0.0) || o->bin_width > o->outlier_gate_px) bad("CalibOptions: bad bin_width");
+    if (!(o->q_floor >= 0.0)) bad("CalibOptions: negative q_floor");
+}
+
+HistSpec hist_spec(const tsgm_calib_options* o) {  // ErrorHistogram(-gate, gate, bw), :9-14
+    HistSpec hs{};
+    hs.lo = -o->outlier_gate_px;
+    hs.hi = o->outlier_gate_px;
+    hs.bw = o->bin_width;
+    if (!(hs.hi > hs.lo) || !(hs.bw > 0.0)) bad("ErrorHistogram: bad bin layout");
+    const double nb = std::ceil((hs.hi - hs.lo) / hs.bw);
+    if (!(nb >= 1.0 && nb <= double(1 << 26))) bad("ErrorHistogram: bad bin layout");
+    hs.nbins = static_cast<int>(nb);
+    return hs;
+}
+
+constexpr int kNoiseBatch = 32;  // frames (or frame pairs) per batched launch
+
+// A context for the calibration stages: images, state and per-pixel buffers
+// for `slots` frames; volumes only when sgm is given (measurement noise).
+std::unique_ptr<tsgm_ctx> noise_ctx(int w, int h, int slots, const tsgm_sgm_params* sgm) {
+    tsgm_config c{};
+    c.width = w;
+    c.height = h;
+    c.max_slots = slots;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    c.device = dev;
+    const int dv = sgm ? sgm->d_max : 1;
+    c.calib = tsgm_stereo_calib{1.0, 0.0, 0.0, 1.0, w, h, dv};
+    c.sgm = sgm ? *sgm : tsgm_sgm_params{6, 65, 8, 0, dv};
+    c.mask_tau = 3.0;
+    c.vol_slots = sgm ? 0 : 1;
+    auto ctx = std::make_unique<tsgm_ctx>();
+    init_ctx(ctx.get(), c);
+    return ctx;
+}
+
+struct NoiseAccum {
+    HistSpec hs;
+    HistAcc acc;
+    tsgm_ctx* ctx;
+    NoiseAccum(tsgm_ctx* c, const HistSpec& h) : hs(h), ctx(c) {
+        acc.counts = c->dalloc<unsigned long long>(h.nbins);
+        acc.tallies = c->dalloc<unsigned long long>(4);
+        acc.partial = c->dalloc<double>(hist_partial_doubles());
+        acc.sums = c->dalloc<double>(2);
+        CK(cudaMemsetAsync(acc.counts, 0, sizeof(unsigned long long) * h.nbins, c->st));
+        CK(cudaMemsetAsync(acc.tallies, 0, sizeof(unsigned long long) * 4, c->st));
+        CK(cudaMemsetAsync(acc.sums, 0, sizeof(double) * 2, c->st));
+    }
+    // NoiseEstimate (noise_calib.cpp:91-99: finish) from the device tallies
+    void finish(tsgm_noise_estimate* out, const char* who) {
+        std::vector<unsigned long long> counts(hs.nbins);
+        unsigned long long tal[4];
+        double sums[2];
+        CK(cudaMemcpyAsync(counts.data(), acc.counts, sizeof(unsigned long long) * hs.nbins,
+                           cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(tal, acc.tallies, sizeof tal, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(sums, acc.sums, sizeof sums, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        CK(cudaGetLastError());
+        const long long gated = static_cast<long long>(tal[3]);
+        const long long total = gated + static_cast<long long>(tal[0] + tal[1]);
+        if (total == 0) throw std::runtime_error(std::string(who) + ": no overlapping valid pixels");
+        double var = 0.0;  // ErrorHistogram::variance, noise_calib.cpp:45-52
+        if (gated >= 2) {
+            const double n = static_cast<double>(gated);
+            const double m = sums[0] / n;
+            const double v = (sums[1] - n * m * m) / (n - 1.0);
+            var = v > 0.0 ? v : 0.0;
+        }
+        out->variance = var;
+        out->samples_used = gated;
+        out->lo = hs.lo;
+        out->hi = hs.hi;
+        out->bin_width = hs.bw;
+        out->underflow = static_cast<int64_t>(tal[0]);
+        out->overflow = static_cast<int64_t>(tal[1]);
+        out->within_1px = static_cast<int64_t>(tal[2]);
+        out->total = total;
+        out->sum = sums[0];
+        out->sum_sq = sums[1];
+        if (out->counts)
+            for (int k = 0; k < hs.nbins; ++k) out->counts[k] = static_cast<int64_t>(counts[k]);
+        out->n_bins = hs.nbins;
+    }
+};
+
+// Frame pairs (k, k+1), k = 0 .. n-2, in batches: slot i holds state_from_gt
+// of frame k0+i warped by relative_motion(pose k0+i, pose k0+i+1)
+// (noise_calib.cpp:115-119); fn(ctx, gt of frames k0+1 .., m) consumes them.
+template <typename Begin, typename Fn, typename End>
+void warp_gt_pairs(int n, int w, int h, const double* gt, const double* poses,
+                   const tsgm_stereo_calib& calib, Begin&& begin, Fn&& fn, End&& end) {
+    const size_t P = static_cast<size_t>(w) * h;
+    const int pairs = n - 1;
+    // validate every pair's motion + homography first (what the reference's
+    // loop would throw on)
+    std::vector<double> H(16 * static_cast<size_t>(pairs));
+    for (int k = 0; k < pairs; ++k) {
+        double r9[9], t3[3];
+        relative_motion(poses + 12 * k, poses + 12 * (k + 1), r9, t3);
+        homography(r9, t3, calib, &H[16 * static_cast<size_t>(k)]);
+    }
+    const int B = std::min(pairs, kNoiseBatch);
+    auto ctx = noise_ctx(w, h, B, nullptr);
+    tsgm_ctx* c = ctx.get();
+    double* dgt = c->dalloc<double>((B + 1) * P);
+    std::vector<int> slots(B);
+    for (int i = 0; i < B; ++i) slots[i] = i;
+    std::vector<const uint8_t*> img(B, c->d_img);
+    begin(c);
+    for (int k0 = 0; k0 < pairs; k0 += B) {
+        const int m = std::min(B, pairs - k0);
+        h2d(c, dgt, gt + static_cast<size_t>(k0) * P, (m + 1) * P);
+        upload_step(c, m, slots.data(), img.data(), img.data(), &H[16 * static_cast<size_t>(k0)]);
+        Launch L = c->L();
+        launch_gt_state(c->b, dgt, m, L);
+        launch_warp(c->b, m, c->b.sd, c->b.sp, c->b.sv, calib.d_max, L);
+        launch_predict_finalize(c->b, m, 0.0, 0, L);
+        fn(c, dgt + P, m);
+        CK(cudaStreamSynchronize(c->st));  // dgt is overwritten by the next batch
+    }
+    end(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsgm_calib_bins(const tsgm_calib_options* opts, int32_t* n_bins) {
+    return guarded([&] {
+        calib_options_validate(opts);
+        if (!n_bins) bad("tsgm_calib_bins: null argument");
+        *n_bins = hist_spec(opts).nbins;
+    });
+}
+
+int tsgm_estimate_process_noise(int32_t n_frames, int32_t w, int32_t h, const double* gt,
+                                const double* poses12, const tsgm_stereo_calib* calib,
+                                const tsgm_calib_options* opts, tsgm_noise_estimate* out) {
+    return guarded([&] {
+        calib_options_validate(opts);
+        if (n_frames < 2) bad("estimate_process_noise: need at least 2 frames");
+        if (!gt || !poses12 || !calib || !out || w < 0 || h < 0)
+            bad("estimate_process_noise: null argument");
+        const HistSpec hs = hist_spec(opts);
+        if (out->counts && out->n_bins < hs.nbins) bad("estimate_process_noise: counts buffer too small");
+        if (static_cast<size_t>(w) * h == 0) {  // no pixels: nothing can overlap
+            for (int k = 0; k + 1 < n_frames; ++k) {
+                double r9[9], t3[3], H[16];
+                relative_motion(poses12 + 12 * k, poses12 + 12 * (k + 1), r9, t3);
+                homography(r9, t3, *calib, H);
+            }
+            throw std::runtime_error("estimate_process_noise: no overlapping valid pixels");
+        }
+        std::unique_ptr<NoiseAccum> acc;
+        warp_gt_pairs(
+            n_frames, w, h, gt, poses12, *calib,
+            [&](tsgm_ctx* c) { acc = std::make_unique<NoiseAccum>(c, hs); },
+            [&](tsgm_ctx* c, const double* tgt, int m) {
+                launch_error_hist_warped(c->b, tgt, m, hs, acc->acc, c->L());
+            },
+            [&](tsgm_ctx*) { acc->finish(out, "estimate_process_noise"); });
+    });
+}
+
+int tsgm_accumulate_error_map(int32_t n_frames, int32_t w, int32_t h, const double* gt,
+                              const double* poses12, const tsgm_stereo_calib* calib, double* acc) {
+    return guarded([&] {
+        if (n_frames < 2) bad("accumulate_error_map: need at least 2 frames");
+        if (!gt || !poses12 || !calib || !acc || w < 0 || h < 0)
+            bad("accumulate_error_map: null argument");
+        const size_t P = static_cast<size_t>(w) * h;
+        if (P == 0) {
+            for (int k = 0; k + 1 < n_frames; ++k) {
+                double r9[9], t3[3], H[16];
+                relative_motion(poses12 + 12 * k, poses12 + 12 * (k + 1), r9, t3);
+                homography(r9, t3, *calib, H);
+            }
+            throw std::runtime_error("accumulate_error_map: no overlapping valid pixels");
+        }
+        double* dacc = nullptr;
+        unsigned long long* dov = nullptr;
+        warp_gt_pairs(
+            n_frames, w, h, gt, poses12, *calib,
+            [&](tsgm_ctx* c) {
+                dacc = c->dalloc<double>(P);
+                dov = c->dalloc<unsigned long long>(1);
+                CK(cudaMemsetAsync(dacc, 0, sizeof(double) * P, c->st));
+                CK(cudaMemsetAsync(dov, 0, sizeof(unsigned long long), c->st));
+            },
+            [&](tsgm_ctx* c, const double* tgt, int m) {
+                launch_error_map(c->b, tgt, m, dacc, dov, c->L());
+            },
+            [&](tsgm_ctx* c) {
+                unsigned long long ov = 0;
+                CK(cudaMemcpyAsync(&ov, dov, sizeof ov, cudaMemcpyDeviceToHost, c->st));
+                d2h(c, acc, dacc, P);
+                sync(c);
+                if (ov == 0) throw std::runtime_error("accumulate_error_map: no overlapping valid pixels");
+            });
+    });
+}
+
+int tsgm_estimate_measurement_noise(int32_t n_frames, int32_t w, int32_t h, const uint8_t* left,
+                                    const uint8_t* right, const double* gt,
+                                    const tsgm_sgm_params* params, const tsgm_calib_options* opts,
+                                    tsgm_noise_estimate* out) {
+    return guarded([&] {
+        calib_options_validate(opts);
+        if (n_frames < 1) bad("estimate_measurement_noise: need at least 1 frame");
+        if (!left || !right || !gt || !params || !out || w < 0 || h < 0)
+            bad("estimate_measurement_noise: null argument");
+        sgm_validate(*params);
+        const HistSpec hs = hist_spec(opts);
+        if (out->counts && out->n_bins < hs.nbins)
+            bad("estimate_measurement_noise: counts buffer too small");
+        // sgm_match on full ranges (noise_calib.cpp:138-140): census, then the volume size
+        if (w < 2 * kCensusRadius + 1 || h < 2 * kCensusRadius + 1)
+            bad("census_transform: image smaller than the 5x5 window");
+        if (1ull * w * h * params->d_max > 0xffffffffull)
+            bad("CostVolume: volume exceeds 32-bit addressing");
+        const size_t P = static_cast<size_t>(w) * h;
+        const int B = std::min<int>(n_frames, kNoiseBatch);
+        auto ctx = noise_ctx(w, h, B, params);
+        tsgm_ctx* c = ctx.get();
+        NoiseAccum acc(c, hs);
+        double* dgt = c->dalloc<double>(B * P);
+        std::vector<int> slots(B);
+        std::vector<const uint8_t*> dl(B), dr(B);
+        for (int i = 0; i < B; ++i) {
+            slots[i] = i;
+            dl[i] = c->d_img + 2 * static_cast<size_t>(i) * P;
+            dr[i] = dl[i] + P;
+        }
+        const std::vector<uint16_t> lo(P, 0), hi(P, static_cast<uint16_t>(params->d_max - 1));
+        std::vector<double> I(16 * static_cast<size_t>(B), 0.0);
+        for (int i = 0; i < B; ++i)
+            for (int j = 0; j < 4; ++j) I[16 * i + 5 * j] = 1.0;
+        for (int k0 = 0; k0 < n_frames; k0 += B) {
+            const int m = std::min(B, n_frames - k0);
+            for (int i = 0; i < m; ++i) {
+                h2d(c, const_cast<uint8_t*>(dl[i]), left + static_cast<size_t>(k0 + i) * P, P);
+                h2d(c, const_cast<uint8_t*>(dr[i]), right + static_cast<size_t>(k0 + i) * P, P);
+                h2d(c, c->b.lo + static_cast<size_t>(i) * P, lo.data(), P);
+                h2d(c, c->b.hi + static_cast<size_t>(i) * P, hi.data(), P);
+            }
+            h2d(c, dgt, gt + static_cast<size_t>(k0) * P, m * P);
+            upload_step(c, m, slots.data(), dl.data(), dr.data(), I.data());
+            Launch L = c->L();
+            const Bufs& b = c->b;
+            launch_ranges_given(b, m, L);
+            launch_offsets(b, m, L);
+            launch_census(b, m, L);
+            const int chunks = (m + c->vol_slots - 1) / c->vol_slots;
+            for (int k = 0, c0 = 0; k < chunks; ++k) {
+                const int mc = (m - c0) / (chunks - k);
+                const Bufs bc = chunk_bufs(b, c0);
+                launch_cost(bc, mc, L);
+                if (!aggregate(c, bc, mc, L, /*fuse_wta=*/true, /*keep_s=*/false, /*full_range=*/true))
+                    launch_wta(bc, mc, L);
+                c0 += mc;
+            }
+            launch_error_hist_wta(b, dgt, m, hs, acc.acc, L);
+            CK(cudaStreamSynchronize(c->st));  // staging buffers are reused by the next batch
+        }
+        acc.finish(out, "estimate_measurement_noise");
+    });
+}
+
+}  // extern "C"

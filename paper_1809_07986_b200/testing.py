@@ -102,3 +102,30 @@ class GpuBackend:
     # ---- outlier metric (eval.cpp) ----
     def count_outliers(self, d, valid, gt, abs_thresh=3.0, rel_thresh=0.05, strict=False):
         return tsgm.count_outliers(d, valid, gt, tsgm.OutlierOptions(abs_thresh, rel_thresh, strict))
+
+    # noise calibration, in the oracle's dict format
+    @staticmethod
+    def _frames(gt, poses=None, left=None, right=None):
+        out = []
+        for k in range(len(gt)):
+            out.append(tsgm.SequenceFrame(
+                k, None if left is None else left[k], None if right is None else right[k],
+                None if poses is None else np.asarray(poses[k]).reshape(3, 4), gt[k]))
+        return out
+
+    @staticmethod
+    def _est(e):
+        h = e.hist
+        return dict(variance=e.variance, mean=h.mean(), within_1px=h.fraction_within_1px(),
+                    samples_used=e.samples_used, total=h.total(), underflow=h.underflow,
+                    overflow=h.overflow, counts=h.counts, sum=h.sum, sum_sq=h.sum_sq)
+
+    def process_noise(self, gt, poses, calib, opts):
+        return self._est(tsgm.estimate_process_noise(self._frames(gt, poses), calib, opts))
+
+    def measurement_noise(self, left, right, gt, params, opts):
+        return self._est(tsgm.estimate_measurement_noise(
+            self._frames(gt, None, left, right), params, 1, opts))
+
+    def error_map(self, gt, poses, calib):
+        return tsgm.accumulate_error_map(self._frames(gt, poses), calib)

@@ -398,6 +398,197 @@ def outlier_rate(d, valid, gt, opts=None):
     return 100.0 * out / ev
 
 
+# ----------------------------------------------------- noise calibration
+# noise_calib.hpp:13-90 / noise_calib.cpp on the GPU.
+@dataclass
+class CalibOptions:  # noise_calib.hpp:43-49
+    outlier_gate_px: float = 10.0
+    bin_width: float = 0.25
+    q_floor: float = 0.1
+
+    def _c(self):
+        return _lib.CalibOptionsC(self.outlier_gate_px, self.bin_width, self.q_floor)
+
+    def validate(self):
+        """CalibOptions::validate (noise_calib.cpp:60-67)."""
+        n = C.c_int32()
+        check(_lib.load().tsgm_calib_bins(C.byref(self._c()), C.byref(n)))
+        return int(n.value)
+
+
+@dataclass
+class SequenceFrame:  # dataset.hpp:18-25 (the fields the calibration reads)
+    index: int = 0
+    left: np.ndarray | None = None
+    right: np.ndarray | None = None
+    pose: np.ndarray | None = None      # 3x4 camera-to-world (Pose, geometry.hpp:106)
+    gt_disp: np.ndarray | None = None   # f64, > 0 = valid
+
+
+@dataclass
+class ErrorHistogram:  # noise_calib.hpp:14-41 (the estimate's histogram)
+    lo: float = -10.0
+    hi: float = 10.0
+    bin_width: float = 0.25
+    counts: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+    underflow: int = 0
+    overflow: int = 0
+    n_gated: int = 0
+    n_within_1: int = 0
+    sum: float = 0.0
+    sum_sq: float = 0.0
+
+    def total(self) -> int:
+        return self.n_gated + self.underflow + self.overflow
+
+    def gated_count(self) -> int:
+        return self.n_gated
+
+    def mean(self) -> float:
+        return self.sum / self.n_gated if self.n_gated > 0 else 0.0
+
+    def variance(self) -> float:
+        if self.n_gated < 2:
+            return 0.0
+        n = float(self.n_gated)
+        m = self.sum / n
+        v = (self.sum_sq - n * m * m) / (n - 1.0)
+        return v if v > 0.0 else 0.0
+
+    def fraction_within_1px(self) -> float:
+        t = self.total()
+        return self.n_within_1 / t if t > 0 else 0.0
+
+
+@dataclass
+class NoiseEstimate:  # noise_calib.hpp:51-55
+    variance: float = 0.0
+    hist: ErrorHistogram = field(default_factory=ErrorHistogram)
+    samples_used: int = 0
+
+
+def _require(frames, who, gt=False, pose=False, images=False):
+    for f in frames:
+        if gt and f.gt_disp is None:
+            raise ValueError(f"{who}: frame {f.index} has no GT disparity")
+        if pose and f.pose is None:
+            raise ValueError(f"{who}: frame {f.index} has no pose")
+
+
+def _stack(arrs, dtype, who):
+    shape = arrs[0].shape
+    for a in arrs:
+        if a.shape != shape:
+            raise ValueError(f"{who}: frame size mismatch")
+    return np.ascontiguousarray(np.stack(arrs), dtype=dtype)
+
+
+def _estimate(fn, args, opts):
+    o = _as(opts or CalibOptions(), CalibOptions)
+    nb = o.validate()
+    counts = np.zeros(nb, np.int64)
+    est = _lib.NoiseEstimateC()
+    est.n_bins = nb
+    est.counts = counts.ctypes.data
+    check(fn(*args, C.byref(o._c()), C.byref(est)))
+    hist = ErrorHistogram(est.lo, est.hi, est.bin_width, counts, int(est.underflow),
+                          int(est.overflow), int(est.samples_used), int(est.within_1px),
+                          float(est.sum), float(est.sum_sq))
+    return NoiseEstimate(float(est.variance), hist, int(est.samples_used))
+
+
+def _pairs_checked(frames, who):
+    if len(frames) < 2:
+        raise ValueError(f"{who}: need at least 2 frames")
+    for k in range(1, len(frames)):  # the reference's per-pair order
+        _require([frames[k - 1], frames[k]], who, gt=True)
+        _require([frames[k - 1], frames[k]], who, pose=True)
+    gt = _stack([f.gt_disp for f in frames], np.float64, who)
+    poses = _stack([np.asarray(f.pose, np.float64).reshape(3, 4) for f in frames], np.float64, who)
+    return gt, poses
+
+
+def estimate_process_noise(frames, calib, opts=None):
+    """estimate_process_noise (noise_calib.cpp:102-128): the GT of frame k-1
+    warped by the relative motion vs the GT of frame k, pooled over pairs."""
+    o = _as(opts or CalibOptions(), CalibOptions)
+    o.validate()
+    gt, poses = _pairs_checked(frames, "estimate_process_noise")
+    n, h, w = gt.shape
+    c = _as(calib, StereoCalib)._c()
+    return _estimate(_lib.load().tsgm_estimate_process_noise,
+                     (n, w, h, ptr(gt), ptr(poses), C.byref(c)), o)
+
+
+def estimate_measurement_noise(frames, params, threads=1, opts=None):
+    """estimate_measurement_noise (noise_calib.cpp:130-147): full-range SGM vs
+    GT per frame, each frame in isolation (batched on the GPU; `threads` is
+    accepted and ignored)."""
+    o = _as(opts or CalibOptions(), CalibOptions)
+    o.validate()
+    if len(frames) == 0:
+        raise ValueError("estimate_measurement_noise: need at least 1 frame")
+    _require(frames, "estimate_measurement_noise", gt=True)
+    who = "estimate_measurement_noise"
+    left = _stack([f.left for f in frames], np.uint8, who)
+    right = _stack([f.right for f in frames], np.uint8, who)
+    gt = _stack([f.gt_disp for f in frames], np.float64, who)
+    if left.shape != right.shape or left.shape != gt.shape:
+        raise ValueError(f"{who}: frame size mismatch")
+    n, h, w = gt.shape
+    p = _as(params, SgmParams)._c()
+    return _estimate(_lib.load().tsgm_estimate_measurement_noise,
+                     (n, w, h, ptr(left), ptr(right), ptr(gt), C.byref(p)), o)
+
+
+def accumulate_error_map(frames, calib):
+    """accumulate_error_map (noise_calib.cpp:149-182): per-pixel sum of
+    |warped GT - GT| over consecutive pairs (bit-exact)."""
+    gt, poses = _pairs_checked(frames, "accumulate_error_map")
+    n, h, w = gt.shape
+    c = _as(calib, StereoCalib)._c()
+    acc = np.zeros((h, w))
+    check(_lib.load().tsgm_accumulate_error_map(n, w, h, ptr(gt), ptr(poses), C.byref(c),
+                                               ptr(acc)))
+    return acc
+
+
+def _g6(x) -> str:
+    """std::ostream << double at precision(6) (%g)."""
+    return f"{x:.6g}"
+
+
+def write_calib_report(path, process, measurement, opts=None):
+    """write_calib_report (noise_calib.cpp:184-217): host text, q/r lines a
+    run config can load."""
+    o = _as(opts or CalibOptions(), CalibOptions)
+    o.validate()
+    q = max(process.variance, o.q_floor)
+    ph, mh = process.hist, measurement.hist
+    lines = ["# noise calibration report",
+             f"# process:     raw variance {_g6(process.variance)} px^2 over "
+             f"{process.samples_used} samples, {_g6(100.0 * ph.fraction_within_1px())}% within +/-1 px",
+             f"# measurement: raw variance {_g6(measurement.variance)} px^2 over "
+             f"{measurement.samples_used} samples, {_g6(100.0 * mh.fraction_within_1px())}% within +/-1 px"]
+    if q != process.variance:
+        lines.append(f"# q floor {_g6(o.q_floor)} applied")
+    lines += [f"q={_g6(q)}", f"r={_g6(measurement.variance)}", "#",
+              f"# error histogram (gate +/-{_g6(o.outlier_gate_px)} px)",
+              "# bin_lo bin_hi process_count measurement_count"]
+    same = (ph.lo == mh.lo and ph.bin_width == mh.bin_width and len(ph.counts) == len(mh.counts))
+    lines.append(f"# -inf {_g6(ph.lo)} {ph.underflow} {mh.underflow}")
+    for i in range(len(ph.counts)):
+        b0 = ph.lo + float(i) * ph.bin_width
+        lines.append(f"# {_g6(b0)} {_g6(b0 + ph.bin_width)} {int(ph.counts[i])} "
+                     f"{int(mh.counts[i]) if same else -1}")
+    lines.append(f"# {_g6(ph.hi)} +inf {ph.overflow} {mh.overflow}")
+    try:
+        with open(path, "w") as f:
+            f.write("\n".join(lines) + "\n")
+    except OSError:
+        raise RuntimeError(f"write_calib_report: cannot open {path}") from None
+
+
 # --------------------------------------------------------------------- engine
 _OUT_DTYPES = dict(state_d=np.float64, state_p=np.float64, state_valid=np.uint8,
                    export_d=np.int32, export_valid=np.uint8, diff=np.float64, mask=np.uint8,
