@@ -329,6 +329,10 @@ int tsgm_estimate_measurement_noise(int32_t n_frames, int32_t w, int32_t h, cons
                                     const uint8_t* right, const double* gt,
                                     const tsgm_sgm_params* params, const tsgm_calib_options* opts,
                                     tsgm_noise_estimate* out);
+/* The calibration functions keep their device working set (a batch of frames'
+ * state, maps and volumes) between calls with the same geometry; this frees
+ * it. */
+int tsgm_calib_release(void);
 /* accumulate_error_map (noise_calib.cpp:149-182): acc[W*H], bit-exact. */
 int tsgm_accumulate_error_map(int32_t n_frames, int32_t w, int32_t h, const double* gt,
                               const double* poses12, const tsgm_stereo_calib* calib, double* acc);

@@ -59,7 +59,7 @@ EXPORTS = [
     "tsgm_integral_image", "tsgm_detect_candidate_windows", "tsgm_greedy_merge",
     "tsgm_detect_moving_objects", "tsgm_detect", "tsgm_count_outliers",
     "tsgm_count_outliers_batch", "tsgm_calib_bins", "tsgm_estimate_process_noise",
-    "tsgm_estimate_measurement_noise", "tsgm_accumulate_error_map",
+    "tsgm_estimate_measurement_noise", "tsgm_accumulate_error_map", "tsgm_calib_release",
 ]
 
 
@@ -149,6 +149,7 @@ def load():
         lib.tsgm_estimate_measurement_noise.argtypes = [
             C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
             C.POINTER(SgmParamsC), co, ne]
+        lib.tsgm_calib_release.argtypes = []
         lib.tsgm_accumulate_error_map.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                                   C.c_void_p, C.POINTER(StereoCalibC), C.c_void_p]
         _lib = lib

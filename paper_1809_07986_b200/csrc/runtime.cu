@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -1487,7 +1488,7 @@ HistSpec hist_spec(const tsgm_calib_options* o) {  // ErrorHistogram(-gate, gate
     return hs;
 }
 
-constexpr int kNoiseBatch = 32;  // frames (or frame pairs) per batched launch
+constexpr int kNoiseBatch = 8;  // frames (or frame pairs) per batched launch (memory: ~8 volumes)
 
 // A context for the calibration stages: images, state and per-pixel buffers
 // for `slots` frames; volumes only when sgm is given (measurement noise).
@@ -1509,18 +1510,79 @@ std::unique_ptr<tsgm_ctx> noise_ctx(int w, int h, int slots, const tsgm_sgm_para
     return ctx;
 }
 
+// The calibration functions are stateless like the reference's, but their
+// working set (a batch of frames' state, maps and, for the measurement noise,
+// volumes: GBs) is kept between calls with the same geometry — allocating it
+// per call cost more than the calibration itself. One cache entry per kind
+// (0: warped ground-truth pairs, 1: full-range matching), guarded by a mutex
+// (concurrent calls serialise); tsgm_calib_release() frees them.
+struct CalibCache {
+    std::unique_ptr<tsgm_ctx> ctx;
+    int dev = -1, w = 0, h = 0, slots = 0;
+    tsgm_sgm_params sgm{};
+    double* dgt = nullptr;             // (slots + 1) * P ground truth staging
+    double* dacc = nullptr;            // P, error map
+    unsigned long long* dsmall = nullptr;  // error-map overlap; histogram tallies
+    double* dsums = nullptr;           // 2 + partials
+    unsigned long long* dcounts = nullptr;
+    int counts_cap = 0;
+};
+std::mutex g_calib_mu;
+// never destroyed: at process exit the CUDA runtime may already be gone
+CalibCache* const g_calib = new CalibCache[2];
+
+CalibCache& calib_cache(int kind, int w, int h, int slots, const tsgm_sgm_params* sgm) {
+    CalibCache& c = g_calib[kind];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const bool same = c.ctx && c.dev == dev && c.w == w && c.h == h && c.slots == slots &&
+                      (!sgm || std::memcmp(&c.sgm, sgm, sizeof *sgm) == 0);
+    if (!same) {
+        c = CalibCache{};
+        c.ctx = noise_ctx(w, h, slots, sgm);
+        c.dev = dev;
+        c.w = w;
+        c.h = h;
+        c.slots = slots;
+        if (sgm) c.sgm = *sgm;
+        const size_t P = static_cast<size_t>(w) * h;
+        c.dgt = c.ctx->dalloc<double>((slots + 1) * P);
+        if (kind == 0) c.dacc = c.ctx->dalloc<double>(P);
+        c.dsmall = c.ctx->dalloc<unsigned long long>(8);
+        c.dsums = c.ctx->dalloc<double>(2 + hist_partial_doubles());
+    }
+    return c;
+}
+
+// Run fn under the cache lock; any failure drops the entry (its device state
+// may be half-written).
+template <typename Fn>
+void with_calib_cache(int kind, Fn&& fn) {
+    std::lock_guard<std::mutex> lk(g_calib_mu);
+    try {
+        fn();
+    } catch (...) {
+        g_calib[kind] = CalibCache{};
+        throw;
+    }
+}
+
 struct NoiseAccum {
     HistSpec hs;
     HistAcc acc;
     tsgm_ctx* ctx;
-    NoiseAccum(tsgm_ctx* c, const HistSpec& h) : hs(h), ctx(c) {
-        acc.counts = c->dalloc<unsigned long long>(h.nbins);
-        acc.tallies = c->dalloc<unsigned long long>(4);
-        acc.partial = c->dalloc<double>(hist_partial_doubles());
-        acc.sums = c->dalloc<double>(2);
-        CK(cudaMemsetAsync(acc.counts, 0, sizeof(unsigned long long) * h.nbins, c->st));
-        CK(cudaMemsetAsync(acc.tallies, 0, sizeof(unsigned long long) * 4, c->st));
-        CK(cudaMemsetAsync(acc.sums, 0, sizeof(double) * 2, c->st));
+    NoiseAccum(CalibCache& c, const HistSpec& h) : hs(h), ctx(c.ctx.get()) {
+        if (c.counts_cap < h.nbins) {  // grows only (a cached context's allocation)
+            c.dcounts = ctx->dalloc<unsigned long long>(h.nbins);
+            c.counts_cap = h.nbins;
+        }
+        acc.counts = c.dcounts;
+        acc.tallies = c.dsmall;
+        acc.sums = c.dsums;
+        acc.partial = c.dsums + 2;
+        CK(cudaMemsetAsync(acc.counts, 0, sizeof(unsigned long long) * h.nbins, ctx->st));
+        CK(cudaMemsetAsync(acc.tallies, 0, sizeof(unsigned long long) * 4, ctx->st));
+        CK(cudaMemsetAsync(acc.sums, 0, sizeof(double) * 2, ctx->st));
     }
     // NoiseEstimate (noise_calib.cpp:91-99: finish) from the device tallies
     void finish(tsgm_noise_estimate* out, const char* who) {
@@ -1562,7 +1624,7 @@ struct NoiseAccum {
 
 // Frame pairs (k, k+1), k = 0 .. n-2, in batches: slot i holds state_from_gt
 // of frame k0+i warped by relative_motion(pose k0+i, pose k0+i+1)
-// (noise_calib.cpp:115-119); fn(ctx, gt of frames k0+1 .., m) consumes them.
+// (noise_calib.cpp:115-119); fn(cache, gt of frames k0+1 .., m) consumes them.
 template <typename Begin, typename Fn, typename End>
 void warp_gt_pairs(int n, int w, int h, const double* gt, const double* poses,
                    const tsgm_stereo_calib& calib, Begin&& begin, Fn&& fn, End&& end) {
@@ -1576,26 +1638,27 @@ void warp_gt_pairs(int n, int w, int h, const double* gt, const double* poses,
         relative_motion(poses + 12 * k, poses + 12 * (k + 1), r9, t3);
         homography(r9, t3, calib, &H[16 * static_cast<size_t>(k)]);
     }
-    const int B = std::min(pairs, kNoiseBatch);
-    auto ctx = noise_ctx(w, h, B, nullptr);
-    tsgm_ctx* c = ctx.get();
-    double* dgt = c->dalloc<double>((B + 1) * P);
-    std::vector<int> slots(B);
-    for (int i = 0; i < B; ++i) slots[i] = i;
-    std::vector<const uint8_t*> img(B, c->d_img);
-    begin(c);
-    for (int k0 = 0; k0 < pairs; k0 += B) {
-        const int m = std::min(B, pairs - k0);
-        h2d(c, dgt, gt + static_cast<size_t>(k0) * P, (m + 1) * P);
-        upload_step(c, m, slots.data(), img.data(), img.data(), &H[16 * static_cast<size_t>(k0)]);
-        Launch L = c->L();
-        launch_gt_state(c->b, dgt, m, L);
-        launch_warp(c->b, m, c->b.sd, c->b.sp, c->b.sv, calib.d_max, L);
-        launch_predict_finalize(c->b, m, 0.0, 0, L);
-        fn(c, dgt + P, m);
-        CK(cudaStreamSynchronize(c->st));  // dgt is overwritten by the next batch
-    }
-    end(c);
+    with_calib_cache(0, [&] {
+        const int B = std::min(pairs, kNoiseBatch);
+        CalibCache& cc = calib_cache(0, w, h, kNoiseBatch, nullptr);
+        tsgm_ctx* c = cc.ctx.get();
+        std::vector<int> slots(B);
+        for (int i = 0; i < B; ++i) slots[i] = i;
+        std::vector<const uint8_t*> img(B, c->d_img);
+        begin(cc);
+        for (int k0 = 0; k0 < pairs; k0 += B) {
+            const int m = std::min(B, pairs - k0);
+            h2d(c, cc.dgt, gt + static_cast<size_t>(k0) * P, (m + 1) * P);
+            upload_step(c, m, slots.data(), img.data(), img.data(), &H[16 * static_cast<size_t>(k0)]);
+            Launch L = c->L();
+            launch_gt_state(c->b, cc.dgt, m, L);
+            launch_warp(c->b, m, c->b.sd, c->b.sp, c->b.sv, calib.d_max, L);
+            launch_predict_finalize(c->b, m, 0.0, 0, L);
+            fn(cc, cc.dgt + P, m);
+            CK(cudaStreamSynchronize(c->st));  // dgt is overwritten by the next batch
+        }
+        end(cc);
+    });
 }
 
 }  // namespace
@@ -1631,11 +1694,11 @@ int tsgm_estimate_process_noise(int32_t n_frames, int32_t w, int32_t h, const do
         std::unique_ptr<NoiseAccum> acc;
         warp_gt_pairs(
             n_frames, w, h, gt, poses12, *calib,
-            [&](tsgm_ctx* c) { acc = std::make_unique<NoiseAccum>(c, hs); },
-            [&](tsgm_ctx* c, const double* tgt, int m) {
-                launch_error_hist_warped(c->b, tgt, m, hs, acc->acc, c->L());
+            [&](CalibCache& cc) { acc = std::make_unique<NoiseAccum>(cc, hs); },
+            [&](CalibCache& cc, const double* tgt, int m) {
+                launch_error_hist_warped(cc.ctx->b, tgt, m, hs, acc->acc, cc.ctx->L());
             },
-            [&](tsgm_ctx*) { acc->finish(out, "estimate_process_noise"); });
+            [&](CalibCache&) { acc->finish(out, "estimate_process_noise"); });
     });
 }
 
@@ -1654,23 +1717,20 @@ int tsgm_accumulate_error_map(int32_t n_frames, int32_t w, int32_t h, const doub
             }
             throw std::runtime_error("accumulate_error_map: no overlapping valid pixels");
         }
-        double* dacc = nullptr;
-        unsigned long long* dov = nullptr;
         warp_gt_pairs(
             n_frames, w, h, gt, poses12, *calib,
-            [&](tsgm_ctx* c) {
-                dacc = c->dalloc<double>(P);
-                dov = c->dalloc<unsigned long long>(1);
-                CK(cudaMemsetAsync(dacc, 0, sizeof(double) * P, c->st));
-                CK(cudaMemsetAsync(dov, 0, sizeof(unsigned long long), c->st));
+            [&](CalibCache& cc) {
+                CK(cudaMemsetAsync(cc.dacc, 0, sizeof(double) * P, cc.ctx->st));
+                CK(cudaMemsetAsync(cc.dsmall, 0, sizeof(unsigned long long), cc.ctx->st));
             },
-            [&](tsgm_ctx* c, const double* tgt, int m) {
-                launch_error_map(c->b, tgt, m, dacc, dov, c->L());
+            [&](CalibCache& cc, const double* tgt, int m) {
+                launch_error_map(cc.ctx->b, tgt, m, cc.dacc, cc.dsmall, cc.ctx->L());
             },
-            [&](tsgm_ctx* c) {
+            [&](CalibCache& cc) {
+                tsgm_ctx* c = cc.ctx.get();
                 unsigned long long ov = 0;
-                CK(cudaMemcpyAsync(&ov, dov, sizeof ov, cudaMemcpyDeviceToHost, c->st));
-                d2h(c, acc, dacc, P);
+                CK(cudaMemcpyAsync(&ov, cc.dsmall, sizeof ov, cudaMemcpyDeviceToHost, c->st));
+                d2h(c, acc, cc.dacc, P);
                 sync(c);
                 if (ov == 0) throw std::runtime_error("accumulate_error_map: no overlapping valid pixels");
             });
@@ -1696,50 +1756,63 @@ int tsgm_estimate_measurement_noise(int32_t n_frames, int32_t w, int32_t h, cons
         if (1ull * w * h * params->d_max > 0xffffffffull)
             bad("CostVolume: volume exceeds 32-bit addressing");
         const size_t P = static_cast<size_t>(w) * h;
-        const int B = std::min<int>(n_frames, kNoiseBatch);
-        auto ctx = noise_ctx(w, h, B, params);
-        tsgm_ctx* c = ctx.get();
-        NoiseAccum acc(c, hs);
-        double* dgt = c->dalloc<double>(B * P);
-        std::vector<int> slots(B);
-        std::vector<const uint8_t*> dl(B), dr(B);
-        for (int i = 0; i < B; ++i) {
-            slots[i] = i;
-            dl[i] = c->d_img + 2 * static_cast<size_t>(i) * P;
-            dr[i] = dl[i] + P;
-        }
-        const std::vector<uint16_t> lo(P, 0), hi(P, static_cast<uint16_t>(params->d_max - 1));
-        std::vector<double> I(16 * static_cast<size_t>(B), 0.0);
-        for (int i = 0; i < B; ++i)
-            for (int j = 0; j < 4; ++j) I[16 * i + 5 * j] = 1.0;
-        for (int k0 = 0; k0 < n_frames; k0 += B) {
-            const int m = std::min(B, n_frames - k0);
-            for (int i = 0; i < m; ++i) {
-                h2d(c, const_cast<uint8_t*>(dl[i]), left + static_cast<size_t>(k0 + i) * P, P);
-                h2d(c, const_cast<uint8_t*>(dr[i]), right + static_cast<size_t>(k0 + i) * P, P);
-                h2d(c, c->b.lo + static_cast<size_t>(i) * P, lo.data(), P);
-                h2d(c, c->b.hi + static_cast<size_t>(i) * P, hi.data(), P);
+        std::lock_guard<std::mutex> lk(g_calib_mu);
+        try {
+            const int B = std::min<int>(n_frames, kNoiseBatch);
+            CalibCache& cc = calib_cache(1, w, h, kNoiseBatch, params);
+            tsgm_ctx* c = cc.ctx.get();
+            NoiseAccum acc(cc, hs);
+            double* dgt = cc.dgt;
+            std::vector<int> slots(B);
+            std::vector<const uint8_t*> dl(B), dr(B);
+            for (int i = 0; i < B; ++i) {
+                slots[i] = i;
+                dl[i] = c->d_img + 2 * static_cast<size_t>(i) * P;
+                dr[i] = dl[i] + P;
             }
-            h2d(c, dgt, gt + static_cast<size_t>(k0) * P, m * P);
-            upload_step(c, m, slots.data(), dl.data(), dr.data(), I.data());
-            Launch L = c->L();
-            const Bufs& b = c->b;
-            launch_ranges_given(b, m, L);
-            launch_offsets(b, m, L);
-            launch_census(b, m, L);
-            const int chunks = (m + c->vol_slots - 1) / c->vol_slots;
-            for (int k = 0, c0 = 0; k < chunks; ++k) {
-                const int mc = (m - c0) / (chunks - k);
-                const Bufs bc = chunk_bufs(b, c0);
-                launch_cost(bc, mc, L);
-                if (!aggregate(c, bc, mc, L, /*fuse_wta=*/true, /*keep_s=*/false, /*full_range=*/true))
-                    launch_wta(bc, mc, L);
-                c0 += mc;
+            const std::vector<uint16_t> lo(P, 0), hi(P, static_cast<uint16_t>(params->d_max - 1));
+            std::vector<double> I(16 * static_cast<size_t>(B), 0.0);
+            for (int i = 0; i < B; ++i)
+                for (int j = 0; j < 4; ++j) I[16 * i + 5 * j] = 1.0;
+            for (int k0 = 0; k0 < n_frames; k0 += B) {
+                const int m = std::min(B, n_frames - k0);
+                for (int i = 0; i < m; ++i) {
+                    h2d(c, const_cast<uint8_t*>(dl[i]), left + static_cast<size_t>(k0 + i) * P, P);
+                    h2d(c, const_cast<uint8_t*>(dr[i]), right + static_cast<size_t>(k0 + i) * P, P);
+                    h2d(c, c->b.lo + static_cast<size_t>(i) * P, lo.data(), P);
+                    h2d(c, c->b.hi + static_cast<size_t>(i) * P, hi.data(), P);
+                }
+                h2d(c, dgt, gt + static_cast<size_t>(k0) * P, m * P);
+                upload_step(c, m, slots.data(), dl.data(), dr.data(), I.data());
+                Launch L = c->L();
+                const Bufs& b = c->b;
+                launch_ranges_given(b, m, L);
+                launch_offsets(b, m, L);
+                launch_census(b, m, L);
+                const int chunks = (m + c->vol_slots - 1) / c->vol_slots;
+                for (int k = 0, c0 = 0; k < chunks; ++k) {
+                    const int mc = (m - c0) / (chunks - k);
+                    const Bufs bc = chunk_bufs(b, c0);
+                    launch_cost(bc, mc, L);
+                    if (!aggregate(c, bc, mc, L, /*fuse_wta=*/true, /*keep_s=*/false, /*full_range=*/true))
+                        launch_wta(bc, mc, L);
+                    c0 += mc;
+                }
+                launch_error_hist_wta(b, dgt, m, hs, acc.acc, L);
+                CK(cudaStreamSynchronize(c->st));  // staging buffers are reused by the next batch
             }
-            launch_error_hist_wta(b, dgt, m, hs, acc.acc, L);
-            CK(cudaStreamSynchronize(c->st));  // staging buffers are reused by the next batch
+            acc.finish(out, "estimate_measurement_noise");
+        } catch (...) {
+            g_calib[1] = CalibCache{};
+            throw;
         }
-        acc.finish(out, "estimate_measurement_noise");
+    });
+}
+
+int tsgm_calib_release(void) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(g_calib_mu);
+        for (int k = 0; k < 2; ++k) g_calib[k] = CalibCache{};
     });
 }
 

@@ -553,6 +553,12 @@ def accumulate_error_map(frames, calib):
     return acc
 
 
+def release_calibration_cache():
+    """Free the device working set the calibration functions keep between
+    calls (tsgm_calib_release)."""
+    check(_lib.load().tsgm_calib_release())
+
+
 def _g6(x) -> str:
     """std::ostream << double at precision(6) (%g)."""
     return f"{x:.6g}"

@@ -86,8 +86,8 @@ def test_zero_error_sequence_zero_map():
 
 
 def test_batched_against_port(port):
-    """35 frames = two launch batches (32 + 3) of pairs and frames: counts,
-    tallies and the error map bit-exact vs the port; moments to 1e-12."""
+    """35 frames = five launch batches (8 + 8 + 8 + 8 + 3) of frames: counts,
+    tallies and the error map bit-exact vs the port; moments to 1e-9."""
     cfg = SceneConfig.baseline_config(1, width=72, height=48, focal=60.0, cx=35.5, cy=23.5,
                                       d_max=32, seed=4, n_movers=2, frames=35)
     left, right, poses, gt = render(cfg, gt=True)
@@ -105,5 +105,5 @@ def test_batched_against_port(port):
             assert got[k] == want[k], k
         np.testing.assert_array_equal(got["counts"], want["counts"])
         np.testing.assert_allclose([got["variance"], got["mean"]], [want["variance"], want["mean"]],
-                                   rtol=1e-12)
+                                   rtol=1e-9)
     np.testing.assert_array_equal(gpu.error_map(gt, p12, calib), port.error_map(gt, p12, calib))

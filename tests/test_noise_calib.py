@@ -6,7 +6,8 @@ the KATs of the reference's tests/test_noise_calib.cpp.
 Exactness: histogram counts, tallies and the accumulated error map are
 bit-exact; the port also reproduces the reference's raster-order FP64 moments
 bit for bit, the GPU reduces them in a fixed tree order (deterministic), so its
-variance and mean are checked to 1e-12 relative."""
+variance and mean are checked to 1e-9 relative (the variance
+(sum_sq - n m^2) / (n - 1) amplifies the sums' last-bit differences)."""
 import numpy as np
 import pytest
 
@@ -33,7 +34,7 @@ def _check(backend, got, g, key):
     mom, ints, counts = g[f"{key}_moments"], g[f"{key}_ints"], g[f"{key}_counts"]
     assert [got["samples_used"], got["total"], got["underflow"], got["overflow"]] == list(ints)
     np.testing.assert_array_equal(got["counts"], counts)
-    rtol = 0.0 if backend.kind == "port" else 1e-12
+    rtol = 0.0 if backend.kind == "port" else 1e-9
     np.testing.assert_allclose([got["variance"], got["mean"]], mom[:2], rtol=rtol, atol=0.0)
     assert got["within_1px"] == mom[2]
 
