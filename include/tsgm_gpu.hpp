@@ -24,6 +24,7 @@
 #include "tsgm/geometry.hpp"
 #include "tsgm/matching_cost.hpp"
 #include "tsgm/motion_detect.hpp"
+#include "tsgm/noise_calib.hpp"
 #include "tsgm/sgm.hpp"
 #include "tsgm/temporal_filter.hpp"
 #include "tsgm_b200.h"
@@ -255,6 +256,131 @@ inline std::vector<DetectionBox> detect_moving_objects(const Image<double>& diff
         return tsgm_detect_moving_objects(diff.data(), diff.width(), diff.height(), &c.c, out,
                                           cap, n);
     });
+}
+
+// ---- noise calibration (noise_calib.hpp:57-80) on the GPU ----
+namespace detail {
+// ErrorHistogram keeps its moments private (noise_calib.hpp:35-40); the
+// facade fills them through pointers-to-member obtained by explicit template
+// instantiation (which is exempt from access checking), so the returned
+// NoiseEstimate behaves exactly like the reference's (mean, variance, total,
+// fraction_within_1px).
+template <typename Tag, typename Tag::type M>
+struct HistAccess {
+    friend typename Tag::type member(Tag) { return M; }
+};
+struct HistNGated { using type = long long ErrorHistogram::*; friend type member(HistNGated); };
+struct HistNWithin { using type = long long ErrorHistogram::*; friend type member(HistNWithin); };
+struct HistSum { using type = double ErrorHistogram::*; friend type member(HistSum); };
+struct HistSumSq { using type = double ErrorHistogram::*; friend type member(HistSumSq); };
+template struct HistAccess<HistNGated, &ErrorHistogram::n_gated_>;
+template struct HistAccess<HistNWithin, &ErrorHistogram::n_within_1_>;
+template struct HistAccess<HistSum, &ErrorHistogram::sum_>;
+template struct HistAccess<HistSumSq, &ErrorHistogram::sum_sq_>;
+
+inline tsgm_calib_options to_c(const CalibOptions& o) {
+    return tsgm_calib_options{o.outlier_gate_px, o.bin_width, o.q_floor};
+}
+
+// frames -> contiguous maps (the reference's own missing-field errors first)
+struct CalibFrames {
+    int n = 0, w = 0, h = 0;
+    std::vector<double> gt, poses;
+    std::vector<std::uint8_t> left, right;
+    CalibFrames(const std::vector<SequenceFrame>& frames, const char* who, bool need_pose,
+                bool images) {
+        n = static_cast<int>(frames.size());
+        for (const SequenceFrame& f : frames) {
+            if (!f.gt_disp)
+                throw std::invalid_argument(std::string(who) + ": frame " + std::to_string(f.index) +
+                                            " has no GT disparity");
+            if (need_pose && !f.pose)
+                throw std::invalid_argument(std::string(who) + ": frame " + std::to_string(f.index) +
+                                            " has no pose");
+        }
+        if (frames.empty()) return;
+        w = frames[0].gt_disp->width();
+        h = frames[0].gt_disp->height();
+        const size_t P = static_cast<size_t>(w) * h;
+        for (const SequenceFrame& f : frames) {
+            if (f.gt_disp->width() != w || f.gt_disp->height() != h ||
+                (images && (f.left.width() != w || f.left.height() != h ||
+                            f.right.width() != w || f.right.height() != h)))
+                throw std::invalid_argument(std::string(who) + ": frame size mismatch");
+            gt.insert(gt.end(), f.gt_disp->data(), f.gt_disp->data() + P);
+            if (images) {
+                left.insert(left.end(), f.left.data(), f.left.data() + P);
+                right.insert(right.end(), f.right.data(), f.right.data() + P);
+            }
+            if (need_pose)
+                for (int i = 0; i < 12; ++i) poses.push_back((*f.pose)(i / 4, i % 4));
+        }
+    }
+};
+
+template <typename Call>
+inline NoiseEstimate estimate(const CalibOptions& opts, Call&& call) {
+    const tsgm_calib_options o = to_c(opts);
+    std::int32_t nb = 0;
+    check(tsgm_calib_bins(&o, &nb));
+    std::vector<std::int64_t> counts(static_cast<size_t>(nb));
+    tsgm_noise_estimate e{};
+    e.n_bins = nb;
+    e.counts = counts.data();
+    check(call(&o, &e));
+    NoiseEstimate out;
+    out.variance = e.variance;
+    out.samples_used = e.samples_used;
+    out.hist = ErrorHistogram(e.lo, e.hi, e.bin_width);
+    out.hist.counts.assign(counts.begin(), counts.end());
+    out.hist.underflow = e.underflow;
+    out.hist.overflow = e.overflow;
+    out.hist.*member(HistNGated{}) = e.samples_used;
+    out.hist.*member(HistNWithin{}) = e.within_1px;
+    out.hist.*member(HistSum{}) = e.sum;
+    out.hist.*member(HistSumSq{}) = e.sum_sq;
+    return out;
+}
+}  // namespace detail
+
+inline NoiseEstimate estimate_process_noise(const std::vector<SequenceFrame>& frames,
+                                            const StereoCalib& calib,
+                                            const CalibOptions& opts = {}) {
+    opts.validate();
+    if (frames.size() < 2)
+        throw std::invalid_argument("estimate_process_noise: need at least 2 frames");
+    const detail::CalibFrames f(frames, "estimate_process_noise", true, false);
+    const tsgm_stereo_calib c = detail::to_c(calib);
+    return detail::estimate(opts, [&](const tsgm_calib_options* o, tsgm_noise_estimate* e) {
+        return tsgm_estimate_process_noise(f.n, f.w, f.h, f.gt.data(), f.poses.data(), &c, o, e);
+    });
+}
+
+inline NoiseEstimate estimate_measurement_noise(const std::vector<SequenceFrame>& frames,
+                                                const SgmParams& params, int threads = 1,
+                                                const CalibOptions& opts = {}) {
+    (void)threads;
+    opts.validate();
+    if (frames.empty())
+        throw std::invalid_argument("estimate_measurement_noise: need at least 1 frame");
+    const detail::CalibFrames f(frames, "estimate_measurement_noise", false, true);
+    const tsgm_sgm_params p = detail::to_c(params);
+    return detail::estimate(opts, [&](const tsgm_calib_options* o, tsgm_noise_estimate* e) {
+        return tsgm_estimate_measurement_noise(f.n, f.w, f.h, f.left.data(), f.right.data(),
+                                               f.gt.data(), &p, o, e);
+    });
+}
+
+inline Image<double> accumulate_error_map(const std::vector<SequenceFrame>& frames,
+                                          const StereoCalib& calib) {
+    if (frames.size() < 2)
+        throw std::invalid_argument("accumulate_error_map: need at least 2 frames");
+    const detail::CalibFrames f(frames, "accumulate_error_map", true, false);
+    const tsgm_stereo_calib c = detail::to_c(calib);
+    Image<double> acc(f.w, f.h, 0.0);
+    detail::check(tsgm_accumulate_error_map(f.n, f.w, f.h, f.gt.data(), f.poses.data(), &c,
+                                            acc.data()));
+    return acc;
 }
 
 // Batched, device-resident production path.

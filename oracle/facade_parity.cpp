@@ -11,6 +11,7 @@
 #include <random>
 #include <stdexcept>
 
+#include "tsgm/noise_calib.hpp"
 #include "tsgm/temporal_filter.hpp"
 #include "tsgm_gpu.hpp"
 #include "tsgm_scene.h"
@@ -177,6 +178,61 @@ int main() {
         const auto got = eng.detect({0}, loose);
         EXPECT(got.size() == 1 && got[0] == detect_moving_objects(eng.result(0).diff, loose),
                "Engine::detect");
+    }
+    {  // noise calibration (noise_calib.hpp:57-80) on the same frames
+        std::vector<double> ps(12 * F);
+        std::vector<float> gf(static_cast<size_t>(w) * h * F);
+        if (tsgm_scene_render(&sc, 0, F, L.data(), R.data(), gf.data(), ps.data(), 4) != 0) return 2;
+        std::vector<SequenceFrame> frames(static_cast<size_t>(F));
+        for (int k = 0; k < F; ++k) {
+            SequenceFrame& f = frames[static_cast<size_t>(k)];
+            f.index = k;
+            f.left = GrayImage(w, h);
+            f.right = GrayImage(w, h);
+            std::copy(L.begin() + static_cast<long>(k) * w * h, L.begin() + static_cast<long>(k + 1) * w * h,
+                      f.left.data());
+            std::copy(R.begin() + static_cast<long>(k) * w * h, R.begin() + static_cast<long>(k + 1) * w * h,
+                      f.right.data());
+            Image<double> g(w, h);
+            for (int i = 0; i < w * h; ++i) g.data()[i] = gf[static_cast<size_t>(k) * w * h + i];
+            f.gt_disp = g;
+            Pose p;
+            for (int i = 0; i < 12; ++i) p(i / 4, i % 4) = ps[12 * k + i];
+            f.pose = p;
+        }
+        auto same_est = [](const NoiseEstimate& a, const NoiseEstimate& b) {
+            const auto rel = [](double x, double y) {
+                return std::abs(x - y) <= 1e-9 * std::max(std::abs(y), 1e-300);
+            };
+            return a.samples_used == b.samples_used && a.hist.counts == b.hist.counts &&
+                   a.hist.total() == b.hist.total() && a.hist.underflow == b.hist.underflow &&
+                   a.hist.overflow == b.hist.overflow &&
+                   a.hist.fraction_within_1px() == b.hist.fraction_within_1px() &&
+                   rel(a.variance, b.variance) && rel(a.hist.variance(), b.hist.variance()) &&
+                   rel(a.hist.mean(), b.hist.mean());
+        };
+        EXPECT(same_est(tsgm::gpu::estimate_process_noise(frames, calib),
+                        estimate_process_noise(frames, calib)),
+               "estimate_process_noise");
+        EXPECT(same_est(tsgm::gpu::estimate_measurement_noise(frames, params),
+                        estimate_measurement_noise(frames, params)),
+               "estimate_measurement_noise");
+        const Image<double> em = accumulate_error_map(frames, calib);
+        const Image<double> eg = tsgm::gpu::accumulate_error_map(frames, calib);
+        EXPECT(std::equal(em.data(), em.data() + em.pixel_count(), eg.data()),
+               "accumulate_error_map");
+        try {
+            tsgm::gpu::estimate_process_noise({frames[0]}, calib);
+            EXPECT(false, "estimate_process_noise with one frame did not throw");
+        } catch (const std::invalid_argument&) {
+        }
+        try {
+            auto broken = frames;
+            broken[1].pose.reset();
+            tsgm::gpu::accumulate_error_map(broken, calib);
+            EXPECT(false, "missing pose did not throw");
+        } catch (const std::invalid_argument&) {
+        }
     }
     std::printf("facade parity: %s (%d failures)\n", fails ? "FAIL" : "ok", fails);
     return fails ? 1 : 0;
