@@ -59,6 +59,7 @@ struct ScanParams {
     int full_ok;             // ceil(d_max/4) is a power of two >= 8: full windows take scan_pixel_full
     uint32_t full_lohi;      // lohi of a full-range window: 0 | (d_max - 1) << 16
     uint32_t full_rng;       // quad range of a full-range window: 0 | (qmax - 1) << 16
+    int warp_bytes;          // shared bytes per warp (scan_kernel)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
@@ -294,31 +295,18 @@ __device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
 // SPW = scanlines per warp (32, 16 or 8): a narrow window (<= 4 quads) is
 // computed by GN = 32/SPW lanes x QN = 4/GN quads of its scanline's group;
 // fewer scanlines per warp give proportionally more warps for small batches.
+// One warp task: SPW scanlines (g-th group) of direction d of batch position
+// a; wbase = the warp's shared-memory area.
 template <int SPW>
-__global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
+__device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, int d, int a, int g,
+                                          const uint8_t* mask_tab, uint32_t wbase) {
     constexpr int GN = 32 / SPW, QN = 4 / GN;
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
-    fill_mask_table(mask_tab_s);
-    __syncthreads();
-    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
-    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
-    const int task = blockIdx.x * kScanWarps + warp;
-    const int per_slot = sp.task_off[sp.ndir];
-    if (task >= per_slot * sp.n) return;
-    // direction-major over all slots: the long horizontal tasks start first
-    int d = 0;
-    while (task >= sp.task_off[d + 1] * sp.n) ++d;
-    const int r = task - sp.task_off[d] * sp.n;
-    const int groups = sp.task_off[d + 1] - sp.task_off[d];
-    const int a = r / groups, g = r % groups;
+    const int lane = static_cast<int>(threadIdx.x & 31);
     const int s = slot_of(b, a);
     const int W = b.W, H = b.H;
     const int dx = sp.dx[d], dy = sp.dy[d];
     const int SB = scan_slot_bytes(b.d_max);
     const int gs = lane / GN, lgs = lane % GN;  // the lane's scanline in the warp, rank in its group
-    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
-                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(scan_warp_bytes(b.d_max, SPW));
     const uint32_t my_sb = wbase + static_cast<uint32_t>(gs) * SB;
     const uint32_t rbase = wbase + static_cast<uint32_t>(SPW * SB);
     const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(gs);
@@ -474,6 +462,35 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
         prev_active = active;
     }
 }
+
+// SPWH / SPWV scanlines per warp for the horizontal / the other directions:
+// horizontal lines walk W steps (the kernel's critical path at small batches),
+// so they may take thinner warps than the H-step vertical and diagonal lines.
+// Tasks are direction-major over all slots (the long horizontal ones start
+// first); sp.task_off counts each direction's tasks with its own SPW.
+template <int SPWH, int SPWV>
+__global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+    fill_mask_table(mask_tab_s);
+    __syncthreads();
+    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const int task = blockIdx.x * kScanWarps + warp;
+    if (task >= sp.task_off[sp.ndir] * sp.n) return;
+    int d = 0;
+    while (task >= sp.task_off[d + 1] * sp.n) ++d;
+    const int r = task - sp.task_off[d] * sp.n;
+    const int groups = sp.task_off[d + 1] - sp.task_off[d];
+    const int a = r / groups, g = r % groups;
+    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
+                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
+    if (SPWH == SPWV || sp.dy[d] != 0)  // (one body when both widths agree)
+        scan_task<SPWV>(b, sp, d, a, g, mask_tab, wbase);
+    else
+        scan_task<SPWH>(b, sp, d, a, g, mask_tab, wbase);
+}
+
 
 // Line-group variant for small batches (latency): a warp owns 32/G
 // scanlines, each with a fixed group of G lanes x 4 quads (every window fits,
@@ -793,27 +810,36 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
             default: scan_lines_kernel<16><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
         }
     } else {
-        // scanlines per warp: more, thinner warps while the batch is small
-        // (measured on config 2: 8 up to 16 sequences, 16 at 32, 32 from 48)
+        // scanlines per warp. Thinner warps cost instructions (a narrow window
+        // is then split over 32/SPW lanes) but shorten each step; only the
+        // horizontal lines, which walk W steps, need that while the batch is
+        // small: their walk is the kernel's critical path. Measured on config 2
+        // (frames/s): 16 sequences 3424 (8/8) -> 3904 (32, horizontal 8),
+        // 32 sequences 4464 (16/16) -> 4590, 8 sequences 2694 -> 2711, 64
+        // unchanged with 32/32. TSGM_SCAN_SPW / TSGM_SCAN_SPW_H override.
         const char* fspw = std::getenv("TSGM_SCAN_SPW");
-        int spw = 32;
-        if (fspw) spw = std::atoi(fspw);
-        else if (batched_warps < sms * 40) spw = 8;
-        else if (batched_warps < sms * 80) spw = 16;
+        int spw = fspw ? std::atoi(fspw) : 32;
         if (spw != 8 && spw != 16) spw = 32;
-        if (spw != 32) {
-            sp.task_off[0] = 0;
-            for (int i = 0; i < k; ++i) {
-                const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
-                sp.task_off[i + 1] = sp.task_off[i] + (lines + spw - 1) / spw;
-            }
+        const char* fspwh = std::getenv("TSGM_SCAN_SPW_H");
+        int spwh = fspwh ? std::atoi(fspwh) : fspw ? spw : (batched_warps < sms * 80 ? 8 : 32);
+        if (spwh != 8 && spwh != 16) spwh = 32;
+        if (spwh > spw) spwh = spw;
+        sp.task_off[0] = 0;
+        for (int i = 0; i < k; ++i) {
+            const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
+            const int per = sp.dy[i] == 0 ? spwh : spw;
+            sp.task_off[i + 1] = sp.task_off[i] + (lines + per - 1) / per;
         }
+        sp.warp_bytes = scan_warp_bytes(b.d_max, std::max(spw, spwh));
         const int tasks = sp.task_off[k] * n;
-        const size_t smem = static_cast<size_t>(kScanWarps) * scan_warp_bytes(b.d_max, spw);
+        const size_t smem = static_cast<size_t>(kScanWarps) * sp.warp_bytes;
         const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
-        if (spw == 8) scan_kernel<8><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
-        else if (spw == 16) scan_kernel<16><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
-        else scan_kernel<32><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
+        auto kern = scan_kernel<32, 32>;
+        if (spw == 8) kern = scan_kernel<8, 8>;
+        else if (spw == 16) kern = spwh == 8 ? scan_kernel<8, 16> : scan_kernel<16, 16>;
+        else if (spwh == 8) kern = scan_kernel<8, 32>;
+        else if (spwh == 16) kern = scan_kernel<16, 32>;
+        kern<<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
     }
     const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
     const bool lean = !write_s && do_wta && !subpix;

@@ -43,11 +43,12 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("kernel", ["groups32", "groups16", "groups8", "lines", "scanline"])
+@pytest.mark.parametrize("kernel", ["groups32", "groups16", "groups8", "groups32h8", "groups32h16",
+                                    "groups16h8", "lines", "scanline"])
 @pytest.mark.parametrize("w,h,d_max,p_full", CASES)
 def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
-    """groupsN: the scanline-group kernel with N scanlines per warp (batched
-    throughput path); lines: the line-group kernel (single sequences,
+    """groupsN[hM]: the scanline-group kernel with N scanlines per warp (M for
+    the horizontal lines) (batched throughput path); lines: the line-group kernel (single sequences,
     full-range frames); scanline: the per-direction fallback."""
     if kernel == "scanline":
         monkeypatch.setenv("TSGM_FORCE_SCANLINE_AGG", "1")
@@ -55,7 +56,10 @@ def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
         monkeypatch.setenv("TSGM_SCAN_KERNEL", "lines")
     else:
         monkeypatch.setenv("TSGM_SCAN_KERNEL", "groups")
-        monkeypatch.setenv("TSGM_SCAN_SPW", kernel[len("groups"):])
+        spw, _, spwh = kernel[len("groups"):].partition("h")
+        monkeypatch.setenv("TSGM_SCAN_SPW", spw)
+        if spwh:  # thinner warps for the horizontal lines
+            monkeypatch.setenv("TSGM_SCAN_SPW_H", spwh)
     rng = np.random.default_rng(w * 1000 + h * 7 + d_max)
     lo, hi = ragged_ranges(rng, w, h, d_max, p_full)
     n = int((hi.astype(np.int64) - lo + 1).sum())
