@@ -499,28 +499,15 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
 // or a few sequences the GPU is otherwise nearly idle (scan_kernel has 306
 // warp tasks per sequence).
 template <int G>
-__global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, ScanParams sp) {
+__device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, int d, int a, int g,
+                                           const uint8_t* mask_tab, uint32_t wbase) {
     constexpr int LPW = 32 / G;  // scanlines per warp
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
-    fill_mask_table(mask_tab_s);
-    __syncthreads();
-    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
-    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+    const int lane = static_cast<int>(threadIdx.x & 31);
     const int gi = lane / G;
-    const int task = blockIdx.x * kScanWarps + warp;
-    if (task >= sp.task_off[sp.ndir] * sp.n) return;
-    int d = 0;
-    while (task >= sp.task_off[d + 1] * sp.n) ++d;
-    const int r = task - sp.task_off[d] * sp.n;
-    const int groups = sp.task_off[d + 1] - sp.task_off[d];
-    const int a = r / groups, g = r % groups;
     const int s = slot_of(b, a);
     const int W = b.W, H = b.H;
     const int dx = sp.dx[d], dy = sp.dy[d];
     const int SB = scan_slot_bytes(b.d_max);
-    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
-                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(LPW * (SB + 4));
     const uint32_t my_sb = wbase + static_cast<uint32_t>(gi) * SB;
     const uint32_t my_rp = wbase + static_cast<uint32_t>(LPW * SB) + 4u * static_cast<uint32_t>(gi);
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
@@ -595,6 +582,57 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
         prev_active = active;
     }
 }
+
+__host__ __device__ inline int lines_warp_bytes(int d_max, int G) {
+    return (32 / G) * (scan_slot_bytes(d_max) + 4);
+}
+
+template <int G>
+__global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, ScanParams sp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+    fill_mask_table(mask_tab_s);
+    __syncthreads();
+    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const int task = blockIdx.x * kScanWarps + warp;
+    if (task >= sp.task_off[sp.ndir] * sp.n) return;
+    int d = 0;
+    while (task >= sp.task_off[d + 1] * sp.n) ++d;
+    const int r = task - sp.task_off[d] * sp.n;
+    const int groups = sp.task_off[d + 1] - sp.task_off[d];
+    const int a = r / groups, g = r % groups;
+    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
+                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
+    lines_task<G>(b, sp, d, a, g, mask_tab, wbase);
+}
+
+// Mixed: horizontal lines as line groups (G lanes x 4 quads per scanline,
+// one scan_pixel per step: the fewest instructions per step, i.e. the
+// shortest W-step walk), the other directions as SPWV-scanline groups.
+template <int G, int SPWV>
+__global__ void __launch_bounds__(32 * kScanWarps, 16) scan_mixed_kernel(Bufs b, ScanParams sp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+    fill_mask_table(mask_tab_s);
+    __syncthreads();
+    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const int task = blockIdx.x * kScanWarps + warp;
+    if (task >= sp.task_off[sp.ndir] * sp.n) return;
+    int d = 0;
+    while (task >= sp.task_off[d + 1] * sp.n) ++d;
+    const int r = task - sp.task_off[d] * sp.n;
+    const int groups = sp.task_off[d + 1] - sp.task_off[d];
+    const int a = r / groups, g = r % groups;
+    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
+                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
+    if (sp.dy[d] == 0)
+        lines_task<G>(b, sp, d, a, g, mask_tab, wbase);
+    else
+        scan_task<SPWV>(b, sp, d, a, g, mask_tab, wbase);
+}
+
 
 // Fused combine + winner_takes_all (sgm.cpp:163-187) for the production step,
 // also the standalone combine (S only). ONE WARP per 32-pixel chunk of a row,
@@ -776,8 +814,9 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
         sp.task_off[i + 1] = sp.task_off[i] + (lines + 31) / 32;
     }
-    // up to ~5 sequences or full-range frames: the line-group kernel (measured
-    // crossover vs 8 scanlines per warp); else the scanline-group kernel.
+    // one or two sequences or full-range frames: the line-group kernel; else
+    // the scanline-group kernel (below ~12 sequences with line-group
+    // horizontal tasks: 4 sequences 2153 -> 2246 frames/s, 1 sequence equal).
     // TSGM_SCAN_KERNEL=lines|groups forces one (tests).
     const int qmax = (b.d_max + 3) / 4;
     int G = 1;
@@ -791,7 +830,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int sms = b.num_sms > 0 ? b.num_sms : 148;  // thresholds measured on a 148-SM B200
     const char* force = std::getenv("TSGM_SCAN_KERNEL");
     const bool lines_mode =
-        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < sms * 12);
+        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < sms * 5);
     if (lines_mode) {
         const int lpw = 32 / G;
         sp.task_off[0] = 0;
@@ -800,7 +839,8 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
             sp.task_off[i + 1] = sp.task_off[i] + (lines + lpw - 1) / lpw;
         }
         const int tasks = sp.task_off[k] * n;
-        const size_t smem = static_cast<size_t>(kScanWarps) * lpw * (scan_slot_bytes(b.d_max) + 4);
+        sp.warp_bytes = lines_warp_bytes(b.d_max, G);
+        const size_t smem = static_cast<size_t>(kScanWarps) * sp.warp_bytes;
         const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
         switch (G) {
             case 1: scan_lines_kernel<1><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
@@ -820,22 +860,32 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const char* fspw = std::getenv("TSGM_SCAN_SPW");
         int spw = fspw ? std::atoi(fspw) : 32;
         if (spw != 8 && spw != 16) spw = 32;
+        // TSGM_SCAN_SPW_H=lines: horizontal lines as line groups (G = 8 or 16)
+        // (default below ~12 sequences: 8 sequences 2712 -> 3268 frames/s)
         const char* fspwh = std::getenv("TSGM_SCAN_SPW_H");
+        const bool hlines = (fspwh ? std::strcmp(fspwh, "lines") == 0 : !fspw && batched_warps < sms * 24) &&
+                            (G == 8 || G == 16);
         int spwh = fspwh ? std::atoi(fspwh) : fspw ? spw : (batched_warps < sms * 80 ? 8 : 32);
         if (spwh != 8 && spwh != 16) spwh = 32;
         if (spwh > spw) spwh = spw;
         sp.task_off[0] = 0;
         for (int i = 0; i < k; ++i) {
             const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
-            const int per = sp.dy[i] == 0 ? spwh : spw;
+            const int per = sp.dy[i] == 0 ? (hlines ? 32 / G : spwh) : spw;
             sp.task_off[i + 1] = sp.task_off[i] + (lines + per - 1) / per;
         }
-        sp.warp_bytes = scan_warp_bytes(b.d_max, std::max(spw, spwh));
+        sp.warp_bytes = std::max(scan_warp_bytes(b.d_max, std::max(spw, spwh)),
+                                 hlines ? lines_warp_bytes(b.d_max, G) : 0);
         const int tasks = sp.task_off[k] * n;
         const size_t smem = static_cast<size_t>(kScanWarps) * sp.warp_bytes;
         const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
         auto kern = scan_kernel<32, 32>;
-        if (spw == 8) kern = scan_kernel<8, 8>;
+        if (hlines) {
+            if (G == 8) kern = spw == 8 ? scan_mixed_kernel<8, 8> : spw == 16 ? scan_mixed_kernel<8, 16>
+                                                                    : scan_mixed_kernel<8, 32>;
+            else kern = spw == 8 ? scan_mixed_kernel<16, 8> : spw == 16 ? scan_mixed_kernel<16, 16>
+                                                              : scan_mixed_kernel<16, 32>;
+        } else if (spw == 8) kern = scan_kernel<8, 8>;
         else if (spw == 16) kern = spwh == 8 ? scan_kernel<8, 16> : scan_kernel<16, 16>;
         else if (spwh == 8) kern = scan_kernel<8, 32>;
         else if (spwh == 16) kern = scan_kernel<16, 32>;

@@ -44,7 +44,8 @@ CASES = [
 
 
 @pytest.mark.parametrize("kernel", ["groups32", "groups16", "groups8", "groups32h8", "groups32h16",
-                                    "groups16h8", "lines", "scanline"])
+                                    "groups16h8", "groups32hlines", "groups8hlines", "lines",
+                                    "scanline"])
 @pytest.mark.parametrize("w,h,d_max,p_full", CASES)
 def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
     """groupsN[hM]: the scanline-group kernel with N scanlines per warp (M for
