@@ -206,13 +206,12 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
 // quads (every lane's 16 levels valid): no masks, no poison, and when the
 // predecessor's window was full range as well its words are used unchecked —
 // the slot's guard words (quads -1 and qmax) hold P2, which is what the masked
-// path reads there. Same arithmetic as scan_pixel<G, 4>.
-template <int G>
+// path reads there. Same arithmetic as scan_pixel<G, Q>.
+template <int G, int Q = 4>
 __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, bool has_pred,
                                                 uint32_t sb, uint32_t rp, const uint8_t* cost,
                                                 uint32_t* out, uint32_t P1x2, uint32_t P2x2,
                                                 uint32_t P2x4, uint32_t full_rng) {
-    constexpr int Q = 4;
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int a0 = lg * Q;
     uint32_t CA[Q], CB[Q], LA[Q], LB[Q];
@@ -498,7 +497,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
 // step. ~8x more warps than scan_kernel, no per-step window classes: for one
 // or a few sequences the GPU is otherwise nearly idle (scan_kernel has 306
 // warp tasks per sequence).
-template <int G>
+template <int G, int Q = 4>
 __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, int d, int a, int g,
                                            const uint8_t* mask_tab, uint32_t wbase) {
     constexpr int LPW = 32 / G;  // scanlines per warp
@@ -572,12 +571,12 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         }
         // the unmasked pass when every active scanline of the warp has a full
         // window of the class size (frames from an empty state)
-        const bool fullw = sp.full_ok == 4 * G && mc.lohi == sp.full_lohi;
+        const bool fullw = sp.full_ok == Q * G && mc.lohi == sp.full_lohi;
         if (__all_sync(0xffffffffu, fullw || !active))
-            scan_pixel_full<G>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                               sp.full_rng);
+            scan_pixel_full<G, Q>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+                                  sp.full_rng);
         else
-            scan_pixel<G, 4>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+            scan_pixel<G, Q>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
                              mask_tab);
         prev_active = active;
     }
@@ -607,10 +606,37 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
     lines_task<G>(b, sp, d, a, g, mask_tab, wbase);
 }
 
+// Line groups everywhere, the horizontal lines with wider groups (GH lanes x
+// QH quads): the W-step horizontal walk is a chain of dependent
+// instructions, so fewer instructions per step (fewer quads per lane) make it
+// shorter. For one or two sequences.
+template <int G, int GH, int QH>
+__global__ void __launch_bounds__(32 * kScanWarps) scan_lines_mixed_kernel(Bufs b, ScanParams sp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
+    fill_mask_table(mask_tab_s);
+    __syncthreads();
+    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const int task = blockIdx.x * kScanWarps + warp;
+    if (task >= sp.task_off[sp.ndir] * sp.n) return;
+    int d = 0;
+    while (task >= sp.task_off[d + 1] * sp.n) ++d;
+    const int r = task - sp.task_off[d] * sp.n;
+    const int groups = sp.task_off[d + 1] - sp.task_off[d];
+    const int a = r / groups, g = r % groups;
+    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
+                           static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
+    if (sp.dy[d] == 0)
+        lines_task<GH, QH>(b, sp, d, a, g, mask_tab, wbase);
+    else
+        lines_task<G, 4>(b, sp, d, a, g, mask_tab, wbase);
+}
+
 // Mixed: horizontal lines as line groups (G lanes x 4 quads per scanline,
 // one scan_pixel per step: the fewest instructions per step, i.e. the
 // shortest W-step walk), the other directions as SPWV-scanline groups.
-template <int G, int SPWV>
+template <int GH, int QH, int SPWV>
 __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_mixed_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
@@ -628,7 +654,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_mixed_kernel(Bufs b,
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (sp.dy[d] == 0)
-        lines_task<G>(b, sp, d, a, g, mask_tab, wbase);
+        lines_task<GH, QH>(b, sp, d, a, g, mask_tab, wbase);
     else
         scan_task<SPWV>(b, sp, d, a, g, mask_tab, wbase);
 }
@@ -833,16 +859,26 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < sms * 5);
     if (lines_mode) {
         const int lpw = 32 / G;
+        // horizontal lines with GH-lane groups (TSGM_LINES_H=8|16|32; G = 8 or 16 only)
+        const char* flh = std::getenv("TSGM_LINES_H");
+        int gh = flh ? std::atoi(flh) : 32;  // (1 sequence: 845 -> 1138 frames/s)
+        if ((G != 8 && G != 16) || gh <= G || (gh != 16 && gh != 32)) gh = G;
         sp.task_off[0] = 0;
         for (int i = 0; i < k; ++i) {
             const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
-            sp.task_off[i + 1] = sp.task_off[i] + (lines + lpw - 1) / lpw;
+            const int per = sp.dy[i] == 0 ? 32 / gh : lpw;
+            sp.task_off[i + 1] = sp.task_off[i] + (lines + per - 1) / per;
         }
         const int tasks = sp.task_off[k] * n;
         sp.warp_bytes = lines_warp_bytes(b.d_max, G);
         const size_t smem = static_cast<size_t>(kScanWarps) * sp.warp_bytes;
         const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
-        switch (G) {
+        if (gh != G) {
+            auto kern = G == 8 ? (gh == 16 ? scan_lines_mixed_kernel<8, 16, 2>
+                                           : scan_lines_mixed_kernel<8, 32, 1>)
+                               : scan_lines_mixed_kernel<16, 32, 2>;
+            kern<<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
+        } else switch (G) {
             case 1: scan_lines_kernel<1><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
             case 2: scan_lines_kernel<2><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
             case 4: scan_lines_kernel<4><<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp); break;
@@ -865,26 +901,39 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const char* fspwh = std::getenv("TSGM_SCAN_SPW_H");
         const bool hlines = (fspwh ? std::strcmp(fspwh, "lines") == 0 : !fspw && batched_warps < sms * 24) &&
                             (G == 8 || G == 16);
+        // the line groups' width: G lanes x 4 quads, or 32 lanes x 4G/32 quads
+        // (fewer instructions per step, 4x the warps): 32 up to ~4 sequences
+        // (4: 2255 -> 2318 frames/s; 8: 3244 -> 2613); TSGM_MIXED_GH=8|32
+        const char* fmg = std::getenv("TSGM_MIXED_GH");
+        const int mgh = fmg ? std::atoi(fmg) : (batched_warps < sms * 9 ? 32 : 8);
+        const int hg = mgh == 32 ? 32 : G;
         int spwh = fspwh ? std::atoi(fspwh) : fspw ? spw : (batched_warps < sms * 80 ? 8 : 32);
         if (spwh != 8 && spwh != 16) spwh = 32;
         if (spwh > spw) spwh = spw;
         sp.task_off[0] = 0;
         for (int i = 0; i < k; ++i) {
             const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
-            const int per = sp.dy[i] == 0 ? (hlines ? 32 / G : spwh) : spw;
+            const int per = sp.dy[i] == 0 ? (hlines ? 32 / hg : spwh) : spw;
             sp.task_off[i + 1] = sp.task_off[i] + (lines + per - 1) / per;
         }
         sp.warp_bytes = std::max(scan_warp_bytes(b.d_max, std::max(spw, spwh)),
-                                 hlines ? lines_warp_bytes(b.d_max, G) : 0);
+                                 hlines ? lines_warp_bytes(b.d_max, hg) : 0);
         const int tasks = sp.task_off[k] * n;
         const size_t smem = static_cast<size_t>(kScanWarps) * sp.warp_bytes;
         const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
         auto kern = scan_kernel<32, 32>;
         if (hlines) {
-            if (G == 8) kern = spw == 8 ? scan_mixed_kernel<8, 8> : spw == 16 ? scan_mixed_kernel<8, 16>
-                                                                    : scan_mixed_kernel<8, 32>;
-            else kern = spw == 8 ? scan_mixed_kernel<16, 8> : spw == 16 ? scan_mixed_kernel<16, 16>
-                                                              : scan_mixed_kernel<16, 32>;
+            if (hg == 32)
+                kern = G == 8 ? (spw == 8 ? scan_mixed_kernel<32, 1, 8> : spw == 16 ? scan_mixed_kernel<32, 1, 16>
+                                                                         : scan_mixed_kernel<32, 1, 32>)
+                              : (spw == 8 ? scan_mixed_kernel<32, 2, 8> : spw == 16 ? scan_mixed_kernel<32, 2, 16>
+                                                                         : scan_mixed_kernel<32, 2, 32>);
+            else if (G == 8)
+                kern = spw == 8 ? scan_mixed_kernel<8, 4, 8> : spw == 16 ? scan_mixed_kernel<8, 4, 16>
+                                                               : scan_mixed_kernel<8, 4, 32>;
+            else
+                kern = spw == 8 ? scan_mixed_kernel<16, 4, 8> : spw == 16 ? scan_mixed_kernel<16, 4, 16>
+                                                                : scan_mixed_kernel<16, 4, 32>;
         } else if (spw == 8) kern = scan_kernel<8, 8>;
         else if (spw == 16) kern = spwh == 8 ? scan_kernel<8, 16> : scan_kernel<16, 16>;
         else if (spwh == 8) kern = scan_kernel<8, 32>;

@@ -44,8 +44,8 @@ CASES = [
 
 
 @pytest.mark.parametrize("kernel", ["groups32", "groups16", "groups8", "groups32h8", "groups32h16",
-                                    "groups16h8", "groups32hlines", "groups8hlines", "lines",
-                                    "scanline"])
+                                    "groups16h8", "groups32hlines", "groups8hlines", "groups32hlines8", "lines",
+                                    "lines16h", "lines32h", "scanline"])
 @pytest.mark.parametrize("w,h,d_max,p_full", CASES)
 def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
     """groupsN[hM]: the scanline-group kernel with N scanlines per warp (M for
@@ -53,11 +53,16 @@ def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
     full-range frames); scanline: the per-direction fallback."""
     if kernel == "scanline":
         monkeypatch.setenv("TSGM_FORCE_SCANLINE_AGG", "1")
-    elif kernel == "lines":
+    elif kernel.startswith("lines"):
         monkeypatch.setenv("TSGM_SCAN_KERNEL", "lines")
+        if kernel != "lines":  # wider groups for the horizontal lines
+            monkeypatch.setenv("TSGM_LINES_H", kernel[len("lines"):-1])
     else:
         monkeypatch.setenv("TSGM_SCAN_KERNEL", "groups")
         spw, _, spwh = kernel[len("groups"):].partition("h")
+        if spwh.startswith("lines") and spwh != "lines":  # line-group width
+            monkeypatch.setenv("TSGM_MIXED_GH", spwh[len("lines"):])
+            spwh = "lines"
         monkeypatch.setenv("TSGM_SCAN_SPW", spw)
         if spwh:  # thinner warps for the horizontal lines
             monkeypatch.setenv("TSGM_SCAN_SPW_H", spwh)
