@@ -861,7 +861,10 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const int lpw = 32 / G;
         // horizontal lines with GH-lane groups (TSGM_LINES_H=8|16|32; G = 8 or 16 only)
         const char* flh = std::getenv("TSGM_LINES_H");
-        int gh = flh ? std::atoi(flh) : 32;  // (1 sequence: 845 -> 1138 frames/s)
+        // (1 sequence: 845 -> 1138 frames/s; not for large full-range batches,
+        // where the 4x warps only add instructions: 64 sequences' frame 0
+        // 21.1 -> 22.9 ms)
+        int gh = flh ? std::atoi(flh) : (batched_warps < sms * 9 ? 32 : G);
         if ((G != 8 && G != 16) || gh <= G || (gh != 16 && gh != 32)) gh = G;
         sp.task_off[0] = 0;
         for (int i = 0; i < k; ++i) {
