@@ -101,11 +101,15 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // min over the G lanes of a group; all 32 lanes must call it.
 template <int G>
 __device__ __forceinline__ uint32_t group_min(uint32_t v) {
-    if (G == 1) return v;
-    if (G == 32) return __reduce_min_sync(0xffffffffu, v);
+    if constexpr (G == 1) {
+        return v;
+    } else if constexpr (G == 32) {
+        return __reduce_min_sync(0xffffffffu, v);
+    } else {
 #pragma unroll
-    for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
+        for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+    }
 }
 
 // lohi = lo | hi << 16, cell / qo = cell and quad offsets, nq = quads of the
@@ -278,17 +282,28 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, boo
 
 // invalid-level masks: entry (lrel, hrel) covers 16 levels = 4 quads x
 // (ivA, ivB); level j is invalid iff j < lrel or j > hrel (hrel in -1..16)
-__device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
-    for (int e = threadIdx.x; e < 4 * 18 * 8; e += blockDim.x) {
-        const int lrel = e / (18 * 8), hrel = (e / 8) % 18 - 1, word = e % 8;
-        const int t = word >> 1, half0 = 4 * t + 2 * (word & 1);
-        uint32_t m = 0u;
-        for (int h = 0; h < 2; ++h) {
-            const int j = half0 + h;
-            if (j < lrel || j > hrel) m |= 0xffffu << (16 * h);
+struct alignas(16) MaskTable {
+    uint32_t v[4 * 18 * 8];
+    constexpr MaskTable() : v() {
+        for (int e = 0; e < 4 * 18 * 8; ++e) {
+            const int lrel = e / (18 * 8), hrel = (e / 8) % 18 - 1, word = e % 8;
+            const int t = word >> 1, half0 = 4 * t + 2 * (word & 1);
+            uint32_t m = 0u;
+            for (int h = 0; h < 2; ++h) {
+                const int j = half0 + h;
+                if (j < lrel || j > hrel) m |= 0xffffu << (16 * h);
+            }
+            v[e] = m;
         }
-        tab[e] = m;
     }
+};
+// built at compile time; each CTA copies it to shared memory (16-byte loads)
+__device__ const MaskTable g_mask_table{};
+
+__device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
+    const uint4* src = reinterpret_cast<const uint4*>(g_mask_table.v);
+    uint4* dst = reinterpret_cast<uint4*>(tab);
+    for (int e = threadIdx.x; e < 4 * 18 * 8 / 4; e += blockDim.x) dst[e] = __ldg(src + e);
 }
 
 // SPW = scanlines per warp (32, 16 or 8): a narrow window (<= 4 quads) is
@@ -374,7 +389,10 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         const PixMeta mc = m1;
         act1 = act2;
         m1 = m2;
-        if (act1 && lgs == 0) {  // step k+1's window towards L1 (its metadata arrived a step ago)
+#ifndef SCAN_PREFETCH
+#define SCAN_PREFETCH 1
+#endif
+        if (SCAN_PREFETCH && act1 && lgs == 0) {  // step k+1's window towards L1 (its metadata arrived a step ago)
             const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
             const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
             const uint8_t* c0 = cost + m1.cell;
