@@ -914,13 +914,20 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         // (frames/s): 16 sequences 3424 (8/8) -> 3904 (32, horizontal 8),
         // 32 sequences 4464 (16/16) -> 4590, 8 sequences 2694 -> 2711, 64
         // unchanged with 32/32. TSGM_SCAN_SPW / TSGM_SCAN_SPW_H override.
+        // Tall images (long vertical walks too: config 4's 2048x1024 chunks of
+        // 16 sequences) keep one width for every direction, from the batch
+        // size: 16/16 522-534 frames/s there vs 502 (32, horizontal 16) and
+        // 485 (32, horizontal 8).
+        const bool tall = b.H >= 768;
         const char* fspw = std::getenv("TSGM_SCAN_SPW");
-        int spw = fspw ? std::atoi(fspw) : 32;
+        int spw = fspw ? std::atoi(fspw)
+                       : !tall ? 32 : batched_warps < sms * 40 ? 8 : batched_warps < sms * 80 ? 16 : 32;
         if (spw != 8 && spw != 16) spw = 32;
         // TSGM_SCAN_SPW_H=lines: horizontal lines as line groups (G = 8 or 16)
         // (default below ~12 sequences: 8 sequences 2712 -> 3268 frames/s)
         const char* fspwh = std::getenv("TSGM_SCAN_SPW_H");
-        const bool hlines = (fspwh ? std::strcmp(fspwh, "lines") == 0 : !fspw && batched_warps < sms * 24) &&
+        const bool hlines = (fspwh ? std::strcmp(fspwh, "lines") == 0
+                                   : !fspw && !tall && batched_warps < sms * 24) &&
                             (G == 8 || G == 16);
         // the line groups' width: G lanes x 4 quads, or 32 lanes x 4G/32 quads
         // (fewer instructions per step, 4x the warps): 32 up to ~4 sequences
@@ -928,7 +935,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const char* fmg = std::getenv("TSGM_MIXED_GH");
         const int mgh = fmg ? std::atoi(fmg) : (batched_warps < sms * 9 ? 32 : 8);
         const int hg = mgh == 32 ? 32 : G;
-        int spwh = fspwh ? std::atoi(fspwh) : fspw ? spw : (batched_warps < sms * 80 ? 8 : 32);
+        int spwh = fspwh ? std::atoi(fspwh) : (fspw || tall) ? spw : (batched_warps < sms * 80 ? 8 : 32);
         if (spwh != 8 && spwh != 16) spwh = 32;
         if (spwh > spw) spwh = spw;
         sp.task_off[0] = 0;
