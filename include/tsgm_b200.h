@@ -337,6 +337,28 @@ int tsgm_calib_release(void);
 int tsgm_accumulate_error_map(int32_t n_frames, int32_t w, int32_t h, const double* gt,
                               const double* poses12, const tsgm_stereo_calib* calib, double* acc);
 
+/* ------------------------------------------------------------------------
+ * Export formats (dataset.hpp:51-59, dataset.cpp:229-269):
+ * the KITTI 16-bit disparity PNG (round(256 d), 0 = invalid; a value that
+ * does not fit fails with the reference's message at the first such pixel in
+ * raster order) and boxes.txt. The quantisation runs on the GPU; the PNG
+ * container (16-bit grayscale, zlib) is written on the host.
+ * ------------------------------------------------------------------------ */
+/* write_disparity_png(const Image<double>&)'s 16-bit image, no file */
+int tsgm_quantize_disparity(const double* disp, int32_t w, int32_t h, uint16_t* raw);
+/* write_disparity_png(const DisparityMap&)'s 16-bit image, no file */
+int tsgm_quantize_disparity_map(const int32_t* d, const uint8_t* valid, int32_t w, int32_t h,
+                                uint16_t* raw);
+int tsgm_write_disparity_png(const char* path, const double* disp, int32_t w, int32_t h);
+int tsgm_write_disparity_png_map(const char* path, const int32_t* d, const uint8_t* valid,
+                                 int32_t w, int32_t h);
+/* The slot's export map (StepResult::export_map) straight from the device, as
+ * tsgm_main's run command writes it (tsgm_main.cpp:157). */
+int tsgm_write_export_png(tsgm_ctx* ctx, int32_t slot, const char* path);
+/* write_boxes: boxes of n_frames frames back to back, counts[f] per frame */
+int tsgm_write_boxes(const char* path, const tsgm_box* boxes, const int64_t* counts,
+                     int32_t n_frames);
+
 #ifdef __cplusplus
 }
 #endif

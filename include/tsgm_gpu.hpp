@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "tsgm/dataset.hpp"
 #include "tsgm/geometry.hpp"
 #include "tsgm/matching_cost.hpp"
 #include "tsgm/motion_detect.hpp"
@@ -381,6 +382,28 @@ inline Image<double> accumulate_error_map(const std::vector<SequenceFrame>& fram
     detail::check(tsgm_accumulate_error_map(f.n, f.w, f.h, f.gt.data(), f.poses.data(), &c,
                                             acc.data()));
     return acc;
+}
+
+// ---- export formats (dataset.hpp:51-59) ----
+// write_disparity_png: quantised on the GPU, 16-bit grayscale PNG on the host
+// (not libpng's bytes; the decoded samples are the reference's).
+inline void write_disparity_png(const std::string& path, const Image<double>& disp) {
+    detail::check(tsgm_write_disparity_png(path.c_str(), disp.data(), disp.width(), disp.height()));
+}
+inline void write_disparity_png(const std::string& path, const DisparityMap& dm) {
+    detail::check(tsgm_write_disparity_png_map(path.c_str(), dm.d.data(), dm.valid.data(),
+                                               dm.d.width(), dm.d.height()));
+}
+inline void write_boxes(const std::string& path,
+                        const std::vector<std::vector<DetectionBox>>& per_frame) {
+    std::vector<tsgm_box> flat;
+    std::vector<std::int64_t> counts;
+    for (const auto& f : per_frame) {
+        counts.push_back(static_cast<std::int64_t>(f.size()));
+        for (const DetectionBox& b : f) flat.push_back(tsgm_box{b.x0, b.y0, b.x1, b.y1, b.score});
+    }
+    detail::check(tsgm_write_boxes(path.c_str(), flat.data(), counts.data(),
+                                   static_cast<std::int32_t>(counts.size())));
 }
 
 // Batched, device-resident production path.

@@ -11,6 +11,7 @@
 #include <random>
 #include <stdexcept>
 
+#include "tsgm/dataset.hpp"
 #include "tsgm/noise_calib.hpp"
 #include "tsgm/temporal_filter.hpp"
 #include "tsgm_gpu.hpp"
@@ -232,6 +233,41 @@ int main() {
             tsgm::gpu::accumulate_error_map(broken, calib);
             EXPECT(false, "missing pose did not throw");
         } catch (const std::invalid_argument&) {
+        }
+    }
+    {  // export formats: boxes.txt byte for byte; the PNG writer round trip is
+       // checked by tests/test_export.py (the reference's libpng writer is
+       // replaced by oracle/io_shim.cpp in this build)
+        std::vector<std::vector<DetectionBox>> per_frame(3);
+        per_frame[0].push_back(DetectionBox{3, 4, 30, 40, 1.0 / 3.0});
+        per_frame[2].push_back(DetectionBox{100, 7, 160, 70, 12.5});
+        per_frame[2].push_back(DetectionBox{0, 0, 20, 20, 1e-7});
+        write_boxes("/tmp/tsgm_facade_boxes_ref.txt", per_frame);
+        tsgm::gpu::write_boxes("/tmp/tsgm_facade_boxes_gpu.txt", per_frame);
+        auto slurp = [](const char* p) {
+            std::FILE* f = std::fopen(p, "rb");
+            std::string out;
+            if (!f) return out;
+            char buf[4096];
+            size_t n;
+            while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) out.append(buf, n);
+            std::fclose(f);
+            return out;
+        };
+        const std::string a = slurp("/tmp/tsgm_facade_boxes_ref.txt");
+        EXPECT(!a.empty() && a == slurp("/tmp/tsgm_facade_boxes_gpu.txt"), "write_boxes");
+        Image<double> disp(16, 8, 0.0);
+        disp(3, 2) = 12.25;
+        tsgm::gpu::write_disparity_png("/tmp/tsgm_facade_disp.png", disp);
+        EXPECT(slurp("/tmp/tsgm_facade_disp.png").size() > 8, "write_disparity_png");
+        try {
+            disp(5, 5) = 300.0;
+            tsgm::gpu::write_disparity_png("/tmp/tsgm_facade_disp_bad.png", disp);
+            EXPECT(false, "non-encodable disparity did not throw");
+        } catch (const std::invalid_argument& e) {
+            EXPECT(std::string(e.what()) ==
+                       "write_disparity_png: disparity 300.000000 not encodable at (5, 5)",
+                   "write_disparity_png message");
         }
     }
     std::printf("facade parity: %s (%d failures)\n", fails ? "FAIL" : "ok", fails);

@@ -869,6 +869,33 @@ Port.measurement_noise = _port_measurement_noise
 Port.error_map = _port_error_map
 
 
+# ------------------------------------------------ export formats (row 2)
+def quantize_disparity(disp):
+    """write_disparity_png's quantisation (dataset.cpp:229-244), numpy
+    restatement: d == 0 -> 0; v = std::lround(d * 256.0) (half away from
+    zero; NaN/out of range -> LONG_MIN); 0 < v <= 65535 else the reference's
+    std::invalid_argument at the first such pixel in raster order."""
+    disp = _f64(disp)
+    x = disp * 256.0
+    t = np.trunc(x)
+    with np.errstate(invalid="ignore"):
+        t = t + np.where(np.abs(x - t) >= 0.5, np.copysign(1.0, x), 0.0)
+        ok_range = (t >= -9.223372036854775808e18) & (t < 9.223372036854775808e18)
+    v = np.where(ok_range, t, -9.223372036854775808e18)
+    bad = (disp != 0.0) & ((v <= 0) | (v > 65535))
+    if bad.any():
+        i = int(np.flatnonzero(bad.ravel())[0])
+        h, w = disp.shape
+        raise ValueError(f"write_disparity_png: disparity {disp.ravel()[i]:f} not encodable at "
+                         f"({i % w}, {i // w})")
+    return np.where(disp == 0.0, 0, v).astype(np.uint16)
+
+
+def quantize_disparity_map(d, valid):
+    """write_disparity_png(const DisparityMap&) (dataset.cpp:246-254)."""
+    return quantize_disparity(np.where(_u8(valid) != 0, np.asarray(d, np.float64), 0.0))
+
+
 _port = None
 _reference = None
 

@@ -27,7 +27,7 @@ CUDA_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-f
               f"-I{INCLUDE}", f"-I{CSRC}"]
 
 CU_SOURCES = ["stereo_kernels.cu", "temporal_kernels.cu", "aggregate_kernels.cu",
-              "aggregate_sweep.cu", "detect.cu", "noise.cu", "runtime.cu"]
+              "aggregate_sweep.cu", "detect.cu", "noise.cu", "export.cu", "runtime.cu"]
 
 
 def lib_path(name: str) -> str:
@@ -74,7 +74,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
                 cmd.insert(1, "-Xptxas=-v")
             subprocess.run(cmd, check=True)
     if force or _stale(out, objs):
-        subprocess.run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"], check=True)
+        subprocess.run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart", "-lz"], check=True)
     return out
 
 

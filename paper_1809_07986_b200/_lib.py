@@ -60,6 +60,8 @@ EXPORTS = [
     "tsgm_detect_moving_objects", "tsgm_detect", "tsgm_count_outliers",
     "tsgm_count_outliers_batch", "tsgm_calib_bins", "tsgm_estimate_process_noise",
     "tsgm_estimate_measurement_noise", "tsgm_accumulate_error_map", "tsgm_calib_release",
+    "tsgm_quantize_disparity", "tsgm_quantize_disparity_map", "tsgm_write_disparity_png",
+    "tsgm_write_disparity_png_map", "tsgm_write_export_png", "tsgm_write_boxes",
 ]
 
 
@@ -150,6 +152,14 @@ def load():
             C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
             C.POINTER(SgmParamsC), co, ne]
         lib.tsgm_calib_release.argtypes = []
+        lib.tsgm_quantize_disparity.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        lib.tsgm_quantize_disparity_map.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                                    C.c_void_p]
+        lib.tsgm_write_disparity_png.argtypes = [C.c_char_p, C.c_void_p, C.c_int32, C.c_int32]
+        lib.tsgm_write_disparity_png_map.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                                     C.c_int32]
+        lib.tsgm_write_export_png.argtypes = [C.c_void_p, C.c_int32, C.c_char_p]
+        lib.tsgm_write_boxes.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int32]
         lib.tsgm_accumulate_error_map.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                                   C.c_void_p, C.POINTER(StereoCalibC), C.c_void_p]
         _lib = lib

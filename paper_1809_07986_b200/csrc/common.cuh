@@ -12,6 +12,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include "../../include/tsgm_b200.h"
 
 namespace tsgm {
@@ -93,14 +95,14 @@ __device__ __forceinline__ double key_double(unsigned long long k) {
 // static_cast<int>(std::lround(x)) as compiled for x86-64 (geometry.cpp:143-144,
 // temporal_filter.cpp:263): round half away from zero to long; out-of-range or
 // NaN yields LONG_MIN (cvttsd2si); the int cast keeps the low 32 bits.
-__device__ __forceinline__ int x86_lround_int(double x) {
+__device__ __forceinline__ long long x86_lround_long(double x) {
     double t = trunc(x);
     if (fabs(x - t) >= 0.5) t += copysign(1.0, x);
-    long long v;
-    if (t >= -9223372036854775808.0 && t < 9223372036854775808.0)
-        v = static_cast<long long>(t);
-    else
-        v = static_cast<long long>(0x8000000000000000ull);
+    if (t >= -9223372036854775808.0 && t < 9223372036854775808.0) return static_cast<long long>(t);
+    return static_cast<long long>(0x8000000000000000ull);
+}
+__device__ __forceinline__ int x86_lround_int(double x) {
+    const long long v = x86_lround_long(x);
     return static_cast<int>(static_cast<unsigned int>(static_cast<unsigned long long>(v)));
 }
 
@@ -174,6 +176,16 @@ void launch_error_hist_wta(const Bufs& b, const double* gt, int n, const HistSpe
                            const HistAcc& acc, Launch L);
 void launch_error_map(const Bufs& b, const double* gt, int n, double* acc,
                       unsigned long long* overlap, Launch L);
+
+// Export formats (export.cu): write_disparity_png's
+// 16-bit quantisation on the device. disp (f64) or (d, valid) maps at
+// base + (slots ? slots[a] : a) * P; raw u16 out at raw + a * P; first_bad[a]
+// = the first raster index not encodable (or ~0), zeroed by the launcher.
+void launch_quantize_disparity(const double* disp, const int32_t* d, const uint8_t* valid,
+                               size_t P, int n, const int* slots, uint16_t* raw,
+                               unsigned long long* first_bad, Launch L);
+// Host PNG encoder (16-bit grayscale, zlib) and boxes.txt writer.
+void write_png16(const std::string& path, const uint16_t* raw, int w, int h);
 
 // Box detector (detect.cu), SURVEY §8(f) row 1.
 constexpr int kMaxDetectWindows = 16;

@@ -1817,3 +1817,152 @@ int tsgm_calib_release(void) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- export formats
+// SURVEY §8(f) row 2 (dataset.cpp:229-269): device quantisation (export.cu)
+// + host PNG / boxes.txt writers.
+namespace {
+
+std::string std_to_string(double v) {  // std::to_string(double): "%f"
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%f", v);
+    return buf;
+}
+
+// write_disparity_png's quantisation of one host map (disp, or d + valid)
+void quantize_host(const double* disp, const int32_t* d, const uint8_t* valid, int w, int h,
+                   uint16_t* raw) {
+    if (w < 0 || h < 0 || !raw || (!disp && (!d || !valid))) bad("write_disparity_png: bad arguments");
+    const size_t P = static_cast<size_t>(w) * h;
+    if (P == 0) return;
+    DevScratch s;
+    const double* ddisp = nullptr;
+    const int32_t* dd = nullptr;
+    const uint8_t* dv = nullptr;
+    if (disp) {
+        double* t = s.alloc<double>(P);
+        CK(cudaMemcpyAsync(t, disp, 8 * P, cudaMemcpyHostToDevice, s.st));
+        ddisp = t;
+    } else {
+        int32_t* t = s.alloc<int32_t>(P);
+        uint8_t* u = s.alloc<uint8_t>(P);
+        CK(cudaMemcpyAsync(t, d, 4 * P, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(u, valid, P, cudaMemcpyHostToDevice, s.st));
+        dd = t;
+        dv = u;
+    }
+    uint16_t* draw = s.alloc<uint16_t>(P);
+    unsigned long long* fb = s.alloc<unsigned long long>(1);
+    launch_quantize_disparity(ddisp, dd, dv, P, 1, nullptr, draw, fb, s.L());
+    CK(cudaGetLastError());
+    unsigned long long first = 0;
+    CK(cudaMemcpyAsync(raw, draw, 2 * P, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaMemcpyAsync(&first, fb, sizeof first, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    if (first != ~0ull) {
+        const double v = disp ? disp[first] : static_cast<double>(d[first]);
+        const std::string msg = "write_disparity_png: disparity " + std_to_string(v) +
+                                " not encodable at (" + std::to_string(first % w) + ", " +
+                                std::to_string(first / w) + ")";
+        bad(msg.c_str());
+    }
+}
+
+void write_png_checked(const char* path, const uint16_t* raw, int w, int h) {
+    if (!path) bad("write_disparity_png: null path");
+    if (w <= 0 || h <= 0) throw std::runtime_error(std::string(path) + ": PNG encode error");
+    write_png16(path, raw, w, h);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsgm_quantize_disparity(const double* disp, int32_t w, int32_t h, uint16_t* raw) {
+    return guarded([&] {
+        if (!disp) bad("write_disparity_png: null map");
+        quantize_host(disp, nullptr, nullptr, w, h, raw);
+    });
+}
+
+int tsgm_quantize_disparity_map(const int32_t* d, const uint8_t* valid, int32_t w, int32_t h,
+                                uint16_t* raw) {
+    return guarded([&] {
+        if (!d || !valid) bad("write_disparity_png: null map");
+        quantize_host(nullptr, d, valid, w, h, raw);
+    });
+}
+
+int tsgm_write_disparity_png(const char* path, const double* disp, int32_t w, int32_t h) {
+    return guarded([&] {
+        if (!disp) bad("write_disparity_png: null map");
+        std::vector<uint16_t> raw(static_cast<size_t>(std::max(0, w)) * std::max(0, h));
+        quantize_host(disp, nullptr, nullptr, w, h, raw.data());
+        write_png_checked(path, raw.data(), w, h);
+    });
+}
+
+int tsgm_write_disparity_png_map(const char* path, const int32_t* d, const uint8_t* valid,
+                                 int32_t w, int32_t h) {
+    return guarded([&] {
+        if (!d || !valid) bad("write_disparity_png: null map");
+        std::vector<uint16_t> raw(static_cast<size_t>(std::max(0, w)) * std::max(0, h));
+        quantize_host(nullptr, d, valid, w, h, raw.data());
+        write_png_checked(path, raw.data(), w, h);
+    });
+}
+
+int tsgm_write_export_png(tsgm_ctx* ctx, int32_t slot, const char* path) {
+    return guarded([&] {
+        if (!ctx || !path) bad("tsgm_write_export_png: null argument");
+        if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_write_export_png: slot out of range");
+        CK(cudaSetDevice(ctx->device));
+        const size_t P = ctx->P;
+        DevScratch s;
+        CK(cudaStreamWaitEvent(s.st, ctx->ev_frame, 0));  // the slot's last step
+        uint16_t* draw = s.alloc<uint16_t>(P);
+        unsigned long long* fb = s.alloc<unsigned long long>(1);
+        const int sl = slot;
+        int* dslot = s.alloc<int>(1);
+        CK(cudaMemcpyAsync(dslot, &sl, sizeof sl, cudaMemcpyHostToDevice, s.st));
+        launch_quantize_disparity(nullptr, ctx->b.ed, ctx->b.ev, P, 1, dslot, draw, fb, s.L());
+        CK(cudaGetLastError());
+        std::vector<uint16_t> raw(P);
+        unsigned long long first = 0;
+        CK(cudaMemcpyAsync(raw.data(), draw, 2 * P, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(&first, fb, sizeof first, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        if (first != ~0ull) {
+            int32_t v = 0;
+            CK(cudaMemcpy(&v, ctx->b.ed + static_cast<size_t>(slot) * P + first, 4,
+                          cudaMemcpyDeviceToHost));
+            const std::string msg = "write_disparity_png: disparity " +
+                                    std_to_string(static_cast<double>(v)) + " not encodable at (" +
+                                    std::to_string(first % ctx->W) + ", " +
+                                    std::to_string(first / ctx->W) + ")";
+            bad(msg.c_str());
+        }
+        write_png_checked(path, raw.data(), ctx->W, ctx->H);
+    });
+}
+
+int tsgm_write_boxes(const char* path, const tsgm_box* boxes, const int64_t* counts,
+                     int32_t n_frames) {
+    return guarded([&] {
+        if (!path || n_frames < 0 || (n_frames > 0 && !counts)) bad("write_boxes: bad arguments");
+        std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "w"), &std::fclose);
+        if (!f) throw std::runtime_error(std::string("write_boxes: cannot open ") + path);
+        bool ok = std::fputs("# frame x0 y0 x1 y1 score\n", f.get()) >= 0;
+        int64_t k = 0;
+        for (int32_t fr = 0; fr < n_frames; ++fr)
+            for (int64_t i = 0; i < counts[fr]; ++i, ++k) {
+                const tsgm_box& b = boxes[k];
+                ok = ok && std::fprintf(f.get(), "%d %d %d %d %d %.17g\n", fr, b.x0, b.y0, b.x1,
+                                        b.y1, b.score) > 0;
+            }
+        if (!ok || std::fflush(f.get()) != 0)
+            throw std::runtime_error(std::string("write_boxes: write failed for ") + path);
+    });
+}
+
+}  // extern "C"

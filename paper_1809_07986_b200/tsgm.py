@@ -398,6 +398,115 @@ def outlier_rate(d, valid, gt, opts=None):
     return 100.0 * out / ev
 
 
+# ----------------------------------------------------------- export formats
+# dataset.hpp:51-59 (write_disparity_png, write_boxes).
+def _quant_args(disp_or_map):
+    if isinstance(disp_or_map, tuple):  # DisparityMap: (d, valid)
+        d, v = _i32(disp_or_map[0]), _u8(disp_or_map[1])
+        if d.shape != v.shape:
+            raise ValueError("write_disparity_png: map size mismatch")
+        return None, d, v
+    return _f64(disp_or_map), None, None
+
+
+def quantize_disparity(disp_or_map):
+    """write_disparity_png's 16-bit image (round(256 d), 0 = invalid) on the
+    GPU, without the file: a f64 map, or a DisparityMap as (d, valid)."""
+    disp, d, v = _quant_args(disp_or_map)
+    h, w = (disp if disp is not None else d).shape
+    raw = np.zeros((h, w), np.uint16)
+    lib = _lib.load()
+    if disp is not None:
+        check(lib.tsgm_quantize_disparity(ptr(disp), w, h, ptr(raw)))
+    else:
+        check(lib.tsgm_quantize_disparity_map(ptr(d), ptr(v), w, h, ptr(raw)))
+    return raw
+
+
+def write_disparity_png(path, disp_or_map):
+    """write_disparity_png (dataset.cpp:229-254): KITTI 16-bit PNG."""
+    disp, d, v = _quant_args(disp_or_map)
+    h, w = (disp if disp is not None else d).shape
+    lib = _lib.load()
+    if disp is not None:
+        check(lib.tsgm_write_disparity_png(str(path).encode(), ptr(disp), w, h))
+    else:
+        check(lib.tsgm_write_disparity_png_map(str(path).encode(), ptr(d), ptr(v), w, h))
+
+
+def read_png16(path):
+    """A 16-bit grayscale PNG's samples (u16 [H, W]), any filter type; what
+    read_disparity_png (dataset.cpp:220-227) reads before dividing by 256."""
+    import struct
+    import zlib
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:8] != b"\x89PNG\r\n\x1a\n":
+        raise RuntimeError(f"{path}: not a PNG")
+    i, idat, ihdr = 8, [], None
+    while i < len(data):
+        (n,) = struct.unpack(">I", data[i:i + 4])
+        typ, body = data[i + 4:i + 8], data[i + 8:i + 8 + n]
+        if typ == b"IHDR":
+            ihdr = struct.unpack(">IIBBBBB", body)
+        elif typ == b"IDAT":
+            idat.append(body)
+        i += 12 + n
+    w, h, depth, color, _, _, interlace = ihdr
+    if depth != 16 or color != 0 or interlace != 0:
+        raise RuntimeError(f"{path}: expected 16-bit single-channel PNG")
+    raw = np.frombuffer(zlib.decompress(b"".join(idat)), np.uint8).reshape(h, 1 + 2 * w)
+    out = np.zeros((h, 2 * w), np.int32)
+    prev = np.zeros(2 * w, np.int32)
+    bpp = 2
+    for y in range(h):  # PNG filters 0-4 on the byte rows
+        ft, line = raw[y, 0], raw[y, 1:].astype(np.int32)
+        cur = np.zeros(2 * w, np.int32)
+        for x in range(2 * w):
+            a = cur[x - bpp] if x >= bpp else 0
+            b = prev[x]
+            c = prev[x - bpp] if x >= bpp else 0
+            if ft == 0:
+                pr = 0
+            elif ft == 1:
+                pr = a
+            elif ft == 2:
+                pr = b
+            elif ft == 3:
+                pr = (a + b) // 2
+            else:
+                p_ = a + b - c
+                pa, pb, pc = abs(p_ - a), abs(p_ - b), abs(p_ - c)
+                pr = a if pa <= pb and pa <= pc else (b if pb <= pc else c)
+            cur[x] = (line[x] + pr) & 0xff
+            if ft == 0:
+                cur[:] = line
+                break
+        out[y] = cur
+        prev = cur
+    return ((out[:, 0::2] << 8) | out[:, 1::2]).astype(np.uint16)
+
+
+def read_disparity_png(path):
+    """read_disparity_png (dataset.cpp:220-227): samples / 256 (0 = invalid)."""
+    return read_png16(path) / 256.0
+
+
+def write_boxes(path, per_frame):
+    """write_boxes (dataset.cpp:256-269): '# frame x0 y0 x1 y1 score' lines,
+    score at 17 significant digits; per_frame = one [n, 5] box array per frame."""
+    counts = np.array([len(b) for b in per_frame], np.int64)
+    total = int(counts.sum())
+    arr = _box_array(total)
+    k = 0
+    for b in per_frame:
+        for r in np.asarray(b, np.float64).reshape(-1, 5):
+            arr[k] = (int(r[0]), int(r[1]), int(r[2]), int(r[3]), r[4])
+            k += 1
+    check(_lib.load().tsgm_write_boxes(str(path).encode(), arr.ctypes.data, ptr(counts),
+                                      len(per_frame)))
+
+
 # ----------------------------------------------------- noise calibration
 # SURVEY §8(f) row 4: noise_calib.hpp:13-90 / noise_calib.cpp on the GPU.
 @dataclass
@@ -737,6 +846,11 @@ class Engine:
                 return [_boxes_out(out[i * cap_each:(i + 1) * cap_each], int(n_each[i]))
                         for i in range(len(sl))]
             cap_each = int(n_each.max())
+
+    def write_export_png(self, slot, path):
+        """The slot's last export map as a KITTI 16-bit PNG (tsgm_main.cpp:157),
+        quantised on the device."""
+        check(self._lib.tsgm_write_export_png(self._h, int(slot), str(path).encode()))
 
     def count_outliers(self, slots, gts, what="export_d", opts=None):
         """count_outliers of each slot's last export map (or WTA map) against

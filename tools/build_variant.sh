@@ -11,4 +11,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -fmad=fals
   -Xcompiler -ffp-contract=off --expt-relaxed-constexpr -Iinclude -I$C "$@" \
   -c $C/aggregate_sweep.cu -o $L/obj/aggregate_sweep$sfx.o
 objs=$(ls $L/obj/*.o | grep -v "aggregate_sweep" )
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $L/libtsgm_b200$sfx.so $objs $L/obj/aggregate_sweep$sfx.o -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $L/libtsgm_b200$sfx.so $objs $L/obj/aggregate_sweep$sfx.o -lcudart -lz
