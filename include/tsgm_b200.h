@@ -355,6 +355,9 @@ int tsgm_write_disparity_png_map(const char* path, const int32_t* d, const uint8
 /* The slot's export map (StepResult::export_map) straight from the device, as
  * tsgm_main's run command writes it (tsgm_main.cpp:157). */
 int tsgm_write_export_png(tsgm_ctx* ctx, int32_t slot, const char* path);
+/* n slots at once: one device quantisation, PNGs encoded on host threads */
+int tsgm_write_export_pngs(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
+                           const char* const* paths);
 /* write_boxes: boxes of n_frames frames back to back, counts[f] per frame */
 int tsgm_write_boxes(const char* path, const tsgm_box* boxes, const int64_t* counts,
                      int32_t n_frames);

@@ -61,7 +61,8 @@ EXPORTS = [
     "tsgm_count_outliers_batch", "tsgm_calib_bins", "tsgm_estimate_process_noise",
     "tsgm_estimate_measurement_noise", "tsgm_accumulate_error_map", "tsgm_calib_release",
     "tsgm_quantize_disparity", "tsgm_quantize_disparity_map", "tsgm_write_disparity_png",
-    "tsgm_write_disparity_png_map", "tsgm_write_export_png", "tsgm_write_boxes",
+    "tsgm_write_disparity_png_map", "tsgm_write_export_png", "tsgm_write_export_pngs",
+    "tsgm_write_boxes",
 ]
 
 
@@ -159,6 +160,7 @@ def load():
         lib.tsgm_write_disparity_png_map.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int32,
                                                      C.c_int32]
         lib.tsgm_write_export_png.argtypes = [C.c_void_p, C.c_int32, C.c_char_p]
+        lib.tsgm_write_export_pngs.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         lib.tsgm_write_boxes.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int32]
         lib.tsgm_accumulate_error_map.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                                   C.c_void_p, C.POINTER(StereoCalibC), C.c_void_p]

@@ -88,7 +88,8 @@ void write_png16(const std::string& path, const uint16_t* raw, int w, int h) {
     }
     uLongf zlen = compressBound(static_cast<uLong>(filt.size()));
     std::vector<uint8_t> z(zlen);
-    if (compress2(z.data(), &zlen, filt.data(), static_cast<uLong>(filt.size()), 6) != Z_OK)
+    // level 1: 3-4x faster than libpng's default level 6 for a few % larger files
+    if (compress2(z.data(), &zlen, filt.data(), static_cast<uLong>(filt.size()), 1) != Z_OK)
         throw std::runtime_error(path + ": PNG encode error");
     std::vector<uint8_t> png = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1a, '\n'};
     std::vector<uint8_t> ihdr;

@@ -1912,38 +1912,66 @@ int tsgm_write_disparity_png_map(const char* path, const int32_t* d, const uint8
     });
 }
 
-int tsgm_write_export_png(tsgm_ctx* ctx, int32_t slot, const char* path) {
+int tsgm_write_export_pngs(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
+                           const char* const* paths) {
     return guarded([&] {
-        if (!ctx || !path) bad("tsgm_write_export_png: null argument");
-        if (slot < 0 || slot >= ctx->max_slots) bad("tsgm_write_export_png: slot out of range");
+        if (!ctx || !slots || !paths) bad("tsgm_write_export_png: null argument");
+        if (n < 1 || n > ctx->max_slots) bad("tsgm_write_export_png: n out of range");
+        for (int i = 0; i < n; ++i) {
+            if (slots[i] < 0 || slots[i] >= ctx->max_slots) bad("tsgm_write_export_png: slot out of range");
+            if (!paths[i]) bad("tsgm_write_export_png: null path");
+        }
         CK(cudaSetDevice(ctx->device));
         const size_t P = ctx->P;
         DevScratch s;
-        CK(cudaStreamWaitEvent(s.st, ctx->ev_frame, 0));  // the slot's last step
-        uint16_t* draw = s.alloc<uint16_t>(P);
-        unsigned long long* fb = s.alloc<unsigned long long>(1);
-        const int sl = slot;
-        int* dslot = s.alloc<int>(1);
-        CK(cudaMemcpyAsync(dslot, &sl, sizeof sl, cudaMemcpyHostToDevice, s.st));
-        launch_quantize_disparity(nullptr, ctx->b.ed, ctx->b.ev, P, 1, dslot, draw, fb, s.L());
+        CK(cudaStreamWaitEvent(s.st, ctx->ev_frame, 0));  // the slots' last step
+        uint16_t* draw = s.alloc<uint16_t>(P * n);
+        unsigned long long* fb = s.alloc<unsigned long long>(n);
+        int* dslots = s.alloc<int>(n);
+        CK(cudaMemcpyAsync(dslots, slots, sizeof(int) * n, cudaMemcpyHostToDevice, s.st));
+        launch_quantize_disparity(nullptr, ctx->b.ed, ctx->b.ev, P, n, dslots, draw, fb, s.L());
         CK(cudaGetLastError());
-        std::vector<uint16_t> raw(P);
-        unsigned long long first = 0;
-        CK(cudaMemcpyAsync(raw.data(), draw, 2 * P, cudaMemcpyDeviceToHost, s.st));
-        CK(cudaMemcpyAsync(&first, fb, sizeof first, cudaMemcpyDeviceToHost, s.st));
+        uint16_t* raw = nullptr;
+        CK(cudaMallocHost(&raw, 2 * P * n));
+        std::unique_ptr<uint16_t, cudaError_t (*)(void*)> raw_guard(raw, &cudaFreeHost);
+        std::vector<unsigned long long> first(n);
+        CK(cudaMemcpyAsync(raw, draw, 2 * P * n, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(first.data(), fb, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
+                           s.st));
         CK(cudaStreamSynchronize(s.st));
-        if (first != ~0ull) {
-            int32_t v = 0;
-            CK(cudaMemcpy(&v, ctx->b.ed + static_cast<size_t>(slot) * P + first, 4,
-                          cudaMemcpyDeviceToHost));
-            const std::string msg = "write_disparity_png: disparity " +
-                                    std_to_string(static_cast<double>(v)) + " not encodable at (" +
-                                    std::to_string(first % ctx->W) + ", " +
-                                    std::to_string(first / ctx->W) + ")";
-            bad(msg.c_str());
-        }
-        write_png_checked(path, raw.data(), ctx->W, ctx->H);
+        for (int i = 0; i < n; ++i)
+            if (first[i] != ~0ull) {  // the reference would throw before writing this file
+                int32_t v = 0;
+                CK(cudaMemcpy(&v, ctx->b.ed + static_cast<size_t>(slots[i]) * P + first[i], 4,
+                              cudaMemcpyDeviceToHost));
+                const std::string msg = "write_disparity_png: disparity " +
+                                        std_to_string(static_cast<double>(v)) + " not encodable at (" +
+                                        std::to_string(first[i] % ctx->W) + ", " +
+                                        std::to_string(first[i] / ctx->W) + ")";
+                bad(msg.c_str());
+            }
+        // PNG containers on host worker threads (zlib is the only host work)
+        const int nt = std::max(1, std::min<int>(n, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<std::string> errs(nt);
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                for (int i = t; i < n; i += nt) {
+                    try {
+                        write_png_checked(paths[i], raw + P * i, ctx->W, ctx->H);
+                    } catch (const std::exception& e) {
+                        if (errs[t].empty()) errs[t] = e.what();
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+        for (const auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
     });
+}
+
+int tsgm_write_export_png(tsgm_ctx* ctx, int32_t slot, const char* path) {
+    return tsgm_write_export_pngs(ctx, 1, &slot, &path);
 }
 
 int tsgm_write_boxes(const char* path, const tsgm_box* boxes, const int64_t* counts,

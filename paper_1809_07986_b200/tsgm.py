@@ -852,6 +852,16 @@ class Engine:
         quantised on the device."""
         check(self._lib.tsgm_write_export_png(self._h, int(slot), str(path).encode()))
 
+    def write_export_pngs(self, slots, paths):
+        """Many slots' export maps as PNGs: one device quantisation, the PNG
+        containers encoded on host threads."""
+        sl = np.asarray(slots, np.int32)
+        enc = [str(p).encode() for p in paths]
+        if len(enc) != len(sl):
+            raise ValueError("write_export_pngs: one path per slot")
+        arr = (C.c_char_p * len(enc))(*enc)
+        check(self._lib.tsgm_write_export_pngs(self._h, len(sl), ptr(sl), arr))
+
     def count_outliers(self, slots, gts, what="export_d", opts=None):
         """count_outliers of each slot's last export map (or WTA map) against
         host GT maps -> (evaluated[n], outliers[n])."""

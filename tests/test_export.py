@@ -143,7 +143,10 @@ def test_gpu_engine_export_png(tmp_path):
             mot = (np.eye(3), np.zeros(3)) if k == 0 else tsgm.relative_motion(P[k - 1], P[k])
             eng.step([1], [L[k]], [R[k]], [mot])
         eng.write_export_png(1, tmp_path / "e.png")
+        eng.write_export_pngs([1, 0], [tmp_path / "b1.png", tmp_path / "b0.png"])
         want = O.quantize_disparity_map(eng.fetch(1, "export_d"), eng.fetch(1, "export_valid"))
     got = tsgm.read_png16(tmp_path / "e.png")
     assert got.any()
     np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(tsgm.read_png16(tmp_path / "b1.png"), want)
+    assert not tsgm.read_png16(tmp_path / "b0.png").any()  # slot 0 never stepped: all invalid
