@@ -318,7 +318,7 @@ def run_ours(args):
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "algorithmic_bytes": int(b_agg), "ms": round(agg_ms, 4),
-                         "cells": int(agg_cells)},
+                         "cells": int(agg_cells), "limiter": load_limiter()},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "accuracy": {"frame": "last (29)", "outlier_rule": "|e| > 3 px and |e|/gt > 5%",
@@ -335,6 +335,27 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def load_limiter():
+    """What actually bounds the aggregation (from the committed ncu captures,
+    profiles/r01_*_ncu_full.json): issue slots, not HBM."""
+    out = {}
+    for name, fn in (("scan", "r01_scan_kernel_ncu_full.json"),
+                     ("combine", "r01_combine_ncu_full.json")):
+        try:
+            with open(os.path.join(ROOT, "profiles", fn)) as f:
+                d = json.load(f)
+            k = next(v for k, v in d.items() if not k.startswith("_"))
+            out[name] = {key: k.get(key) for key in ("issue_slots_busy_pct", "dram_throughput_pct",
+                                                      "eligible_warps_per_scheduler",
+                                                      "achieved_occupancy_pct")}
+        except (OSError, ValueError, StopIteration):
+            pass
+    if out:
+        out["reading"] = ("the scan is integer-issue bound (exact u16x2 min-plus recursions, "
+                          "~20 lane-instructions per cell-direction); see DESIGN.md section 4")
+    return out or None
 
 
 def load_traffic(cells: float):
