@@ -396,7 +396,11 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
             const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
             const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
             const uint8_t* c0 = cost + m1.cell;
-            for (int o = 0; o < n_n + 4; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + o));
+            // straight-line (windows are <= 256 levels, sweep_supported): 0.8%
+            // faster than the loop
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(c0));
+            if (n_n + 4 > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 128));
+            if (n_n + 4 > 256) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 256));
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
