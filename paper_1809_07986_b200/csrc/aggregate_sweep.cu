@@ -463,15 +463,20 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         const bool owner = active && lgs == 0;
         const bool fullw = sp.full_ok && mc.lohi == sp.full_lohi;
         const unsigned bf = __ballot_sync(0xffffffffu, owner && fullw);
-        const bool part = owner && !fullw;
-        const unsigned b2 = __ballot_sync(0xffffffffu, part && nq > 4 && nq <= 8);
-        if (b2) wide(std::integral_constant<int, 2>{}, b2, false);
-        const unsigned b4 = __ballot_sync(0xffffffffu, part && nq > 8 && nq <= 16);
-        if (b4) wide(std::integral_constant<int, 4>{}, b4, false);
-        const unsigned b8 = __ballot_sync(0xffffffffu, part && nq > 16 && nq <= 32);
-        if (b8) wide(std::integral_constant<int, 8>{}, b8, false);
-        const unsigned b16 = __ballot_sync(0xffffffffu, part && nq > 32);
-        if (b16) wide(std::integral_constant<int, 16>{}, b16, false);
+        const bool part = owner && !fullw && nq > 4;
+        // the four partial-wide classes only when the step has such a window
+        // (rare: 5+ quads, not full range): one vote instead of four ballots
+        // (aggregation 8.10 -> 7.84 ms)
+        if (__any_sync(0xffffffffu, part)) {
+            const unsigned b2 = __ballot_sync(0xffffffffu, part && nq <= 8);
+            if (b2) wide(std::integral_constant<int, 2>{}, b2, false);
+            const unsigned b4 = __ballot_sync(0xffffffffu, part && nq > 8 && nq <= 16);
+            if (b4) wide(std::integral_constant<int, 4>{}, b4, false);
+            const unsigned b8 = __ballot_sync(0xffffffffu, part && nq > 16 && nq <= 32);
+            if (b8) wide(std::integral_constant<int, 8>{}, b8, false);
+            const unsigned b16 = __ballot_sync(0xffffffffu, part && nq > 32);
+            if (b16) wide(std::integral_constant<int, 16>{}, b16, false);
+        }
         if (bf) {
             switch (sp.full_ok) {  // = 4G of the full window's class
                 case 8: wide(std::integral_constant<int, 2>{}, bf, true); break;
