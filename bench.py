@@ -371,6 +371,18 @@ def load_traffic(cells: float):
 
 
 # ---------------------------------------------------------------------- reference (CPU)
+def cpu_model() -> str:
+    """The host CPU (report the CPU model with the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(args, budget_s: float = 20.0, threads: int | None = None):
     """Reference CPU step on the host cores: one sequence per thread (step()
     is re-entrant), frame 0 (full range) plus reduced frames, timed per frame
@@ -417,6 +429,7 @@ def cpu_reference_sample(args, budget_s: float = 20.0, threads: int | None = Non
     per_seq = t_first + (N_FRAMES - 1) * t_red
     fps = threads * N_FRAMES / per_seq
     return {"value": round(fps, 3), "unit": "frames/s", "cores": threads, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": (f"{threads} config-2 sequences (one per thread), frame 0 + {n_red} "
                        f"reduced frames each, {wall:.1f}s wall; frames/s for the 30-frame mix "
                        f"= cores*30/(t0 + 29*t_reduced), t0={t_first:.3f}s "
