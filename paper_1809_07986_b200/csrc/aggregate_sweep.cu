@@ -167,14 +167,15 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     }
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
     const uint32_t prng = lds32(rp);
-    const int pq0 = static_cast<int>(prng & 0xffffu);
-    const uint32_t span = (prng >> 16) - static_cast<uint32_t>(pq0);
+    // no predecessor: every word reads 0 (an empty range no quad falls in)
+    const int pq0 = has_pred ? static_cast<int>(prng & 0xffffu) : -(1 << 20);
+    const uint32_t span = has_pred ? (prng >> 16) - static_cast<uint32_t>(pq0) : 0u;
+    const uint32_t fill = has_pred ? P2x4 : 0u;
     uint32_t w[Q + 2];
 #pragma unroll
     for (int u = 0; u < Q + 2; ++u) {
         const uint32_t raw = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
-        const bool in = static_cast<uint32_t>(a0 - 1 + u - pq0) <= span;
-        w[u] = has_pred ? (in ? raw : P2x4) : 0u;
+        w[u] = static_cast<uint32_t>(a0 - 1 + u - pq0) <= span ? raw : fill;
     }
     // levels outside the window carry a poisoned cost (kPoison): they lose every
     // min and normalise to exactly P2 below, so no masking is needed
@@ -444,7 +445,7 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
                 __syncwarp();
                 PixMeta pw;
                 pw.nq = 0u;  // unused by scan_pixel
-                pw.lohi = __shfl_sync(0xffffffffu, mc.lohi, src);
+                pw.lohi = full ? sp.full_lohi : __shfl_sync(0xffffffffu, mc.lohi, src);
                 pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
                 const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
