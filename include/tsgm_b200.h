@@ -358,6 +358,10 @@ int tsgm_write_export_png(tsgm_ctx* ctx, int32_t slot, const char* path);
 /* n slots at once: one device quantisation, PNGs encoded on host threads */
 int tsgm_write_export_pngs(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
                            const char* const* paths);
+/* read_disparity_png (dataset.cpp:220-227): a 16-bit grayscale PNG (any row
+ * filter) as samples / 256 (0 = invalid); host-side. Call with disp = NULL to
+ * get w, h; then with a buffer of cap >= w*h doubles. */
+int tsgm_read_disparity_png(const char* path, int32_t* w, int32_t* h, double* disp, size_t cap);
 /* write_boxes: boxes of n_frames frames back to back, counts[f] per frame */
 int tsgm_write_boxes(const char* path, const tsgm_box* boxes, const int64_t* counts,
                      int32_t n_frames);

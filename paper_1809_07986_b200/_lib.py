@@ -62,7 +62,7 @@ EXPORTS = [
     "tsgm_estimate_measurement_noise", "tsgm_accumulate_error_map", "tsgm_calib_release",
     "tsgm_quantize_disparity", "tsgm_quantize_disparity_map", "tsgm_write_disparity_png",
     "tsgm_write_disparity_png_map", "tsgm_write_export_png", "tsgm_write_export_pngs",
-    "tsgm_write_boxes",
+    "tsgm_write_boxes", "tsgm_read_disparity_png",
 ]
 
 
@@ -162,6 +162,8 @@ def load():
         lib.tsgm_write_export_png.argtypes = [C.c_void_p, C.c_int32, C.c_char_p]
         lib.tsgm_write_export_pngs.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         lib.tsgm_write_boxes.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int32]
+        lib.tsgm_read_disparity_png.argtypes = [C.c_char_p, C.POINTER(C.c_int32),
+                                                C.POINTER(C.c_int32), C.c_void_p, C.c_size_t]
         lib.tsgm_accumulate_error_map.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                                   C.c_void_p, C.POINTER(StereoCalibC), C.c_void_p]
         _lib = lib

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/tsgm_b200.h"
 
@@ -186,6 +187,7 @@ void launch_quantize_disparity(const double* disp, const int32_t* d, const uint8
                                unsigned long long* first_bad, Launch L);
 // Host PNG encoder (16-bit grayscale, zlib) and boxes.txt writer.
 void write_png16(const std::string& path, const uint16_t* raw, int w, int h);
+void read_png16(const std::string& path, std::vector<uint16_t>& raw, int& w, int& h);
 
 // Box detector (detect.cu), SURVEY §8(f) row 1.
 constexpr int kMaxDetectWindows = 16;

@@ -14,6 +14,7 @@
 #include <zlib.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -103,6 +104,81 @@ void write_png16(const std::string& path, const uint16_t* raw, int w, int h) {
     if (!f) throw std::runtime_error("cannot open file: " + path);  // image_io.cpp:25-29
     if (std::fwrite(png.data(), 1, png.size(), f.get()) != png.size())
         throw std::runtime_error(path + ": PNG encode error");
+}
+
+// read_disparity_png's decode (dataset.cpp:220-227 via image_io.cpp:172-193):
+// a 16-bit single-channel, non-interlaced PNG, any of the five row filters,
+// IDAT chunks concatenated and inflated with zlib. w/h out; raw resized.
+void read_png16(const std::string& path, std::vector<uint16_t>& raw, int& w, int& h) {
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path.c_str(), "rb"), &std::fclose);
+    if (!f) throw std::runtime_error("cannot open file: " + path);
+    std::vector<uint8_t> data;
+    uint8_t buf[65536];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof buf, f.get())) > 0) data.insert(data.end(), buf, buf + n);
+    static const uint8_t sig[8] = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1a, '\n'};
+    if (data.size() < 8 || std::memcmp(data.data(), sig, 8) != 0)
+        throw std::runtime_error(path + ": unsupported image format (expected PGM or PNG)");
+    auto be32 = [&](size_t i) {
+        return (uint32_t(data[i]) << 24) | (uint32_t(data[i + 1]) << 16) | (uint32_t(data[i + 2]) << 8) |
+               uint32_t(data[i + 3]);
+    };
+    std::vector<uint8_t> idat;
+    bool have_hdr = false;
+    int depth = 0, color = 0, interlace = 0;
+    for (size_t i = 8; i + 8 <= data.size();) {
+        const uint32_t len = be32(i);
+        if (i + 12 + len > data.size()) throw std::runtime_error(path + ": PNG decode error");
+        const uint8_t* type = data.data() + i + 4;
+        const uint8_t* body = data.data() + i + 8;
+        if (!std::memcmp(type, "IHDR", 4) && len >= 13) {
+            w = static_cast<int>(be32(i + 8));
+            h = static_cast<int>(be32(i + 12));
+            depth = body[8];
+            color = body[9];
+            interlace = body[12];
+            have_hdr = true;
+        } else if (!std::memcmp(type, "IDAT", 4)) {
+            idat.insert(idat.end(), body, body + len);
+        } else if (!std::memcmp(type, "IEND", 4)) {
+            break;
+        }
+        i += 12 + len;
+    }
+    if (!have_hdr || depth != 16 || color != 0 || interlace != 0 || w <= 0 || h <= 0)
+        throw std::runtime_error(path + ": expected 16-bit single-channel PNG");
+    const size_t row = 2 * static_cast<size_t>(w);
+    std::vector<uint8_t> fl((row + 1) * static_cast<size_t>(h));
+    uLongf got = static_cast<uLongf>(fl.size());
+    if (uncompress(fl.data(), &got, idat.data(), static_cast<uLong>(idat.size())) != Z_OK ||
+        got != fl.size())
+        throw std::runtime_error(path + ": PNG decode error");
+    std::vector<uint8_t> prev(row, 0), cur(row);
+    raw.assign(static_cast<size_t>(w) * h, 0);
+    for (int y = 0; y < h; ++y) {
+        const uint8_t ft = fl[(row + 1) * y];
+        const uint8_t* in = fl.data() + (row + 1) * y + 1;
+        for (size_t x = 0; x < row; ++x) {
+            const int a = x >= 2 ? cur[x - 2] : 0, b = prev[x], c = x >= 2 ? prev[x - 2] : 0;
+            int pr = 0;
+            switch (ft) {
+                case 0: pr = 0; break;
+                case 1: pr = a; break;
+                case 2: pr = b; break;
+                case 3: pr = (a + b) / 2; break;
+                case 4: {
+                    const int p = a + b - c, pa = std::abs(p - a), pb = std::abs(p - b), pc = std::abs(p - c);
+                    pr = (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
+                    break;
+                }
+                default: throw std::runtime_error(path + ": PNG decode error");
+            }
+            cur[x] = static_cast<uint8_t>(in[x] + pr);
+        }
+        for (int x = 0; x < w; ++x)
+            raw[static_cast<size_t>(y) * w + x] = static_cast<uint16_t>((cur[2 * x] << 8) | cur[2 * x + 1]);
+        std::swap(prev, cur);
+    }
 }
 
 }  // namespace tsgm

@@ -1974,6 +1974,21 @@ int tsgm_write_export_png(tsgm_ctx* ctx, int32_t slot, const char* path) {
     return tsgm_write_export_pngs(ctx, 1, &slot, &path);
 }
 
+int tsgm_read_disparity_png(const char* path, int32_t* w, int32_t* h, double* disp, size_t cap) {
+    return guarded([&] {
+        if (!path || !w || !h) bad("read_disparity_png: null argument");
+        std::vector<uint16_t> raw;
+        int ww = 0, hh = 0;
+        read_png16(path, raw, ww, hh);
+        *w = ww;
+        *h = hh;
+        if (disp) {
+            if (cap < raw.size()) bad("read_disparity_png: buffer too small");
+            for (size_t i = 0; i < raw.size(); ++i) disp[i] = raw[i] / 256.0;  // dataset.cpp:224-225
+        }
+    });
+}
+
 int tsgm_write_boxes(const char* path, const tsgm_box* boxes, const int64_t* counts,
                      int32_t n_frames) {
     return guarded([&] {

@@ -488,8 +488,15 @@ def read_png16(path):
 
 
 def read_disparity_png(path):
-    """read_disparity_png (dataset.cpp:220-227): samples / 256 (0 = invalid)."""
-    return read_png16(path) / 256.0
+    """read_disparity_png (dataset.cpp:220-227): samples / 256 (0 = invalid),
+    decoded by the library (zlib, any PNG row filter)."""
+    lib = _lib.load()
+    w, h = C.c_int32(), C.c_int32()
+    check(lib.tsgm_read_disparity_png(str(path).encode(), C.byref(w), C.byref(h), None, 0))
+    out = np.zeros((h.value, w.value))
+    check(lib.tsgm_read_disparity_png(str(path).encode(), C.byref(w), C.byref(h), ptr(out),
+                                     out.size))
+    return out
 
 
 def write_boxes(path, per_frame):

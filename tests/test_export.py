@@ -150,3 +150,23 @@ def test_gpu_engine_export_png(tmp_path):
     np.testing.assert_array_equal(got, want)
     np.testing.assert_array_equal(tsgm.read_png16(tmp_path / "b1.png"), want)
     assert not tsgm.read_png16(tmp_path / "b0.png").any()  # slot 0 never stepped: all invalid
+
+
+def test_png_reader_rejects(tmp_path):
+    """read_disparity_png's errors (image_io.cpp:25-33, 180-182): a missing
+    file, a non-PNG, an 8-bit PNG."""
+    import struct
+    from paper_1809_07986_b200 import tsgm
+    with pytest.raises(RuntimeError, match="cannot open file"):
+        tsgm.read_disparity_png(tmp_path / "missing.png")
+    (tmp_path / "x.png").write_bytes(b"P5\n2 2\n255\n\x00\x00\x00\x00")
+    with pytest.raises(RuntimeError):
+        tsgm.read_disparity_png(tmp_path / "x.png")
+
+    def chunk(t, d):
+        return struct.pack(">I", len(d)) + t + d + struct.pack(">I", zlib.crc32(t + d) & 0xffffffff)
+    png8 = (b"\x89PNG\r\n\x1a\n" + chunk(b"IHDR", struct.pack(">IIBBBBB", 2, 2, 8, 0, 0, 0, 0)) +
+            chunk(b"IDAT", zlib.compress(b"\x00\x01\x02\x00\x03\x04")) + chunk(b"IEND", b""))
+    (tmp_path / "g8.png").write_bytes(png8)
+    with pytest.raises(RuntimeError, match="expected 16-bit single-channel PNG"):
+        tsgm.read_disparity_png(tmp_path / "g8.png")
