@@ -394,6 +394,13 @@ inline void write_disparity_png(const std::string& path, const DisparityMap& dm)
     detail::check(tsgm_write_disparity_png_map(path.c_str(), dm.d.data(), dm.valid.data(),
                                                dm.d.width(), dm.d.height()));
 }
+inline Image<double> read_disparity_png(const std::string& path) {
+    std::int32_t w = 0, h = 0;
+    detail::check(tsgm_read_disparity_png(path.c_str(), &w, &h, nullptr, 0));
+    Image<double> img(w, h, 0.0);
+    detail::check(tsgm_read_disparity_png(path.c_str(), &w, &h, img.data(), img.pixel_count()));
+    return img;
+}
 inline void write_boxes(const std::string& path,
                         const std::vector<std::vector<DetectionBox>>& per_frame) {
     std::vector<tsgm_box> flat;

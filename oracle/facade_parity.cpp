@@ -260,6 +260,9 @@ int main() {
         disp(3, 2) = 12.25;
         tsgm::gpu::write_disparity_png("/tmp/tsgm_facade_disp.png", disp);
         EXPECT(slurp("/tmp/tsgm_facade_disp.png").size() > 8, "write_disparity_png");
+        const Image<double> back = tsgm::gpu::read_disparity_png("/tmp/tsgm_facade_disp.png");
+        EXPECT(back.width() == 16 && back.height() == 8 && back(3, 2) == 12.25 && back(0, 0) == 0.0,
+               "read_disparity_png round trip");
         try {
             disp(5, 5) = 300.0;
             tsgm::gpu::write_disparity_png("/tmp/tsgm_facade_disp_bad.png", disp);
