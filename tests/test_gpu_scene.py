@@ -260,3 +260,15 @@ def test_subpixel_extension(port):
         assert (np.abs(got[v] - ref["meas_d"][v]) <= 0.5).all()
         state = (ref["d"], ref["p"], ref["valid"])
     eng.close()
+
+
+@pytest.mark.parametrize("n_seq", [4, 8, 16])
+def test_config2_per_gpu_shares(port, n_seq):
+    """Config 2 at full size with the per-GPU batch of 16, 8 and 4 sequences
+    (the strong-scaling shares of 4 and 8 GPUs and a smaller one), 3 frames:
+    every output bit-exact through the default small-batch kernel choices
+    (mixed scan kernels: 32-lane or G-lane horizontal groups, 8-scanline
+    horizontal warps)."""
+    cfgs = [SceneConfig.baseline_config(2, seed=s, n_movers=s % 5, frames=3) for s in range(n_seq)]
+    run_parity(port, cfgs, 3, tsgm.SgmParams(10, 120, 8, 0, 128),
+               tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=3.0))
