@@ -68,6 +68,25 @@ typedef struct tsgm_ctx tsgm_ctx;
  * sub-pixel disparity by a parabola through S(d-1), S(d), S(d+1) around the
  * WTA minimum, f32, exported only (never fed back into the Kalman state). */
 #define TSGM_SUBPIXEL 4u
+/* Record a CUDA event at the end of every stage of each step, so that
+ * tsgm_last_stage_timings() can report StepResult::timings. */
+#define TSGM_STAGE_TIMINGS 8u
+
+/* StepTimings (temporal_filter.hpp:57-62) with its SgmStageTimings
+ * (sgm.hpp:59-64) flattened: seconds of DEVICE time per stage, measured with
+ * CUDA events on the context stream (the reference times each stage with
+ * steady_clock, temporal_filter.cpp:209-221, sgm.cpp:236-255). Stage map of
+ * the GPU pipeline: predict = warp + tie-break + variance + reject + fill;
+ * ranges = derive_search_ranges; census; cost = make_cost_volume offsets +
+ * matching costs; aggregate = the 8 (or 4) path scans; wta = the direction
+ * sum fused with winner_takes_all (the production step never materialises
+ * S); correct = correct + diff + mask + render + export median (the
+ * reference times correct() alone and leaves diff/median untimed). */
+typedef struct {
+    double predict_s, ranges_s;
+    double census_s, cost_s, aggregate_s, wta_s; /* SgmStageTimings */
+    double correct_s;
+} tsgm_stage_timings;
 
 typedef struct {
     int32_t width, height;     /* image size (must equal calib.width/height) */
@@ -77,7 +96,8 @@ typedef struct {
     tsgm_sgm_params sgm;
     tsgm_filter_config filter;
     double mask_tau;           /* A21 extension: Mahalanobis gate, 3.0 */
-    uint32_t flags;            /* TSGM_KEEP_VOLUMES | TSGM_FORCE_SCANLINE_AGG | TSGM_SUBPIXEL */
+    uint32_t flags;            /* TSGM_KEEP_VOLUMES | TSGM_FORCE_SCANLINE_AGG | TSGM_SUBPIXEL |
+                                  TSGM_STAGE_TIMINGS */
     /* Volume working set: how many sequences' per-frame volumes (C, S and the
      * per-direction path costs, up to ~9 B per cell of W*H*d_max) are resident
      * at once. The Kalman state and per-pixel outputs are always resident for
@@ -109,10 +129,27 @@ int tsgm_set_state(tsgm_ctx* ctx, int32_t slot, const double* d, const double* p
  * staging copy; outputs stay on the device until tsgm_fetch. */
 int tsgm_step(tsgm_ctx* ctx, int32_t n, const int32_t* slots, const uint8_t* const* left,
               const uint8_t* const* right, const double* motion);
-/* Same with DEVICE image pointers (inputs already resident in HBM). */
+/* Same with DEVICE image pointers (inputs already resident in HBM). The
+ * step runs on the context's own stream and is NOT ordered after any other
+ * stream: the images must be complete before the call and must stay
+ * unmodified until the step's census has read them (tsgm_sync, or
+ * tsgm_inputs_consumed below). */
 int tsgm_step_device(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
                      const uint8_t* const* d_left, const uint8_t* const* d_right,
                      const double* motion);
+/* tsgm_step_device ordered after all work enqueued so far on
+ * `producer_stream` (a cudaStream_t; NULL = the legacy default stream), e.g.
+ * the copy or kernel that produced the images. */
+int tsgm_step_device_after(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
+                           const uint8_t* const* d_left, const uint8_t* const* d_right,
+                           const double* motion, void* producer_stream);
+/* Makes `consumer_stream` (a cudaStream_t) wait until the last step has
+ * finished reading its input images (its census), so the caller may refill
+ * them on that stream without a host synchronisation. */
+int tsgm_inputs_consumed(tsgm_ctx* ctx, void* consumer_stream);
+/* Per-stage device time of the context's last step (whole batch), for a
+ * context created with TSGM_STAGE_TIMINGS; waits for that step. */
+int tsgm_last_stage_timings(tsgm_ctx* ctx, tsgm_stage_timings* out);
 
 /* Outputs of the last step of a slot (StepResult, temporal_filter.hpp:64-69,
  * plus the intermediates parity tests compare). */
@@ -185,6 +222,11 @@ int tsgm_median_refine(const int32_t* d, const uint8_t* valid, int32_t w, int32_
 int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
                    const uint16_t* lo, const uint16_t* hi, const tsgm_sgm_params* params,
                    int32_t* d, uint8_t* valid);
+/* sgm_match with its SgmStageTimings* argument (sgm.hpp:67-69): census_s,
+ * cost_s, aggregate_s, wta_s filled (the other fields 0); may be NULL. */
+int tsgm_sgm_match_t(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
+                     const uint16_t* lo, const uint16_t* hi, const tsgm_sgm_params* params,
+                     int32_t* d, uint8_t* valid, tsgm_stage_timings* timings);
 /* relative_motion (geometry.hpp:111, geometry.cpp:189-197); poses row-major 3x4 */
 int tsgm_relative_motion(const double* prev12, const double* cur12, double* r9, double* t3);
 /* disparity_homography (geometry.hpp:87, geometry.cpp:77-110); row-major 4x4 */
@@ -223,6 +265,13 @@ int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_
                    const tsgm_stereo_calib* calib, const tsgm_sgm_params* params,
                    const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov,
                    int32_t* ed, uint8_t* ev, double* diff);
+/* tsgm_step_once that also fills StepResult::timings (may be NULL). */
+int tsgm_step_once_t(const double* sd, const double* sp, const uint8_t* sv, int32_t state_w,
+                     int32_t state_h, const uint8_t* left, const uint8_t* right, int32_t w,
+                     int32_t h, const double* r9, const double* t3,
+                     const tsgm_stereo_calib* calib, const tsgm_sgm_params* params,
+                     const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov,
+                     int32_t* ed, uint8_t* ev, double* diff, tsgm_stage_timings* timings);
 
 /* ------------------------------------------------------------------------
  * Moving-object box detector on the diff map (

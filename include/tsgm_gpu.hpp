@@ -54,6 +54,15 @@ inline tsgm_filter_config to_c(const FilterConfig& f) {
 inline tsgm_stereo_calib to_c(const StereoCalib& c) {
     return tsgm_stereo_calib{c.focal_px, c.cx, c.cy, c.baseline_m, c.width, c.height, c.d_max};
 }
+inline void to_timings(const tsgm_stage_timings& t, StepTimings& out) {
+    out.predict_s = t.predict_s;
+    out.ranges_s = t.ranges_s;
+    out.sgm.census_s = t.census_s;
+    out.sgm.cost_s = t.cost_s;
+    out.sgm.aggregate_s = t.aggregate_s;
+    out.sgm.wta_s = t.wta_s;
+    out.correct_s = t.correct_s;
+}
 inline void motion12(const RigidMotion& m, double* r9, double* t3) {
     for (int i = 0; i < 3; ++i) {
         for (int j = 0; j < 3; ++j) r9[i * 3 + j] = m.rotation(i, j);
@@ -80,11 +89,14 @@ inline StepResult step(const DisparityState& state, const GrayImage& left,
     res.state = DisparityState(w, h);
     res.export_map = DisparityMap(w, h);
     res.diff = Image<double>(w, h, 0.0);
-    detail::check(tsgm_step_once(state.d.data(), state.p.data(), state.valid.data(),
-                                 state.width(), state.height(), left.data(), right.data(), w, h,
-                                 r9, t3, &c, &p, &f, res.state.d.data(), res.state.p.data(),
-                                 res.state.valid.data(), res.export_map.d.data(),
-                                 res.export_map.valid.data(), res.diff.data()));
+    // StepResult::timings: per-stage device seconds (tsgm_stage_timings)
+    tsgm_stage_timings t{};
+    detail::check(tsgm_step_once_t(state.d.data(), state.p.data(), state.valid.data(),
+                                   state.width(), state.height(), left.data(), right.data(), w, h,
+                                   r9, t3, &c, &p, &f, res.state.d.data(), res.state.p.data(),
+                                   res.state.valid.data(), res.export_map.d.data(),
+                                   res.export_map.valid.data(), res.diff.data(), &t));
+    detail::to_timings(t, res.timings);
     return res;
 }
 
@@ -96,19 +108,25 @@ inline CensusMap census_transform(const GrayImage& img, int threads = 1) {
     return m;
 }
 
-// sgm_match (sgm.hpp:67-69); stage timings are not reported
+// sgm_match (sgm.hpp:67-69); `timings` gets per-stage device seconds
 inline DisparityMap sgm_match(const GrayImage& left, const GrayImage& right,
                               const SearchRangeMap& ranges, const SgmParams& params,
                               int threads = 1, SgmStageTimings* timings = nullptr) {
     (void)threads;
-    (void)timings;
     if (!left.same_size(right)) throw std::invalid_argument("sgm_match: image size mismatch");
     if (!left.same_size(ranges.lo)) throw std::invalid_argument("sgm_match: range map size mismatch");
     DisparityMap dm(left.width(), left.height());
     const tsgm_sgm_params p = detail::to_c(params);
-    detail::check(tsgm_sgm_match(left.data(), right.data(), left.width(), left.height(),
-                                 ranges.lo.data(), ranges.hi.data(), &p, dm.d.data(),
-                                 dm.valid.data()));
+    tsgm_stage_timings t{};
+    detail::check(tsgm_sgm_match_t(left.data(), right.data(), left.width(), left.height(),
+                                   ranges.lo.data(), ranges.hi.data(), &p, dm.d.data(),
+                                   dm.valid.data(), timings ? &t : nullptr));
+    if (timings) {
+        timings->census_s = t.census_s;
+        timings->cost_s = t.cost_s;
+        timings->aggregate_s = t.aggregate_s;
+        timings->wta_s = t.wta_s;
+    }
     return dm;
 }
 
@@ -431,6 +449,7 @@ public:
         c.flags = flags;
         c.vol_slots = vol_slots;
         detail::check(tsgm_create(&c, &ctx_));
+        timed_ = (flags & TSGM_STAGE_TIMINGS) != 0;
         w_ = calib.width;
         h_ = calib.height;
     }
@@ -445,6 +464,18 @@ public:
               const std::vector<const GrayImage*>& rights,
               const std::vector<RigidMotion>& motions) {
         const int n = static_cast<int>(slots.size());
+        // the C-ABI reads W*H bytes per image: check what step() would
+        // (temporal_filter.cpp:198-199) before handing over raw pointers
+        if (lefts.size() != slots.size() || rights.size() != slots.size() ||
+            motions.size() != slots.size())
+            throw std::invalid_argument("Engine::step: slots, images and motions differ in length");
+        for (int i = 0; i < n; ++i) {
+            if (!lefts[i] || !rights[i]) throw std::invalid_argument("Engine::step: null image");
+            if (!lefts[i]->same_size(*rights[i]))
+                throw std::invalid_argument("step: left/right dimension mismatch");
+            if (lefts[i]->width() != w_ || lefts[i]->height() != h_)
+                throw std::invalid_argument("step: state dimension mismatch");
+        }
         std::vector<const std::uint8_t*> l(n), r(n);
         std::vector<double> m(12 * static_cast<size_t>(n));
         for (int i = 0; i < n; ++i) {
@@ -455,7 +486,18 @@ public:
         detail::check(tsgm_step(ctx_, n, slots.data(), l.data(), r.data(), m.data()));
     }
 
-    // StepResult of a slot's last frame (state, export map, diff).
+    // Per-stage device time of the last step, whole batch (engine created
+    // with flags |= TSGM_STAGE_TIMINGS).
+    StepTimings timings() const {
+        tsgm_stage_timings t{};
+        detail::check(tsgm_last_stage_timings(ctx_, &t));
+        StepTimings out;
+        detail::to_timings(t, out);
+        return out;
+    }
+
+    // StepResult of a slot's last frame (state, export map, diff; timings of
+    // the batch when the engine records them).
     StepResult result(int slot) const {
         StepResult res;
         res.state = DisparityState(w_, h_);
@@ -467,6 +509,7 @@ public:
         fetch(slot, TSGM_OUT_EXPORT_D, res.export_map.d.data(), 4);
         fetch(slot, TSGM_OUT_EXPORT_VALID, res.export_map.valid.data(), 1);
         fetch(slot, TSGM_OUT_DIFF, res.diff.data(), 8);
+        if (timed_) res.timings = timings();
         return res;
     }
 
@@ -507,6 +550,7 @@ private:
     }
     tsgm_ctx* ctx_ = nullptr;
     int w_ = 0, h_ = 0;
+    bool timed_ = false;
 };
 
 }  // namespace gpu

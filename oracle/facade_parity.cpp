@@ -91,6 +91,12 @@ int main() {
         EXPECT(ref.state.p == gpu.state.p, "state.p");
         EXPECT(ref.export_map == gpu.export_map, "export_map");
         EXPECT(ref.diff == gpu.diff, "diff");
+        // StepResult::timings filled like the reference's (temporal_filter.cpp:209-221)
+        EXPECT(gpu.timings.predict_s > 0 && gpu.timings.ranges_s > 0 &&
+                   gpu.timings.sgm.census_s > 0 && gpu.timings.sgm.cost_s > 0 &&
+                   gpu.timings.sgm.aggregate_s > 0 && gpu.timings.sgm.wta_s > 0 &&
+                   gpu.timings.correct_s > 0,
+               "StepResult::timings");
         s_ref = ref.state;
         s_gpu = gpu.state;
         // sub-stage facades on the same frame
@@ -101,8 +107,11 @@ int main() {
         const SearchRangeMap rg = tsgm::gpu::derive_search_ranges(pg, calib, cfg);
         EXPECT(rr.lo == rg.lo && rr.hi == rg.hi, "derive_search_ranges");
         const DisparityMap mr = sgm_match(left, right, rr, params);
-        const DisparityMap mg = tsgm::gpu::sgm_match(left, right, rg, params);
+        SgmStageTimings st;
+        const DisparityMap mg = tsgm::gpu::sgm_match(left, right, rg, params, 1, &st);
         EXPECT(mr == mg, "sgm_match");
+        EXPECT(st.census_s > 0 && st.cost_s > 0 && st.aggregate_s > 0 && st.wta_s > 0,
+               "sgm_match timings");
         EXPECT(median_refine(mr) == tsgm::gpu::median_refine(mg), "median_refine");
         const DisparityState cr = correct(pr, mr, cfg);
         const DisparityState cg = tsgm::gpu::correct(pg, mg, cfg);
@@ -124,9 +133,29 @@ int main() {
         EXPECT(false, "size mismatch did not throw");
     } catch (const std::invalid_argument&) {
     }
+    // Engine::step checks image sizes before the C-ABI reads raw pointers
+    {
+        tsgm::gpu::Engine eng(calib, params, cfg, 1);
+        GrayImage a(w, h), b(w - 1, h), c(w - 1, h);
+        try {
+            eng.step({0}, {&a}, {&b}, {RigidMotion{}});
+            EXPECT(false, "Engine::step left/right mismatch did not throw");
+        } catch (const std::invalid_argument&) {
+        }
+        try {
+            eng.step({0}, {&b}, {&c}, {RigidMotion{}});
+            EXPECT(false, "Engine::step wrong size did not throw");
+        } catch (const std::invalid_argument&) {
+        }
+        try {
+            eng.step({0}, {&a}, {&a, &a}, {RigidMotion{}});
+            EXPECT(false, "Engine::step length mismatch did not throw");
+        } catch (const std::invalid_argument&) {
+        }
+    }
     // batched engine == per-call facade
     {
-        tsgm::gpu::Engine eng(calib, params, cfg, 2);
+        tsgm::gpu::Engine eng(calib, params, cfg, 2, 0, 3.0, TSGM_STAGE_TIMINGS);
         DisparityState s;
         for (int k = 0; k < 3; ++k) {
             GrayImage left(w, h), right(w, h);
@@ -137,6 +166,8 @@ int main() {
             const StepResult batched = eng.result(1);
             EXPECT(one.state.d == batched.state.d && one.export_map == batched.export_map,
                    "Engine vs step");
+            EXPECT(batched.timings.sgm.aggregate_s > 0 && batched.timings.correct_s > 0,
+                   "Engine timings");
             s = one.state;
         }
     }

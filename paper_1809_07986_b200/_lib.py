@@ -18,6 +18,15 @@ OUT = dict(
 TSGM_KEEP_VOLUMES = 1
 TSGM_FORCE_SCANLINE_AGG = 2
 TSGM_SUBPIXEL = 4
+TSGM_STAGE_TIMINGS = 8
+
+
+class StageTimingsC(C.Structure):
+    """tsgm_stage_timings (StepTimings + SgmStageTimings, temporal_filter.hpp:57-62,
+    sgm.hpp:59-64), seconds of device time."""
+    _fields_ = [("predict_s", C.c_double), ("ranges_s", C.c_double), ("census_s", C.c_double),
+                ("cost_s", C.c_double), ("aggregate_s", C.c_double), ("wta_s", C.c_double),
+                ("correct_s", C.c_double)]
 
 
 class SgmParamsC(C.Structure):
@@ -55,7 +64,8 @@ EXPORTS = [
     "tsgm_winner_takes_all", "tsgm_median_refine", "tsgm_sgm_match", "tsgm_relative_motion",
     "tsgm_disparity_homography", "tsgm_warp_state_ex", "tsgm_predict",
     "tsgm_reject_discontinuities", "tsgm_fill_zoom_holes", "tsgm_derive_search_ranges",
-    "tsgm_correct", "tsgm_step_once",
+    "tsgm_correct", "tsgm_step_once", "tsgm_step_once_t", "tsgm_sgm_match_t",
+    "tsgm_step_device_after", "tsgm_inputs_consumed", "tsgm_last_stage_timings",
     "tsgm_integral_image", "tsgm_detect_candidate_windows", "tsgm_greedy_merge",
     "tsgm_detect_moving_objects", "tsgm_detect", "tsgm_count_outliers",
     "tsgm_count_outliers_batch", "tsgm_calib_bins", "tsgm_estimate_process_noise",
@@ -121,6 +131,10 @@ def load():
         for name in ("tsgm_step", "tsgm_step_device"):
             getattr(lib, name).argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p]
+        lib.tsgm_step_device_after.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                               C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.tsgm_inputs_consumed.argtypes = [C.c_void_p, C.c_void_p]
+        lib.tsgm_last_stage_timings.argtypes = [C.c_void_p, C.POINTER(StageTimingsC)]
         lib.tsgm_fetch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t]
         lib.tsgm_fetch_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                                          C.c_size_t]

@@ -980,6 +980,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         else if (spwh == 16) kern = scan_kernel<16, 32>;
         kern<<<grid, 32 * kScanWarps, smem, L.st>>>(b, sp);
     }
+    L.end_stage(kStAggregate);
     const size_t cwsmem = kCwWarps * cw_warp_bytes(b.d_max, subpix);
     const bool lean = !write_s && do_wta && !subpix;
     auto kern = k == 8 ? (lean ? combine_wta_kernel<8, true> : combine_wta_kernel<8, false>)
@@ -995,6 +996,8 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     kern<<<static_cast<unsigned>((warps + kCwWarps - 1) / kCwWarps), 32 * kCwWarps, cwsmem, L.st>>>(
         b, n, write_s, do_wta, subpix);
     *L.counter += 2;
+    // the direction sum is fused with winner_takes_all (when do_wta)
+    L.end_stage(do_wta ? kStWta : kStAggregate);
 }
 
 }  // namespace tsgm

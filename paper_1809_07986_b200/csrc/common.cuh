@@ -121,9 +121,20 @@ __device__ __forceinline__ bool census_defined(int x, int y, int W, int H) {
 
 // ------------------------------------------------------------------ launchers
 // (defined in the .cu files; all enqueue on `st` and count launches)
+// Stages of StepTimings / SgmStageTimings (temporal_filter.hpp:57-62,
+// sgm.hpp:59-64) a launcher may mark the end of (tsgm_stage_timings).
+enum Stage { kStPredict = 0, kStRanges, kStCensus, kStCost, kStAggregate, kStWta, kStCorrect,
+             kStCount };
+
 struct Launch {
     cudaStream_t st;
     unsigned long long* counter;
+    // optional: records a CUDA event marking the end of `stage` on `st`
+    void (*mark)(void* arg, int stage) = nullptr;
+    void* mark_arg = nullptr;
+    void end_stage(int stage) const {
+        if (mark) mark(mark_arg, stage);
+    }
 };
 
 void launch_census(const Bufs& b, int n, Launch L);
@@ -190,7 +201,7 @@ void write_png16(const std::string& path, const uint16_t* raw, int w, int h);
 void read_png16(const std::string& path, std::vector<uint16_t>& raw, int& w, int& h);
 
 // Box detector (detect.cu), SURVEY §8(f) row 1.
-constexpr int kMaxDetectWindows = 16;
+constexpr int kMaxDetectWindows = 64;  // kernel-parameter table (1.6 KB); INTEGRATION.md
 struct DetectWindows {
     int n;
     int ww[kMaxDetectWindows], wh[kMaxDetectWindows];

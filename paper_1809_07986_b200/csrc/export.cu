@@ -131,6 +131,9 @@ void read_png16(const std::string& path, std::vector<uint16_t>& raw, int& w, int
         if (i + 12 + len > data.size()) throw std::runtime_error(path + ": PNG decode error");
         const uint8_t* type = data.data() + i + 4;
         const uint8_t* body = data.data() + i + 8;
+        // every chunk's CRC-32 over type + data, as libpng checks it
+        const uLong crc = crc32(crc32(0L, Z_NULL, 0), type, 4 + len);
+        if (crc != be32(i + 8 + len)) throw std::runtime_error(path + ": PNG decode error");
         if (!std::memcmp(type, "IHDR", 4) && len >= 13) {
             w = static_cast<int>(be32(i + 8));
             h = static_cast<int>(be32(i + 12));

@@ -241,6 +241,15 @@ struct tsgm_ctx {
     // outlier metric (tsgm_count_outliers_batch): uploaded GT maps and counts
     double* eval_gt = nullptr;
     unsigned long long* eval_counts = nullptr;
+    // per-stage device times of the last step (StepResult::timings,
+    // temporal_filter.hpp:57-69): events recorded at stage ends on `st`
+    bool stage_timing = false;
+    std::vector<cudaEvent_t> tev;
+    std::vector<int> tstage;
+    int tev_used = 0;
+    // tsgm_step_device_after / tsgm_inputs_consumed: the input-release event
+    cudaEvent_t ev_inputs = nullptr, ev_consumed = nullptr;
+    bool consumed_recorded = false;
 
     template <typename T>
     T* dalloc(size_t count) {
@@ -267,6 +276,9 @@ struct tsgm_ctx {
         if (ev_frame) cudaEventDestroy(ev_frame);
         for (auto e : ev_snap_copied)
             if (e) cudaEventDestroy(e);
+        for (auto e : tev) cudaEventDestroy(e);
+        if (ev_inputs) cudaEventDestroy(ev_inputs);
+        if (ev_consumed) cudaEventDestroy(ev_consumed);
         if (ev_direct_copied) cudaEventDestroy(ev_direct_copied);
         for (int i = 0; i < kImgBufs; ++i) {
             if (ev_img_ready[i]) cudaEventDestroy(ev_img_ready[i]);
@@ -276,7 +288,40 @@ struct tsgm_ctx {
         if (up_st) cudaStreamDestroy(up_st);
         if (st) cudaStreamDestroy(st);
     }
-    Launch L() { return Launch{st, &launches}; }
+    // records the end of `stage` (or the step's start, stage < 0)
+    void mark(int stage) {
+        if (!stage_timing) return;
+        if (tev_used == static_cast<int>(tev.size())) {
+            cudaEvent_t e = nullptr;
+            if (cudaEventCreate(&e) != cudaSuccess) throw std::runtime_error("cudaEventCreate failed");
+            tev.push_back(e);
+            tstage.push_back(-1);
+        }
+        if (cudaEventRecord(tev[tev_used], st) != cudaSuccess) throw std::runtime_error("cudaEventRecord failed");
+        tstage[tev_used++] = stage;
+    }
+    static void mark_cb(void* self, int stage) { static_cast<tsgm_ctx*>(self)->mark(stage); }
+    Launch L() {
+        Launch l{st, &launches};
+        if (stage_timing) {
+            l.mark = &tsgm_ctx::mark_cb;
+            l.mark_arg = this;
+        }
+        return l;
+    }
+    // seconds per stage between the recorded marks (waits for the last one)
+    void stage_seconds(double* t) {
+        for (int k = 0; k < kStCount; ++k) t[k] = 0.0;
+        if (tev_used < 2) return;
+        if (cudaEventSynchronize(tev[tev_used - 1]) != cudaSuccess)
+            throw std::runtime_error("cudaEventSynchronize failed");
+        for (int i = 1; i < tev_used; ++i) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, tev[i - 1], tev[i]) != cudaSuccess)
+                throw std::runtime_error("cudaEventElapsedTime failed");
+            if (tstage[i] >= 0 && tstage[i] < kStCount) t[tstage[i]] += 1e-3 * ms;
+        }
+    }
 };
 
 namespace {
@@ -318,6 +363,9 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     }
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
+    CK(cudaEventCreateWithFlags(&ctx->ev_inputs, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_consumed, cudaEventDisableTiming));
+    ctx->stage_timing = (c.flags & TSGM_STAGE_TIMINGS) != 0;
     const size_t S = c.max_slots, P = ctx->P;
     Bufs& b = ctx->b;
     b.W = ctx->W;
@@ -500,16 +548,25 @@ void run_step(tsgm_ctx* ctx, int n) {
     const Bufs& b = ctx->b;
     const tsgm_config& c = ctx->cfg;
     Launch L = ctx->L();
+    ctx->tev_used = 0;
+    ctx->mark(-1);
     // predict (A5-A9)
     launch_warp(b, n, b.sd, b.sp, b.sv, c.calib.d_max, L);
     launch_predict_finalize(b, n, c.filter.q, 1, L);
     launch_reject_fill(b, n, b.wd, b.wp, b.wv, b.pd, b.pp, b.pv, c.filter.disc_thresh, 1, 1, L);
-    // derive_search_ranges + offsets (A10, A11)
+    ctx->mark(kStPredict);
+    // derive_search_ranges (A10); the offsets (A11) belong to make_cost_volume
     launch_ranges_from_pred(b, n, c.filter.min_range_halfwidth, c.filter.range_use_stddev,
                             c.filter.range_stddev_gain, L);
+    ctx->mark(kStRanges);
     launch_offsets(b, n, L);
+    ctx->mark(kStCost);
     // sgm_match (A12-A15)
     launch_census(b, n, L);
+    ctx->mark(kStCensus);
+    // the census is the last reader of the step's images (tsgm_inputs_consumed)
+    CK(cudaEventRecord(ctx->ev_consumed, ctx->st));
+    ctx->consumed_recorded = true;
     // Release the upload buffer right after the census, its only reader. (The
     // release must come early in the frame: recorded after the cost kernels
     // instead, it measurably serialised the next uploads behind the copy-outs.)
@@ -519,7 +576,10 @@ void run_step(tsgm_ctx* ctx, int n) {
         ctx->img_pending_free = -1;
     }
     // the volume stages in balanced chunks of at most vol_slots sequences;
-    // cost, agg and pdir are indexed by the position within the chunk
+    // cost, agg and pdir are indexed by the position within the chunk. No
+    // position keeps an owner from an earlier frame: a slot's volumes are
+    // resident (tsgm_fetch COST/AGG) only if it is in this frame's last chunk.
+    std::fill(ctx->vol_owner.begin(), ctx->vol_owner.end(), -1);
     const int chunks = (n + ctx->vol_slots - 1) / ctx->vol_slots;
     for (int k = 0, c0 = 0; k < chunks; ++k) {
         const int m = (n - c0) / (chunks - k);
@@ -527,14 +587,19 @@ void run_step(tsgm_ctx* ctx, int n) {
         bool full = true;  // every sequence of the chunk starts empty: full-range windows
         for (int a = 0; a < m; ++a) full = full && ctx->fresh[ctx->h_slots[c0 + a]];
         launch_cost(bc, m, L);
-        if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0, full))
+        ctx->mark(kStCost);
+        if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0, full)) {
+            ctx->mark(kStAggregate);
             launch_wta(bc, m, L);
+            ctx->mark(kStWta);
+        }
         for (int a = 0; a < m; ++a) ctx->vol_owner[a] = ctx->h_slots[c0 + a];
         c0 += m;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
     wait_direct_copies(ctx);  // the previous frame's outputs may still be copying out
     launch_correct_median(b, n, c.filter.r, c.mask_tau, L);
+    ctx->mark(kStCorrect);
     for (int i = 0; i < n; ++i) ctx->fresh[ctx->h_slots[i]] = 0;
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev_frame, ctx->st));
@@ -642,6 +707,16 @@ unsigned long long ranges_total(const uint16_t* lo, const uint16_t* hi, size_t n
     return total;
 }
 
+void fill_timings(const double* t, tsgm_stage_timings* out) {
+    out->predict_s = t[kStPredict];
+    out->ranges_s = t[kStRanges];
+    out->census_s = t[kStCensus];
+    out->cost_s = t[kStCost];
+    out->aggregate_s = t[kStAggregate];
+    out->wta_s = t[kStWta];
+    out->correct_s = t[kStCorrect];
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -724,6 +799,40 @@ int tsgm_step_device(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
     return guarded([&] {
         if (!ctx || !slots || !d_left || !d_right || !motion) bad("tsgm_step_device: null argument");
         step_impl(ctx, n, slots, d_left, d_right, motion);
+    });
+}
+
+int tsgm_step_device_after(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
+                           const uint8_t* const* d_left, const uint8_t* const* d_right,
+                           const double* motion, void* producer_stream) {
+    return guarded([&] {
+        if (!ctx || !slots || !d_left || !d_right || !motion) bad("tsgm_step_device: null argument");
+        CK(cudaSetDevice(ctx->device));
+        // the step's kernels start only after the work enqueued so far on the
+        // producer stream (e.g. the copy or kernel that filled the images)
+        CK(cudaEventRecord(ctx->ev_inputs, static_cast<cudaStream_t>(producer_stream)));
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_inputs, 0));
+        step_impl(ctx, n, slots, d_left, d_right, motion);
+    });
+}
+
+int tsgm_inputs_consumed(tsgm_ctx* ctx, void* consumer_stream) {
+    return guarded([&] {
+        if (!ctx) bad("tsgm_inputs_consumed: null argument");
+        CK(cudaSetDevice(ctx->device));
+        if (ctx->consumed_recorded)
+            CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), ctx->ev_consumed, 0));
+    });
+}
+
+int tsgm_last_stage_timings(tsgm_ctx* ctx, tsgm_stage_timings* out) {
+    return guarded([&] {
+        if (!ctx || !out) bad("tsgm_last_stage_timings: null argument");
+        if (!ctx->stage_timing) bad("tsgm_last_stage_timings: context created without TSGM_STAGE_TIMINGS");
+        CK(cudaSetDevice(ctx->device));
+        double t[kStCount];
+        ctx->stage_seconds(t);
+        fill_timings(t, out);
     });
 }
 
@@ -842,9 +951,7 @@ int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t
         std::vector<const uint8_t*> dl(n, ctx->d_img), dr(n, ctx->d_img);
         std::vector<double> H(16 * static_cast<size_t>(n), 0.0);
         upload_step(ctx, n, slots, dl.data(), dr.data(), H.data());
-        const tsgm_config& c = ctx->cfg;
-        Launch L = ctx->L();
-        (void)c;
+        Launch L{ctx->st, &ctx->launches};  // (no stage marks)
         aggregate(ctx, ctx->b, n, L);  // warm
         CK(cudaEventRecord(ctx->ev0, ctx->st));
         for (int r = 0; r < reps; ++r) aggregate(ctx, ctx->b, n, L);
@@ -960,9 +1067,9 @@ int tsgm_median_refine(const int32_t* d, const uint8_t* valid, int32_t w, int32_
     });
 }
 
-int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
-                   const uint16_t* lo, const uint16_t* hi, const tsgm_sgm_params* params,
-                   int32_t* d, uint8_t* valid) {
+int tsgm_sgm_match_t(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
+                     const uint16_t* lo, const uint16_t* hi, const tsgm_sgm_params* params,
+                     int32_t* d, uint8_t* valid, tsgm_stage_timings* timings) {
     return guarded([&] {
         // sgm_match, sgm.cpp:229-234: params, then ranges.validate(d_max)
         sgm_validate(*params);
@@ -973,21 +1080,40 @@ int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t
             bad("census_transform: image smaller than the 5x5 window");
         auto ctx = scratch(w, h, params->d_max);
         tsgm_ctx* c = ctx.get();
+        c->stage_timing = timings != nullptr;
         h2d(c, c->d_img, left, P);
         h2d(c, c->d_img + P, right, P);
         h2d(c, c->b.lo, lo, P);
         h2d(c, c->b.hi, hi, P);
+        c->tev_used = 0;
+        c->mark(-1);
+        // sgm.cpp:236-255: census, cost (make_cost_volume + matching costs),
+        // aggregate, WTA
+        launch_census(c->b, 1, c->L());
+        c->mark(kStCensus);
         launch_ranges_given(c->b, 1, c->L());
         launch_offsets(c->b, 1, c->L());
-        launch_census(c->b, 1, c->L());
         launch_cost(c->b, 1, c->L());
+        c->mark(kStCost);
         c->cfg.sgm = *params;
         aggregate(c, c->b, 1, c->L());
         launch_wta(c->b, 1, c->L());
+        c->mark(kStWta);
         d2h(c, d, c->b.md, P);
         d2h(c, valid, c->b.mv, P);
         sync(c);
+        if (timings) {
+            double t[kStCount];
+            c->stage_seconds(t);
+            fill_timings(t, timings);
+        }
     });
+}
+
+int tsgm_sgm_match(const uint8_t* left, const uint8_t* right, int32_t w, int32_t h,
+                   const uint16_t* lo, const uint16_t* hi, const tsgm_sgm_params* params,
+                   int32_t* d, uint8_t* valid) {
+    return tsgm_sgm_match_t(left, right, w, h, lo, hi, params, d, valid, nullptr);
 }
 
 int tsgm_relative_motion(const double* prev12, const double* cur12, double* r9, double* t3) {
@@ -1122,6 +1248,16 @@ int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_
                    const tsgm_stereo_calib* calib, const tsgm_sgm_params* params,
                    const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov,
                    int32_t* ed, uint8_t* ev, double* diff) {
+    return tsgm_step_once_t(sd, sp, sv, state_w, state_h, left, right, w, h, r9, t3, calib, params,
+                            cfg, od, op, ov, ed, ev, diff, nullptr);
+}
+
+int tsgm_step_once_t(const double* sd, const double* sp, const uint8_t* sv, int32_t state_w,
+                     int32_t state_h, const uint8_t* left, const uint8_t* right, int32_t w,
+                     int32_t h, const double* r9, const double* t3,
+                     const tsgm_stereo_calib* calib, const tsgm_sgm_params* params,
+                     const tsgm_filter_config* cfg, double* od, double* op, uint8_t* ov,
+                     int32_t* ed, uint8_t* ev, double* diff, tsgm_stage_timings* timings) {
     return guarded([&] {
         // step(), temporal_filter.cpp:198-206
         const bool empty = state_w == 0 && state_h == 0;
@@ -1171,6 +1307,7 @@ int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_
         const uint8_t* l = x->d_img;
         const uint8_t* r = x->d_img + P;
         upload_step(x, 1, &zero, &l, &r, H);
+        x->stage_timing = timings != nullptr;
         run_step(x, 1);
         d2h(x, od, x->b.sd, P);
         d2h(x, op, x->b.sp, P);
@@ -1179,6 +1316,11 @@ int tsgm_step_once(const double* sd, const double* sp, const uint8_t* sv, int32_
         d2h(x, ev, x->b.ev, P);
         d2h(x, diff, x->b.diff, P);
         sync(x);
+        if (timings) {
+            double t[kStCount];
+            x->stage_seconds(t);
+            fill_timings(t, timings);
+        }
     });
 }
 
@@ -1192,7 +1334,7 @@ namespace {
 void detect_validate(const tsgm_detect_config* c) {
     if (!c) bad("DetectConfig: null configuration");
     if (c->n_windows < 1 || !c->window_wh) bad("DetectConfig: no window sizes");
-    if (c->n_windows > kMaxDetectWindows) bad("DetectConfig: at most 16 window sizes");
+    if (c->n_windows > kMaxDetectWindows) bad("DetectConfig: at most 64 window sizes (GPU limit, INTEGRATION.md)");
     for (int i = 0; i < c->n_windows; ++i)
         if (c->window_wh[2 * i] < 1 || c->window_wh[2 * i + 1] < 1)
             bad("DetectConfig: non-positive window size");
@@ -1939,34 +2081,50 @@ int tsgm_write_export_pngs(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
         CK(cudaMemcpyAsync(first.data(), fb, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
                            s.st));
         CK(cudaStreamSynchronize(s.st));
+        // slot by slot like the reference's write_disparity_png calls: the
+        // files of the slots before the first non-encodable map are written,
+        // then that map's error is raised (dataset.cpp:229-254)
+        int n_ok = n;
         for (int i = 0; i < n; ++i)
-            if (first[i] != ~0ull) {  // the reference would throw before writing this file
-                int32_t v = 0;
-                CK(cudaMemcpy(&v, ctx->b.ed + static_cast<size_t>(slots[i]) * P + first[i], 4,
-                              cudaMemcpyDeviceToHost));
-                const std::string msg = "write_disparity_png: disparity " +
-                                        std_to_string(static_cast<double>(v)) + " not encodable at (" +
-                                        std::to_string(first[i] % ctx->W) + ", " +
-                                        std::to_string(first[i] / ctx->W) + ")";
-                bad(msg.c_str());
+            if (first[i] != ~0ull) {
+                n_ok = i;
+                break;
             }
         // PNG containers on host worker threads (zlib is the only host work)
-        const int nt = std::max(1, std::min<int>(n, static_cast<int>(std::thread::hardware_concurrency())));
+        const int nt = std::max(1, std::min<int>(std::max(n_ok, 1),
+                                                 static_cast<int>(std::thread::hardware_concurrency())));
         std::vector<std::string> errs(nt);
+        std::vector<int> err_at(nt, n);
         std::vector<std::thread> pool;
         for (int t = 0; t < nt; ++t)
             pool.emplace_back([&, t] {
-                for (int i = t; i < n; i += nt) {
+                for (int i = t; i < n_ok; i += nt) {
                     try {
                         write_png_checked(paths[i], raw + P * i, ctx->W, ctx->H);
                     } catch (const std::exception& e) {
-                        if (errs[t].empty()) errs[t] = e.what();
+                        if (i < err_at[t]) {
+                            err_at[t] = i;
+                            errs[t] = e.what();
+                        }
                     }
                 }
             });
         for (auto& th : pool) th.join();
-        for (const auto& e : errs)
-            if (!e.empty()) throw std::runtime_error(e);
+        int t_err = -1;  // the first failing slot in batch order
+        for (int t = 0; t < nt; ++t)
+            if (!errs[t].empty() && (t_err < 0 || err_at[t] < err_at[t_err])) t_err = t;
+        if (t_err >= 0) throw std::runtime_error(errs[t_err]);
+        if (n_ok < n) {
+            const int i = n_ok;
+            int32_t v = 0;
+            CK(cudaMemcpy(&v, ctx->b.ed + static_cast<size_t>(slots[i]) * P + first[i], 4,
+                          cudaMemcpyDeviceToHost));
+            const std::string msg = "write_disparity_png: disparity " +
+                                    std_to_string(static_cast<double>(v)) + " not encodable at (" +
+                                    std::to_string(first[i] % ctx->W) + ", " +
+                                    std::to_string(first[i] / ctx->W) + ")";
+            bad(msg.c_str());
+        }
     });
 }
 

@@ -153,19 +153,26 @@ def median_refine(d, valid):
     return od, ov
 
 
-def sgm_match(left, right, lo, hi, params):
-    """sgm_match (sgm.cpp:226-257): census -> cost -> aggregate -> WTA."""
+def sgm_match(left, right, lo, hi, params, timings=None):
+    """sgm_match (sgm.cpp:226-257): census -> cost -> aggregate -> WTA. A dict
+    passed as ``timings`` receives the SgmStageTimings (device seconds)."""
     left, right, lo, hi = _u8(left), _u8(right), _u16(lo), _u16(hi)
     if left.shape != right.shape:
         raise ValueError("sgm_match: image size mismatch")
     if lo.shape != left.shape:
         raise ValueError("sgm_match: range map size mismatch")
     w, h = _hw(left)
+    if hi.shape != left.shape:
+        raise ValueError("sgm_match: range map size mismatch")
     p = _as(params, SgmParams)._c()
     d = np.zeros((h, w), np.int32)
     v = np.zeros((h, w), np.uint8)
-    check(_lib.load().tsgm_sgm_match(ptr(left), ptr(right), w, h, ptr(lo), ptr(hi), C.byref(p),
-                                    ptr(d), ptr(v)))
+    t = _lib.StageTimingsC()
+    check(_lib.load().tsgm_sgm_match_t(ptr(left), ptr(right), w, h, ptr(lo), ptr(hi),
+                                      C.byref(p), ptr(d), ptr(v), C.byref(t)))
+    if timings is not None:  # SgmStageTimings* (sgm.hpp:59-69)
+        for k in ("census_s", "cost_s", "aggregate_s", "wta_s"):
+            timings[k] = getattr(t, k)
     return d, v
 
 
@@ -266,7 +273,8 @@ def step(state, left, right, R, t, calib, params, cfg):
 
     ``state`` is ``(d, p, valid)`` or ``None`` for the default (empty) state.
     Returns a dict with the StepResult fields: d, p, valid (posterior),
-    export_d, export_valid (median-refined map) and diff."""
+    export_d, export_valid (median-refined map), diff and timings (StepTimings
+    as a dict of device seconds, temporal_filter.hpp:57-62)."""
     left, right = _u8(left), _u8(right)
     if left.shape != right.shape:
         raise ValueError("step: left/right dimension mismatch")
@@ -280,15 +288,28 @@ def step(state, left, right, R, t, calib, params, cfg):
         sw = sh = 0
     else:
         sd, spp, sv = _f64(state[0]), _f64(state[1]), _u8(state[2])
+        if sd.shape != sv.shape or spp.shape != sv.shape:
+            raise ValueError("step: state dimension mismatch")
         sh, sw = sv.shape
     out = dict(d=np.zeros((h, w)), p=np.zeros((h, w)), valid=np.zeros((h, w), np.uint8),
                export_d=np.zeros((h, w), np.int32), export_valid=np.zeros((h, w), np.uint8),
                diff=np.zeros((h, w)))
-    check(_lib.load().tsgm_step_once(
+    tm = _lib.StageTimingsC()
+    check(_lib.load().tsgm_step_once_t(
         ptr(sd), ptr(spp), ptr(sv), sw, sh, ptr(left), ptr(right), w, h, ptr(R), ptr(t),
         C.byref(c), C.byref(sp), C.byref(f), ptr(out["d"]), ptr(out["p"]), ptr(out["valid"]),
-        ptr(out["export_d"]), ptr(out["export_valid"]), ptr(out["diff"])))
+        ptr(out["export_d"]), ptr(out["export_valid"]), ptr(out["diff"]), C.byref(tm)))
+    out["timings"] = _timings_dict(tm)
     return out
+
+
+def _timings_dict(t):
+    """StepTimings (temporal_filter.hpp:57-62) with its SgmStageTimings nested
+    under "sgm", as the reference's struct."""
+    return dict(predict_s=t.predict_s, ranges_s=t.ranges_s,
+                sgm=dict(census_s=t.census_s, cost_s=t.cost_s, aggregate_s=t.aggregate_s,
+                         wta_s=t.wta_s),
+                correct_s=t.correct_s)
 
 
 # --------------------------------------------------------------------- detector
@@ -447,6 +468,9 @@ def read_png16(path):
     while i < len(data):
         (n,) = struct.unpack(">I", data[i:i + 4])
         typ, body = data[i + 4:i + 8], data[i + 8:i + 8 + n]
+        (crc,) = struct.unpack(">I", data[i + 8 + n:i + 12 + n])
+        if zlib.crc32(typ + body) & 0xffffffff != crc:
+            raise RuntimeError(f"{path}: PNG decode error")
         if typ == b"IHDR":
             ihdr = struct.unpack(">IIBBBBB", body)
         elif typ == b"IDAT":
@@ -730,6 +754,7 @@ class EngineConfig:
     keep_volumes: bool = True
     subpixel: bool = False  # A22 extension: export-only sub-pixel WTA (f32)
     vol_slots: int = 0  # volume working set (0 = auto: max_slots, capped to free memory)
+    stage_timings: bool = False  # record per-stage device times (Engine.timings)
 
 
 class Engine:
@@ -741,7 +766,8 @@ class Engine:
         c = ConfigC(cal.width, cal.height, cfg.max_slots, cfg.device, cal._c(),
                     _as(cfg.sgm, SgmParams)._c(), _as(cfg.filter, FilterConfig)._c(),
                     cfg.mask_tau, (_lib.TSGM_KEEP_VOLUMES if cfg.keep_volumes else 0) |
-                    (_lib.TSGM_SUBPIXEL if cfg.subpixel else 0), cfg.vol_slots)
+                    (_lib.TSGM_SUBPIXEL if cfg.subpixel else 0) |
+                    (_lib.TSGM_STAGE_TIMINGS if cfg.stage_timings else 0), cfg.vol_slots)
         self._lib = _lib.load()
         h = C.c_void_p()
         check(self._lib.tsgm_create(C.byref(c), C.byref(h)))
@@ -769,9 +795,19 @@ class Engine:
     def reset(self, slot: int):
         check(self._lib.tsgm_reset(self._h, slot))
 
+    def _image(self, a, conv, what):
+        """The C-ABI reads W*H elements per pointer: check the shape first
+        (the reference's step() messages, temporal_filter.cpp:198-204)."""
+        a = conv(a)
+        if a.shape != (self.height, self.width):
+            raise ValueError(what)
+        return a
+
     def set_state(self, slot, d, p, valid):
-        check(self._lib.tsgm_set_state(self._h, slot, ptr(_f64(d)), ptr(_f64(p)),
-                                       ptr(_u8(valid))))
+        d = None if d is None else self._image(d, _f64, "step: state dimension mismatch")
+        p = None if p is None else self._image(p, _f64, "step: state dimension mismatch")
+        v = None if valid is None else self._image(valid, _u8, "step: state dimension mismatch")
+        check(self._lib.tsgm_set_state(self._h, slot, ptr(d), ptr(p), ptr(v)))
 
     @staticmethod
     def _motions(motions, n):
@@ -786,21 +822,50 @@ class Engine:
         [(R 3x3, t 3)] (identity for a first frame)."""
         n = len(slots)
         sl = np.asarray(slots, np.int32)
-        ls = [_u8(x) for x in lefts]
-        rs = [_u8(x) for x in rights]
+        if len(lefts) != n or len(rights) != n or len(motions) != n:
+            raise ValueError("Engine.step: slots, images and motions differ in length")
+        for a, b in zip(lefts, rights):
+            if np.shape(a) != np.shape(b):
+                raise ValueError("step: left/right dimension mismatch")
+        ls = [self._image(x, _u8, "step: state dimension mismatch") for x in lefts]
+        rs = [self._image(x, _u8, "step: state dimension mismatch") for x in rights]
         lp = (C.c_void_p * n)(*[x.ctypes.data for x in ls])
         rp = (C.c_void_p * n)(*[x.ctypes.data for x in rs])
         m = self._motions(motions, n)
         check(self._lib.tsgm_step(self._h, n, ptr(sl), lp, rp, ptr(m)))
 
-    def step_device(self, slots, left_ptrs, right_ptrs, motion12):
-        """Device-resident inputs: raw CUDA pointers, motion12 f64 [n, 12]."""
+    def step_device(self, slots, left_ptrs, right_ptrs, motion12, after_stream=None):
+        """Device-resident inputs: raw CUDA pointers (W*H bytes each), motion12
+        f64 [n, 12]. With ``after_stream`` (a cudaStream_t handle, e.g.
+        ``torch.cuda.current_stream().cuda_stream``) the step is ordered after
+        the work enqueued on it so far; otherwise the images must already be
+        complete (tsgm_step_device)."""
         n = len(slots)
         sl = np.asarray(slots, np.int32)
+        if len(left_ptrs) != n or len(right_ptrs) != n:
+            raise ValueError("Engine.step_device: slots and image pointers differ in length")
         lp = (C.c_void_p * n)(*left_ptrs)
         rp = (C.c_void_p * n)(*right_ptrs)
         m = _f64(motion12)
-        check(self._lib.tsgm_step_device(self._h, n, ptr(sl), lp, rp, ptr(m)))
+        if m.shape != (n, 12):
+            raise ValueError("Engine.step_device: motion12 must be [n, 12]")
+        if after_stream is None:
+            check(self._lib.tsgm_step_device(self._h, n, ptr(sl), lp, rp, ptr(m)))
+        else:
+            check(self._lib.tsgm_step_device_after(self._h, n, ptr(sl), lp, rp, ptr(m),
+                                                   C.c_void_p(after_stream)))
+
+    def inputs_consumed(self, stream):
+        """Make ``stream`` (cudaStream_t handle) wait until the last step has
+        read its input images (after that they may be refilled)."""
+        check(self._lib.tsgm_inputs_consumed(self._h, C.c_void_p(stream)))
+
+    def timings(self):
+        """StepTimings of the last step (whole batch, device seconds); needs
+        ``EngineConfig(stage_timings=True)``."""
+        t = _lib.StageTimingsC()
+        check(self._lib.tsgm_last_stage_timings(self._h, C.byref(t)))
+        return _timings_dict(t)
 
     def cells(self, slot) -> int:
         v = C.c_uint64()
@@ -825,8 +890,15 @@ class Engine:
         host arrays for overlap); completes at the next :meth:`sync`."""
         n = len(slots)
         sl = np.asarray(slots, np.int32)
+        if len(outs) != n:
+            raise ValueError("Engine.fetch_batch: one output array per slot")
+        for o in outs:
+            if not (isinstance(o, np.ndarray) and o.flags.c_contiguous and o.flags.writeable):
+                raise ValueError("Engine.fetch_batch: outputs must be writeable C-contiguous arrays")
+        # every destination must hold a whole map: pass the smallest size
         dp = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
-        check(self._lib.tsgm_fetch_batch(self._h, n, ptr(sl), OUT[what], dp, outs[0].nbytes))
+        check(self._lib.tsgm_fetch_batch(self._h, n, ptr(sl), OUT[what], dp,
+                                         min(o.nbytes for o in outs)))
 
     def sync(self):
         check(self._lib.tsgm_sync(self._h))

@@ -170,3 +170,16 @@ def test_png_reader_rejects(tmp_path):
     (tmp_path / "g8.png").write_bytes(png8)
     with pytest.raises(RuntimeError, match="expected 16-bit single-channel PNG"):
         tsgm.read_disparity_png(tmp_path / "g8.png")
+
+
+def test_png_reader_checks_crc(tmp_path):
+    """A chunk whose CRC-32 does not match fails like libpng's read."""
+    from paper_1809_07986_b200 import tsgm
+    raw = golden("export")["f64_1__raw"]
+    data = bytearray(_png(raw, [0]))
+    data[33 + 8] ^= 0x01  # first byte of the IDAT data: its CRC no longer matches
+    (tmp_path / "c.png").write_bytes(bytes(data))
+    with pytest.raises(RuntimeError, match="PNG decode error"):
+        tsgm.read_disparity_png(tmp_path / "c.png")
+    with pytest.raises(RuntimeError, match="PNG decode error"):
+        tsgm.read_png16(tmp_path / "c.png")
