@@ -147,6 +147,10 @@ int tsgm_step_device_after(tsgm_ctx* ctx, int32_t n, const int32_t* slots,
  * finished reading its input images (its census), so the caller may refill
  * them on that stream without a host synchronisation. */
 int tsgm_inputs_consumed(tsgm_ctx* ctx, void* consumer_stream);
+/* Names of the aggregation kernels (scan + direction sum/WTA) the last step
+ * chose for its batch size and windows, e.g. "scan_kernel<32,32>+
+ * combine_wta_kernel<8,1>" (tests and bench.py record which variant ran). */
+int tsgm_last_kernels(tsgm_ctx* ctx, char* buf, size_t cap);
 /* Per-stage device time of the context's last step (whole batch), for a
  * context created with TSGM_STAGE_TIMINGS; waits for that step. */
 int tsgm_last_stage_timings(tsgm_ctx* ctx, tsgm_stage_timings* out);

@@ -78,6 +78,20 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return out
 
 
+def build_render_tool(force: bool = False) -> str:
+    """tools/bin/render_frames: the scene generator as a plain C program, so
+    the reference arm of bench.py gets its frames from a separate process that
+    is not Python and maps no product library."""
+    out = os.path.join(ROOT, "tools", "bin", "render_frames")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    srcs = [os.path.join(ROOT, "tools", "render_frames.c"), os.path.join(CSRC, "scene.c")]
+    if force or _stale(out, [*srcs, os.path.join(INCLUDE, "tsgm_scene.h")]):
+        subprocess.run(["gcc", "-std=gnu11", "-O2", "-pthread", f"-I{INCLUDE}", "-o", out, *srcs,
+                        "-lm"], check=True)
+    return out
+
+
 def build_all(force: bool = False) -> None:
     build_scene(force)
+    build_render_tool(force)
     build_cuda(force)

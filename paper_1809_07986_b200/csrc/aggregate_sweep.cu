@@ -28,6 +28,7 @@
 // (SgmParams::validate, sgm.cpp:21-22), so the grouping is exact.
 #include "common.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -843,6 +844,11 @@ __global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : 16)
     }
 }
 
+// name of the scan + combine kernels the last launch on this thread chose
+// (tsgm_last_kernels: tests and the bench assert which variant they measured)
+thread_local char g_variant[128];
+const char* last_sweep_variant() { return g_variant; }
+
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
                             int write_s, int do_wta, Launch L, int subpix, bool full_range) {
     ScanParams sp{};
@@ -906,6 +912,11 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         sp.warp_bytes = lines_warp_bytes(b.d_max, G);
         const size_t smem = static_cast<size_t>(kScanWarps) * sp.warp_bytes;
         const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
+        if (gh != G)
+            std::snprintf(g_variant, sizeof g_variant, "scan_lines_mixed_kernel<%d,%d,%d>", G, gh,
+                          4 * G / gh);
+        else
+            std::snprintf(g_variant, sizeof g_variant, "scan_lines_kernel<%d>", G);
         if (gh != G) {
             auto kern = G == 8 ? (gh == 16 ? scan_lines_mixed_kernel<8, 16, 2>
                                            : scan_lines_mixed_kernel<8, 32, 1>)
@@ -962,6 +973,12 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const size_t smem = static_cast<size_t>(kScanWarps) * sp.warp_bytes;
         const unsigned grid = static_cast<unsigned>((tasks + kScanWarps - 1) / kScanWarps);
         auto kern = scan_kernel<32, 32>;
+        if (hlines)
+            std::snprintf(g_variant, sizeof g_variant, "scan_mixed_kernel<%d,%d,%d>", hg,
+                          hg == 32 ? 4 * G / 32 : 4, spw);
+        else
+            std::snprintf(g_variant, sizeof g_variant, "scan_kernel<%d,%d>",
+                          spw == 8 ? 8 : spwh, spw);
         if (hlines) {
             if (hg == 32)
                 kern = G == 8 ? (spw == 8 ? scan_mixed_kernel<32, 1, 8> : spw == 16 ? scan_mixed_kernel<32, 1, 16>
@@ -985,6 +1002,11 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const bool lean = !write_s && do_wta && !subpix;
     auto kern = k == 8 ? (lean ? combine_wta_kernel<8, true> : combine_wta_kernel<8, false>)
                        : (lean ? combine_wta_kernel<4, true> : combine_wta_kernel<4, false>);
+    {
+        const size_t used = std::strlen(g_variant);
+        std::snprintf(g_variant + used, sizeof g_variant - used, "+combine_wta_kernel<%d,%d>", k,
+                      lean ? 1 : 0);
+    }
     static size_t cw_set[4] = {48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024};  // opt in once per variant
     const int vi = (k == 8 ? 2 : 0) + (lean ? 1 : 0);
     if (cwsmem > cw_set[vi]) {

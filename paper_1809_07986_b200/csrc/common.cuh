@@ -162,6 +162,7 @@ void launch_aggregate(const Bufs& b, int n, int p1, int p2, int paths, int path_
 // Line-sweep aggregation (aggregate_sweep.cu): returns false when the
 // configuration does not fit its shared-memory plan (caller falls back).
 bool sweep_supported(int W, int H, int d_max, int p2);
+const char* last_sweep_variant();  // kernels of the calling thread's last sweep launch
 // write_s: store S in the ragged volume; do_wta: fuse winner_takes_all
 // (writes md/mv). At least one of the two must be set. full_range: every
 // window spans d_max (frames from an empty state): the line-group scan wins.

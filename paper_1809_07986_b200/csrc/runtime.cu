@@ -243,6 +243,7 @@ struct tsgm_ctx {
     unsigned long long* eval_counts = nullptr;
     // per-stage device times of the last step (StepResult::timings,
     // temporal_filter.hpp:57-69): events recorded at stage ends on `st`
+    std::string last_kernels;  // aggregation kernels of the last step's last chunk
     bool stage_timing = false;
     std::vector<cudaEvent_t> tev;
     std::vector<int> tstage;
@@ -519,10 +520,12 @@ bool aggregate(tsgm_ctx* ctx, const Bufs& b, int n, Launch L, bool fuse_wta = fa
         launch_aggregate_sweep(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
                                (keep_s || !fuse_wta) ? 1 : 0, fuse_wta ? 1 : 0, L,
                                (fuse_wta && b.sub) ? 1 : 0, full_range);
+        ctx->last_kernels = last_sweep_variant();
         return fuse_wta;
     }
     if (b.sub) bad("TSGM_SUBPIXEL needs the scan aggregation (P2 + 24 <= 255, d_max <= 256)");
     launch_aggregate(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
+    ctx->last_kernels = "aggregate_kernels(scanline fallback)+wta_kernel";
     return false;
 }
 
@@ -822,6 +825,13 @@ int tsgm_inputs_consumed(tsgm_ctx* ctx, void* consumer_stream) {
         CK(cudaSetDevice(ctx->device));
         if (ctx->consumed_recorded)
             CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), ctx->ev_consumed, 0));
+    });
+}
+
+int tsgm_last_kernels(tsgm_ctx* ctx, char* buf, size_t cap) {
+    return guarded([&] {
+        if (!ctx || !buf || cap == 0) bad("tsgm_last_kernels: null argument");
+        std::snprintf(buf, cap, "%s", ctx->last_kernels.c_str());
     });
 }
 

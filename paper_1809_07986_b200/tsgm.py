@@ -860,6 +860,12 @@ class Engine:
         read its input images (after that they may be refilled)."""
         check(self._lib.tsgm_inputs_consumed(self._h, C.c_void_p(stream)))
 
+    def last_kernels(self) -> str:
+        """The aggregation kernels the last step ran (scan + combine/WTA)."""
+        buf = C.create_string_buffer(256)
+        check(self._lib.tsgm_last_kernels(self._h, buf, 256))
+        return buf.value.decode()
+
     def timings(self):
         """StepTimings of the last step (whole batch, device seconds); needs
         ``EngineConfig(stage_timings=True)``."""
