@@ -52,6 +52,7 @@ struct Bufs {
     uint4* tmeta;        // [slot][W][H] column-major {lohi, off, qoff, quads} (horizontal scanlines)
     uint4* rmeta;        // [slot][H][W] row-major {lohi, off, qoff, quads} (the other scanlines)
     uint32_t* qrow_sum;  // [slot][H]
+    uint2* tsum;         // [slot][H][ceil(W/32)] (cells, quads) of 32-px tile rows -> tile offsets
     unsigned long long* ncells;  // [slot]
     unsigned long long* nquads;  // [slot]
     int* overflow;       // [slot] volume >= 2^32
@@ -114,6 +115,29 @@ __device__ __forceinline__ int x86_cvtt_int(double x) {
     return static_cast<int>(0x80000000u);
 }
 
+// derive_search_ranges for a valid prediction, temporal_filter.cpp:115-137
+__device__ __forceinline__ void derive_range(double d, double p, int top, int min_len,
+                                             int use_stddev, double gain, int& lo, int& hi) {
+    const double half = use_stddev ? gain * sqrt(p) : p;
+    lo = x86_cvtt_int(floor(d - half));
+    hi = x86_cvtt_int(ceil(d + half));
+    lo = max(0, min(top, lo));
+    hi = max(0, min(top, hi));
+    const int deficit = min_len - (hi - lo + 1);
+    if (deficit > 0) {
+        lo -= deficit / 2;
+        hi += deficit - deficit / 2;
+        if (lo < 0) {
+            hi = min(top, hi - lo);
+            lo = 0;
+        }
+        if (hi > top) {
+            lo = max(0, lo - (hi - top));
+            hi = top;
+        }
+    }
+}
+
 __device__ __forceinline__ bool census_defined(int x, int y, int W, int H) {
     return x >= kCensusRadius && x < W - kCensusRadius && y >= kCensusRadius &&
            y < H - kCensusRadius;
@@ -138,6 +162,13 @@ struct Launch {
 };
 
 void launch_census(const Bufs& b, int n, Launch L);
+// the step's fused chain: forward warp (no pass-1 cache), then the predict
+// tile kernel (variance, reject, fill, ranges, tile counts), then offsets +
+// scan records + key re-arm
+void launch_warp_step(const Bufs& b, int n, int d_max, Launch L);
+void launch_predict_tile(const Bufs& b, int n, double q, double disc_thresh, int min_hw,
+                         int use_stddev, double gain, Launch L);
+void launch_offsets_step(const Bufs& b, int n, Launch L);
 void launch_ranges_from_pred(const Bufs& b, int n, int min_hw, int use_stddev, double gain,
                              Launch L);
 void launch_ranges_given(const Bufs& b, int n, Launch L);  // lo/hi already set

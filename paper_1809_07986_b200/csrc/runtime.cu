@@ -397,6 +397,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.tmeta = ctx->dalloc<uint4>(S * P);
     b.rmeta = ctx->dalloc<uint4>(S * P);
     b.qrow_sum = ctx->dalloc<uint32_t>(S * ctx->H);
+    b.tsum = ctx->dalloc<uint2>(S * ctx->H * static_cast<size_t>((ctx->W + 31) / 32));
     b.nquads = ctx->dalloc<unsigned long long>(S);
     b.ncells = ctx->dalloc<unsigned long long>(S);
     b.overflow = ctx->dalloc<int>(S);
@@ -553,16 +554,15 @@ void run_step(tsgm_ctx* ctx, int n) {
     Launch L = ctx->L();
     ctx->tev_used = 0;
     ctx->mark(-1);
-    // predict (A5-A9)
-    launch_warp(b, n, b.sd, b.sp, b.sv, c.calib.d_max, L);
-    launch_predict_finalize(b, n, c.filter.q, 1, L);
-    launch_reject_fill(b, n, b.wd, b.wp, b.wv, b.pd, b.pp, b.pv, c.filter.disc_thresh, 1, 1, L);
+    // predict (A5-A9): the forward warp, then one fused tile kernel for the
+    // variance step, reject, fill and derive_search_ranges (A10)
+    launch_warp_step(b, n, c.calib.d_max, L);
     ctx->mark(kStPredict);
-    // derive_search_ranges (A10); the offsets (A11) belong to make_cost_volume
-    launch_ranges_from_pred(b, n, c.filter.min_range_halfwidth, c.filter.range_use_stddev,
-                            c.filter.range_stddev_gain, L);
+    launch_predict_tile(b, n, c.filter.q, c.filter.disc_thresh, c.filter.min_range_halfwidth,
+                        c.filter.range_use_stddev, c.filter.range_stddev_gain, L);
     ctx->mark(kStRanges);
-    launch_offsets(b, n, L);
+    // make_cost_volume's offsets (A11) + the scan records; re-arms the keys
+    launch_offsets_step(b, n, L);
     ctx->mark(kStCost);
     // sgm_match (A12-A15)
     launch_census(b, n, L);

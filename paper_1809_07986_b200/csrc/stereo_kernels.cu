@@ -52,28 +52,6 @@ void launch_census(const Bufs& b, int n, Launch L) {
 // One CTA per (row, active slot); row totals go to row_sum.
 constexpr int kRowThreads = 256;
 
-__device__ __forceinline__ void derive_range(double d, double p, int top, int min_len,
-                                             int use_stddev, double gain, int& lo, int& hi) {
-    const double half = use_stddev ? gain * sqrt(p) : p;
-    lo = x86_cvtt_int(floor(d - half));
-    hi = x86_cvtt_int(ceil(d + half));
-    lo = max(0, min(top, lo));
-    hi = max(0, min(top, hi));
-    const int deficit = min_len - (hi - lo + 1);
-    if (deficit > 0) {
-        lo -= deficit / 2;
-        hi += deficit - deficit / 2;
-        if (lo < 0) {
-            hi = min(top, hi - lo);
-            lo = 0;
-        }
-        if (hi > top) {
-            lo = max(0, lo - (hi - top));
-            hi = top;
-        }
-    }
-}
-
 // Block-wide exclusive scan of one u32 per thread; returns the block total.
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& excl) {
     __shared__ uint32_t warp_tot[kRowThreads / 32];
@@ -247,6 +225,117 @@ __global__ void offsets_finalize_kernel(Bufs b) {
 void launch_offsets(const Bufs& b, int n, Launch L) {
     row_scan_kernel<<<dim3(n, 2), 1024, 0, L.st>>>(b);
     offsets_finalize_kernel<<<dim3((b.W + 31) / 32, (b.H + 31) / 32, n), dim3(32, 8), 0, L.st>>>(b);
+    *L.counter += 2;
+}
+
+// The step's offsets from predict_tile_kernel's per-tile row counts (tsum,
+// [slot][H][tiles_x] of (cells, quads) over 32-pixel tile rows).
+// tile_scan_kernel: per slot, the row totals' exclusive scan in u64 (the
+// reference throws for N >= 2^32, matching_cost.cpp:43-44: validate_config
+// bounds W*H*d_max below that), then each tile row's exclusive offset in
+// place. One CTA per (slot, cells|quads).
+__global__ void tile_scan_kernel(Bufs b) {
+    const int a = blockIdx.x, s = slot_of(b, a), which = blockIdx.y;
+    const int tiles_x = (b.W + 31) / 32;
+    __shared__ unsigned long long carry;
+    __shared__ unsigned long long part[1024];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    uint32_t* ts = reinterpret_cast<uint32_t*>(b.tsum + static_cast<size_t>(s) * b.H * tiles_x) + which;
+    for (int base = 0; base < b.H; base += 1024) {
+        const int y = base + threadIdx.x;
+        unsigned long long v = 0ull;
+        if (y < b.H)
+            for (int t = 0; t < tiles_x; ++t) v += ts[2 * (static_cast<size_t>(y) * tiles_x + t)];
+        part[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele, H is small
+            const unsigned long long t = threadIdx.x >= o ? part[threadIdx.x - o] : 0ull;
+            __syncthreads();
+            part[threadIdx.x] += t;
+            __syncthreads();
+        }
+        const unsigned long long incl = part[threadIdx.x] + carry;
+        __syncthreads();
+        if (y < b.H) {
+            unsigned long long run = incl - v;
+            for (int t = 0; t < tiles_x; ++t) {
+                uint32_t* e = ts + 2 * (static_cast<size_t>(y) * tiles_x + t);
+                const uint32_t c = *e;
+                *e = static_cast<uint32_t>(run);
+                run += c;
+            }
+        }
+        if (threadIdx.x == 1023) carry = incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const size_t last = static_cast<size_t>(s) * (b.P + 1) + b.P;
+        if (which == 0) {
+            b.ncells[s] = carry;
+            b.overflow[s] = carry > 0xffffffffull ? 1 : 0;
+            b.off[last] = static_cast<uint32_t>(carry);
+        } else {
+            b.nquads[s] = carry;
+            b.qoff[last] = static_cast<uint32_t>(carry);
+        }
+    }
+}
+
+// Cell and quad offsets of every pixel (tile offset + in-tile exclusive warp
+// scan), the packed scan records (rmeta row-major, tmeta column-major via a
+// 32x32 shared-memory transpose) and, for the step, the warp keys re-armed
+// for the next frame (kd = 0, (kp, ks) = ~0: nothing reads them after the
+// predict tile kernel).
+__global__ void offsets_tile_kernel(Bufs b, int arm_keys) {
+    __shared__ uint4 tile[32][33];
+    const int a = blockIdx.z, s = slot_of(b, a);
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tiles_x = (b.W + 31) / 32;
+    const size_t obase = static_cast<size_t>(s) * (b.P + 1), pbase = static_cast<size_t>(s) * b.P;
+    for (int j = ty; j < 32; j += 8) {  // (uniform per warp: a warp is one tile row)
+        const int y = y0 + j, x = x0 + tx;
+        const bool in = y < b.H && x < b.W;
+        const size_t g = pbase + static_cast<size_t>(y) * b.W + x;
+        const uint32_t lh = in ? b.lohi[g] : 0u;
+        const uint32_t nc = in ? (lh >> 16) - (lh & 0xffffu) + 1u : 0u;
+        const uint32_t nq = in ? (lh >> 18) - ((lh & 0xffffu) >> 2) + 1u : 0u;
+        uint32_t ic = nc, iq = nq;  // inclusive warp scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t c = __shfl_up_sync(0xffffffffu, ic, o);
+            const uint32_t qq = __shfl_up_sync(0xffffffffu, iq, o);
+            if (tx >= o) {
+                ic += c;
+                iq += qq;
+            }
+        }
+        if (in) {
+            const uint2 tb = b.tsum[(static_cast<size_t>(s) * b.H + y) * tiles_x + blockIdx.x];
+            const uint32_t off = tb.x + ic - nc, qo = tb.y + iq - nq;
+            const size_t o = obase + static_cast<size_t>(y) * b.W + x;
+            b.off[o] = off;
+            b.qoff[o] = qo;
+            const uint4 rec = make_uint4(lh, off, qo, nq);
+            b.rmeta[g] = rec;
+            tile[j][tx] = rec;
+            if (arm_keys) {
+                b.kd[g] = 0ull;
+                b.kps[g] = make_ulonglong2(~0ull, ~0ull);
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+        const int x = x0 + j, y = y0 + tx;
+        if (y < b.H && x < b.W) b.tmeta[pbase + static_cast<size_t>(x) * b.H + y] = tile[tx][j];
+    }
+}
+
+void launch_offsets_step(const Bufs& b, int n, Launch L) {
+    tile_scan_kernel<<<dim3(n, 2), 1024, 0, L.st>>>(b);
+    offsets_tile_kernel<<<dim3((b.W + 31) / 32, (b.H + 31) / 32, n), dim3(32, 8), 0, L.st>>>(b, 1);
     *L.counter += 2;
 }
 

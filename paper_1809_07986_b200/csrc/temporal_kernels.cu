@@ -42,6 +42,10 @@ __device__ __forceinline__ Mapped map_source(const double* H, int x, int y, doub
     return m;
 }
 
+// kCache: pass 1 stores each source's (target, d' key) for pass 2 (stage
+// API); the step recomputes the mapping in pass 2 instead (a few FP64 ops
+// per source against 24 B/px of cache traffic).
+template <bool kCache>
 __global__ void warp_map_kernel(Bufs b, const double* src_d, const uint8_t* src_v, int d_max) {
     const int a = blockIdx.y, s = slot_of(b, a);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -58,8 +62,10 @@ __global__ void warp_map_kernel(Bufs b, const double* src_d, const uint8_t* src_
             atomicMax(&b.kd[base + m.t], kd);
         }
     }
-    b.wtgt[base + i] = tgt;
-    b.wdk[base + i] = kd;
+    if (kCache) {
+        b.wtgt[base + i] = tgt;
+        b.wdk[base + i] = kd;
+    }
 }
 
 __device__ __forceinline__ ulonglong2 cas128(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val) {
@@ -80,15 +86,29 @@ __device__ __forceinline__ bool lex_less(ulonglong2 a, ulonglong2 b) {
     return a.x < b.x || (a.x == b.x && a.y < b.y);
 }
 
-__global__ void warp_tiebreak_kernel(Bufs b, const double* src_d, const double* src_p) {
+template <bool kCached>
+__global__ void warp_tiebreak_kernel(Bufs b, const double* src_d, const double* src_p,
+                                     const uint8_t* src_v, int d_max) {
     const int a = blockIdx.y, s = slot_of(b, a);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= b.P) return;
     const size_t base = static_cast<size_t>(s) * b.P;
-    const int tgt = b.wtgt[base + i];
-    if (tgt < 0) return;
+    int tgt;
+    unsigned long long dk;
+    if (kCached) {
+        tgt = b.wtgt[base + i];
+        if (tgt < 0) return;
+        dk = b.wdk[base + i];
+    } else {  // the same mapping as pass 1 (deterministic: same ops, same inputs)
+        if (!src_v[base + i]) return;
+        const Mapped m = map_source(b.H16 + 16 * a, i % b.W, i / b.W, src_d[base + i], b.W, b.H,
+                                    d_max);
+        if (m.t < 0) return;
+        tgt = m.t;
+        dk = ord_key(m.dp);
+    }
     const size_t t = base + tgt;
-    if (b.kd[t] != b.wdk[base + i]) return;
+    if (b.kd[t] != dk) return;
     const ulonglong2 mine = make_ulonglong2(ord_key(src_p[base + i]), ord_key(src_d[base + i]));
     ulonglong2* addr = b.kps + t;
     // start from the armed value: only the CAS reads the pair atomically (a
@@ -104,8 +124,15 @@ __global__ void warp_tiebreak_kernel(Bufs b, const double* src_d, const double* 
 void launch_warp(const Bufs& b, int n, const double* src_d, const double* src_p,
                  const uint8_t* src_v, int d_max, Launch L) {
     dim3 grid((b.P + 255) / 256, n);
-    warp_map_kernel<<<grid, 256, 0, L.st>>>(b, src_d, src_v, d_max);
-    warp_tiebreak_kernel<<<grid, 256, 0, L.st>>>(b, src_d, src_p);
+    warp_map_kernel<true><<<grid, 256, 0, L.st>>>(b, src_d, src_v, d_max);
+    warp_tiebreak_kernel<true><<<grid, 256, 0, L.st>>>(b, src_d, src_p, src_v, d_max);
+    *L.counter += 2;
+}
+
+void launch_warp_step(const Bufs& b, int n, int d_max, Launch L) {
+    dim3 grid((b.P + 255) / 256, n);
+    warp_map_kernel<false><<<grid, 256, 0, L.st>>>(b, b.sd, b.sv, d_max);
+    warp_tiebreak_kernel<false><<<grid, 256, 0, L.st>>>(b, b.sd, b.sp, b.sv, d_max);
     *L.counter += 2;
 }
 
@@ -244,6 +271,136 @@ void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* 
     ++*L.counter;
 }
 
+
+// ---------------------------------------------------------------- fused predict tile (A6-A10)
+// The step's per-pixel chain after the forward warp, one 32x8 tile per CTA:
+// decode the warp winners (warp_state_ex output, geometry.cpp:127-156) and
+// apply predict's variance step (temporal_filter.cpp:35-47) for the tile and
+// its 2-px halo, reject_discontinuities on the 1-px ring (:51-74, decided on
+// its input), fill_zoom_holes on the tile (:76-106, decided on reject's
+// output), then derive_search_ranges (:108-143). Writes the prediction
+// (pd/pp/pv), the windows (lo, hi, packed lohi) and each tile row's window
+// and quad counts (tsum) for make_cost_volume's prefix sum
+// (matching_cost.cpp:30-48). Halo values are recomputed from the same keys
+// with the same operations as the neighbouring tiles, so they agree bit for
+// bit. The keys stay untouched (other tiles read them as halo); the offsets
+// kernel re-arms them.
+constexpr int kPtW = 32, kPtH = 8;
+
+__global__ void __launch_bounds__(kPtW * kPtH) predict_tile_kernel(Bufs b, double q, double thr,
+                                                                   int min_hw, int use_stddev,
+                                                                   double gain) {
+    __shared__ double td[kPtH + 4][kPtW + 4];
+    __shared__ double tp[kPtH + 4][kPtW + 4];
+    __shared__ uint8_t tv[kPtH + 4][kPtW + 4];
+    __shared__ uint8_t rv[kPtH + 2][kPtW + 2];
+    const int a = blockIdx.z, s = slot_of(b, a);
+    const size_t base = static_cast<size_t>(s) * b.P;
+    const int W = b.W, H = b.H;
+    const int x0 = blockIdx.x * kPtW - 2, y0 = blockIdx.y * kPtH - 2;
+    const int tid = threadIdx.y * kPtW + threadIdx.x;
+    for (int k = tid; k < (kPtH + 4) * (kPtW + 4); k += kPtW * kPtH) {
+        const int ty = k / (kPtW + 4), tx = k % (kPtW + 4);
+        const int gx = x0 + tx, gy = y0 + ty;
+        double d = 0.0, p = 0.0;
+        uint8_t v = 0;
+        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+            const size_t t = base + static_cast<size_t>(gy) * W + gx;
+            const unsigned long long kd = b.kd[t];
+            if (kd != 0ull) {
+                const ulonglong2 k2 = b.kps[t];
+                const double src = key_double(k2.y);
+                if (src > 0.0) {  // predict: invalidate unless the source d > 0
+                    d = key_double(kd);
+                    const double phi = d / src;
+                    p = __dadd_rn(__dmul_rn(__dmul_rn(phi, phi), key_double(k2.x)), q);
+                    v = 1;
+                } else {
+                    d = 0.0;
+                }
+            }
+        }
+        td[ty][tx] = d;
+        tp[ty][tx] = p;
+        tv[ty][tx] = v;
+    }
+    __syncthreads();
+    for (int k = tid; k < (kPtH + 2) * (kPtW + 2); k += kPtW * kPtH) {
+        const int ry = k / (kPtW + 2), rx = k % (kPtW + 2);
+        const int ty = ry + 1, tx = rx + 1;
+        const int gx = x0 + tx, gy = y0 + ty;
+        bool v = tv[ty][tx] != 0;
+        if (v) {  // neighbour order (1,0), (-1,0), (0,1), (0,-1) as kDx/kDy at :52-53
+            const double di = td[ty][tx];
+            if (gx + 1 < W && tv[ty][tx + 1] && fabs(di - td[ty][tx + 1]) > thr) v = false;
+            else if (gx - 1 >= 0 && tv[ty][tx - 1] && fabs(di - td[ty][tx - 1]) > thr) v = false;
+            else if (gy + 1 < H && tv[ty + 1][tx] && fabs(di - td[ty + 1][tx]) > thr) v = false;
+            else if (gy - 1 >= 0 && tv[ty - 1][tx] && fabs(di - td[ty - 1][tx]) > thr) v = false;
+        }
+        rv[ry][rx] = v;
+    }
+    __syncthreads();
+    const int x = blockIdx.x * kPtW + threadIdx.x, y = blockIdx.y * kPtH + threadIdx.y;
+    const bool inb = x < W && y < H;
+    uint32_t cells = 0u, quads = 0u;
+    if (inb) {
+        const int tx = threadIdx.x + 2, ty = threadIdx.y + 2, rx = threadIdx.x + 1, ry = threadIdx.y + 1;
+        double od = td[ty][tx], op = tp[ty][tx];
+        uint8_t ov = tv[ty][tx];
+        if (ov && !rv[ry][rx]) {
+            od = op = 0.0;  // DisparityState::invalidate, geometry.hpp:70-74
+            ov = 0;
+        }
+        if (!ov) {
+            const bool horiz = x - 1 >= 0 && x + 1 < W && rv[ry][rx - 1] && rv[ry][rx + 1];
+            const bool vert = y - 1 >= 0 && y + 1 < H && rv[ry - 1][rx] && rv[ry + 1][rx];
+            if (horiz || vert) {
+                double ds = 0.0, ps = 0.0;
+                int nn = 0;
+                if (horiz) {
+                    ds = __dadd_rn(ds, __dadd_rn(td[ty][tx - 1], td[ty][tx + 1]));
+                    ps = __dadd_rn(ps, __dadd_rn(tp[ty][tx - 1], tp[ty][tx + 1]));
+                    nn += 2;
+                }
+                if (vert) {
+                    ds = __dadd_rn(ds, __dadd_rn(td[ty - 1][tx], td[ty + 1][tx]));
+                    ps = __dadd_rn(ps, __dadd_rn(tp[ty - 1][tx], tp[ty + 1][tx]));
+                    nn += 2;
+                }
+                od = ds / nn;
+                op = ps / nn;
+                ov = 1;
+            }
+        }
+        const size_t g = base + static_cast<size_t>(y) * W + x;
+        b.pd[g] = od;
+        b.pp[g] = op;
+        b.pv[g] = ov;
+        const int top = b.d_max - 1;
+        int lo = 0, hi = top;
+        if (ov) derive_range(od, op, top, 2 * min_hw + 1, use_stddev, gain, lo, hi);
+        b.lo[g] = static_cast<uint16_t>(lo);
+        b.hi[g] = static_cast<uint16_t>(hi);
+        b.lohi[g] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        cells = static_cast<uint32_t>(hi - lo + 1);
+        quads = static_cast<uint32_t>((hi >> 2) - (lo >> 2) + 1);
+    }
+    // this tile row's counts (one warp = one row of 32 pixels)
+    cells = __reduce_add_sync(0xffffffffu, cells);
+    quads = __reduce_add_sync(0xffffffffu, quads);
+    if (threadIdx.x == 0 && y < H) {
+        const int tiles_x = (W + kPtW - 1) / kPtW;
+        b.tsum[(static_cast<size_t>(s) * H + y) * tiles_x + blockIdx.x] = make_uint2(cells, quads);
+    }
+}
+
+void launch_predict_tile(const Bufs& b, int n, double q, double disc_thresh, int min_hw,
+                         int use_stddev, double gain, Launch L) {
+    dim3 grid((b.W + kPtW - 1) / kPtW, (b.H + kPtH - 1) / kPtH, n);
+    predict_tile_kernel<<<grid, dim3(kPtW, kPtH), 0, L.st>>>(b, q, disc_thresh, min_hw, use_stddev,
+                                                             gain);
+    ++*L.counter;
+}
 
 // ---------------------------------------------------------------- correct (A16-A18, A21)
 // correct (temporal_filter.cpp:145-170), the diff map (:223-229), the
