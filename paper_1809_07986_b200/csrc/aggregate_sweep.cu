@@ -76,14 +76,13 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
     return d;
 }
 
-__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
+// shared-window byte address -> shared pointer: plain (non-asm) accesses let
+// the compiler fold constant offsets into LDS/STS immediates
+__device__ __forceinline__ volatile uint32_t* sptr(uint32_t addr) {
+    return reinterpret_cast<volatile uint32_t*>(__cvta_shared_to_generic(addr));
 }
-__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) { return *sptr(addr); }
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) { *sptr(addr) = v; }
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.cta.shared.u32 %0, [%1];"
@@ -203,7 +202,7 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
         const uint32_t ma = __viaddmin_u16x2(LA[t], neg, P2x2);
         const uint32_t mb = __viaddmin_u16x2(LB[t], neg, P2x2);
         sts32(sb + 4u + 4u * static_cast<uint32_t>(a0 + t), prmt(ma, mb, 0x6420u));
-        out[pm.qo + static_cast<uint32_t>(k0 + t)] = prmt(LA[t], LB[t], 0x6420u);
+        (out + pm.qo + k0)[t] = prmt(LA[t], LB[t], 0x6420u);
     }
     if (pix && lg == 0) sts32(rp, static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16));
 }
@@ -276,7 +275,7 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, boo
             const uint32_t ma = __viaddmin_u16x2(LA[t], neg, P2x2);
             const uint32_t mb = __viaddmin_u16x2(LB[t], neg, P2x2);
             sts32(sb + 4u + 4u * static_cast<uint32_t>(a0 + t), prmt(ma, mb, 0x6420u));
-            out[pm.qo + static_cast<uint32_t>(a0 + t)] = prmt(LA[t], LB[t], 0x6420u);
+            (out + pm.qo + a0)[t] = prmt(LA[t], LB[t], 0x6420u);
         }
         if (lg == 0) sts32(rp, full_rng);
     }
@@ -702,7 +701,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, GH == 32 ? 16 : 12) scan_mixe
 // then lane = pixel writes the WTA result.
 constexpr int kCwWarps = 2;
 #ifndef CW_LEAN_MINB
-#define CW_LEAN_MINB 20
+#define CW_LEAN_MINB 16
 #endif
 
 // per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
@@ -814,11 +813,36 @@ __global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : 16)
         finish(q, w0);
         finish(q + 32, w1);
     }
-    for (; q < nq; q += 32) {  // (lean: one quad per lane and iteration, fewer registers)
-        uint32_t w0[NDIR];
+    if (kLean) {
+        // two consecutive quads per lane and iteration, every direction's
+        // 8-byte pair loaded up front (more bytes in flight per warp); the
+        // pairs are 2-quad aligned in the partial buffers, so a quad on each
+        // side may belong to the neighbouring chunks and is skipped
+        const uint32_t qa = qbase & ~1u;
+        const uint32_t span = qbase - qa + nq;
+        for (uint32_t g = 2u * static_cast<uint32_t>(lane); g < span; g += 64u) {
+            uint2 w2[NDIR];
 #pragma unroll
-        for (int d = 0; d < NDIR; ++d) w0[d] = __ldg(pd + d * dstride + qbase + q);
-        finish(q, w0);
+            for (int d = 0; d < NDIR; ++d)
+                w2[d] = __ldg(reinterpret_cast<const uint2*>(pd + d * dstride + qa + g));
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t qq = qa + g + static_cast<uint32_t>(j) - qbase;  // chunk-relative
+                if (qq < nq) {
+                    uint32_t w0[NDIR];
+#pragma unroll
+                    for (int d = 0; d < NDIR; ++d) w0[d] = j == 0 ? w2[d].x : w2[d].y;
+                    finish(qq, w0);
+                }
+            }
+        }
+    } else {
+        for (; q < nq; q += 32) {
+            uint32_t w0[NDIR];
+#pragma unroll
+            for (int d = 0; d < NDIR; ++d) w0[d] = __ldg(pd + d * dstride + qbase + q);
+            finish(q, w0);
+        }
     }
     __syncwarp();
     if (do_wta && lane < np) {

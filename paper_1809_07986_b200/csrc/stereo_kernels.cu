@@ -7,42 +7,76 @@
 namespace tsgm {
 
 // ---------------------------------------------------------------- census (A12)
-// census_transform, matching_cost.cpp:53-79. One thread per pixel of a
-// 32x8 tile; the 36x12 input tile (2-px halo) is staged in shared memory.
-constexpr int kCtW = 32, kCtH = 8;
+// census_transform, matching_cost.cpp:53-79, four horizontally adjacent
+// pixels per thread in byte-SIMD (SWAR) form: the 5x5 neighbour bytes of the
+// four pixels are 4-byte funnel shifts of the tile's row words, one strict
+// unsigned compare against the four centres yields the four census bits in
+// the bytes' MSBs (3 logic/add ops), and three accumulators collect 8 bits
+// per byte lane each (the signature's bytes), assembled per pixel at the end.
+// Bit order as the reference: raster order, first compare in bit 23. A CTA
+// covers 128 x 8 pixels; the 136 x 12 byte tile (2-px halo, word aligned) is
+// staged in shared memory.
+constexpr int kCsW = 128, kCsH = 8, kCsPitch = kCsW + 8;
 
-__global__ void census_kernel(Bufs b) {
-    __shared__ uint8_t tile[kCtH + 4][kCtW + 4];
+__device__ __forceinline__ uint32_t lt_msb(uint32_t x, uint32_t c_lo7, uint32_t c) {
+    // per byte: MSB set iff x < c (unsigned): borrow-free subtract on the low
+    // 7 bits, then the top bits decide (checked on all 65536 byte pairs)
+    const uint32_t d = (x | 0x80808080u) - c_lo7;
+    return (~x & c) | (~(x ^ c) & ~d);
+}
+
+__global__ void __launch_bounds__(256) census_kernel(Bufs b) {
+    __shared__ __align__(16) uint8_t tile[kCsH + 4][kCsPitch];
     const int a = blockIdx.z >> 1, which = blockIdx.z & 1;
     const int s = slot_of(b, a);
     const uint8_t* img = which ? b.right[a] : b.left[a];
     uint32_t* sig = (which ? b.sigr : b.sigl) + static_cast<size_t>(s) * b.P;
-    const int x0 = blockIdx.x * kCtW - 2, y0 = blockIdx.y * kCtH - 2;
-    for (int i = threadIdx.y * kCtW + threadIdx.x; i < (kCtH + 4) * (kCtW + 4); i += kCtW * kCtH) {
-        const int ty = i / (kCtW + 4), tx = i % (kCtW + 4);
-        const int gx = x0 + tx, gy = y0 + ty;
+    const int x0 = blockIdx.x * kCsW, y0 = blockIdx.y * kCsH;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int i = tid; i < (kCsH + 4) * kCsPitch; i += 256) {
+        const int ty = i / kCsPitch, tx = i % kCsPitch;
+        const int gx = x0 - 4 + tx, gy = y0 - 2 + ty;
         tile[ty][tx] = (gx >= 0 && gx < b.W && gy >= 0 && gy < b.H) ? img[gy * b.W + gx] : 0;
     }
     __syncthreads();
-    const int x = blockIdx.x * kCtW + threadIdx.x, y = blockIdx.y * kCtH + threadIdx.y;
-    if (x >= b.W || y >= b.H) return;
-    uint32_t v = 0;
-    if (census_defined(x, y, b.W, b.H)) {
-        const uint8_t c = tile[threadIdx.y + 2][threadIdx.x + 2];
+    const int xg = x0 + 4 * static_cast<int>(threadIdx.x), y = y0 + static_cast<int>(threadIdx.y);
+    if (xg >= b.W || y >= b.H) return;
+    uint32_t nb[5][5];  // neighbour words: [dy][dx] = bytes of x+dx-2 for the four pixels
 #pragma unroll
-        for (int dy = 0; dy < 5; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 5; ++dx) {
-                if (dx == 2 && dy == 2) continue;
-                v = (v << 1) | (tile[threadIdx.y + dy][threadIdx.x + dx] < c ? 1u : 0u);
-            }
+    for (int dy = 0; dy < 5; ++dy) {
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(&tile[threadIdx.y + dy][0]);
+        const uint32_t A = row[threadIdx.x], B = row[threadIdx.x + 1], C = row[threadIdx.x + 2];
+        nb[dy][0] = __funnelshift_r(A, B, 16);
+        nb[dy][1] = __funnelshift_r(A, B, 24);
+        nb[dy][2] = B;
+        nb[dy][3] = __funnelshift_r(B, C, 8);
+        nb[dy][4] = __funnelshift_r(B, C, 16);
     }
-    sig[y * b.W + x] = v;
+    const uint32_t c = nb[2][2], c_lo7 = c & 0x7f7f7f7fu;
+    uint32_t acc[3] = {0u, 0u, 0u};  // signature bits 16-23, 8-15, 0-7
+    // compare k (raster order, centre skipped) lands in bit 23 - k: insert
+    // each byte lane's 8 bits from the last compare of its group to the first
+#pragma unroll
+    for (int k = 23; k >= 0; --k) {
+        const int pos = k < 12 ? k : k + 1;  // skip the centre (position 12)
+        const uint32_t t = lt_msb(nb[pos / 5][pos % 5], c_lo7, c);
+        uint32_t& r = acc[k >> 3];
+        r = ((r >> 1) & 0x7f7f7f7fu) | (t & 0x80808080u);
+    }
+    uint32_t* out = sig + static_cast<size_t>(y) * b.W + xg;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int x = xg + i;
+        if (x >= b.W) break;
+        uint32_t v = __byte_perm(acc[2], acc[1], static_cast<uint32_t>(i | ((i + 4) << 4)));  // bits 0-15
+        v = __byte_perm(v, acc[0], static_cast<uint32_t>(0x10 | (i + 4) << 8)) & 0x00ffffffu;
+        out[i] = census_defined(x, y, b.W, b.H) ? v : 0u;
+    }
 }
 
 void launch_census(const Bufs& b, int n, Launch L) {
-    dim3 grid((b.W + kCtW - 1) / kCtW, (b.H + kCtH - 1) / kCtH, 2 * n);
-    census_kernel<<<grid, dim3(kCtW, kCtH), 0, L.st>>>(b);
+    dim3 grid((b.W + kCsW - 1) / kCsW, (b.H + kCsH - 1) / kCsH, 2 * n);
+    census_kernel<<<grid, dim3(32, kCsH), 0, L.st>>>(b);
     ++*L.counter;
 }
 
@@ -340,6 +374,9 @@ void launch_offsets_step(const Bufs& b, int n, Launch L) {
 }
 
 // ---------------------------------------------------------------- cost (A13)
+// (Tried: computing each chunk into a shared-memory staging buffer and
+// writing it out with 16-byte stores: 0.85 -> 1.14 ms for 64 sequences'
+// reduced frames; the byte stores below are not the limiter.)
 // build_cost_volume, matching_cost.cpp:88-117. One CTA per (row, slot); the
 // row's census signatures are staged in shared memory. Warps take 32-pixel
 // chunks: a window of <= 16 levels is written by its own lane, a wider window

@@ -129,11 +129,11 @@ void launch_warp(const Bufs& b, int n, const double* src_d, const double* src_p,
     *L.counter += 2;
 }
 
+// (measured: recomputing the mapping in pass 2 instead of the 12 B/px cache
+// doubled the tie-break kernel, 0.35 -> 0.70 ms for 64 sequences: FP64
+// divisions cost more than the cache traffic)
 void launch_warp_step(const Bufs& b, int n, int d_max, Launch L) {
-    dim3 grid((b.P + 255) / 256, n);
-    warp_map_kernel<false><<<grid, 256, 0, L.st>>>(b, b.sd, b.sv, d_max);
-    warp_tiebreak_kernel<false><<<grid, 256, 0, L.st>>>(b, b.sd, b.sp, b.sv, d_max);
-    *L.counter += 2;
+    launch_warp(b, n, b.sd, b.sp, b.sv, d_max, L);
 }
 
 // Decode the winners (warp_state_ex output) and apply predict's variance step,
@@ -285,7 +285,7 @@ void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* 
 // with the same operations as the neighbouring tiles, so they agree bit for
 // bit. The keys stay untouched (other tiles read them as halo); the offsets
 // kernel re-arms them.
-constexpr int kPtW = 32, kPtH = 8;
+constexpr int kPtW = 32, kPtH = 16;
 
 __global__ void __launch_bounds__(kPtW * kPtH) predict_tile_kernel(Bufs b, double q, double thr,
                                                                    int min_hw, int use_stddev,
@@ -299,25 +299,37 @@ __global__ void __launch_bounds__(kPtW * kPtH) predict_tile_kernel(Bufs b, doubl
     const int W = b.W, H = b.H;
     const int x0 = blockIdx.x * kPtW - 2, y0 = blockIdx.y * kPtH - 2;
     const int tid = threadIdx.y * kPtW + threadIdx.x;
-    for (int k = tid; k < (kPtH + 4) * (kPtW + 4); k += kPtW * kPtH) {
+    constexpr int kHalo = (kPtH + 4) * (kPtW + 4), kT = kPtW * kPtH;
+    static_assert(kHalo <= 2 * kT, "two halo pixels per thread");
+    // both halo pixels' keys loaded up front (the pair unconditionally: most
+    // pixels hold a prediction, and the dependent load would cost a round trip)
+    unsigned long long kd[2];
+    ulonglong2 k2[2];
+    bool in[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int k = tid + u * kT;
         const int ty = k / (kPtW + 4), tx = k % (kPtW + 4);
         const int gx = x0 + tx, gy = y0 + ty;
+        in[u] = k < kHalo && gx >= 0 && gx < W && gy >= 0 && gy < H;
+        const size_t t = base + (in[u] ? static_cast<size_t>(gy) * W + gx : 0);
+        kd[u] = in[u] ? b.kd[t] : 0ull;
+        k2[u] = in[u] ? b.kps[t] : make_ulonglong2(0ull, 0ull);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int k = tid + u * kT;
+        if (k >= kHalo) break;
+        const int ty = k / (kPtW + 4), tx = k % (kPtW + 4);
         double d = 0.0, p = 0.0;
         uint8_t v = 0;
-        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-            const size_t t = base + static_cast<size_t>(gy) * W + gx;
-            const unsigned long long kd = b.kd[t];
-            if (kd != 0ull) {
-                const ulonglong2 k2 = b.kps[t];
-                const double src = key_double(k2.y);
-                if (src > 0.0) {  // predict: invalidate unless the source d > 0
-                    d = key_double(kd);
-                    const double phi = d / src;
-                    p = __dadd_rn(__dmul_rn(__dmul_rn(phi, phi), key_double(k2.x)), q);
-                    v = 1;
-                } else {
-                    d = 0.0;
-                }
+        if (kd[u] != 0ull) {
+            const double src = key_double(k2[u].y);
+            if (src > 0.0) {  // predict: invalidate unless the source d > 0
+                d = key_double(kd[u]);
+                const double phi = d / src;
+                p = __dadd_rn(__dmul_rn(__dmul_rn(phi, phi), key_double(k2[u].x)), q);
+                v = 1;
             }
         }
         td[ty][tx] = d;
