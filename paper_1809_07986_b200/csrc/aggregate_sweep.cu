@@ -888,6 +888,19 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     if (paths == 8 || path_set == 1)
         for (int i = 0; i < 4; ++i, ++k) { sp.dx[k] = diag[i][0]; sp.dy[k] = diag[i][1]; }
     sp.ndir = k;
+    // TSGM_SCAN_DIRS=<bitmask over the directions above> (profiling only:
+    // time direction classes separately; the result is then not S)
+    if (const char* fd = std::getenv("TSGM_SCAN_DIRS")) {
+        const int mask = std::atoi(fd);
+        int m = 0;
+        for (int i = 0; i < k; ++i)
+            if (mask >> i & 1) {
+                sp.dx[m] = sp.dx[i];
+                sp.dy[m] = sp.dy[i];
+                ++m;
+            }
+        sp.ndir = k = m;
+    }
     {
         const int qm = (b.d_max + 3) / 4;
         const bool pow2 = (qm & (qm - 1)) == 0;

@@ -285,9 +285,9 @@ void launch_reject_fill(const Bufs& b, int n, const double* in_d, const double* 
 // with the same operations as the neighbouring tiles, so they agree bit for
 // bit. The keys stay untouched (other tiles read them as halo); the offsets
 // kernel re-arms them.
-constexpr int kPtW = 32, kPtH = 16;
+constexpr int kPtW = 32, kPtH = 8;
 
-__global__ void __launch_bounds__(kPtW * kPtH) predict_tile_kernel(Bufs b, double q, double thr,
+__global__ void __launch_bounds__(kPtW * kPtH, 5) predict_tile_kernel(Bufs b, double q, double thr,
                                                                    int min_hw, int use_stddev,
                                                                    double gain) {
     __shared__ double td[kPtH + 4][kPtW + 4];
@@ -489,7 +489,7 @@ __device__ __forceinline__ void cm_swap(int32_t& a, int32_t& b) {
     b = hi;
 }
 
-__global__ void correct_median_kernel(Bufs b, double r, double tau) {
+__global__ void __launch_bounds__(kCmW * kCmH) correct_median_kernel(Bufs b, double r, double tau) {
     __shared__ int32_t key[kCmH + 2][kCmW + 2];
     __shared__ uint8_t okv[kCmH + 2][kCmW + 2];
     const int a = blockIdx.z, s = slot_of(b, a);

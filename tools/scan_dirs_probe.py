@@ -1,6 +1,10 @@
-"""Small driver for ncu captures: a few batched frames of the BASELINE config-2
-workload (S sequences x F frames), then the standalone C->S aggregation on the
-last frame's volumes. Usage: python tools/profile_step.py [S] [F] [reps]"""
+"""Profiling probe: the standalone aggregation of 64 config-2 sequences' 4th
+frame with only some directions (TSGM_SCAN_DIRS bitmask: 3 = horizontal,
+12 = vertical, 240 = diagonal, 255 = all), to see where the scan's time goes
+per direction class. Run under ncu's launch list for per-kernel times.
+
+    python tools/scan_dirs_probe.py [S]
+"""
 import os
 import sys
 
@@ -13,9 +17,8 @@ from paper_1809_07986_b200.scene import SceneConfig, render  # noqa: E402
 
 
 def main():
-    S = int(sys.argv[1]) if len(sys.argv) > 1 else 16
-    F = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    S = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    F = 4
     calib = tsgm.StereoCalib(720.0, 621.0, 187.5, 0.54, 1242, 375, 128)
     sgm = tsgm.SgmParams(10, 120, 8, 0, 128)
     filt = tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=3.0)
@@ -27,9 +30,11 @@ def main():
         eng.step(list(range(S)), [L[k] for (L, _, _, _) in seqs], [R[k] for (_, R, _, _) in seqs],
                  mots)
     eng.sync()
-    ms, cells = eng.bench_aggregate(list(range(S)), reps=reps)
-    b = 3.0 * cells + 4.0 * 1242 * 375 * S
-    print(f"aggregation: {ms:.3f} ms for {cells/1e6:.1f} M cells -> {b/ms/1e6:.1f} GB/s")
+    for mask in (255, 3, 12, 240):
+        os.environ["TSGM_SCAN_DIRS"] = str(mask)
+        ms, cells = eng.bench_aggregate(list(range(S)), reps=2)
+        print(f"dirs {mask:3d}: {ms:.3f} ms (scan + combine) for {cells / 1e6:.1f} M cells", flush=True)
+    os.environ.pop("TSGM_SCAN_DIRS")
 
 
 if __name__ == "__main__":
