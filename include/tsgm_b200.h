@@ -151,6 +151,11 @@ int tsgm_inputs_consumed(tsgm_ctx* ctx, void* consumer_stream);
  * chose for its batch size and windows, e.g. "scan_kernel<32,32>+
  * combine_wta_kernel<8,1>" (tests and bench.py record which variant ran). */
 int tsgm_last_kernels(tsgm_ctx* ctx, char* buf, size_t cap);
+/* Volume chunks the last step ran its cost -> aggregation -> WTA stages in.
+ * Volumes are packed by the frame's actual cell counts (make_cost_volume's
+ * N, matching_cost.cpp:30-48) into a pool of tsgm_volume_slots worst-case
+ * volumes, so reduced frames usually need one chunk. */
+int tsgm_last_chunks(tsgm_ctx* ctx, int32_t* chunks);
 /* Per-stage device time of the context's last step (whole batch), for a
  * context created with TSGM_STAGE_TIMINGS; waits for that step. */
 int tsgm_last_stage_timings(tsgm_ctx* ctx, tsgm_stage_timings* out);

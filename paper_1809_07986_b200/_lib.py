@@ -66,7 +66,7 @@ EXPORTS = [
     "tsgm_reject_discontinuities", "tsgm_fill_zoom_holes", "tsgm_derive_search_ranges",
     "tsgm_correct", "tsgm_step_once", "tsgm_step_once_t", "tsgm_sgm_match_t",
     "tsgm_step_device_after", "tsgm_inputs_consumed", "tsgm_last_stage_timings",
-    "tsgm_last_kernels",
+    "tsgm_last_kernels", "tsgm_last_chunks",
     "tsgm_integral_image", "tsgm_detect_candidate_windows", "tsgm_greedy_merge",
     "tsgm_detect_moving_objects", "tsgm_detect", "tsgm_count_outliers",
     "tsgm_count_outliers_batch", "tsgm_calib_bins", "tsgm_estimate_process_noise",
@@ -136,6 +136,7 @@ def load():
                                                C.c_void_p, C.c_void_p, C.c_void_p]
         lib.tsgm_inputs_consumed.argtypes = [C.c_void_p, C.c_void_p]
         lib.tsgm_last_kernels.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+        lib.tsgm_last_chunks.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         lib.tsgm_last_stage_timings.argtypes = [C.c_void_p, C.POINTER(StageTimingsC)]
         lib.tsgm_fetch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t]
         lib.tsgm_fetch_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,

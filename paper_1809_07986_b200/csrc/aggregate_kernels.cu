@@ -52,8 +52,8 @@ aggregate_dir_kernel(Bufs b, int dx, int dy, int p1, int p2, int first) {
     uint16_t* bufB = bufA + b.d_max;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
     const uint16_t* lo = b.lo + static_cast<size_t>(s) * b.P;
-    const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
-    uint16_t* agg = b.agg + static_cast<size_t>(a) * b.vol_cap;
+    const uint8_t* cost = b.cost + b.vbase[a];
+    uint16_t* agg = b.agg + b.vbase[a];
 
     int x, y;
     line_start(line, W, H, dx, dy, x, y);

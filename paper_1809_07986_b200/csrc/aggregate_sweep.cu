@@ -335,9 +335,9 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
     }
 
-    const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
+    const uint8_t* cost = b.cost + b.vbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
-        b.pdir + (static_cast<size_t>(d) * b.vol_slots + a) * b.quad_cap * 4);
+        b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
 
     // line geometry: horizontal directions sweep x with lane = row; the others
     // sweep y with lane = line c, pixel x = c + sl*y (sl = dx*dy)
@@ -545,9 +545,9 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         sts32(my_sb, P2x4);
         sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
     }
-    const uint8_t* cost = b.cost + static_cast<size_t>(a) * b.vol_cap;
+    const uint8_t* cost = b.cost + b.vbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
-        b.pdir + (static_cast<size_t>(d) * b.vol_slots + a) * b.quad_cap * 4);
+        b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
     const bool horiz = dy == 0;
     const int nsteps = horiz ? W : H;
     const int sl = dx * dy;
@@ -755,9 +755,9 @@ __global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : 16)
     const int np = min(32, W - x0);
     const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W + x0;
     const size_t obase = static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W + x0;
-    const size_t dstride = static_cast<size_t>(b.vol_slots) * b.quad_cap;
-    const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) + static_cast<size_t>(a) * b.quad_cap;
-    uint16_t* agg = b.agg + static_cast<size_t>(a) * b.vol_cap;
+    const size_t dstride = b.pool_quads;
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(b.pdir) + b.vqbase[a];
+    uint16_t* agg = b.agg + b.vbase[a];
 
     uint32_t my_q = 0, my_lh = 0;
     if (lane < np) {

@@ -1,9 +1,12 @@
 // Shared device-side definitions for the tsgm sm_100a kernels.
 //
 // Batched layout in HBM: every per-pixel map is slot-major, [max_slots][W*H]
-// (offsets: [max_slots][W*H+1]); ragged cost volumes are [vol_slots][cap]
-// with cap = W*H*d_max cells, cell (x, y, lo+j) at off[y*W+x] + j exactly as in
-// the reference's CostVolume (include/tsgm/matching_cost.hpp:50-73). A launch
+// (offsets: [max_slots][W*H+1]); ragged cost volumes live in a pool sized by
+// the frame's ACTUAL cell counts: position a of a volume chunk starts at cell
+// vbase[a] (prefix of the chunk's ncells), and within it cell (x, y, lo+j)
+// sits at off[y*W+x] + j exactly as in the reference's CostVolume
+// (include/tsgm/matching_cost.hpp:50-73; make_cost_volume sizes by N too,
+// matching_cost.cpp:30-48). A launch
 // covers `n` active slots; blockIdx.{y,z} selects the active index a, and
 // slots[a] the slot. Per-pixel maps are indexed by the slot, volumes by a
 // (the volume stages run in chunks of at most vol_slots sequences).
@@ -24,11 +27,16 @@ constexpr int kMaxCost = 24;      // matching_cost.hpp:13
 
 struct Bufs {
     int W, H, P, d_max;
-    size_t vol_cap;  // cells per volume position in cost/agg
+    size_t vol_cap;  // worst-case cells of one sequence's volume (W*H*d_max)
     // cost, agg and pdir are indexed by the position a of the slot in the
-    // launch's batch (a volume chunk of at most vol_slots sequences), not by
-    // the slot: only the per-pixel state and outputs are slot-resident
+    // launch's batch (a volume chunk), not by the slot: only the per-pixel
+    // state and outputs are slot-resident. vol_slots = the pool in worst-case
+    // sequences; a chunk holds as many sequences as their actual cells fit.
     int vol_slots;
+    const unsigned long long* vbase;   // [position] first cell in cost/agg (volume_plan_kernel)
+    const unsigned long long* vqbase;  // [position] first quad in each direction's pdir region
+    size_t pool_cells;                 // cells of the cost/agg pools
+    size_t pool_quads;                 // quads per direction region of pdir
     const int* slots;  // device [n] slot ids of the active batch
     // posterior state (A2)
     double *sd, *sp;
@@ -60,12 +68,12 @@ struct Bufs {
     uint32_t *sigl, *sigr;
     const uint8_t* const* left;   // device [n] image pointers
     const uint8_t* const* right;
-    uint8_t* cost;   // [vol pos][vol_cap]; 16 bytes of padding on both ends
-    uint16_t* agg;   // [vol pos][vol_cap]
+    uint8_t* cost;   // [pool_cells] (position a at vbase[a]); 16 bytes of padding on both ends
+    uint16_t* agg;   // [pool_cells] (position a at vbase[a])
     // scanline-group aggregation: per-direction path costs (u8) in the quad
-    // layout (qoff), [dir][vol pos][quad_cap][4]
+    // layout (qoff), [dir][pool_quads][4] (position a at vqbase[a])
     uint8_t* pdir;
-    size_t quad_cap;  // quads per volume position
+    size_t quad_cap;  // worst-case quads of one sequence
     int max_slots;
     int num_sms;     // of the context's device (kernel-choice thresholds)
     int* work;
@@ -173,6 +181,7 @@ void launch_ranges_from_pred(const Bufs& b, int n, int min_hw, int use_stddev, d
                              Launch L);
 void launch_ranges_given(const Bufs& b, int n, Launch L);  // lo/hi already set
 void launch_offsets(const Bufs& b, int n, Launch L);       // row scan + finalize
+void launch_volume_plan(const Bufs& b, int m, Launch L);
 void launch_cost(const Bufs& b, int n, Launch L);
 void launch_wta(const Bufs& b, int n, Launch L);
 void launch_median(const Bufs& b, int n, const int32_t* in_d, const uint8_t* in_v,

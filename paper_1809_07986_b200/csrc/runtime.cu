@@ -181,8 +181,10 @@ struct tsgm_ctx {
     tsgm_config cfg{};
     int W = 0, H = 0, P = 0, d_max = 0, max_slots = 0;
     size_t vol_cap = 0;
-    int vol_slots = 0;            // volume working set (positions of cost/agg/pdir)
+    int vol_slots = 0;            // volume pool, in worst-case (full-range) sequences
     std::vector<int> vol_owner;   // slot whose volumes sit at each position (-1: none)
+    unsigned long long* d_vb = nullptr;  // [2][max_slots] position bases (volume_plan_kernel)
+    std::vector<unsigned long long> h_cells, h_quads;  // readback for chunk planning
     std::vector<int> h_slots;     // host copy of the current batch's slots
     std::vector<char> fresh;      // slot holds the empty state (its next frame is full range)
     int device = 0;
@@ -244,6 +246,7 @@ struct tsgm_ctx {
     // per-stage device times of the last step (StepResult::timings,
     // temporal_filter.hpp:57-69): events recorded at stage ends on `st`
     std::string last_kernels;  // aggregation kernels of the last step's last chunk
+    int last_chunks = 0;       // volume chunks of the last step
     bool stage_timing = false;
     std::vector<cudaEvent_t> tev;
     std::vector<int> tstage;
@@ -443,14 +446,23 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
         if (vs < 1) throw std::runtime_error("tsgm_create: device memory too small for one frame's volumes");
     }
     ctx->vol_slots = vs;
-    ctx->vol_owner.assign(vs, -1);
+    ctx->vol_owner.assign(c.max_slots, -1);
     ctx->fresh.assign(c.max_slots, 1);
     b.vol_slots = vs;
+    // The pool holds vs worst-case volumes (plus the per-position rounding of
+    // volume_plan_kernel); a chunk packs as many sequences as their ACTUAL
+    // cells fit (reduced frames need ~10x fewer than P*d_max).
+    b.pool_cells = static_cast<size_t>(vs) * ctx->vol_cap + 16 * S;
+    b.pool_quads = static_cast<size_t>(vs) * b.quad_cap + 4 * S;
+    ctx->d_vb = ctx->dalloc<unsigned long long>(2 * S);
+    CK(cudaMemsetAsync(ctx->d_vb, 0, sizeof(unsigned long long) * 2 * S, ctx->st));
+    b.vbase = ctx->d_vb;
+    b.vqbase = ctx->d_vb + S;
     // 16 bytes of padding on both sides: the sweep reads aligned words around
     // each window
-    b.cost = ctx->dalloc<uint8_t>(vs * ctx->vol_cap + 32) + 16;
-    b.agg = ctx->dalloc<uint16_t>(vs * ctx->vol_cap);
-    if (ctx->use_sweep) b.pdir = ctx->dalloc<uint8_t>(8 * vs * b.quad_cap * 4);
+    b.cost = ctx->dalloc<uint8_t>(b.pool_cells + 32) + 16;
+    b.agg = ctx->dalloc<uint16_t>(b.pool_cells);
+    if (ctx->use_sweep) b.pdir = ctx->dalloc<uint8_t>(8 * b.pool_quads * 4);
     b.slots = ctx->d_slots;
     b.left = ctx->d_left;
     b.right = ctx->d_right;
@@ -542,9 +554,59 @@ Bufs chunk_bufs(const Bufs& b, int c0) {
 
 // Volume position of a slot whose volumes are still resident (last chunk).
 int vol_pos(tsgm_ctx* ctx, int slot) {
-    for (int a = 0; a < ctx->vol_slots; ++a)
+    for (int a = 0; a < static_cast<int>(ctx->vol_owner.size()); ++a)
         if (ctx->vol_owner[a] == slot) return a;
     bad("tsgm_fetch: the volumes of this slot are not resident (not in the last volume chunk)");
+}
+
+// Volume chunks of the n active slots (sizes, in batch order). When n
+// worst-case volumes fit the pool: one chunk, nothing read back. Otherwise
+// this frame's actual sizes (make_cost_volume's N, matching_cost.cpp:30-48,
+// from the offsets kernels) are read back and packed: K = the greedy chunk
+// count, then K chunks balanced by cells where they fit (else greedy).
+std::vector<int> plan_chunks(tsgm_ctx* ctx, int n) {
+    if (n <= ctx->vol_slots) return {n};
+    const Bufs& b = ctx->b;
+    const size_t S = ctx->max_slots;
+    ctx->h_cells.resize(S);
+    ctx->h_quads.resize(S);
+    CK(cudaMemcpyAsync(ctx->h_cells.data(), b.ncells, 8 * S, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(ctx->h_quads.data(), b.nquads, 8 * S, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    std::vector<unsigned long long> rc(n), rq(n);
+    unsigned long long total = 0;
+    for (int i = 0; i < n; ++i) {
+        const int s = ctx->h_slots[i];
+        rc[i] = (ctx->h_cells[s] + 15) & ~15ull;
+        rq[i] = (ctx->h_quads[s] + 3) & ~3ull;
+        total += rc[i];
+    }
+    auto pack = [&](double target) {
+        std::vector<int> m;
+        unsigned long long c = 0, q = 0, done = 0;
+        int cnt = 0;
+        for (int i = 0; i < n; ++i) {
+            const bool over = c + rc[i] > b.pool_cells || q + rq[i] > b.pool_quads;
+            const bool bal = target > 0 && cnt > 0 &&
+                             static_cast<double>(done + c + rc[i]) >
+                                 target * static_cast<double>(m.size() + 1) * 1.0001;
+            if (cnt > 0 && (over || bal)) {
+                m.push_back(cnt);
+                done += c;
+                c = q = 0;
+                cnt = 0;
+            }
+            c += rc[i];
+            q += rq[i];
+            ++cnt;
+        }
+        m.push_back(cnt);
+        return m;
+    };
+    const std::vector<int> greedy = pack(0.0);
+    if (greedy.size() == 1) return greedy;
+    const std::vector<int> bal = pack(static_cast<double>(total) / static_cast<double>(greedy.size()));
+    return bal.size() <= greedy.size() ? bal : greedy;
 }
 
 // The per-frame pipeline of step() (temporal_filter.cpp:195-232) for n slots.
@@ -583,12 +645,26 @@ void run_step(tsgm_ctx* ctx, int n) {
     // position keeps an owner from an earlier frame: a slot's volumes are
     // resident (tsgm_fetch COST/AGG) only if it is in this frame's last chunk.
     std::fill(ctx->vol_owner.begin(), ctx->vol_owner.end(), -1);
-    const int chunks = (n + ctx->vol_slots - 1) / ctx->vol_slots;
-    for (int k = 0, c0 = 0; k < chunks; ++k) {
-        const int m = (n - c0) / (chunks - k);
+    // all-fresh batches are full range (every volume worst case): balanced by count
+    bool all_fresh = true;
+    for (int i = 0; i < n; ++i) all_fresh = all_fresh && ctx->fresh[ctx->h_slots[i]];
+    std::vector<int> sizes;
+    if (all_fresh) {
+        const int chunks = (n + ctx->vol_slots - 1) / ctx->vol_slots;
+        for (int k = 0, c0 = 0; k < chunks; ++k) {
+            sizes.push_back((n - c0) / (chunks - k));
+            c0 += sizes.back();
+        }
+    } else {
+        sizes = plan_chunks(ctx, n);
+    }
+    ctx->last_chunks = static_cast<int>(sizes.size());
+    for (int k = 0, c0 = 0; k < static_cast<int>(sizes.size()); ++k) {
+        const int m = sizes[k];
         const Bufs bc = chunk_bufs(b, c0);
         bool full = true;  // every sequence of the chunk starts empty: full-range windows
         for (int a = 0; a < m; ++a) full = full && ctx->fresh[ctx->h_slots[c0 + a]];
+        launch_volume_plan(bc, m, L);
         launch_cost(bc, m, L);
         ctx->mark(kStCost);
         if (!aggregate(ctx, bc, m, L, /*fuse_wta=*/true, (c.flags & TSGM_KEEP_VOLUMES) != 0, full)) {
@@ -828,6 +904,13 @@ int tsgm_inputs_consumed(tsgm_ctx* ctx, void* consumer_stream) {
     });
 }
 
+int tsgm_last_chunks(tsgm_ctx* ctx, int32_t* chunks) {
+    return guarded([&] {
+        if (!ctx || !chunks) bad("tsgm_last_chunks: null argument");
+        *chunks = ctx->last_chunks;
+    });
+}
+
 int tsgm_last_kernels(tsgm_ctx* ctx, char* buf, size_t cap) {
     return guarded([&] {
         if (!ctx || !buf || cap == 0) bad("tsgm_last_kernels: null argument");
@@ -853,12 +936,17 @@ int tsgm_fetch(tsgm_ctx* ctx, int32_t slot, int32_t what, void* dst, size_t byte
         const OutDesc o = out_desc(ctx, what);
         size_t count = o.stride;
         size_t pos = static_cast<size_t>(slot);
+        size_t first = pos * o.stride;  // first element
         if (what == TSGM_OUT_COST || what == TSGM_OUT_AGG) {
             count = cells_of(ctx, slot);
             pos = static_cast<size_t>(vol_pos(ctx, slot));
+            unsigned long long vb = 0;
+            CK(cudaMemcpyAsync(&vb, ctx->d_vb + pos, sizeof vb, cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            first = static_cast<size_t>(vb);
         }
         if (bytes < count * o.elem) bad("tsgm_fetch: destination too small");
-        const char* src = static_cast<const char*>(o.base) + pos * o.stride * o.elem;
+        const char* src = static_cast<const char*>(o.base) + first * o.elem;
         CK(cudaMemcpyAsync(dst, src, count * o.elem, cudaMemcpyDeviceToHost, ctx->st));
         sync(ctx);
     });
@@ -953,7 +1041,8 @@ int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t
                          float* ms_per_launch, uint64_t* cells) {
     return guarded([&] {
         check_slots(ctx, n, slots);
-        if (n > ctx->vol_slots) bad("tsgm_bench_aggregate: more slots than the volume working set");
+        if (n > static_cast<int>(ctx->vol_owner.size()))
+            bad("tsgm_bench_aggregate: more slots than the volume working set");
         for (int i = 0; i < n; ++i)
             if (ctx->vol_owner[i] != slots[i])
                 bad("tsgm_bench_aggregate: slots must be the last volume chunk, in step order");
@@ -1945,6 +2034,7 @@ int tsgm_estimate_measurement_noise(int32_t n_frames, int32_t w, int32_t h, cons
                 for (int k = 0, c0 = 0; k < chunks; ++k) {
                     const int mc = (m - c0) / (chunks - k);
                     const Bufs bc = chunk_bufs(b, c0);
+                    launch_volume_plan(bc, mc, L);
                     launch_cost(bc, mc, L);
                     if (!aggregate(c, bc, mc, L, /*fuse_wta=*/true, /*keep_s=*/false, /*full_range=*/true))
                         launch_wta(bc, mc, L);

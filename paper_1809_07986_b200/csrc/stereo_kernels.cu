@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
         sr[x] = b.sigr[pbase + x];
     }
     __syncthreads();
-    uint8_t* base = b.cost + static_cast<size_t>(a) * b.vol_cap;
+    uint8_t* base = b.cost + b.vbase[a];
     const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
     const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
     const int nwarps = static_cast<int>(blockDim.x >> 5);
@@ -458,6 +458,45 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
     }
 }
 
+// Volume plan of a chunk of m positions: position a
+// starts at the prefix of the chunk's ACTUAL cell and quad counts (the N of
+// make_cost_volume, matching_cost.cpp:30-48), rounded up to 16 cells / 4
+// quads, instead of a worst-case P*d_max stride. One warp, u64 warp scans.
+__global__ void volume_plan_kernel(Bufs b, int m, unsigned long long* vb) {
+    const int lane = static_cast<int>(threadIdx.x);
+    unsigned long long cc = 0, cq = 0;  // carries
+    for (int a0 = 0; a0 < m; a0 += 32) {
+        const int a = a0 + lane;
+        unsigned long long c = 0, q = 0;
+        if (a < m) {
+            const int s = b.slots[a];
+            c = (b.ncells[s] + 15ull) & ~15ull;
+            q = (b.nquads[s] + 3ull) & ~3ull;
+        }
+        unsigned long long ic = c, iq = q;  // inclusive scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long tc = __shfl_up_sync(0xffffffffu, ic, o);
+            const unsigned long long tq = __shfl_up_sync(0xffffffffu, iq, o);
+            if (lane >= o) {
+                ic += tc;
+                iq += tq;
+            }
+        }
+        if (a < m) {
+            vb[a] = cc + ic - c;
+            vb[b.max_slots + a] = cq + iq - q;
+        }
+        cc += __shfl_sync(0xffffffffu, ic, 31);
+        cq += __shfl_sync(0xffffffffu, iq, 31);
+    }
+}
+
+void launch_volume_plan(const Bufs& b, int m, Launch L) {
+    volume_plan_kernel<<<1, 32, 0, L.st>>>(b, m, const_cast<unsigned long long*>(b.vbase));
+    ++*L.counter;
+}
+
 void launch_cost(const Bufs& b, int n, Launch L) {
     const size_t smem = sizeof(uint32_t) * 2 * b.W;
     cost_kernel<<<dim3(b.H, n), 512, smem, L.st>>>(b);
@@ -473,7 +512,7 @@ __global__ void wta_kernel(Bufs b) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t* off = b.off + static_cast<size_t>(s) * (b.P + 1);
-    const uint16_t* agg = b.agg + static_cast<size_t>(a) * b.vol_cap;
+    const uint16_t* agg = b.agg + b.vbase[a];
     for (int i = warp; i < b.P; i += nwarps) {
         const int x = i % b.W, y = i / b.W;
         const size_t pi = static_cast<size_t>(s) * b.P + i;

@@ -866,6 +866,12 @@ class Engine:
         check(self._lib.tsgm_last_kernels(self._h, buf, 256))
         return buf.value.decode()
 
+    def last_chunks(self) -> int:
+        """Volume chunks the last step needed (volumes packed by actual cells)."""
+        v = C.c_int32(0)
+        check(self._lib.tsgm_last_chunks(self._h, C.byref(v)))
+        return v.value
+
     def timings(self):
         """StepTimings of the last step (whole batch, device seconds); needs
         ``EngineConfig(stage_timings=True)``."""

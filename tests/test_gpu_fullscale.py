@@ -7,8 +7,8 @@ sequence per host thread, EVERY frame, at the BASELINE sizes:
 * config 2: 64 sequences x 30 frames at 1242x375 (the bench workload; reduced
   frames run scan_kernel<32,32> + combine_wta_kernel<8,1>);
 * config 1: one sequence x 30 frames at 1242x375 (the small-batch kernels);
-* config 4: 4 sequences x 20 frames at 2048x1024, D=256, through two volume
-  chunks per frame (vol_slots=2, the config-4 memory plan).
+* config 4: 4 sequences x 20 frames at 2048x1024, D=256, with a 2-volume pool:
+  frame 0 in two chunks, reduced frames packed by actual cells into one.
 
 Checked per frame and sequence: WTA (meas_d/meas_valid), posterior d/p/valid,
 export map, diff and mask, all with np.array_equal (integer stages bit-exact;
@@ -45,6 +45,7 @@ def run_fullscale(port, cfgs, frames, params, filt, vol_slots=0):
     slots = list(range(n))
     states = [None] * n
     kernels = []
+    chunks = []
 
     def mot(i, k):
         P = seqs[i][2]
@@ -55,6 +56,7 @@ def run_fullscale(port, cfgs, frames, params, filt, vol_slots=0):
             motions = [mot(i, k) for i in range(n)]
             eng.step(slots, [s[0][k] for s in seqs], [s[1][k] for s in seqs], motions)
             kernels.append(eng.last_kernels())
+            chunks.append(eng.last_chunks())
             refs = list(pool.map(
                 lambda i: port.step(states[i], seqs[i][0][k], seqs[i][1][k], motions[i][0],
                                     motions[i][1], calib, params, filt, debug=True), range(n)))
@@ -67,13 +69,14 @@ def run_fullscale(port, cfgs, frames, params, filt, vol_slots=0):
                                              f"({kernels[-1]})")
                 states[i] = (ref["d"], ref["p"], ref["valid"])
     eng.close()
-    return kernels
+    return kernels, chunks
 
 
 def test_config2_bench_workload_64x30(port):
     cfgs = [SceneConfig.baseline_config(2, seed=s, n_movers=s % 5, frames=30) for s in range(64)]
-    kernels = run_fullscale(port, cfgs, 30, tsgm.SgmParams(10, 120, 8, 0, 128),
-                            tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=3.0))
+    kernels, chunks = run_fullscale(port, cfgs, 30, tsgm.SgmParams(10, 120, 8, 0, 128),
+                                    tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=3.0))
+    assert set(chunks) == {1}
     # the reduced frames ran the kernels bench.py times at 64 sequences per GPU
     assert set(kernels[1:]) == {"scan_kernel<32,32>+combine_wta_kernel<8,1>"}, set(kernels)
 
@@ -86,6 +89,10 @@ def test_config1_full_size_30_frames(port):
 
 def test_config4_full_size_chunked(port):
     cfgs = [SceneConfig.baseline_config(4, seed=s, frames=20) for s in range(4)]
-    run_fullscale(port, cfgs, 20, tsgm.SgmParams(10, 120, 8, 0, 256),
-                  tsgm.FilterConfig(p_init=16384.0, range_use_stddev=True, range_stddev_gain=3.0),
-                  vol_slots=2)
+    _, chunks = run_fullscale(port, cfgs, 20, tsgm.SgmParams(10, 120, 8, 0, 256),
+                              tsgm.FilterConfig(p_init=16384.0, range_use_stddev=True,
+                                                range_stddev_gain=3.0),
+                              vol_slots=2)
+    # frame 0 is full range (4 worst-case volumes: two chunks of 2); reduced
+    # frames are packed by their actual cells into the 2-volume pool: one chunk
+    assert chunks[0] == 2 and set(chunks[1:]) == {1}, chunks

@@ -2,6 +2,7 @@
 
     python tools/summarize_ncu.py full  <report.ncu-rep> <out.json>   # --set full capture
     python tools/summarize_ncu.py list  <launches.csv>   <out.json>   # gpu__time_duration list
+    python tools/summarize_ncu.py csv   <details.csv>,<raw.csv> <out.json>  # exported pages
 
 `full` extracts duration, DRAM bytes (read+write), executed instructions,
 issue/occupancy figures and pipe utilisation per profiled kernel; `list` sums
@@ -34,10 +35,16 @@ FULL_METRICS = {
 }
 
 
-def full(rep, out):
-    txt = subprocess.run([NCU, "-i", rep, "--page", "details", "--csv"], capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(io.StringIO(txt)))
+def _page(rep, page):
+    if rep.endswith(".csv"):  # an exported page (--page details|raw --csv) from the GPU box
+        return open(rep).read()
+    return subprocess.run([NCU, "-i", rep, "--page", page, "--csv"], capture_output=True,
+                          text=True).stdout
+
+
+def full(rep, out, raw_rep=None):
+    """One entry per profiled launch ("<ID> <kernel>"), details + raw pipe metrics."""
+    rows = list(csv.reader(io.StringIO(_page(rep, "details"))))
     hdr = rows[0]
     ki, si, ni, ui, vi = (hdr.index(k) for k in ("Kernel Name", "Section Name", "Metric Name",
                                                   "Metric Unit", "Metric Value"))
@@ -45,13 +52,11 @@ def full(rep, out):
     for r in rows[1:]:
         if len(r) <= vi:
             continue
-        k = r[ki].split("(")[0]
+        k = f'{r[hdr.index("ID")]} {r[ki].split("(")[0]}'
         d = kern.setdefault(k, {})
         if r[ni] in FULL_METRICS:
             d[FULL_METRICS[r[ni]]] = f"{r[vi]} {r[ui]}".strip()
-    raw = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
-    rr = list(csv.reader(io.StringIO(raw)))
+    rr = list(csv.reader(io.StringIO(_page(raw_rep or rep, "raw"))))
     if len(rr) > 2:
         h = rr[0]
         want = ["dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -64,7 +69,7 @@ def full(rep, out):
                 "gpu__time_duration.sum"]
         units = rr[1]
         for row in rr[2:]:
-            k = row[h.index("Kernel Name")].split("(")[0] if "Kernel Name" in h else "kernel"
+            k = f'{row[h.index("ID")]} {row[h.index("Kernel Name")].split("(")[0]}'
             d = kern.setdefault(k, {})
             for w in want:
                 if w in h:
@@ -97,4 +102,8 @@ def launch_list(path, out):
 
 if __name__ == "__main__":
     mode, src, dst = sys.argv[1:4]
-    (full if mode == "full" else launch_list)(src, dst)
+    if mode == "csv":
+        det, raw = src.split(",")
+        full(det, dst, raw)
+    else:
+        (full if mode == "full" else launch_list)(src, dst)
