@@ -8,7 +8,11 @@ auto-sized to free memory), so the matching stages execute in chunks. Reports
 frames/s through the host-image API, the working set and device memory, and
 spot-checks sequence 0's first frames bit-exact against the oracle.
 
-    python tools/config4_stress.py [sequences] [frames] [check_frames]
+    python tools/config4_stress.py [sequences] [frames] [check_frames] [vol_slots]
+
+vol_slots = the volume pool in worst-case (full-range) sequences (0 = auto).
+Volumes are packed by their actual cells, so frame 0 (full range) needs
+ceil(S / vol_slots) chunks and the reduced frames usually one.
 """
 import json
 import os
@@ -28,6 +32,7 @@ def main():
     S = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     F = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     check = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    vs = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     import torch
     cfgs = [SceneConfig.baseline_config(4, seed=s, frames=F) for s in range(S)]
     c0 = cfgs[0]
@@ -38,16 +43,19 @@ def main():
     seqs = [render(c) for c in cfgs]
     t_render = time.time() - t0
     free0, total = torch.cuda.mem_get_info()
-    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=S, keep_volumes=False))
+    eng = tsgm.Engine(tsgm.EngineConfig(calib, params, filt, max_slots=S, keep_volumes=False,
+                                        vol_slots=vs))
     free1, _ = torch.cuda.mem_get_info()
     slots = list(range(S))
     mots = [[(np.eye(3), np.zeros(3)) if k == 0 else tsgm.relative_motion(P[k - 1], P[k])
              for k in range(F)] for (_, _, P, _) in seqs]
     ed0 = []
+    chunks = []
     eng.sync()
     eng.timer_begin()
     for k in range(F):
         eng.step(slots, [s[0][k] for s in seqs], [s[1][k] for s in seqs], [m[k] for m in mots])
+        chunks.append(eng.last_chunks())
         if k < check:
             ed0.append((eng.fetch(0, "export_d"), eng.fetch(0, "state_p"), eng.fetch(0, "mask")))
     ms = eng.timer_end()
@@ -69,7 +77,7 @@ def main():
         "frames_per_s_host_api": round(S * F / (ms * 1e-3), 2),
         "ms_total": round(ms, 1),
         "vol_slots": vol_slots,
-        "volume_chunks_per_frame": -(-S // vol_slots),
+        "volume_chunks_per_frame": chunks,
         "device_mem_gb": {"total": round(total / 2**30, 1),
                           "context": round((free0 - free1) / 2**30, 1)},
         "render_s": round(t_render, 1),
