@@ -66,9 +66,16 @@ struct ScanParams {
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     return __byte_perm(a, b, s);
 }
+// PRMT with the selector nibbles' msb honoured (sign replication of the
+// selected byte); __byte_perm uses only the low 3 bits of each nibble.
+__device__ __forceinline__ uint32_t prmt_sx(uint32_t a, uint32_t s) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(a), "r"(s));
+    return d;
+}
 // Cost of a level outside the window: L = C + min(...) stays < 2^16 and
-// L - min L >= kPoison - 255 > P2, so it never wins a min and normalises to P2.
-constexpr uint32_t kPoison2 = 0x3f003f00u;
+// L - min L >= kPoisonQ - 255 > P2, so it never wins a min and normalises to P2.
+constexpr uint32_t kPoisonQ = 0x3fff3fffu;
 
 __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
@@ -126,43 +133,32 @@ struct PixMeta {
 // `rp` are the shared addresses of the scanline's slot and quad range.
 template <int G, int Q>
 __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has_pred,
-                                           uint32_t sb, uint32_t rp, const uint8_t* cost,
+                                           uint32_t sb, uint32_t rp, const uint32_t* costq,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
-                                           uint32_t P2x4, const uint8_t* mask_tab) {
+                                           uint32_t P2x4) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
     const int k0 = lg * Q;                  // first window quad of this lane
     const int a0 = q0 + min(k0, nq - 1);    // absolute quad (clamped into the window)
 
-    uint32_t CA[Q], CB[Q], ivA[Q], ivB[Q], LA[Q], LB[Q];
+    uint32_t CA[Q], CB[Q], LA[Q], LB[Q];
     bool act[Q];
     {
-        // matching costs of levels 4*a0 .. 4*a0 + 4Q - 1 (bytes outside the window masked)
-        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + pm.cell + (4 * a0 - lo);
-        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-        const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
-        uint32_t c[Q + 1];
-#pragma unroll
-        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
-        // invalid-level masks of the lane's 16 levels from the table:
-        // row = levels below lo in the first quad, col = last valid level + 1
-        const int start = 4 * (q0 + k0);  // unclamped first level of the lane
-        const int lrel = k0 == 0 ? (lo & 3) : 0;
-        const int hrel = pix ? min(max(hi - start, -1), 16) : -1;
-        const uint4* row = reinterpret_cast<const uint4*>(
-            mask_tab + 32u * static_cast<uint32_t>(lrel * 18 + hrel + 1));
-        const uint4 m0 = row[0], m1 = row[1];
-        ivA[0] = m0.x; ivB[0] = m0.y;
-        if (Q > 1) { ivA[1] = m0.z; ivB[1] = m0.w; }
-        if (Q > 2) { ivA[2] = m1.x; ivB[2] = m1.y; }
-        if (Q > 3) { ivA[3] = m1.z; ivB[3] = m1.w; }
+        // matching costs of window quads a0 - q0 .. a0 - q0 + Q - 1 in the quad
+        // layout (launch_cost): a level outside [lo, hi] inside the window's
+        // quads holds 0xff, whose sign-replicated u16 0xffff masks to the
+        // poison 0x3fff; quads past the window (and lanes without a pixel) are
+        // poisoned whole. Poisoned levels lose every min and normalise to P2.
+        const uint32_t* cw = costq + pm.qo + static_cast<uint32_t>(a0 - q0);
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
-            const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
-            CA[t] = prmt(cq, 0u, 0x4140u) | (ivA[t] & kPoison2);
-            CB[t] = prmt(cq, 0u, 0x4342u) | (ivB[t] & kPoison2);
             act[t] = pix && k0 + t < nq;
+            const uint32_t c = __ldg(cw + t);
+            const uint32_t am = act[t] ? 0xffffffffu : 0u;
+            // kPoisonQ & (x | ~am): x masked to 14 bits, or the poison when inactive
+            CA[t] = kPoisonQ & (prmt_sx(c, 0x9180u) | ~am);
+            CB[t] = kPoisonQ & (prmt_sx(c, 0xb3a2u) | ~am);
         }
     }
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
@@ -214,25 +210,21 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
 // path reads there. Same arithmetic as scan_pixel<G, Q>.
 template <int G, int Q = 4>
 __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, bool has_pred,
-                                                uint32_t sb, uint32_t rp, const uint8_t* cost,
+                                                uint32_t sb, uint32_t rp, const uint32_t* costq,
                                                 uint32_t* out, uint32_t P1x2, uint32_t P2x2,
                                                 uint32_t P2x4, uint32_t full_rng) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int a0 = lg * Q;
     uint32_t CA[Q], CB[Q], LA[Q], LB[Q];
     {
-        // (a group without a pixel reads the volume's first window instead: in bounds)
-        const uintptr_t addr = reinterpret_cast<uintptr_t>(cost) + (pix ? pm.cell : 0u) + 4 * a0;
-        const uint32_t* aw = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-        const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
-        uint32_t c[Q + 1];
-#pragma unroll
-        for (int t = 0; t <= Q; ++t) c[t] = __ldg(aw + t);
+        // (a group without a pixel reads the volume's first window instead: in
+        // bounds); a full window's quads hold no pad bytes
+        const uint32_t* cw = costq + (pix ? pm.qo : 0u) + a0;
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
-            const uint32_t cq = __funnelshift_r(c[t], c[t + 1], sh);
-            CA[t] = prmt(cq, 0u, 0x4140u);
-            CB[t] = prmt(cq, 0u, 0x4342u);
+            const uint32_t c = __ldg(cw + t);
+            CA[t] = prmt(c, 0u, 0x4140u);
+            CB[t] = prmt(c, 0u, 0x4342u);
         }
     }
     const uint32_t prng = lds32(rp);
@@ -281,32 +273,6 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, boo
     }
 }
 
-// invalid-level masks: entry (lrel, hrel) covers 16 levels = 4 quads x
-// (ivA, ivB); level j is invalid iff j < lrel or j > hrel (hrel in -1..16)
-struct alignas(16) MaskTable {
-    uint32_t v[4 * 18 * 8];
-    constexpr MaskTable() : v() {
-        for (int e = 0; e < 4 * 18 * 8; ++e) {
-            const int lrel = e / (18 * 8), hrel = (e / 8) % 18 - 1, word = e % 8;
-            const int t = word >> 1, half0 = 4 * t + 2 * (word & 1);
-            uint32_t m = 0u;
-            for (int h = 0; h < 2; ++h) {
-                const int j = half0 + h;
-                if (j < lrel || j > hrel) m |= 0xffffu << (16 * h);
-            }
-            v[e] = m;
-        }
-    }
-};
-// built at compile time; each CTA copies it to shared memory (16-byte loads)
-__device__ const MaskTable g_mask_table{};
-
-__device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
-    const uint4* src = reinterpret_cast<const uint4*>(g_mask_table.v);
-    uint4* dst = reinterpret_cast<uint4*>(tab);
-    for (int e = threadIdx.x; e < 4 * 18 * 8 / 4; e += blockDim.x) dst[e] = __ldg(src + e);
-}
-
 // SPW = scanlines per warp (32, 16 or 8): a narrow window (<= 4 quads) is
 // computed by GN = 32/SPW lanes x QN = 4/GN quads of its scanline's group;
 // fewer scanlines per warp give proportionally more warps for small batches.
@@ -314,7 +280,7 @@ __device__ __forceinline__ void fill_mask_table(uint32_t* tab) {
 // a; wbase = the warp's shared-memory area.
 template <int SPW>
 __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, int d, int a, int g,
-                                          const uint8_t* mask_tab, uint32_t wbase) {
+                                          uint32_t wbase) {
     constexpr int GN = 32 / SPW, QN = 4 / GN;
     const int lane = static_cast<int>(threadIdx.x & 31);
     const int s = slot_of(b, a);
@@ -335,7 +301,7 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
     }
 
-    const uint8_t* cost = b.cost + b.vbase[a];
+    const uint32_t* costq = b.costq + b.vqbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
 
@@ -394,14 +360,13 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
 #define SCAN_PREFETCH 1
 #endif
         if (SCAN_PREFETCH && act1 && lgs == 0) {  // step k+1's window towards L1 (its metadata arrived a step ago)
-            const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
-            const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
-            const uint8_t* c0 = cost + m1.cell;
-            // straight-line (windows are <= 256 levels, sweep_supported): 0.8%
+            const int nb = 4 * static_cast<int>(m1.nq);  // the window's bytes in the quad layout
+            const char* c0 = reinterpret_cast<const char*>(costq + m1.qo);
+            // straight-line (windows are <= 64 quads, sweep_supported): 0.8%
             // faster than the loop
             asm volatile("prefetch.global.L1 [%0];" ::"l"(c0));
-            if (n_n + 4 > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 128));
-            if (n_n + 4 > 256) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 256));
+            if (nb + 4 > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 128));
+            if (nb + 4 > 256) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 256));
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
@@ -415,18 +380,17 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
             // windows of <= 4 quads: the lane itself, Q = the warp's widest such window
             const int qn = __reduce_max_sync(0xffffffffu, narrow ? nq : 0);
             if (qn > 3)
-                scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2,
-                                 P2x4, mask_tab);
+                scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2,
+                                 P2x4);
             else if (qn == 3)
-                scan_pixel<1, 3>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2,
-                                 P2x4, mask_tab);
+                scan_pixel<1, 3>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2,
+                                 P2x4);
             else if (qn > 0)
-                scan_pixel<1, 2>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2,
-                                 P2x4, mask_tab);
+                scan_pixel<1, 2>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2,
+                                 P2x4);
         } else if (__any_sync(0xffffffffu, narrow)) {
             // windows of <= 4 quads: the scanline's GN lanes x QN quads
-            scan_pixel<GN, QN>(narrow, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                               mask_tab);
+            scan_pixel<GN, QN>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
         }
         // wider windows: groups of G lanes x 4 quads, 32/G windows per pass;
         // a window's owner is the first lane of its scanline's group
@@ -451,11 +415,11 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
                 const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
                 const uint32_t sline = static_cast<uint32_t>(src / GN);
                 if (full)
-                    scan_pixel_full<G>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, cost,
+                    scan_pixel_full<G>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, costq,
                                        out, P1x2, P2x2, P2x4, sp.full_rng);
                 else
-                    scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, cost,
-                                     out, P1x2, P2x2, P2x4, mask_tab);
+                    scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, costq,
+                                     out, P1x2, P2x2, P2x4);
                 bw &= ~done;
             }
         };
@@ -498,10 +462,6 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
 template <int SPWH, int SPWV>
 __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
-    fill_mask_table(mask_tab_s);
-    __syncthreads();
-    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
@@ -513,9 +473,9 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (SPWH == SPWV || sp.dy[d] != 0)  // (one body when both widths agree)
-        scan_task<SPWV>(b, sp, d, a, g, mask_tab, wbase);
+        scan_task<SPWV>(b, sp, d, a, g, wbase);
     else
-        scan_task<SPWH>(b, sp, d, a, g, mask_tab, wbase);
+        scan_task<SPWH>(b, sp, d, a, g, wbase);
 }
 
 
@@ -527,7 +487,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanP
 // warp tasks per sequence).
 template <int G, int Q = 4>
 __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, int d, int a, int g,
-                                           const uint8_t* mask_tab, uint32_t wbase) {
+                                           uint32_t wbase) {
     constexpr int LPW = 32 / G;  // scanlines per warp
     const int lane = static_cast<int>(threadIdx.x & 31);
     const int gi = lane / G;
@@ -545,7 +505,7 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         sts32(my_sb, P2x4);
         sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
     }
-    const uint8_t* cost = b.cost + b.vbase[a];
+    const uint32_t* costq = b.costq + b.vqbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
     const bool horiz = dy == 0;
@@ -585,11 +545,9 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         const PixMeta mc = m1;
         act1 = act2;
         m1 = m2;
-        if (act1) {  // this lane's 16 levels of step k+1 towards L1
-            const int lo_n = static_cast<int>(m1.lohi & 0xffffu);
-            const int n_n = static_cast<int>(m1.lohi >> 16) - lo_n + 1;
-            if (16 * lg < n_n + 4)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(cost + m1.cell + 16 * lg));
+        if (act1) {  // this lane's 4 quads of step k+1 towards L1
+            if (4u * static_cast<uint32_t>(lg) < m1.nq)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(costq + m1.qo + 4 * lg));
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
@@ -601,11 +559,10 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         // window of the class size (frames from an empty state)
         const bool fullw = sp.full_ok == Q * G && mc.lohi == sp.full_lohi;
         if (__all_sync(0xffffffffu, fullw || !active))
-            scan_pixel_full<G, Q>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
+            scan_pixel_full<G, Q>(active, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4,
                                   sp.full_rng);
         else
-            scan_pixel<G, Q>(active, mc, prev_active, my_sb, my_rp, cost, out, P1x2, P2x2, P2x4,
-                             mask_tab);
+            scan_pixel<G, Q>(active, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
         prev_active = active;
     }
 }
@@ -617,10 +574,6 @@ __host__ __device__ inline int lines_warp_bytes(int d_max, int G) {
 template <int G>
 __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
-    fill_mask_table(mask_tab_s);
-    __syncthreads();
-    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
@@ -631,7 +584,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
     const int a = r / groups, g = r % groups;
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
-    lines_task<G>(b, sp, d, a, g, mask_tab, wbase);
+    lines_task<G>(b, sp, d, a, g, wbase);
 }
 
 // Line groups everywhere, the horizontal lines with wider groups (GH lanes x
@@ -641,10 +594,6 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
 template <int G, int GH, int QH>
 __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_mixed_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
-    fill_mask_table(mask_tab_s);
-    __syncthreads();
-    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
@@ -656,9 +605,9 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_mixed_kernel(Bufs 
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (sp.dy[d] == 0)
-        lines_task<GH, QH>(b, sp, d, a, g, mask_tab, wbase);
+        lines_task<GH, QH>(b, sp, d, a, g, wbase);
     else
-        lines_task<G, 4>(b, sp, d, a, g, mask_tab, wbase);
+        lines_task<G, 4>(b, sp, d, a, g, wbase);
 }
 
 // Mixed: horizontal lines as line groups (G lanes x 4 quads per scanline,
@@ -669,10 +618,6 @@ template <int GH, int QH, int SPWV>
 // 3264 -> 3483 frames/s; 32-lane groups keep 16: 4 sequences 2447 vs 2099)
 __global__ void __launch_bounds__(32 * kScanWarps, GH == 32 ? 16 : 12) scan_mixed_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ __align__(16) uint32_t mask_tab_s[4 * 18 * 8];
-    fill_mask_table(mask_tab_s);
-    __syncthreads();
-    const uint8_t* mask_tab = reinterpret_cast<const uint8_t*>(mask_tab_s);
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
@@ -684,9 +629,9 @@ __global__ void __launch_bounds__(32 * kScanWarps, GH == 32 ? 16 : 12) scan_mixe
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (sp.dy[d] == 0)
-        lines_task<GH, QH>(b, sp, d, a, g, mask_tab, wbase);
+        lines_task<GH, QH>(b, sp, d, a, g, wbase);
     else
-        scan_task<SPWV>(b, sp, d, a, g, mask_tab, wbase);
+        scan_task<SPWV>(b, sp, d, a, g, wbase);
 }
 
 

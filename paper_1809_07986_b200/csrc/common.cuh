@@ -68,7 +68,8 @@ struct Bufs {
     uint32_t *sigl, *sigr;
     const uint8_t* const* left;   // device [n] image pointers
     const uint8_t* const* right;
-    uint8_t* cost;   // [pool_cells] (position a at vbase[a]); 16 bytes of padding on both ends
+    uint8_t* cost;   // [pool_cells] (position a at vbase[a]): the reference layout, on demand
+    uint32_t* costq; // [pool_quads] (position a at vqbase[a]): quad layout, 0xff outside [lo, hi]
     uint16_t* agg;   // [pool_cells] (position a at vbase[a])
     // scanline-group aggregation: per-direction path costs (u8) in the quad
     // layout (qoff), [dir][pool_quads][4] (position a at vqbase[a])
@@ -182,7 +183,9 @@ void launch_ranges_from_pred(const Bufs& b, int n, int min_hw, int use_stddev, d
 void launch_ranges_given(const Bufs& b, int n, Launch L);  // lo/hi already set
 void launch_offsets(const Bufs& b, int n, Launch L);       // row scan + finalize
 void launch_volume_plan(const Bufs& b, int m, Launch L);
-void launch_cost(const Bufs& b, int n, Launch L);
+void launch_cost(const Bufs& b, int n, Launch L);  // quad layout (costq), the aggregation's input
+void launch_cost_ragged(const Bufs& b, int n, Launch L);  // reference layout (cost)
+void launch_cost_quads_from_ragged(const Bufs& b, int n, Launch L);
 void launch_wta(const Bufs& b, int n, Launch L);
 void launch_median(const Bufs& b, int n, const int32_t* in_d, const uint8_t* in_v,
                    int32_t* out_d, uint8_t* out_v, Launch L);

@@ -247,6 +247,7 @@ struct tsgm_ctx {
     // temporal_filter.hpp:57-69): events recorded at stage ends on `st`
     std::string last_kernels;  // aggregation kernels of the last step's last chunk
     int last_chunks = 0;       // volume chunks of the last step
+    int last_c0 = 0;           // batch index of the last chunk's first sequence
     bool stage_timing = false;
     std::vector<cudaEvent_t> tev;
     std::vector<int> tstage;
@@ -345,6 +346,12 @@ void validate_config(const tsgm_config& c) {
     if (c.max_slots < 1) bad("tsgm_create: max_slots must be >= 1");
 }
 
+// The reference-layout cost pool, allocated on first need (16 bytes of
+// padding on both sides: the fallback and stage kernels read aligned words).
+void ensure_ragged_cost(tsgm_ctx* ctx) {
+    if (!ctx->b.cost) ctx->b.cost = ctx->dalloc<uint8_t>(ctx->b.pool_cells + 32) + 16;
+}
+
 void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     ctx->cfg = c;
     ctx->W = c.width;
@@ -434,7 +441,8 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     // the per-frame volumes last: C (u8), S (u16) and, for the scan
     // aggregation, 8 directions of u8 path costs per cell, for vol_slots
     // sequences at a time (the rest of the batch runs in further chunks)
-    const size_t vol_bytes = 3 * ctx->vol_cap + (ctx->use_sweep ? 8 * b.quad_cap * 4 : 0);
+    // (the reference-layout cost is allocated on demand: fetch, stage API, fallback)
+    const size_t vol_bytes = 2 * ctx->vol_cap + 4 * b.quad_cap + (ctx->use_sweep ? 8 * b.quad_cap * 4 : 0);
     int vs = c.vol_slots > 0 ? std::min(c.vol_slots, c.max_slots) : c.max_slots;
     if (c.vol_slots <= 0) {
         size_t free_b = 0, total_b = 0;
@@ -460,7 +468,10 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.vqbase = ctx->d_vb + S;
     // 16 bytes of padding on both sides: the sweep reads aligned words around
     // each window
-    b.cost = ctx->dalloc<uint8_t>(b.pool_cells + 32) + 16;
+    b.cost = nullptr;
+    if (!ctx->use_sweep || c.max_slots == 1) ensure_ragged_cost(ctx);
+    // (+64 words: a narrow lane reads up to 3 quads past its window)
+    b.costq = ctx->dalloc<uint32_t>(b.pool_quads + 64);
     b.agg = ctx->dalloc<uint16_t>(b.pool_cells);
     if (ctx->use_sweep) b.pdir = ctx->dalloc<uint8_t>(8 * b.pool_quads * 4);
     b.slots = ctx->d_slots;
@@ -526,10 +537,13 @@ void check_slots(tsgm_ctx* ctx, int n, const int32_t* slots) {
 // configuration fits it, else the per-direction scanline kernels. With
 // fuse_wta, winner_takes_all is fused into the combine (S is then written
 // only if keep_s) and the caller skips launch_wta.
+// cost_in_ragged: the matching costs come from a caller (b.cost, reference
+// layout) instead of launch_cost (b.costq, quad layout).
 bool aggregate(tsgm_ctx* ctx, const Bufs& b, int n, Launch L, bool fuse_wta = false,
-               bool keep_s = true, bool full_range = false) {
+               bool keep_s = true, bool full_range = false, bool cost_in_ragged = false) {
     const tsgm_config& c = ctx->cfg;
     if (ctx->use_sweep && sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2)) {
+        if (cost_in_ragged) launch_cost_quads_from_ragged(b, n, L);
         launch_aggregate_sweep(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set,
                                (keep_s || !fuse_wta) ? 1 : 0, fuse_wta ? 1 : 0, L,
                                (fuse_wta && b.sub) ? 1 : 0, full_range);
@@ -537,6 +551,8 @@ bool aggregate(tsgm_ctx* ctx, const Bufs& b, int n, Launch L, bool fuse_wta = fa
         return fuse_wta;
     }
     if (b.sub) bad("TSGM_SUBPIXEL needs the scan aggregation (P2 + 24 <= 255, d_max <= 256)");
+    // the per-direction fallback reads the reference layout
+    if (!cost_in_ragged) launch_cost_ragged(b, n, L);
     launch_aggregate(b, n, c.sgm.p1, c.sgm.p2, c.sgm.paths, c.sgm.path_set, L);
     ctx->last_kernels = "aggregate_kernels(scanline fallback)+wta_kernel";
     return false;
@@ -673,6 +689,7 @@ void run_step(tsgm_ctx* ctx, int n) {
             ctx->mark(kStWta);
         }
         for (int a = 0; a < m; ++a) ctx->vol_owner[a] = ctx->h_slots[c0 + a];
+        ctx->last_c0 = c0;
         c0 += m;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
@@ -940,13 +957,22 @@ int tsgm_fetch(tsgm_ctx* ctx, int32_t slot, int32_t what, void* dst, size_t byte
         if (what == TSGM_OUT_COST || what == TSGM_OUT_AGG) {
             count = cells_of(ctx, slot);
             pos = static_cast<size_t>(vol_pos(ctx, slot));
+            if (what == TSGM_OUT_COST) {
+                // the reference layout from the census of the slot's last step
+                ensure_ragged_cost(ctx);
+                Bufs one = chunk_bufs(ctx->b, ctx->last_c0 + static_cast<int>(pos));
+                one.vbase = ctx->b.vbase + pos;
+                one.vqbase = ctx->b.vqbase + pos;
+                launch_cost_ragged(one, 1, ctx->L());
+            }
             unsigned long long vb = 0;
             CK(cudaMemcpyAsync(&vb, ctx->d_vb + pos, sizeof vb, cudaMemcpyDeviceToHost, ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
             first = static_cast<size_t>(vb);
         }
         if (bytes < count * o.elem) bad("tsgm_fetch: destination too small");
-        const char* src = static_cast<const char*>(o.base) + first * o.elem;
+        const void* base = what == TSGM_OUT_COST ? static_cast<const void*>(ctx->b.cost) : o.base;
+        const char* src = static_cast<const char*>(base) + first * o.elem;
         CK(cudaMemcpyAsync(dst, src, count * o.elem, cudaMemcpyDeviceToHost, ctx->st));
         sync(ctx);
     });
@@ -1106,7 +1132,7 @@ int tsgm_build_cost_volume(const uint8_t* left, const uint8_t* right, int32_t w,
         launch_ranges_given(c->b, 1, c->L());
         launch_offsets(c->b, 1, c->L());
         launch_census(c->b, 1, c->L());
-        launch_cost(c->b, 1, c->L());
+        launch_cost_ragged(c->b, 1, c->L());
         d2h(c, offsets, c->b.off, c->P + 1);
         d2h(c, cost, c->b.cost, total);
         sync(c);
@@ -1127,7 +1153,7 @@ int tsgm_aggregate_paths(const uint8_t* cost, const uint16_t* lo, const uint16_t
         launch_ranges_given(c->b, 1, c->L());
         launch_offsets(c->b, 1, c->L());
         c->cfg.sgm = *params;
-        aggregate(c, c->b, 1, c->L());
+        aggregate(c, c->b, 1, c->L(), false, true, false, /*cost_in_ragged=*/true);
         d2h(c, agg, c->b.agg, total);
         sync(c);
     });

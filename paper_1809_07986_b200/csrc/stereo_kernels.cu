@@ -458,6 +458,101 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
     }
 }
 
+// The aggregation's cost input (build_cost_volume,
+// matching_cost.cpp:88-117) in the QUAD layout of the path-cost partials:
+// pixel i's levels 4*(lo/4) .. 4*(hi/4)+3 as u32 words at qoff[i], levels
+// outside [lo, hi] as 0xff (valid costs are <= 24), so the scan reads aligned
+// words and poisons out-of-window levels from the byte itself. The
+// reference's ragged layout (cost_kernel) is produced only where a caller
+// asks for it (tsgm_fetch COST, build_cost_volume, the fallback aggregation).
+// One CTA per (row, position); census rows staged in shared memory; a window
+// of <= 4 quads is written by its own lane, wider ones by the warp (lanes
+// across quads, coalesced 32-bit stores).
+__device__ __forceinline__ uint32_t quad_cost(uint32_t slx, const uint32_t* sr, int x, int d0,
+                                              int lo, int hi, int W, bool xdef) {
+    uint32_t word = 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int d = d0 + u;
+        const int xr = x - d;
+        const bool ok = xdef && xr >= kCensusRadius && xr < W - kCensusRadius;
+        const uint32_t c = ok ? static_cast<uint32_t>(__popc(slx ^ sr[ok ? xr : 0]))
+                              : static_cast<uint32_t>(kMaxCost);
+        word |= (d >= lo && d <= hi ? c : 0xffu) << (8 * u);
+    }
+    return word;
+}
+
+__global__ void __launch_bounds__(256) cost_quad_kernel(Bufs b) {
+    extern __shared__ uint32_t sm[];
+    const int a = blockIdx.y, s = slot_of(b, a), y = blockIdx.x;
+    const int W = b.W;
+    uint32_t* sl = sm;
+    uint32_t* sr = sl + W;
+    const size_t pbase = static_cast<size_t>(s) * b.P + static_cast<size_t>(y) * W;
+    const uint32_t* qoff = b.qoff + static_cast<size_t>(s) * (b.P + 1) + static_cast<size_t>(y) * W;
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+        sl[x] = b.sigl[pbase + x];
+        sr[x] = b.sigr[pbase + x];
+    }
+    __syncthreads();
+    uint32_t* cq = b.costq + b.vqbase[a];
+    const bool row_def = y >= kCensusRadius && y < b.H - kCensusRadius;
+    const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+    const int nwarps = static_cast<int>(blockDim.x >> 5);
+    for (int x0 = warp * 32; x0 < W; x0 += 32 * nwarps) {
+        const int x = x0 + lane;
+        const bool active = x < W;
+        const uint32_t lh = active ? __ldg(b.lohi + pbase + x) : 0u;
+        const uint32_t qo = active ? __ldg(qoff + x) : 0u;
+        const int lo = static_cast<int>(lh & 0xffffu), hi = static_cast<int>(lh >> 16);
+        const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
+        const bool xdef = row_def && x >= kCensusRadius && x < W - kCensusRadius;
+        const bool narrow = active && nq <= 4;
+        if (narrow) {
+            const uint32_t slx = sl[x];
+            for (int t = 0; t < nq; ++t) cq[qo + t] = quad_cost(slx, sr, x, 4 * (q0 + t), lo, hi, W, xdef);
+        }
+        unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
+        while (bw) {
+            const int src = __ffs(bw) - 1;
+            bw &= bw - 1;
+            const int xw = x0 + src;
+            const int lo_w = __shfl_sync(0xffffffffu, lo, src);
+            const int hi_w = __shfl_sync(0xffffffffu, hi, src);
+            const uint32_t qo_w = __shfl_sync(0xffffffffu, qo, src);
+            const bool xdef_w = __shfl_sync(0xffffffffu, xdef, src);
+            const int q0w = lo_w >> 2, nqw = (hi_w >> 2) - q0w + 1;
+            const uint32_t slx = sl[xw];
+            for (int t = lane; t < nqw; t += 32)
+                cq[qo_w + t] = quad_cost(slx, sr, xw, 4 * (q0w + t), lo_w, hi_w, W, xdef_w);
+        }
+    }
+}
+
+// Ragged (reference layout) -> quad layout, for a caller-provided cost volume
+// (tsgm_aggregate_paths). One thread per pixel.
+__global__ void quads_from_ragged_kernel(Bufs b) {
+    const int a = blockIdx.y, s = slot_of(b, a);
+    const uint8_t* cost = b.cost + b.vbase[a];
+    uint32_t* cq = b.costq + b.vqbase[a];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < b.P; i += gridDim.x * blockDim.x) {
+        const uint32_t lh = b.lohi[static_cast<size_t>(s) * b.P + i];
+        const int lo = static_cast<int>(lh & 0xffffu), hi = static_cast<int>(lh >> 16);
+        const uint32_t o = b.off[static_cast<size_t>(s) * (b.P + 1) + i];
+        const uint32_t qo = b.qoff[static_cast<size_t>(s) * (b.P + 1) + i];
+        const int q0 = lo >> 2, nq = (hi >> 2) - q0 + 1;
+        for (int t = 0; t < nq; ++t) {
+            uint32_t word = 0u;
+            for (int u = 0; u < 4; ++u) {
+                const int d = 4 * (q0 + t) + u;
+                word |= (d >= lo && d <= hi ? static_cast<uint32_t>(cost[o + (d - lo)]) : 0xffu) << (8 * u);
+            }
+            cq[qo + t] = word;
+        }
+    }
+}
+
 // Volume plan of a chunk of m positions: position a
 // starts at the prefix of the chunk's ACTUAL cell and quad counts (the N of
 // make_cost_volume, matching_cost.cpp:30-48), rounded up to 16 cells / 4
@@ -499,7 +594,18 @@ void launch_volume_plan(const Bufs& b, int m, Launch L) {
 
 void launch_cost(const Bufs& b, int n, Launch L) {
     const size_t smem = sizeof(uint32_t) * 2 * b.W;
+    cost_quad_kernel<<<dim3(b.H, n), 256, smem, L.st>>>(b);
+    ++*L.counter;
+}
+
+void launch_cost_ragged(const Bufs& b, int n, Launch L) {
+    const size_t smem = sizeof(uint32_t) * 2 * b.W;
     cost_kernel<<<dim3(b.H, n), 512, smem, L.st>>>(b);
+    ++*L.counter;
+}
+
+void launch_cost_quads_from_ragged(const Bufs& b, int n, Launch L) {
+    quads_from_ragged_kernel<<<dim3((b.P + 255) / 256 < 1024 ? (b.P + 255) / 256 : 1024, n), 256, 0, L.st>>>(b);
     ++*L.counter;
 }
 
