@@ -76,6 +76,10 @@ __device__ __forceinline__ uint32_t prmt_sx(uint32_t a, uint32_t s) {
 // Cost of a level outside the window: L = C + min(...) stays < 2^16 and
 // L - min L >= kPoisonQ - 255 > P2, so it never wins a min and normalises to P2.
 constexpr uint32_t kPoisonQ = 0x3fff3fffu;
+// Quad range of a scanline with no predecessor yet (task start; a scanline's
+// active pixels are contiguous, so this is the only case): no quad falls in
+// it, and the out-of-range words read 0 instead of P2 (sgm.cpp:93-99: L = C).
+constexpr uint32_t kNoPred = 0x7fff7fffu;
 
 __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
@@ -132,7 +136,7 @@ struct PixMeta {
 // false: no pixel for this group; everything masked, nothing stored). `sb` /
 // `rp` are the shared addresses of the scanline's slot and quad range.
 template <int G, int Q>
-__device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has_pred,
+__device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
                                            uint32_t sb, uint32_t rp, const uint32_t* costq,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
                                            uint32_t P2x4) {
@@ -164,9 +168,9 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
     // predecessor words of quads a0-1 .. a0+Q (quad x at sb + 4 + 4x)
     const uint32_t prng = lds32(rp);
     // no predecessor: every word reads 0 (an empty range no quad falls in)
-    const int pq0 = has_pred ? static_cast<int>(prng & 0xffffu) : -(1 << 20);
-    const uint32_t span = has_pred ? (prng >> 16) - static_cast<uint32_t>(pq0) : 0u;
-    const uint32_t fill = has_pred ? P2x4 : 0u;
+    const int pq0 = static_cast<int>(prng & 0xffffu);
+    const uint32_t span = (prng >> 16) - static_cast<uint32_t>(pq0);
+    const uint32_t fill = prng == kNoPred ? 0u : P2x4;
     uint32_t w[Q + 2];
 #pragma unroll
     for (int u = 0; u < Q + 2; ++u) {
@@ -209,7 +213,7 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm, bool has
 // the slot's guard words (quads -1 and qmax) hold P2, which is what the masked
 // path reads there. Same arithmetic as scan_pixel<G, Q>.
 template <int G, int Q = 4>
-__device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, bool has_pred,
+__device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm,
                                                 uint32_t sb, uint32_t rp, const uint32_t* costq,
                                                 uint32_t* out, uint32_t P1x2, uint32_t P2x2,
                                                 uint32_t P2x4, uint32_t full_rng) {
@@ -233,16 +237,17 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm, boo
 #pragma unroll
         for (int u = 0; u < Q + 2; ++u) {
             const uint32_t raw = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
-            w[u] = has_pred ? raw : 0u;
+            w[u] = raw;
         }
     } else {
         const int pq0 = static_cast<int>(prng & 0xffffu);
         const uint32_t span = (prng >> 16) - static_cast<uint32_t>(pq0);
+        const uint32_t fill = prng == kNoPred ? 0u : P2x4;
 #pragma unroll
         for (int u = 0; u < Q + 2; ++u) {
             const uint32_t raw = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
             const bool in = static_cast<uint32_t>(a0 - 1 + u - pq0) <= span;
-            w[u] = has_pred ? (in ? raw : P2x4) : 0u;
+            w[u] = in ? raw : fill;
         }
     }
     uint32_t mn = 0xffffffffu;
@@ -299,7 +304,9 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         const int qmax = (b.d_max + 3) / 4;
         sts32(my_sb, P2x4);
         sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
+        sts32(my_rp, kNoPred);
     }
+    __syncwarp();
 
     const uint32_t* costq = b.costq + b.vqbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
@@ -311,7 +318,6 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
     const int nsteps = horiz ? W : H;
     const int sl = dx * dy;
     const int c = (horiz ? 0 : (sl == 1 ? -(H - 1) : 0)) + SPW * g + gs;
-    bool prev_active = false;
 
     // p: the metadata index of step k (column-major for horizontal lines)
     auto pixel_at = [&](int k, int& p) -> bool {
@@ -370,27 +376,27 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
-        if (__ballot_sync(0xffffffffu, active) == 0u) {
-            prev_active = false;
-            continue;
-        }
+        // the step's window classes in ONE warp reduction: bits 1..4 = narrow
+        // windows of that many quads, 8 = full range, 9 = other wide windows
         const int nq = static_cast<int>(mc.nq);
         const bool narrow = active && nq <= 4;
+        const bool owner = active && lgs == 0;
+        const bool fullw = sp.full_ok && mc.lohi == sp.full_lohi;
+        const bool part = owner && !fullw && nq > 4;
+        const uint32_t cls = __reduce_or_sync(
+            0xffffffffu, (narrow ? 1u << nq : 0u) | (owner && fullw ? 0x100u : 0u) | (part ? 0x200u : 0u));
+        if (cls == 0u) continue;  // no pixel on any of the warp's scanlines
         if (SPW == 32) {
             // windows of <= 4 quads: the lane itself, Q = the warp's widest such window
-            const int qn = __reduce_max_sync(0xffffffffu, narrow ? nq : 0);
-            if (qn > 3)
-                scan_pixel<1, 4>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2,
-                                 P2x4);
-            else if (qn == 3)
-                scan_pixel<1, 3>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2,
-                                 P2x4);
-            else if (qn > 0)
-                scan_pixel<1, 2>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2,
-                                 P2x4);
-        } else if (__any_sync(0xffffffffu, narrow)) {
+            if (cls & 0x10u)
+                scan_pixel<1, 4>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+            else if (cls & 0x8u)
+                scan_pixel<1, 3>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+            else if (cls & 0x6u)
+                scan_pixel<1, 2>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+        } else if (cls & 0x1eu) {
             // windows of <= 4 quads: the scanline's GN lanes x QN quads
-            scan_pixel<GN, QN>(narrow, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+            scan_pixel<GN, QN>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
         }
         // wider windows: groups of G lanes x 4 quads, 32/G windows per pass;
         // a window's owner is the first lane of its scanline's group
@@ -412,27 +418,19 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
                 pw.lohi = full ? sp.full_lohi : __shfl_sync(0xffffffffu, mc.lohi, src);
                 pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
-                const bool hp = __shfl_sync(0xffffffffu, prev_active, src);
                 const uint32_t sline = static_cast<uint32_t>(src / GN);
                 if (full)
-                    scan_pixel_full<G>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, costq,
+                    scan_pixel_full<G>(gi < cnt, pw, wbase + sline * SB, rbase + 4u * sline, costq,
                                        out, P1x2, P2x2, P2x4, sp.full_rng);
                 else
-                    scan_pixel<G, 4>(gi < cnt, pw, hp, wbase + sline * SB, rbase + 4u * sline, costq,
+                    scan_pixel<G, 4>(gi < cnt, pw, wbase + sline * SB, rbase + 4u * sline, costq,
                                      out, P1x2, P2x2, P2x4);
                 bw &= ~done;
             }
         };
-        // full-range windows (when their class covers them exactly) take the
-        // unmasked pass
-        const bool owner = active && lgs == 0;
-        const bool fullw = sp.full_ok && mc.lohi == sp.full_lohi;
-        const unsigned bf = __ballot_sync(0xffffffffu, owner && fullw);
-        const bool part = owner && !fullw && nq > 4;
         // the four partial-wide classes only when the step has such a window
-        // (rare: 5+ quads, not full range): one vote instead of four ballots
-        // (aggregation 8.10 -> 7.84 ms)
-        if (__any_sync(0xffffffffu, part)) {
+        // (rare: 5+ quads, not full range) (aggregation 8.10 -> 7.84 ms)
+        if (cls & 0x200u) {
             const unsigned b2 = __ballot_sync(0xffffffffu, part && nq <= 8);
             if (b2) wide(std::integral_constant<int, 2>{}, b2, false);
             const unsigned b4 = __ballot_sync(0xffffffffu, part && nq > 8 && nq <= 16);
@@ -442,7 +440,10 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
             const unsigned b16 = __ballot_sync(0xffffffffu, part && nq > 32);
             if (b16) wide(std::integral_constant<int, 16>{}, b16, false);
         }
-        if (bf) {
+        // full-range windows (when their class covers them exactly) take the
+        // unmasked pass
+        if (cls & 0x100u) {
+            const unsigned bf = __ballot_sync(0xffffffffu, owner && fullw);
             switch (sp.full_ok) {  // = 4G of the full window's class
                 case 8: wide(std::integral_constant<int, 2>{}, bf, true); break;
                 case 16: wide(std::integral_constant<int, 4>{}, bf, true); break;
@@ -450,7 +451,6 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
                 default: wide(std::integral_constant<int, 16>{}, bf, true); break;
             }
         }
-        prev_active = active;
     }
 }
 
@@ -459,8 +459,11 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
 // so they may take thinner warps than the H-step vertical and diagonal lines.
 // Tasks are direction-major over all slots (the long horizontal ones start
 // first); sp.task_off counts each direction's tasks with its own SPW.
+#ifndef SCAN_MINB
+#define SCAN_MINB 16
+#endif
 template <int SPWH, int SPWV>
-__global__ void __launch_bounds__(32 * kScanWarps, 16) scan_kernel(Bufs b, ScanParams sp) {
+__global__ void __launch_bounds__(32 * kScanWarps, SCAN_MINB) scan_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
@@ -500,11 +503,13 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
     const uint32_t P2x4 = static_cast<uint32_t>(sp.p2) * 0x01010101u;
-    if ((lane & (G - 1)) == 0) {  // guard words of the scanline's slot
+    if ((lane & (G - 1)) == 0) {  // guard words of the scanline's slot, no predecessor yet
         const int qmax = (b.d_max + 3) / 4;
         sts32(my_sb, P2x4);
         sts32(my_sb + 4u + 4u * static_cast<uint32_t>(qmax), P2x4);
+        sts32(my_rp, kNoPred);
     }
+    __syncwarp();
     const uint32_t* costq = b.costq + b.vqbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
@@ -531,7 +536,6 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         m.qo = v.z;
         m.nq = v.w;
     };
-    bool prev_active = false;
     int p_tmp = 0;
     bool act1 = pixel_at(0, p_tmp);
     PixMeta m1{0u, 0u, 0u, 0u};
@@ -551,19 +555,15 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
-        if (__ballot_sync(0xffffffffu, active) == 0u) {
-            prev_active = false;
-            continue;
-        }
+        if (__ballot_sync(0xffffffffu, active) == 0u) continue;
         // the unmasked pass when every active scanline of the warp has a full
         // window of the class size (frames from an empty state)
         const bool fullw = sp.full_ok == Q * G && mc.lohi == sp.full_lohi;
         if (__all_sync(0xffffffffu, fullw || !active))
-            scan_pixel_full<G, Q>(active, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4,
+            scan_pixel_full<G, Q>(active, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4,
                                   sp.full_rng);
         else
-            scan_pixel<G, Q>(active, mc, prev_active, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
-        prev_active = active;
+            scan_pixel<G, Q>(active, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
     }
 }
 
