@@ -470,17 +470,27 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
 // across quads, coalesced 32-bit stores).
 __device__ __forceinline__ uint32_t quad_cost(uint32_t slx, const uint32_t* sr, int x, int d0,
                                               int lo, int hi, int W, bool xdef) {
+    // levels d0 .. d0+3 outside [lo, hi] are pads (0xff)
+    const int lr = min(max(lo - d0, 0), 4), hr = min(max(hi - d0 + 1, 0), 4);
+    const uint32_t pad = ~(__funnelshift_lc(0u, 0xffffffffu, 8 * lr) & ~__funnelshift_lc(0u, 0xffffffffu, 8 * hr));
+    if (xdef && x - d0 - 3 >= kCensusRadius && x - d0 < W - kCensusRadius) {
+        // both census pixels defined for all four levels (all but the image
+        // borders): four popcounts packed by IMAD, pads ORed in
+        const uint32_t* r = sr + (x - d0 - 3);  // levels d0+3 .. d0 at r[0..3]
+        const uint32_t c3 = __popc(slx ^ r[0]), c2 = __popc(slx ^ r[1]);
+        const uint32_t c1 = __popc(slx ^ r[2]), c0 = __popc(slx ^ r[3]);
+        return (c0 + (c1 << 8) + (c2 << 16) + (c3 << 24)) | pad;
+    }
     uint32_t word = 0u;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        const int d = d0 + u;
-        const int xr = x - d;
+        const int xr = x - d0 - u;
         const bool ok = xdef && xr >= kCensusRadius && xr < W - kCensusRadius;
         const uint32_t c = ok ? static_cast<uint32_t>(__popc(slx ^ sr[ok ? xr : 0]))
                               : static_cast<uint32_t>(kMaxCost);
-        word |= (d >= lo && d <= hi ? c : 0xffu) << (8 * u);
+        word |= c << (8 * u);
     }
-    return word;
+    return word | pad;
 }
 
 __global__ void __launch_bounds__(256) cost_quad_kernel(Bufs b) {

@@ -60,6 +60,13 @@ def main():
             ed0.append((eng.fetch(0, "export_d"), eng.fetch(0, "state_p"), eng.fetch(0, "mask")))
     ms = eng.timer_end()
     vol_slots = eng.vol_slots
+    # the standalone C->S aggregation on the last frame's volumes (one chunk)
+    agg_ms, agg_cells = eng.bench_aggregate(slots, reps=3)
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        peak = 6650.0
+    agg_frac = (3.0 * agg_cells + 4.0 * c0.width * c0.height * S) / (agg_ms * 1e-3) / (peak * 1e9)
     eng.close()
     from oracle import Port
     port = Port()
@@ -77,6 +84,8 @@ def main():
         "frames_per_s_host_api": round(S * F / (ms * 1e-3), 2),
         "ms_total": round(ms, 1),
         "vol_slots": vol_slots,
+        "aggregation_ms": round(agg_ms, 3), "aggregation_cells": agg_cells,
+        "aggregation_hbm_frac": round(agg_frac, 4),
         "volume_chunks_per_frame": chunks,
         "device_mem_gb": {"total": round(total / 2**30, 1),
                           "context": round((free0 - free1) / 2**30, 1)},

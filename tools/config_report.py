@@ -27,6 +27,13 @@ from paper_1809_07986_b200 import tsgm  # noqa: E402
 from paper_1809_07986_b200.scene import SceneConfig, render  # noqa: E402
 
 
+def peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
 def summarize(ms):
     rest = ms[1:]
     return {"frame0_ms": round(ms[0], 3),
@@ -49,8 +56,10 @@ def gpu_run(L, R, mots, calib, params, filt, reset_each):
             ms.append(eng.timer_end())
         out = ms
     cells = eng.cells(0)
+    # the standalone C->S aggregation on the last frame's volume
+    agg_ms, agg_cells = eng.bench_aggregate([0], reps=5)
     eng.close()
-    return out, cells
+    return out, cells, (agg_ms, agg_cells)
 
 
 def ref_run(ref, L, R, mots, calib, params, filt, reset_each, frames, threads):
@@ -91,7 +100,8 @@ def main():
             filt = tsgm.FilterConfig(range_use_stddev=True, range_stddev_gain=1e-9,
                                      min_range_halfwidth=mode)
         reset_each = mode == "full"
-        gms, cells = gpu_run(L, R, mots, calib, params, filt, reset_each)
+        gms, cells, (agg_ms, agg_cells) = gpu_run(L, R, mots, calib, params, filt, reset_each)
+        agg_frac = (3.0 * agg_cells + 4.0 * cfg.width * cfg.height) / (agg_ms * 1e-3) / (peak() * 1e9)
         nf = min(ref_frames, frames)
         r1 = ref_run(ref, L, R, mots, calib, params, filt, reset_each, nf, 1)
         rn = ref_run(ref, L, R, mots, calib, params, filt, reset_each, nf, nproc)
@@ -102,6 +112,7 @@ def main():
                      "d_max": d_max, "last_frame_cells": cells,
                      "gpu": g, "gpu_frames_per_s": round(1e3 * frames / sum(gms), 1),
                      "gpu_gdisp_evals_per_s_last_frame": round(cells / (gms[-1] * 1e-3) / 1e9, 2),
+                     "aggregation_ms": round(agg_ms, 4), "aggregation_hbm_frac": round(agg_frac, 4),
                      "reference_threads_1": dict(c1, frames_timed=nf),
                      f"reference_threads_{nproc}": dict(cn, frames_timed=nf),
                      "speedup_vs_ref_nproc_frames_ge1": round(cn[key] / g[key], 1)
