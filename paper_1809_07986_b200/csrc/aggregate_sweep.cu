@@ -648,6 +648,9 @@ constexpr int kCwWarps = 2;
 #ifndef CW_LEAN_MINB
 #define CW_LEAN_MINB 24  // 40 registers (24 B spilled): 48 resident warps, 1.38 -> 1.23 ms (64 sequences)
 #endif
+#ifndef CW_FULL_MINB
+#define CW_FULL_MINB 20  // standalone C->S: 7.53 -> 7.46 ms (64 sequences)
+#endif
 
 // per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
 // best[32] (u32), qsum[32*qmax] (uint2, sub-pixel only)
@@ -673,7 +676,7 @@ __device__ __forceinline__ float subpixel_of(int d, int sm1, int s0, int sp1, bo
 // kLean: the production step's variant (WTA only: no S, no sub-pixel) —
 // compiled without those paths it needs fewer registers and runs more warps.
 template <int NDIR, bool kLean>
-__global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : 16)
+__global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : CW_FULL_MINB)
     combine_wta_kernel(Bufs b, int n, int write_s_in, int do_wta_in, int subpix_in) {
     const int write_s = kLean ? 0 : write_s_in, do_wta = kLean ? 1 : do_wta_in;
     const int subpix = kLean ? 0 : subpix_in;
