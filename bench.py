@@ -410,7 +410,7 @@ def run_ours(args):
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "algorithmic_bytes": int(b_agg), "ms": round(agg_ms, 4),
-                         "cells": int(agg_cells), "limiter": load_limiter()},
+                         "cells": int(agg_cells), "limiter": load_limiter(achieved / peak)},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "accuracy": {"outlier_rule": "|e| > 3 px and |e|/gt > 5%",
@@ -427,10 +427,20 @@ def run_ours(args):
     return result
 
 
-def load_limiter():
-    """What actually bounds the aggregation (from the committed ncu captures,
-    profiles/r0*_*_ncu_full.json): issue slots, not HBM."""
-    out = {}
+def _num(v):
+    try:
+        return float(str(v).split()[0].replace(",", ""))
+    except (TypeError, ValueError):
+        return None
+
+
+def load_limiter(frac=None):
+    """What actually bounds the aggregation, from the committed ncu captures of
+    the same standalone C->S launch (profiles/r0*_*_ncu_full.json): issue
+    slots and DRAM per kernel, the measured DRAM bytes per cell, the scan's
+    lane-instructions per cell-direction, and the two ceilings they imply for
+    roofline.frac (all DRAM bytes at peak; the scan at 100% issue)."""
+    out, caps = {}, {}
     for name, fns in (("scan", ("r02_scan_kernel_ncu_full.json", "r01_scan_kernel_ncu_full.json")),
                       ("combine", ("r02_combine_ncu_full.json", "r01_combine_ncu_full.json"))):
         for fn in fns:
@@ -442,9 +452,24 @@ def load_limiter():
                                                           "eligible_warps_per_scheduler",
                                                           "achieved_occupancy_pct")}
                 out[name]["capture"] = fn
+                caps[name] = (k, d.get("_cells"))
                 break
             except (OSError, ValueError, StopIteration):
                 continue
+    if "scan" in caps and "combine" in caps and caps["scan"][1]:
+        (ks, cells), (kc, _) = caps["scan"], caps["combine"]
+        dram = sum(_num(k.get(m)) or 0.0 for k in (ks, kc)
+                   for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        unit = 1e9 if "Gbyte" in str(ks.get("dram__bytes_read.sum")) else 1.0
+        bpc = dram * unit / cells
+        lipcd = (_num(ks.get("executed_instructions")) or 0.0) * 32.0 / (8.0 * cells)
+        out["capture_cells"] = int(cells)
+        out["dram_bytes_per_cell"] = round(bpc, 2)
+        out["scan_lane_instr_per_cell_direction"] = round(lipcd, 2)
+        out["ceiling_frac_all_bytes_at_peak"] = round(3.17 / bpc, 4)
+        issue = _num(ks.get("issue_slots_busy_pct"))
+        if frac is not None and issue:
+            out["ceiling_frac_scan_at_full_issue"] = round(frac * 100.0 / issue, 4)
     if out:
         out["reading"] = ("the scan is integer-issue bound (exact u16x2 min-plus recursions); "
                           "see DESIGN.md section 4")
