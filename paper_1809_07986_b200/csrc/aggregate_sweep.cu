@@ -123,13 +123,15 @@ __device__ __forceinline__ uint32_t group_min(uint32_t v) {
     }
 }
 
-// lohi = lo | hi << 16, cell / qo = cell and quad offsets, nq = quads of the
-// window. The packed records carry nq in their 4th word so that all four
-// loaded registers stay live (a dead one gets reused while the load is still
-// in flight, and its next writer then waits for the load).
+// lohi = lo | hi << 16, qo = the window's first quad in the quad layout (the
+// 8-byte scan record written by the offsets kernel).
 struct PixMeta {
-    uint32_t lohi, cell, qo, nq;
+    uint32_t lohi, qo;
 };
+// quads of the window
+__device__ __forceinline__ uint32_t quads_of(uint32_t lohi) {
+    return (lohi >> 18) - ((lohi & 0xffffu) >> 2) + 1u;
+}
 
 // One pixel, processed by a group of G lanes; lane lg owns the Q consecutive
 // quads [lg*Q, lg*Q + Q) of the window. All lanes of the warp call it (pix =
@@ -331,31 +333,23 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         p = y * W + x;
         return x >= 0 && x < W;
     };
-    const uint4* tmeta = b.tmeta + static_cast<size_t>(s) * b.P;
-    const uint4* rmeta = b.rmeta + static_cast<size_t>(s) * b.P;
+    const uint2* tmeta = b.tmeta + static_cast<size_t>(s) * b.P;
+    const uint2* rmeta = b.rmeta + static_cast<size_t>(s) * b.P;
     auto load_meta = [&](int p, PixMeta& m) {
-        if (horiz) {  // lanes = consecutive rows: one coalesced 16-byte record each
-            const uint4 v = __ldg(tmeta + p);
-            m.lohi = v.x;
-            m.cell = v.y;
-            m.qo = v.z;
-            m.nq = v.w;
-        } else {  // lanes = adjacent pixels of a row
-            const uint4 v = __ldg(rmeta + p);
-            m.lohi = v.x;
-            m.cell = v.y;
-            m.qo = v.z;
-            m.nq = v.w;
-        }
+        // horizontal: lanes = consecutive rows (the column-major copy), else
+        // adjacent pixels of a row: one coalesced 8-byte record each
+        const uint2 v = __ldg((horiz ? tmeta : rmeta) + p);
+        m.lohi = v.x;
+        m.qo = v.y;
     };
 
     // metadata two steps ahead, costs of the next step prefetched into L1
     int p_tmp = 0;
     bool act1 = pixel_at(0, p_tmp);
-    PixMeta m1{0u, 0u, 0u, 0u};
+    PixMeta m1{0u, 0u};
     if (act1) load_meta(p_tmp, m1);
     bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
-    PixMeta m2{0u, 0u, 0u, 0u};
+    PixMeta m2{0u, 0u};
     if (act2) load_meta(p_tmp, m2);
     for (int k = 0; k < nsteps; ++k) {
         const bool active = act1;
@@ -366,7 +360,7 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
 #define SCAN_PREFETCH 1
 #endif
         if (SCAN_PREFETCH && act1 && lgs == 0) {  // step k+1's window towards L1 (its metadata arrived a step ago)
-            const int nb = 4 * static_cast<int>(m1.nq);  // the window's bytes in the quad layout
+            const int nb = 4 * static_cast<int>(quads_of(m1.lohi));  // the window's bytes (quad layout)
             const char* c0 = reinterpret_cast<const char*>(costq + m1.qo);
             // straight-line (windows are <= 64 quads, sweep_supported): 0.8%
             // faster than the loop
@@ -378,7 +372,7 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         if (act2) load_meta(p_tmp, m2);
         // the step's window classes in ONE warp reduction: bits 1..4 = narrow
         // windows of that many quads, 8 = full range, 9 = other wide windows
-        const int nq = static_cast<int>(mc.nq);
+        const int nq = static_cast<int>(quads_of(mc.lohi));
         const bool narrow = active && nq <= 4;
         const bool owner = active && lgs == 0;
         const bool fullw = sp.full_ok && mc.lohi == sp.full_lohi;
@@ -414,9 +408,7 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
                 const int src = gi < cnt ? static_cast<int>(lds32(srcbase + 4u * static_cast<uint32_t>(gi))) : lane;
                 __syncwarp();
                 PixMeta pw;
-                pw.nq = 0u;  // unused by scan_pixel
                 pw.lohi = full ? sp.full_lohi : __shfl_sync(0xffffffffu, mc.lohi, src);
-                pw.cell = __shfl_sync(0xffffffffu, mc.cell, src);
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
                 const uint32_t sline = static_cast<uint32_t>(src / GN);
                 if (full)
@@ -517,7 +509,7 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
     const int nsteps = horiz ? W : H;
     const int sl = dx * dy;
     const int c = (horiz ? 0 : (sl == 1 ? -(H - 1) : 0)) + LPW * g + gi;
-    const uint4* meta = (horiz ? b.tmeta : b.rmeta) + static_cast<size_t>(s) * b.P;
+    const uint2* meta = (horiz ? b.tmeta : b.rmeta) + static_cast<size_t>(s) * b.P;
     auto pixel_at = [&](int k, int& p) -> bool {
         if (horiz) {
             const int x = dx < 0 ? k : W - 1 - k;
@@ -530,18 +522,16 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         return x >= 0 && x < W;
     };
     auto load_meta = [&](int p, PixMeta& m) {
-        const uint4 v = __ldg(meta + p);
+        const uint2 v = __ldg(meta + p);
         m.lohi = v.x;
-        m.cell = v.y;
-        m.qo = v.z;
-        m.nq = v.w;
+        m.qo = v.y;
     };
     int p_tmp = 0;
     bool act1 = pixel_at(0, p_tmp);
-    PixMeta m1{0u, 0u, 0u, 0u};
+    PixMeta m1{0u, 0u};
     if (act1) load_meta(p_tmp, m1);
     bool act2 = nsteps > 1 && pixel_at(1, p_tmp);
-    PixMeta m2{0u, 0u, 0u, 0u};
+    PixMeta m2{0u, 0u};
     if (act2) load_meta(p_tmp, m2);
     const int lg = lane & (G - 1);
     for (int k = 0; k < nsteps; ++k) {
@@ -550,7 +540,7 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         act1 = act2;
         m1 = m2;
         if (act1) {  // this lane's 4 quads of step k+1 towards L1
-            if (4u * static_cast<uint32_t>(lg) < m1.nq)
+            if (4u * static_cast<uint32_t>(lg) < quads_of(m1.lohi))
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(costq + m1.qo + 4 * lg));
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);

@@ -57,8 +57,8 @@ struct Bufs {
     uint32_t* off;       // [slot][P+1]
     uint32_t* row_sum;   // [slot][H]
     uint32_t* qoff;      // [slot][P+1] quad-aligned offsets (aggregation partials)
-    uint4* tmeta;        // [slot][W][H] column-major {lohi, off, qoff, quads} (horizontal scanlines)
-    uint4* rmeta;        // [slot][H][W] row-major {lohi, off, qoff, quads} (the other scanlines)
+    uint2* tmeta;        // [slot][W][H] column-major {lohi, qoff} (horizontal scanlines)
+    uint2* rmeta;        // [slot][H][W] row-major {lohi, qoff} (the other scanlines)
     uint32_t* qrow_sum;  // [slot][H]
     uint2* tsum;         // [slot][H][ceil(W/32)] (cells, quads) of 32-px tile rows -> tile offsets
     unsigned long long* ncells;  // [slot]

@@ -404,8 +404,8 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     b.off = ctx->dalloc<uint32_t>(S * (P + 1));
     b.row_sum = ctx->dalloc<uint32_t>(S * ctx->H);
     b.qoff = ctx->dalloc<uint32_t>(S * (P + 1));
-    b.tmeta = ctx->dalloc<uint4>(S * P);
-    b.rmeta = ctx->dalloc<uint4>(S * P);
+    b.tmeta = ctx->dalloc<uint2>(S * P);
+    b.rmeta = ctx->dalloc<uint2>(S * P);
     b.qrow_sum = ctx->dalloc<uint32_t>(S * ctx->H);
     b.tsum = ctx->dalloc<uint2>(S * ctx->H * static_cast<size_t>((ctx->W + 31) / 32));
     b.nquads = ctx->dalloc<unsigned long long>(S);

@@ -224,11 +224,11 @@ __global__ void row_scan_kernel(Bufs b) {
 }
 
 // Adds the row bases to the in-row offsets, and writes the packed records
-// {lohi, off, qoff, quads} the scan kernel loads with one 16-byte access: row-major
+// {lohi, qoff} the scan kernel loads with one 8-byte access: row-major
 // (lanes = adjacent pixels of a row) and column-major (horizontal scanlines,
 // lanes = consecutive rows). 32x32 tiles through shared memory.
 __global__ void offsets_finalize_kernel(Bufs b) {
-    __shared__ uint4 tile[32][33];
+    __shared__ uint2 tile[32][33];
     const int a = blockIdx.z, s = slot_of(b, a);
     const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -243,8 +243,7 @@ __global__ void offsets_finalize_kernel(Bufs b) {
             b.off[o] = off;
             b.qoff[o] = qo;
             const uint32_t lh = b.lohi[pbase + static_cast<size_t>(y) * b.W + x];
-            const uint32_t nq = (lh >> 18) - ((lh & 0xffffu) >> 2) + 1u;  // quads of the window
-            const uint4 rec = make_uint4(lh, off, qo, nq);
+            const uint2 rec = make_uint2(lh, qo);
             b.rmeta[pbase + static_cast<size_t>(y) * b.W + x] = rec;
             tile[j][tx] = rec;
         }
@@ -322,7 +321,7 @@ __global__ void tile_scan_kernel(Bufs b) {
 // for the next frame (kd = 0, (kp, ks) = ~0: nothing reads them after the
 // predict tile kernel).
 __global__ void offsets_tile_kernel(Bufs b, int arm_keys) {
-    __shared__ uint4 tile[32][33];
+    __shared__ uint2 tile[32][33];
     const int a = blockIdx.z, s = slot_of(b, a);
     const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -351,7 +350,7 @@ __global__ void offsets_tile_kernel(Bufs b, int arm_keys) {
             const size_t o = obase + static_cast<size_t>(y) * b.W + x;
             b.off[o] = off;
             b.qoff[o] = qo;
-            const uint4 rec = make_uint4(lh, off, qo, nq);
+            const uint2 rec = make_uint2(lh, qo);
             b.rmeta[g] = rec;
             tile[j][tx] = rec;
             if (arm_keys) {
