@@ -56,12 +56,39 @@ struct ScanParams {
     int ndir;
     int dx[8], dy[8];        // predecessor offsets of the active directions
     int task_off[9];         // prefix of warp tasks per direction (per slot)
+    int nlead;               // leading directions ordered direction-major (the horizontals)
     int n;                   // active slots
     int full_ok;             // ceil(d_max/4) is a power of two >= 8: full windows take scan_pixel_full
     uint32_t full_lohi;      // lohi of a full-range window: 0 | (d_max - 1) << 16
     uint32_t full_rng;       // quad range of a full-range window: 0 | (qmax - 1) << 16
     int warp_bytes;          // shared bytes per warp (scan_kernel)
 };
+
+// Task order (blockIdx order ~ dispatch order): the first nlead directions
+// (the W-step horizontal walks, the kernel's longest tasks) direction-major
+// over all slots, so they start first; then the other directions
+// SEQUENCE-major, so one sequence's downward (and upward) scans are resident
+// together and sweep the same cost / record rows at the same time: those rows
+// are read from L2 instead of DRAM by all but the first of them.
+__device__ __forceinline__ void decode_task(const ScanParams& sp, int task, int& d, int& a, int& g) {
+    const int lead = sp.task_off[sp.nlead] * sp.n;
+    if (task < lead) {
+        d = 0;
+        while (task >= sp.task_off[d + 1] * sp.n) ++d;
+        const int r = task - sp.task_off[d] * sp.n;
+        const int groups = sp.task_off[d + 1] - sp.task_off[d];
+        a = r / groups;
+        g = r % groups;
+    } else {
+        const int per = sp.task_off[sp.ndir] - sp.task_off[sp.nlead];  // tasks per slot
+        const int t = task - lead;
+        a = t / per;
+        const int r = t % per + sp.task_off[sp.nlead];
+        d = sp.nlead;
+        while (r >= sp.task_off[d + 1]) ++d;
+        g = r - sp.task_off[d];
+    }
+}
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     return __byte_perm(a, b, s);
@@ -460,11 +487,8 @@ __global__ void __launch_bounds__(32 * kScanWarps, SCAN_MINB) scan_kernel(Bufs b
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
-    int d = 0;
-    while (task >= sp.task_off[d + 1] * sp.n) ++d;
-    const int r = task - sp.task_off[d] * sp.n;
-    const int groups = sp.task_off[d + 1] - sp.task_off[d];
-    const int a = r / groups, g = r % groups;
+    int d, a, g;
+    decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (SPWH == SPWV || sp.dy[d] != 0)  // (one body when both widths agree)
@@ -567,11 +591,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
-    int d = 0;
-    while (task >= sp.task_off[d + 1] * sp.n) ++d;
-    const int r = task - sp.task_off[d] * sp.n;
-    const int groups = sp.task_off[d + 1] - sp.task_off[d];
-    const int a = r / groups, g = r % groups;
+    int d, a, g;
+    decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     lines_task<G>(b, sp, d, a, g, wbase);
@@ -587,11 +608,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_mixed_kernel(Bufs 
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
-    int d = 0;
-    while (task >= sp.task_off[d + 1] * sp.n) ++d;
-    const int r = task - sp.task_off[d] * sp.n;
-    const int groups = sp.task_off[d + 1] - sp.task_off[d];
-    const int a = r / groups, g = r % groups;
+    int d, a, g;
+    decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (sp.dy[d] == 0)
@@ -611,11 +629,8 @@ __global__ void __launch_bounds__(32 * kScanWarps, GH == 32 ? 16 : 12) scan_mixe
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;
     if (task >= sp.task_off[sp.ndir] * sp.n) return;
-    int d = 0;
-    while (task >= sp.task_off[d + 1] * sp.n) ++d;
-    const int r = task - sp.task_off[d] * sp.n;
-    const int groups = sp.task_off[d + 1] - sp.task_off[d];
-    const int a = r / groups, g = r % groups;
+    int d, a, g;
+    decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (sp.dy[d] == 0)
@@ -838,6 +853,14 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
                 ++m;
             }
         sp.ndir = k = m;
+    }
+    // task order (decode_task): the leading horizontal directions direction-
+    // major, the rest sequence-major (TSGM_SCAN_ORDER=dir: all direction-major)
+    {
+        int nl = 0;
+        while (nl < k && sp.dy[nl] == 0) ++nl;
+        const char* fo = std::getenv("TSGM_SCAN_ORDER");
+        sp.nlead = (fo && std::strcmp(fo, "dir") == 0) ? k : nl;
     }
     {
         const int qm = (b.d_max + 3) / 4;
