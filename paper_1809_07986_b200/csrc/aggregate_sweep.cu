@@ -956,7 +956,11 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const char* fmg = std::getenv("TSGM_MIXED_GH");
         const int mgh = fmg ? std::atoi(fmg) : (batched_warps < sms * 9 ? 32 : 8);
         const int hg = mgh == 32 ? 32 : G;
-        int spwh = fspwh ? std::atoi(fspwh) : (fspw || tall) ? spw : (batched_warps < sms * 80 ? 8 : 32);
+        // (round 2, frames/s: 32 sequences 5759 (8) -> 5948 (16); 16 sequences
+        // 5005 (8) vs 4234 (16); 64 equal for 16 and 32)
+        int spwh = fspwh ? std::atoi(fspwh)
+                         : (fspw || tall) ? spw
+                                          : (batched_warps < sms * 50 ? 8 : batched_warps < sms * 80 ? 16 : 32);
         if (spwh != 8 && spwh != 16) spwh = 32;
         if (spwh > spw) spwh = spw;
         sp.task_off[0] = 0;

@@ -32,11 +32,33 @@ __global__ void __launch_bounds__(256) census_kernel(Bufs b) {
     const uint8_t* img = which ? b.right[a] : b.left[a];
     uint32_t* sig = (which ? b.sigr : b.sigl) + static_cast<size_t>(s) * b.P;
     const int x0 = blockIdx.x * kCsW, y0 = blockIdx.y * kCsH;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    for (int i = tid; i < (kCsH + 4) * kCsPitch; i += 256) {
-        const int ty = i / kCsPitch, tx = i % kCsPitch;
-        const int gx = x0 - 4 + tx, gy = y0 - 2 + ty;
-        tile[ty][tx] = (gx >= 0 && gx < b.W && gy >= 0 && gy < b.H) ? img[gy * b.W + gx] : 0;
+    // the tile as 32-bit words (rows are not word-aligned in the image when W
+    // % 4 != 0: two aligned loads and a funnel shift per word); CTAs whose
+    // halo (plus the 3 bytes a misaligned last word may touch) leaves the
+    // image row take the bytewise path
+    const int gx0 = x0 - 4;
+    if (gx0 >= 0 && gx0 + kCsPitch + 4 <= b.W) {
+        for (int ty = threadIdx.y; ty < kCsH + 4; ty += kCsH) {
+            const int gy = y0 - 2 + ty;
+            uint32_t* trow = reinterpret_cast<uint32_t*>(&tile[ty][0]);
+            if (gy < 0 || gy >= b.H) {
+                for (int w = threadIdx.x; w < kCsPitch / 4; w += 32) trow[w] = 0u;
+                continue;
+            }
+            const uintptr_t A = reinterpret_cast<uintptr_t>(img + static_cast<size_t>(gy) * b.W + gx0);
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(A & ~static_cast<uintptr_t>(3));
+            const uint32_t sh = 8u * static_cast<uint32_t>(A & 3);
+            for (int w = threadIdx.x; w < kCsPitch / 4; w += 32) {
+                const uint32_t lo = __ldg(aw + w), hi = sh ? __ldg(aw + w + 1) : 0u;
+                trow[w] = __funnelshift_r(lo, hi, sh);
+            }
+        }
+    } else {
+        for (int ty = threadIdx.y; ty < kCsH + 4; ty += kCsH)
+            for (int tx = threadIdx.x; tx < kCsPitch; tx += 32) {
+                const int gx = gx0 + tx, gy = y0 - 2 + ty;
+                tile[ty][tx] = (gx >= 0 && gx < b.W && gy >= 0 && gy < b.H) ? img[gy * b.W + gx] : 0;
+            }
     }
     __syncthreads();
     const int xg = x0 + 4 * static_cast<int>(threadIdx.x), y = y0 + static_cast<int>(threadIdx.y);

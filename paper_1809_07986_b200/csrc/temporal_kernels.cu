@@ -379,8 +379,10 @@ __global__ void __launch_bounds__(kPtW * kPtH, 5) predict_tile_kernel(Bufs b, do
                     ps = __dadd_rn(ps, __dadd_rn(tp[ty - 1][tx], tp[ty + 1][tx]));
                     nn += 2;
                 }
-                od = ds / nn;
-                op = ps / nn;
+                // (nn is 2 or 4: the division is the exact scaling by 1/nn)
+                const double inv = nn == 2 ? 0.5 : 0.25;
+                od = __dmul_rn(ds, inv);
+                op = __dmul_rn(ps, inv);
                 ov = 1;
             }
         }
