@@ -860,7 +860,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         int nl = 0;
         while (nl < k && sp.dy[nl] == 0) ++nl;
         const char* fo = std::getenv("TSGM_SCAN_ORDER");
-        sp.nlead = (fo && std::strcmp(fo, "dir") == 0) ? k : nl;
+        sp.nlead = (fo && std::strcmp(fo, "dir") == 0) ? k : (fo && std::strcmp(fo, "seq") == 0) ? 0 : nl;
     }
     {
         const int qm = (b.d_max + 3) / 4;

@@ -30,7 +30,7 @@ def main():
         eng.step(list(range(S)), [L[k] for (L, _, _, _) in seqs], [R[k] for (_, R, _, _) in seqs],
                  mots)
     eng.sync()
-    for mask in (255, 3, 12, 240):
+    for mask in (255, 3, 12, 240, 252):
         os.environ["TSGM_SCAN_DIRS"] = str(mask)
         ms, cells = eng.bench_aggregate(list(range(S)), reps=2)
         print(f"dirs {mask:3d}: {ms:.3f} ms (scan + combine) for {cells / 1e6:.1f} M cells", flush=True)
