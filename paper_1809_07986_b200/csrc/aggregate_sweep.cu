@@ -164,11 +164,13 @@ __device__ __forceinline__ uint32_t quads_of(uint32_t lohi) {
 // quads [lg*Q, lg*Q + Q) of the window. All lanes of the warp call it (pix =
 // false: no pixel for this group; everything masked, nothing stored). `sb` /
 // `rp` are the shared addresses of the scanline's slot and quad range.
-template <int G, int Q>
+// kPre: the window's cost words were loaded a step early (pre[0..Q-1], from
+// costq + qo + min(k0, nq - 1), see lines_task).
+template <int G, int Q, bool kPre = false>
 __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
                                            uint32_t sb, uint32_t rp, const uint32_t* costq,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
-                                           uint32_t P2x4) {
+                                           uint32_t P2x4, const uint32_t* pre = nullptr) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int lo = static_cast<int>(pm.lohi & 0xffffu), hi = static_cast<int>(pm.lohi >> 16);
     const int q0 = lo >> 2, q1 = hi >> 2, nq = q1 - q0 + 1;
@@ -187,7 +189,7 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             act[t] = pix && k0 + t < nq;
-            const uint32_t c = __ldg(cw + t);
+            const uint32_t c = kPre ? pre[t] : __ldg(cw + t);
             const uint32_t am = act[t] ? 0xffffffffu : 0u;
             // kPoisonQ & (x | ~am): x masked to 14 bits, or the poison when inactive
             CA[t] = kPoisonQ & (prmt_sx(c, 0x9180u) | ~am);
@@ -241,11 +243,12 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
 // predecessor's window was full range as well its words are used unchecked —
 // the slot's guard words (quads -1 and qmax) hold P2, which is what the masked
 // path reads there. Same arithmetic as scan_pixel<G, Q>.
-template <int G, int Q = 4>
+template <int G, int Q = 4, bool kPre = false>
 __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm,
                                                 uint32_t sb, uint32_t rp, const uint32_t* costq,
                                                 uint32_t* out, uint32_t P1x2, uint32_t P2x2,
-                                                uint32_t P2x4, uint32_t full_rng) {
+                                                uint32_t P2x4, uint32_t full_rng,
+                                                const uint32_t* pre = nullptr) {
     const int lg = static_cast<int>(threadIdx.x & (G - 1));
     const int a0 = lg * Q;
     uint32_t CA[Q], CB[Q], LA[Q], LB[Q];
@@ -255,7 +258,7 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm,
         const uint32_t* cw = costq + (pix ? pm.qo : 0u) + a0;
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
-            const uint32_t c = __ldg(cw + t);
+            const uint32_t c = kPre ? pre[t] : __ldg(cw + t);
             CA[t] = prmt(c, 0u, 0x4140u);
             CB[t] = prmt(c, 0u, 0x4342u);
         }
@@ -558,15 +561,28 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
     PixMeta m2{0u, 0u};
     if (act2) load_meta(p_tmp, m2);
     const int lg = lane & (G - 1);
+    // the lane's Q cost words of the NEXT step's window, loaded a step early
+    // (a line-group walk is latency-bound: the cost load was its top stall);
+    // the same words for the masked and the full-range pass: window quads
+    // min(k0, nq - 1) .. + Q - 1 (zeros without a pixel)
+    uint32_t cn[Q];
+    auto preload = [&](bool act, const PixMeta& m) {
+        const uint32_t nqn = quads_of(m.lohi);
+        const uint32_t k0 = static_cast<uint32_t>(lg * Q);
+        const uint32_t* cw = costq + m.qo + (k0 < nqn ? k0 : nqn - 1u);
+#pragma unroll
+        for (int t = 0; t < Q; ++t) cn[t] = act ? __ldg(cw + t) : 0u;
+    };
+    preload(act1, m1);
     for (int k = 0; k < nsteps; ++k) {
         const bool active = act1;
         const PixMeta mc = m1;
+        uint32_t cc[Q];
+#pragma unroll
+        for (int t = 0; t < Q; ++t) cc[t] = cn[t];
         act1 = act2;
         m1 = m2;
-        if (act1) {  // this lane's 4 quads of step k+1 towards L1
-            if (4u * static_cast<uint32_t>(lg) < quads_of(m1.lohi))
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(costq + m1.qo + 4 * lg));
-        }
+        preload(act1, m1);
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
         if (__ballot_sync(0xffffffffu, active) == 0u) continue;
@@ -574,10 +590,10 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         // window of the class size (frames from an empty state)
         const bool fullw = sp.full_ok == Q * G && mc.lohi == sp.full_lohi;
         if (__all_sync(0xffffffffu, fullw || !active))
-            scan_pixel_full<G, Q>(active, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4,
-                                  sp.full_rng);
+            scan_pixel_full<G, Q, true>(active, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4,
+                                        sp.full_rng, cc);
         else
-            scan_pixel<G, Q>(active, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+            scan_pixel<G, Q, true>(active, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4, cc);
     }
 }
 
