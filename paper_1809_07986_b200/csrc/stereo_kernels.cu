@@ -489,18 +489,16 @@ __global__ void __launch_bounds__(512) cost_kernel(Bufs b) {
 // One CTA per (row, position); census rows staged in shared memory; a window
 // of <= 4 quads is written by its own lane, wider ones by the warp (lanes
 // across quads, coalesced 32-bit stores).
-__device__ __forceinline__ uint32_t quad_cost(uint32_t slx, const uint32_t* sr, int x, int d0,
-                                              int lo, int hi, int W, bool xdef) {
-    // levels d0 .. d0+3 outside [lo, hi] are pads (0xff)
-    const int lr = min(max(lo - d0, 0), 4), hr = min(max(hi - d0 + 1, 0), 4);
-    const uint32_t pad = ~(__funnelshift_lc(0u, 0xffffffffu, 8 * lr) & ~__funnelshift_lc(0u, 0xffffffffu, 8 * hr));
+// Costs of levels d0 .. d0+3 at pixel x (24 where a census pixel is undefined).
+__device__ __forceinline__ uint32_t quad_raw(uint32_t slx, const uint32_t* sr, int x, int d0, int W,
+                                             bool xdef) {
     if (xdef && x - d0 - 3 >= kCensusRadius && x - d0 < W - kCensusRadius) {
         // both census pixels defined for all four levels (all but the image
-        // borders): four popcounts packed by IMAD, pads ORed in
+        // borders): four popcounts packed by IMAD
         const uint32_t* r = sr + (x - d0 - 3);  // levels d0+3 .. d0 at r[0..3]
         const uint32_t c3 = __popc(slx ^ r[0]), c2 = __popc(slx ^ r[1]);
         const uint32_t c1 = __popc(slx ^ r[2]), c0 = __popc(slx ^ r[3]);
-        return (c0 + (c1 << 8) + (c2 << 16) + (c3 << 24)) | pad;
+        return c0 + (c1 << 8) + (c2 << 16) + (c3 << 24);
     }
     uint32_t word = 0u;
 #pragma unroll
@@ -511,7 +509,14 @@ __device__ __forceinline__ uint32_t quad_cost(uint32_t slx, const uint32_t* sr, 
                               : static_cast<uint32_t>(kMaxCost);
         word |= c << (8 * u);
     }
-    return word | pad;
+    return word;
+}
+
+// Pad bytes (0xff) of the levels d0 .. d0+3 outside [lo, hi]: only a window's
+// first and last quads have any.
+__device__ __forceinline__ uint32_t quad_pad(int d0, int lo, int hi) {
+    const int lr = min(max(lo - d0, 0), 4), hr = min(max(hi - d0 + 1, 0), 4);
+    return ~(__funnelshift_lc(0u, 0xffffffffu, 8 * lr) & ~__funnelshift_lc(0u, 0xffffffffu, 8 * hr));
 }
 
 __global__ void __launch_bounds__(256) cost_quad_kernel(Bufs b) {
@@ -542,7 +547,11 @@ __global__ void __launch_bounds__(256) cost_quad_kernel(Bufs b) {
         const bool narrow = active && nq <= 4;
         if (narrow) {
             const uint32_t slx = sl[x];
-            for (int t = 0; t < nq; ++t) cq[qo + t] = quad_cost(slx, sr, x, 4 * (q0 + t), lo, hi, W, xdef);
+            for (int t = 0; t < nq; ++t) {
+                const int d0 = 4 * (q0 + t);
+                const uint32_t w = quad_raw(slx, sr, x, d0, W, xdef);
+                cq[qo + t] = (t == 0 || t == nq - 1) ? w | quad_pad(d0, lo, hi) : w;
+            }
         }
         unsigned bw = __ballot_sync(0xffffffffu, active && !narrow);
         while (bw) {
@@ -555,8 +564,11 @@ __global__ void __launch_bounds__(256) cost_quad_kernel(Bufs b) {
             const bool xdef_w = __shfl_sync(0xffffffffu, xdef, src);
             const int q0w = lo_w >> 2, nqw = (hi_w >> 2) - q0w + 1;
             const uint32_t slx = sl[xw];
-            for (int t = lane; t < nqw; t += 32)
-                cq[qo_w + t] = quad_cost(slx, sr, xw, 4 * (q0w + t), lo_w, hi_w, W, xdef_w);
+            for (int t = lane; t < nqw; t += 32) {
+                const int d0 = 4 * (q0w + t);
+                const uint32_t w = quad_raw(slx, sr, xw, d0, W, xdef_w);
+                cq[qo_w + t] = (t == 0 || t == nqw - 1) ? w | quad_pad(d0, lo_w, hi_w) : w;
+            }
         }
     }
 }
