@@ -315,7 +315,10 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm,
 // fewer scanlines per warp give proportionally more warps for small batches.
 // One warp task: SPW scanlines (g-th group) of direction d of batch position
 // a; wbase = the warp's shared-memory area.
-template <int SPW>
+// kQ8: full-range windows as G x 8 quads (half the passes; the small-batch
+// mixed kernel, where each pass's latency chain is on the critical path)
+// instead of 2G x 4 (large batches, where the extra live registers cost)
+template <int SPW, bool kQ8 = false>
 __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, int d, int a, int g,
                                           uint32_t wbase) {
     constexpr int GN = 32 / SPW, QN = 4 / GN;
@@ -424,8 +427,9 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         }
         // wider windows: groups of G lanes x 4 quads, 32/G windows per pass;
         // a window's owner is the first lane of its scanline's group
-        const auto wide = [&](auto gtag, unsigned bw, bool full) {
+        const auto wide = [&](auto gtag, auto qtag, unsigned bw, bool full) {
             constexpr int G = decltype(gtag)::value;
+            constexpr int QQ = decltype(qtag)::value;  // quads per lane (full windows)
             constexpr int PER = 32 / G;
             const int gi = lane / G;
             while (bw) {
@@ -442,8 +446,8 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
                 const uint32_t sline = static_cast<uint32_t>(src / GN);
                 if (full)
-                    scan_pixel_full<G>(gi < cnt, pw, wbase + sline * SB, rbase + 4u * sline, costq,
-                                       out, P1x2, P2x2, P2x4, sp.full_rng);
+                    scan_pixel_full<G, QQ>(gi < cnt, pw, wbase + sline * SB, rbase + 4u * sline,
+                                           costq, out, P1x2, P2x2, P2x4, sp.full_rng);
                 else
                     scan_pixel<G, 4>(gi < cnt, pw, wbase + sline * SB, rbase + 4u * sline, costq,
                                      out, P1x2, P2x2, P2x4);
@@ -454,23 +458,33 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         // (rare: 5+ quads, not full range) (aggregation 8.10 -> 7.84 ms)
         if (cls & 0x200u) {
             const unsigned b2 = __ballot_sync(0xffffffffu, part && nq <= 8);
-            if (b2) wide(std::integral_constant<int, 2>{}, b2, false);
+            if (b2) wide(std::integral_constant<int, 2>{}, std::integral_constant<int, 4>{}, b2, false);
             const unsigned b4 = __ballot_sync(0xffffffffu, part && nq > 8 && nq <= 16);
-            if (b4) wide(std::integral_constant<int, 4>{}, b4, false);
+            if (b4) wide(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, b4, false);
             const unsigned b8 = __ballot_sync(0xffffffffu, part && nq > 16 && nq <= 32);
-            if (b8) wide(std::integral_constant<int, 8>{}, b8, false);
+            if (b8) wide(std::integral_constant<int, 8>{}, std::integral_constant<int, 4>{}, b8, false);
             const unsigned b16 = __ballot_sync(0xffffffffu, part && nq > 32);
-            if (b16) wide(std::integral_constant<int, 16>{}, b16, false);
+            if (b16) wide(std::integral_constant<int, 16>{}, std::integral_constant<int, 4>{}, b16, false);
         }
         // full-range windows (when their class covers them exactly) take the
         // unmasked pass
         if (cls & 0x100u) {
             const unsigned bf = __ballot_sync(0xffffffffu, owner && fullw);
-            switch (sp.full_ok) {  // = 4G of the full window's class
-                case 8: wide(std::integral_constant<int, 2>{}, bf, true); break;
-                case 16: wide(std::integral_constant<int, 4>{}, bf, true); break;
-                case 32: wide(std::integral_constant<int, 8>{}, bf, true); break;
-                default: wide(std::integral_constant<int, 16>{}, bf, true); break;
+            // G lanes x Q quads = the window's quads; with kQ8, Q = 8 where
+            // the group source table allows (G >= 2): half the passes, the
+            // per-pass dispatch, min and shared-memory overhead spread over 32
+            // levels per lane. Measured (frames/s): 8 sequences 4101 -> 4266,
+            // 64 sequences 6480 -> 6432 (64 registers, so not there).
+            constexpr bool FULL_Q4 = !kQ8;
+            using I2 = std::integral_constant<int, 2>;
+            using I4 = std::integral_constant<int, 4>;
+            using I8 = std::integral_constant<int, 8>;
+            using I16 = std::integral_constant<int, 16>;
+            switch (sp.full_ok) {  // quads of the full window
+                case 8: wide(I2{}, I4{}, bf, true); break;
+                case 16: if (FULL_Q4) wide(I4{}, I4{}, bf, true); else wide(I2{}, I8{}, bf, true); break;
+                case 32: if (FULL_Q4) wide(I8{}, I4{}, bf, true); else wide(I4{}, I8{}, bf, true); break;
+                default: if (FULL_Q4) wide(I16{}, I4{}, bf, true); else wide(I8{}, I8{}, bf, true); break;
             }
         }
     }
@@ -484,6 +498,9 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
 #ifndef SCAN_MINB
 #define SCAN_MINB 16
 #endif
+#ifndef SCAN_Q8
+#define SCAN_Q8 false  // (scan_kernel: 2G x 4-quad full-range passes, see scan_task)
+#endif
 template <int SPWH, int SPWV>
 __global__ void __launch_bounds__(32 * kScanWarps, SCAN_MINB) scan_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -495,9 +512,9 @@ __global__ void __launch_bounds__(32 * kScanWarps, SCAN_MINB) scan_kernel(Bufs b
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
     if (SPWH == SPWV || sp.dy[d] != 0)  // (one body when both widths agree)
-        scan_task<SPWV>(b, sp, d, a, g, wbase);
+        scan_task<SPWV, SCAN_Q8>(b, sp, d, a, g, wbase);
     else
-        scan_task<SPWH>(b, sp, d, a, g, wbase);
+        scan_task<SPWH, SCAN_Q8>(b, sp, d, a, g, wbase);
 }
 
 
@@ -652,7 +669,7 @@ __global__ void __launch_bounds__(32 * kScanWarps, GH == 32 ? 16 : 12) scan_mixe
     if (sp.dy[d] == 0)
         lines_task<GH, QH>(b, sp, d, a, g, wbase);
     else
-        scan_task<SPWV>(b, sp, d, a, g, wbase);
+        scan_task<SPWV, true>(b, sp, d, a, g, wbase);
 }
 
 
