@@ -62,6 +62,7 @@ struct ScanParams {
     uint32_t full_lohi;      // lohi of a full-range window: 0 | (d_max - 1) << 16
     uint32_t full_rng;       // quad range of a full-range window: 0 | (qmax - 1) << 16
     int warp_bytes;          // shared bytes per warp (scan_kernel)
+    int rline;               // line groups with register state: 1 = horizontal tasks, 2 = every direction
 };
 
 // Task order (blockIdx order ~ dispatch order): the first nlead directions
@@ -614,6 +615,153 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
     }
 }
 
+// Line groups with LANES OVER LEVELS and the path state in REGISTERS: a warp
+// owns 32/G scanlines of one direction, each a group of G lanes; lane lg of a
+// group owns the absolute quads [lg*Q, lg*Q + Q) (G*Q >= qmax: the line
+// groups' G x 4, or 32 x 1 (D <= 128) / 32 x 2 (D <= 256) — one scanline per
+// warp, the shortest step, for the W-step horizontal walks that are the
+// scan's critical path at small batches). A step has no shared memory, no
+// quad-range bookkeeping and a short dependent chain: two neighbour shuffles,
+// the min-plus update of the lane's own quads, one REDUX (G = 32) or log2 G
+// shuffles for the pixel's minimum — ~75 instructions per step for 32 x 1 and
+// ~130 for 8 x 4 (4 scanlines), against ~100 and ~260 in lines_task. Same
+// arithmetic and masking as scan_pixel: a level of a quad outside the
+// predecessor's quad range reads P2 (the register holds P2 there), every
+// level reads 0 at the scanline's first pixel, pad levels are poisoned by
+// their cost bytes 0xff. Records come from the row-major copy, RING steps
+// ahead, and the cost words PF steps ahead: no load is on the chain.
+// Records come from the row-major copy, RING steps ahead, and the cost words
+// PF steps ahead, in register rings. (Measured and dropped: the same pipeline
+// with cp.async into shared-memory rings — 100 instead of 86 instructions per
+// step for 32 x 1, and these walks are issue-bound even for one sequence: 1
+// sequence 1700 -> 1620 frames/s, 4 sequences 2790 -> 2400.)
+template <int G, int Q>
+__device__ __forceinline__ void rline_task(const Bufs& b, const ScanParams& sp, int d, int a, int g) {
+    constexpr int PF = Q >= 4 ? 2 : 4, RING = 2 * PF, LPW = 32 / G;
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    const int lg = lane & (G - 1);
+    const int W = b.W, H = b.H;
+    const int dx = sp.dx[d], dy = sp.dy[d];
+    const bool horiz = dy == 0;
+    const int nsteps = horiz ? W : H;
+    const int sl = dx * dy;
+    // scanline c: a row (horizontal), else the line x = c + sl*y (lines_task's numbering)
+    const int c = (horiz ? 0 : (sl == 1 ? -(H - 1) : 0)) + LPW * g + lane / G;
+    const int s = slot_of(b, a);
+    const uint2* meta = b.rmeta + static_cast<size_t>(s) * b.P;
+    const uint32_t* costq = b.costq + b.vqbase[a];
+    uint32_t* out = reinterpret_cast<uint32_t*>(
+        b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
+    const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
+    const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
+    const int ql = lg * Q;  // the lane's first absolute quad
+
+    // the line's records are a linear walk through the row-major copy: step k
+    // at i0 + k*di, for the steps [ka, kb) on which the line has a pixel;
+    // elsewhere {~0, 0} (a window no quad falls in)
+    int i0, di, ka = 0, kb = nsteps;
+    if (horiz) {
+        i0 = c * W + (dx < 0 ? 0 : W - 1);
+        di = dx < 0 ? 1 : -1;
+        if (c >= H) kb = 0;
+    } else {
+        const int y0 = dy < 0 ? 0 : H - 1, dyy = dy < 0 ? 1 : -1;
+        i0 = y0 * W + c + sl * y0;
+        di = dyy * (W + sl);
+        // x(k) = c + sl*(y0 + k*dyy) in [0, W)
+        if (sl == 0) {
+            if (c < 0 || c >= W) kb = 0;
+        } else {
+            const int x0 = c + sl * y0, dxx = sl * dyy;  // x(k) = x0 + k*dxx
+            if (dxx > 0) {
+                ka = max(0, -x0);
+                kb = min(nsteps, W - x0);
+            } else {
+                ka = max(0, x0 - (W - 1));
+                kb = min(nsteps, x0 + 1);
+            }
+        }
+    }
+    const uint2* mp = meta + i0;
+    auto rec_at = [&](int k) -> uint2 {
+        if (k < ka || k >= kb) return make_uint2(0xffffffffu, 0u);
+        return __ldg(mp + k * di);
+    };
+    // the lane's cost words of a window (zeros outside it)
+    auto cost_of = [&](const uint2& r, uint32_t (&cw)[Q]) {
+        const int q0 = static_cast<int>((r.x & 0xffffu) >> 2), q1 = static_cast<int>(r.x >> 18);
+        const uint32_t i = r.y + static_cast<uint32_t>(ql - q0);  // (used only where q >= q0)
+#pragma unroll
+        for (int t = 0; t < Q; ++t) {
+            const int q = ql + t;
+            cw[t] = (q >= q0 && q <= q1) ? __ldg(costq + (i + t)) : 0u;
+        }
+    };
+    uint2 rec[RING];
+    uint32_t cst[PF][Q];
+#pragma unroll
+    for (int j = 0; j < RING; ++j) rec[j] = rec_at(j);
+#pragma unroll
+    for (int j = 0; j < PF; ++j) cost_of(rec[j], cst[j]);
+    uint32_t MA[Q], MB[Q];  // M(4q), M(4q+1) | M(4q+2), M(4q+3) as u16x2
+#pragma unroll
+    for (int t = 0; t < Q; ++t) MA[t] = MB[t] = 0u;
+
+    for (int k0 = 0; k0 < nsteps; k0 += RING) {
+#pragma unroll
+        for (int j = 0; j < RING; ++j) {
+            const int k = k0 + j;
+            if (k >= nsteps) break;
+            const uint2 r = rec[j];
+            uint32_t cw[Q];
+#pragma unroll
+            for (int t = 0; t < Q; ++t) cw[t] = cst[j % PF][t];
+            // refill the rings: step k + PF's cost words, step k + RING's record
+            cost_of(rec[(j + PF) % RING], cst[j % PF]);
+            rec[j] = rec_at(k + RING);
+
+            const int q0 = static_cast<int>((r.x & 0xffffu) >> 2), q1 = static_cast<int>(r.x >> 18);
+            const bool act = r.x != 0xffffffffu;
+            // neighbour levels across the group's lanes; the ends of the level axis read P2
+            uint32_t left = P2x2, right = P2x2;
+            if constexpr (G > 1) {
+                const uint32_t l = __shfl_up_sync(0xffffffffu, MB[Q - 1], 1, G);
+                const uint32_t rr = __shfl_down_sync(0xffffffffu, MA[0], 1, G);
+                if (lg != 0) left = l;
+                if (lg != G - 1) right = rr;
+            }
+            uint32_t LA[Q], LB[Q];
+            bool in[Q];
+            uint32_t mn = 0xffffffffu;
+#pragma unroll
+            for (int t = 0; t < Q; ++t) {
+                const int q = ql + t;
+                in[t] = q >= q0 && q <= q1;  // (never where the line has no pixel)
+                const uint32_t CA = kPoisonQ & prmt_sx(cw[t], 0x9180u);
+                const uint32_t CB = kPoisonQ & prmt_sx(cw[t], 0xb3a2u);
+                const uint32_t lw = t == 0 ? left : MB[t > 0 ? t - 1 : 0];
+                const uint32_t rw = t == Q - 1 ? right : MA[t < Q - 1 ? t + 1 : 0];
+                const uint32_t mma = prmt(lw, MA[t], 0x5432u);     // M(d0-1), M(d0)
+                const uint32_t mpa = prmt(MA[t], MB[t], 0x5432u);  // M(d0+1), M(d0+2)
+                const uint32_t mpb = prmt(MB[t], rw, 0x5432u);     // M(d0+3), M(d0+4)
+                LA[t] = mad_u32(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, MA[t]), 1u, CA);
+                LB[t] = mad_u32(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, MB[t]), 1u, CB);
+                if (in[t]) mn = __vimin3_u16x2(mn, LA[t], LB[t]);
+            }
+            const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
+            const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
+            if (act) {
+#pragma unroll
+                for (int t = 0; t < Q; ++t) {
+                    MA[t] = in[t] ? __viaddmin_u16x2(LA[t], neg, P2x2) : P2x2;
+                    MB[t] = in[t] ? __viaddmin_u16x2(LB[t], neg, P2x2) : P2x2;
+                    if (in[t]) out[r.y + static_cast<uint32_t>(ql - q0) + t] = prmt(LA[t], LB[t], 0x6420u);
+                }
+            }
+        }
+    }
+}
+
 __host__ __device__ inline int lines_warp_bytes(int d_max, int G) {
     return (32 / G) * (scan_slot_bytes(d_max) + 4);
 }
@@ -628,7 +776,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
     decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
-    lines_task<G>(b, sp, d, a, g, wbase);
+    if (sp.rline >= (sp.dy[d] == 0 ? 1 : 2)) rline_task<G, 4>(b, sp, d, a, g);
+    else lines_task<G>(b, sp, d, a, g, wbase);
 }
 
 // Line groups everywhere, the horizontal lines with wider groups (GH lanes x
@@ -645,10 +794,13 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_mixed_kernel(Bufs 
     decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
-    if (sp.dy[d] == 0)
-        lines_task<GH, QH>(b, sp, d, a, g, wbase);
-    else
-        lines_task<G, 4>(b, sp, d, a, g, wbase);
+    if (sp.dy[d] == 0) {
+        if (sp.rline >= 1) rline_task<GH, QH>(b, sp, d, a, g);
+        else lines_task<GH, QH>(b, sp, d, a, g, wbase);
+    } else {
+        if (sp.rline >= 2) rline_task<G, 4>(b, sp, d, a, g);
+        else lines_task<G, 4>(b, sp, d, a, g, wbase);
+    }
 }
 
 // Mixed: horizontal lines as line groups (G lanes x 4 quads per scanline,
@@ -666,10 +818,12 @@ __global__ void __launch_bounds__(32 * kScanWarps, GH == 32 ? 16 : 12) scan_mixe
     decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
-    if (sp.dy[d] == 0)
-        lines_task<GH, QH>(b, sp, d, a, g, wbase);
-    else
+    if (sp.dy[d] == 0) {
+        if (sp.rline >= 1) rline_task<GH, QH>(b, sp, d, a, g);
+        else lines_task<GH, QH>(b, sp, d, a, g, wbase);
+    } else {
         scan_task<SPWV, true>(b, sp, d, a, g, wbase);
+    }
 }
 
 
@@ -906,6 +1060,10 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     for (int i = 0; i < k; ++i) {
         const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
         sp.task_off[i + 1] = sp.task_off[i] + (lines + 31) / 32;
+    }
+    {
+        const char* fr = std::getenv("TSGM_RLINE");
+        sp.rline = fr ? std::atoi(fr) : 1;
     }
     // one or two sequences or full-range frames: the line-group kernel; else
     // the scanline-group kernel (below ~12 sequences with line-group
