@@ -5,7 +5,7 @@ The product is the CUDA library ``lib/libtsgm_b200.so`` behind the C-ABI in
 ``include/tsgm_b200.h``; this package is its Python mirror of the reference's
 ``tsgm::`` API (see :mod:`.tsgm`)."""
 from .tsgm import (  # noqa: F401
-    DIAGONAL, NONDIAGONAL, DetectConfig, Engine, EngineConfig, FilterConfig, SgmParams,
+    DIAGONAL, NONDIAGONAL, DetectConfig, Engine, EngineConfig, FilterConfig, PipelinedEngine, SgmParams,
     OutlierOptions, StereoCalib, count_outliers, detect_candidate_windows, detect_moving_objects,
     greedy_merge, integral_image, outlier_rate,
     aggregate_paths, build_cost_volume, census_transform, correct, derive_search_ranges,

@@ -264,23 +264,19 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm,
             CB[t] = prmt(c, 0u, 0x4342u);
         }
     }
-    const uint32_t prng = lds32(rp);
+    // (a group without a pixel stays on the unchecked path: nothing is stored)
+    const uint32_t prng = pix ? lds32(rp) : full_rng;
     uint32_t w[Q + 2];
-    if (prng == full_rng) {
 #pragma unroll
-        for (int u = 0; u < Q + 2; ++u) {
-            const uint32_t raw = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
-            w[u] = raw;
-        }
-    } else {
+    for (int u = 0; u < Q + 2; ++u) w[u] = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
+    if (prng != full_rng) {
         const int pq0 = static_cast<int>(prng & 0xffffu);
         const uint32_t span = (prng >> 16) - static_cast<uint32_t>(pq0);
         const uint32_t fill = prng == kNoPred ? 0u : P2x4;
 #pragma unroll
         for (int u = 0; u < Q + 2; ++u) {
-            const uint32_t raw = lds32(sb + 4u * static_cast<uint32_t>(a0 + u));
             const bool in = static_cast<uint32_t>(a0 - 1 + u - pq0) <= span;
-            w[u] = in ? raw : fill;
+            w[u] = in ? w[u] : fill;
         }
     }
     uint32_t mn = 0xffffffffu;
@@ -434,14 +430,31 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
             constexpr int PER = 32 / G;
             const int gi = lane / G;
             while (bw) {
-                const bool mine = (bw >> lane) & 1u;
-                const int rank = __popc(bw & ((1u << lane) - 1u));
-                const bool go = mine && rank < PER;
-                if (go) sts32(srcbase + 4u * static_cast<uint32_t>(rank), static_cast<uint32_t>(lane));
-                const unsigned done = __ballot_sync(0xffffffffu, go);
-                const int cnt = __popc(done);
-                const int src = gi < cnt ? static_cast<int>(lds32(srcbase + 4u * static_cast<uint32_t>(gi))) : lane;
-                __syncwarp();
+                int src, cnt;
+                if constexpr (PER <= 4) {
+                    // the pass's windows = the lowest PER set bits of bw; group
+                    // gi takes the gi-th of them (warp-uniform bit arithmetic:
+                    // no shared-memory table, vote or barrier on the chain)
+                    unsigned nxt = bw, bsel = 0u;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) {
+                        if (j == gi) bsel = nxt;
+                        nxt &= nxt - 1u;
+                    }
+                    cnt = bsel != 0u ? PER : 0;  // (gi < cnt <=> the group has a window)
+                    src = bsel != 0u ? __ffs(bsel) - 1 : lane;
+                    bw = nxt;
+                } else {
+                    const bool mine = (bw >> lane) & 1u;
+                    const int rank = __popc(bw & ((1u << lane) - 1u));
+                    const bool go = mine && rank < PER;
+                    if (go) sts32(srcbase + 4u * static_cast<uint32_t>(rank), static_cast<uint32_t>(lane));
+                    const unsigned done = __ballot_sync(0xffffffffu, go);
+                    cnt = __popc(done);
+                    src = gi < cnt ? static_cast<int>(lds32(srcbase + 4u * static_cast<uint32_t>(gi))) : lane;
+                    __syncwarp();
+                    bw &= ~done;
+                }
                 PixMeta pw;
                 pw.lohi = full ? sp.full_lohi : __shfl_sync(0xffffffffu, mc.lohi, src);
                 pw.qo = __shfl_sync(0xffffffffu, mc.qo, src);
@@ -452,7 +465,6 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
                 else
                     scan_pixel<G, 4>(gi < cnt, pw, wbase + sline * SB, rbase + 4u * sline, costq,
                                      out, P1x2, P2x2, P2x4);
-                bw &= ~done;
             }
         };
         // the four partial-wide classes only when the step has such a window
@@ -809,7 +821,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_mixed_kernel(Bufs 
 template <int GH, int QH, int SPWV>
 // (G-lane groups: 12 CTAs per SM = 80 registers, no spills: 8 sequences
 // 3264 -> 3483 frames/s; 32-lane groups keep 16: 4 sequences 2447 vs 2099)
-__global__ void __launch_bounds__(32 * kScanWarps, GH == 32 ? 16 : 12) scan_mixed_kernel(Bufs b, ScanParams sp) {
+__global__ void __launch_bounds__(32 * kScanWarps, (GH == 32 && QH == 1) ? 16 : 12) scan_mixed_kernel(Bufs b, ScanParams sp) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int task = blockIdx.x * kScanWarps + warp;

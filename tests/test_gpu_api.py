@@ -133,3 +133,41 @@ def test_step_device_after_producer_stream(port):
         np.testing.assert_array_equal(eng.fetch(0, "state_p"), ref["p"])
         state = (ref["d"], ref["p"], ref["valid"])
     eng.close()
+
+
+def test_pipelined_engine_matches_one_context():
+    """PipelinedEngine (the batch over several contexts, each with its own
+    streams) returns exactly what one context returns: sequences are
+    independent (eval.cpp:114-144). 5 sequences over 2 and 3 contexts (uneven
+    groups), interleaved slot order, host and batched fetches."""
+    frames, S = 3, 5
+    scenes = []
+    for s in range(S):
+        cfg, calib = _scene(seed=10 + s, frames=frames)
+        L, R, P, _ = render(cfg)
+        scenes.append((L, R, P))
+    base = _engine(calib, max_slots=S)
+    order = [3, 0, 4, 1, 2]
+    for groups in (2, 3):
+        pe = tsgm.PipelinedEngine(base.cfg, groups)
+        assert len(pe.engines) == groups
+        for s in range(S):
+            base.reset(s)
+            pe.reset(s)
+        for k in range(frames):
+            mots = [EYE if k == 0 else tsgm.relative_motion(scenes[s][2][k - 1], scenes[s][2][k])
+                    for s in order]
+            ls, rs = [scenes[s][0][k] for s in order], [scenes[s][1][k] for s in order]
+            base.step(order, ls, rs, mots)
+            pe.step(order, ls, rs, mots)
+            outs = [np.zeros((H, W), np.int32) for _ in order]
+            pe.fetch_batch(order, "export_d", outs)
+            pe.sync()
+            for s, o in zip(order, outs):
+                assert np.array_equal(o, base.fetch(s, "export_d"))
+                for what in ("state_d", "state_p", "state_valid", "diff", "mask"):
+                    assert np.array_equal(pe.fetch(s, what), base.fetch(s, what)), (groups, k, s, what)
+                assert pe.cells(s) == base.cells(s)
+        assert pe.launches > 0
+        pe.close()
+    base.close()
