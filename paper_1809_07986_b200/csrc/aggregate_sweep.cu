@@ -38,7 +38,14 @@ namespace tsgm {
 constexpr int kScanWarps = 2;  // warps per CTA (one task each)
 
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
-__host__ __device__ inline int scan_slot_bytes(int d_max) { return 4 * ((d_max + 3) / 4 + 2); }
+#ifndef SCAN_SLOT_ODD
+#define SCAN_SLOT_ODD 1
+#endif
+__host__ __device__ inline int scan_slot_bytes(int d_max) {
+    const int w = (d_max + 3) / 4 + 2;
+    // (an odd word stride spreads the 32 scanlines' slots over the banks)
+    return 4 * (SCAN_SLOT_ODD ? (w | 1) : w);
+}
 // shared bytes per warp: 32 scanline slots, 32 quad ranges, 16 group sources
 __host__ __device__ inline int scan_warp_bytes(int d_max, int spw = 32) {
     return spw * (scan_slot_bytes(d_max) + 4) + 64;
@@ -187,10 +194,17 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
         // poison 0x3fff; quads past the window (and lanes without a pixel) are
         // poisoned whole. Poisoned levels lose every min and normalise to P2.
         const uint32_t* cw = costq + pm.qo + static_cast<uint32_t>(a0 - q0);
+        // a window's own lane (G = 1): its 4 allocated quads in one 128-bit
+        // load (windows are 16-byte aligned, alloc_quads)
+        uint32_t c4[4] = {0u, 0u, 0u, 0u};
+        if constexpr (G == 1 && !kPre) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(costq + pm.qo));
+            c4[0] = v.x; c4[1] = v.y; c4[2] = v.z; c4[3] = v.w;
+        }
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             act[t] = pix && k0 + t < nq;
-            const uint32_t c = kPre ? pre[t] : __ldg(cw + t);
+            const uint32_t c = kPre ? pre[t] : (G == 1 ? c4[t] : __ldg(cw + t));
             const uint32_t am = act[t] ? 0xffffffffu : 0u;
             // kPoisonQ & (x | ~am): x masked to 14 bits, or the poison when inactive
             CA[t] = kPoisonQ & (prmt_sx(c, 0x9180u) | ~am);
@@ -228,13 +242,23 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
     const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
     const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
     if (G > 1) __syncwarp();  // the group's reads of this slot are done
+    if constexpr (G == 1 && !kPre) {
+        // the 4 allocated quads in one 128-bit store (the words past the
+        // window's last quad are padding nobody reads)
+        if (pix) {
+            uint32_t o4[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int t = 0; t < Q; ++t) o4[t] = prmt(LA[t], LB[t], 0x6420u);
+            *reinterpret_cast<uint4*>(out + pm.qo) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+        }
+    }
 #pragma unroll
     for (int t = 0; t < Q; ++t) {
         if (!act[t]) continue;
         const uint32_t ma = __viaddmin_u16x2(LA[t], neg, P2x2);
         const uint32_t mb = __viaddmin_u16x2(LB[t], neg, P2x2);
         sts32(sb + 4u + 4u * static_cast<uint32_t>(a0 + t), prmt(ma, mb, 0x6420u));
-        (out + pm.qo + k0)[t] = prmt(LA[t], LB[t], 0x6420u);
+        if constexpr (!(G == 1 && !kPre)) (out + pm.qo + k0)[t] = prmt(LA[t], LB[t], 0x6420u);
     }
     if (pix && lg == 0) sts32(rp, static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16));
 }
@@ -257,11 +281,22 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm,
         // (a group without a pixel reads the volume's first window instead: in
         // bounds); a full window's quads hold no pad bytes
         const uint32_t* cw = costq + (pix ? pm.qo : 0u) + a0;
+        uint32_t cc[Q];
+        if constexpr (Q % 4 == 0 && !kPre) {
+            // the lane's quads as 128-bit loads (16-byte aligned windows)
+#pragma unroll
+            for (int t = 0; t < Q; t += 4) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(cw + t));
+                cc[t] = v.x; cc[t + 1] = v.y; cc[t + 2] = v.z; cc[t + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < Q; ++t) cc[t] = kPre ? pre[t] : __ldg(cw + t);
+        }
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
-            const uint32_t c = kPre ? pre[t] : __ldg(cw + t);
-            CA[t] = prmt(c, 0u, 0x4140u);
-            CB[t] = prmt(c, 0u, 0x4342u);
+            CA[t] = prmt(cc[t], 0u, 0x4140u);
+            CB[t] = prmt(cc[t], 0u, 0x4342u);
         }
     }
     // (a group without a pixel stays on the unchecked path: nothing is stored)
@@ -296,12 +331,21 @@ __device__ __forceinline__ void scan_pixel_full(bool pix, const PixMeta& pm,
     const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
     if (G > 1) __syncwarp();
     if (pix) {
+        uint32_t o[Q];
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             const uint32_t ma = __viaddmin_u16x2(LA[t], neg, P2x2);
             const uint32_t mb = __viaddmin_u16x2(LB[t], neg, P2x2);
             sts32(sb + 4u + 4u * static_cast<uint32_t>(a0 + t), prmt(ma, mb, 0x6420u));
-            (out + pm.qo + a0)[t] = prmt(LA[t], LB[t], 0x6420u);
+            o[t] = prmt(LA[t], LB[t], 0x6420u);
+        }
+        if constexpr (Q % 4 == 0) {
+#pragma unroll
+            for (int t = 0; t < Q; t += 4)
+                *reinterpret_cast<uint4*>(out + pm.qo + a0 + t) = make_uint4(o[t], o[t + 1], o[t + 2], o[t + 3]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < Q; ++t) (out + pm.qo + a0)[t] = o[t];
         }
         if (lg == 0) sts32(rp, full_rng);
     }
@@ -389,7 +433,7 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
 #ifndef SCAN_PREFETCH
 #define SCAN_PREFETCH 1
 #endif
-        if (SCAN_PREFETCH && act1 && lgs == 0) {  // step k+1's window towards L1 (its metadata arrived a step ago)
+        if (SCAN_PREFETCH == 1 && act1 && lgs == 0) {  // step k+1's window towards L1 (its metadata arrived a step ago)
             const int nb = 4 * static_cast<int>(quads_of(m1.lohi));  // the window's bytes (quad layout)
             const char* c0 = reinterpret_cast<const char*>(costq + m1.qo);
             // straight-line (windows are <= 64 quads, sweep_supported): 0.8%
@@ -397,6 +441,17 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
             asm volatile("prefetch.global.L1 [%0];" ::"l"(c0));
             if (nb + 4 > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 128));
             if (nb + 4 > 256) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 256));
+        }
+        // SCAN_PREFETCH 2: prefetches issued a pass, not a step, before their
+        // use (a step is ~6000 cycles under load and the L1 turns over in less):
+        // this step's WIDE window here (used after the narrow pass), the next
+        // step's narrow window after this step's narrow pass
+        if (SCAN_PREFETCH == 2 && active && lgs == 0 && quads_of(mc.lohi) > 4u) {
+            const int nb = 4 * static_cast<int>(quads_of(mc.lohi));
+            const char* c0 = reinterpret_cast<const char*>(costq + mc.qo);
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(c0));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 124));
+            if (nb > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 252));
         }
         act2 = k + 2 < nsteps && pixel_at(k + 2, p_tmp);
         if (act2) load_meta(p_tmp, m2);
@@ -421,6 +476,11 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         } else if (cls & 0x1eu) {
             // windows of <= 4 quads: the scanline's GN lanes x QN quads
             scan_pixel<GN, QN>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+        }
+        if (SCAN_PREFETCH == 2 && act1 && lgs == 0 && quads_of(m1.lohi) <= 4u) {
+            const char* c0 = reinterpret_cast<const char*>(costq + m1.qo);
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(c0));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + 12));  // (a window across two lines)
         }
         // wider windows: groups of G lanes x 4 quads, 32/G windows per pass;
         // a window's owner is the first lane of its scanline's group
@@ -859,7 +919,7 @@ constexpr int kCwWarps = 2;
 // per-warp shared bytes: qo[33], lh[32], cl[32] (u32), own[32*qmax] (u8),
 // best[32] (u32), qsum[32*qmax] (uint2, sub-pixel only)
 __host__ __device__ inline size_t cw_warp_bytes(int d_max, int subpix) {
-    const size_t qm = static_cast<size_t>((d_max - 1) / 4 + 1);
+    const size_t qm = alloc_quads(static_cast<uint32_t>((d_max - 1) / 4 + 1));  // allocated quads per pixel
     size_t bytes = 4 * 100 + 32 * qm;       // qo, lh, cl + own
     bytes = (bytes + 7) & ~static_cast<size_t>(7);
     bytes += 4 * 32;                         // best
@@ -886,7 +946,7 @@ __global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : CW_FULL_
     const int subpix = kLean ? 0 : subpix_in;
     extern __shared__ __align__(16) uint8_t cwm[];
     const int W = b.W, H = b.H;
-    const int qmax = (b.d_max - 1) / 4 + 1;
+    const int qmax = static_cast<int>(alloc_quads(static_cast<uint32_t>((b.d_max - 1) / 4 + 1)));
     const int lane = static_cast<int>(threadIdx.x & 31), wib = static_cast<int>(threadIdx.x >> 5);
     const int chunks = (W + 31) / 32;
     const long long task = static_cast<long long>(blockIdx.x) * kCwWarps + wib;
@@ -919,7 +979,9 @@ __global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : CW_FULL_
     }
     best_s[lane] = 0xffffffffu;
     const uint32_t qbase = __shfl_sync(0xffffffffu, my_q, 0);
-    const int my_nq = lane < np ? static_cast<int>(my_lh >> 18) - static_cast<int>((my_lh & 0xffffu) >> 2) + 1 : 0;
+    // the pixel's allocated quads (alloc_quads: pad quads hold no level of
+    // [lo, hi] and fall out in finish())
+    const int my_nq = lane < np ? static_cast<int>(alloc_quads((my_lh >> 18) - ((my_lh & 0xffffu) >> 2) + 1u)) : 0;
     const uint32_t rq = my_q - qbase;
     if (lane < np) {
         qo[lane] = rq;

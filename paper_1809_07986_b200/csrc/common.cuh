@@ -91,6 +91,16 @@ struct Bufs {
 
 __device__ __forceinline__ int slot_of(const Bufs& b, int a) { return b.slots[a]; }
 
+// Quads ALLOCATED to a window of nq quads in the quad layout (costq, pdir):
+// a multiple of kQuadAlign, so every window starts 16-byte aligned and the
+// scan moves a narrow window, or a lane's 4 quads of a wide one, as one
+// 128-bit access instead of 3-4 32-bit ones (the scan runs at ~74% L1/LSU
+// throughput with 4-byte accesses: 945 M L1 tag requests per 0.70 G cells).
+constexpr uint32_t kQuadAlign = 4;
+__host__ __device__ inline uint32_t alloc_quads(uint32_t nq) {
+    return (nq + (kQuadAlign - 1)) & ~(kQuadAlign - 1);
+}
+
 // Doubles -> u64 keys whose unsigned order is the numeric order; -0.0 is
 // canonicalised to +0.0 so ties behave like the reference's `!=` tests
 // (geometry.cpp:116-123).

@@ -418,7 +418,7 @@ void init_ctx(tsgm_ctx* ctx, const tsgm_config& c) {
     ctx->use_sweep = !force_scan &&
                      sweep_supported(ctx->W, ctx->H, ctx->d_max, c.sgm.p2);
     // multiple of 4 quads: the combine reads each direction 16 bytes at a time
-    b.quad_cap = (P * static_cast<size_t>((ctx->d_max - 1) / 4 + 1) + 3) & ~static_cast<size_t>(3);
+    b.quad_cap = (P * static_cast<size_t>(alloc_quads(static_cast<uint32_t>((ctx->d_max - 1) / 4 + 1))) + 3) & ~static_cast<size_t>(3);
     b.max_slots = c.max_slots;
     b.work = ctx->dalloc<int>(1);
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device));

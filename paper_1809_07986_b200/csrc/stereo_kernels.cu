@@ -139,8 +139,9 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& e
 
 // Quads of a window: aligned groups of 4 levels covering [lo, hi]; the
 // aggregation partials use a quad-aligned copy of the ragged layout.
+// (the layout allocates alloc_quads() of them: 16-byte aligned windows)
 __device__ __forceinline__ uint32_t quads_of(int lo, int hi) {
-    return static_cast<uint32_t>((hi >> 2) - (lo >> 2) + 1);
+    return alloc_quads(static_cast<uint32_t>((hi >> 2) - (lo >> 2) + 1));
 }
 
 template <bool kDerive>
@@ -355,7 +356,7 @@ __global__ void offsets_tile_kernel(Bufs b, int arm_keys) {
         const size_t g = pbase + static_cast<size_t>(y) * b.W + x;
         const uint32_t lh = in ? b.lohi[g] : 0u;
         const uint32_t nc = in ? (lh >> 16) - (lh & 0xffffu) + 1u : 0u;
-        const uint32_t nq = in ? (lh >> 18) - ((lh & 0xffffu) >> 2) + 1u : 0u;
+        const uint32_t nq = in ? alloc_quads((lh >> 18) - ((lh & 0xffffu) >> 2) + 1u) : 0u;
         uint32_t ic = nc, iq = nq;  // inclusive warp scans
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kPtW * kPtH, 5) predict_tile_kernel(Bufs b, do
         b.hi[g] = static_cast<uint16_t>(hi);
         b.lohi[g] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
         cells = static_cast<uint32_t>(hi - lo + 1);
-        quads = static_cast<uint32_t>((hi >> 2) - (lo >> 2) + 1);
+        quads = alloc_quads(static_cast<uint32_t>((hi >> 2) - (lo >> 2) + 1));
     }
     // this tile row's counts (one warp = one row of 32 pixels)
     cells = __reduce_add_sync(0xffffffffu, cells);
