@@ -369,9 +369,9 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
     const int dx = sp.dx[d], dy = sp.dy[d];
     const int SB = scan_slot_bytes(b.d_max);
     const int gs = lane / GN, lgs = lane % GN;  // the lane's scanline in the warp, rank in its group
-    const uint32_t my_sb = wbase + static_cast<uint32_t>(gs) * SB;
-    const uint32_t rbase = wbase + static_cast<uint32_t>(SPW * SB);
-    const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(gs);
+    uint32_t my_sb = wbase + static_cast<uint32_t>(gs) * SB;
+    uint32_t rbase = wbase + static_cast<uint32_t>(SPW * SB);
+    uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(gs);
     const uint32_t srcbase = rbase + 4u * SPW;  // 16 group source lanes
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
@@ -387,6 +387,15 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
     const uint32_t* costq = b.costq + b.vqbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
+#ifndef SCAN_PIN
+#define SCAN_PIN 0
+#endif
+#if SCAN_PIN
+    // (tuning: make the loop invariants opaque so they stay in registers
+    // instead of being recomputed every step: 33 instructions per step)
+    asm volatile("" : "+r"(my_sb), "+r"(my_rp), "+r"(rbase));
+    asm volatile("" : "+l"(costq), "+l"(out));
+#endif
 
     // line geometry: horizontal directions sweep x with lane = row; the others
     // sweep y with lane = line c, pixel x = c + sl*y (sl = dx*dy)
@@ -660,8 +669,14 @@ __device__ __forceinline__ void lines_task(const Bufs& b, const ScanParams& sp, 
         const uint32_t nqn = quads_of(m.lohi);
         const uint32_t k0 = static_cast<uint32_t>(lg * Q);
         const uint32_t* cw = costq + m.qo + (k0 < nqn ? k0 : nqn - 1u);
+        if (Q == 4 && act && k0 + 4u <= nqn) {
+            // (the lane's 4 quads lie inside a 16-byte aligned window: one load)
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(cw));
+            cn[0] = v.x; cn[1] = v.y; cn[2 % Q] = v.z; cn[3 % Q] = v.w;
+        } else {
 #pragma unroll
-        for (int t = 0; t < Q; ++t) cn[t] = act ? __ldg(cw + t) : 0u;
+            for (int t = 0; t < Q; ++t) cn[t] = act ? __ldg(cw + t) : 0u;
+        }
     };
     preload(act1, m1);
     for (int k = 0; k < nsteps; ++k) {
