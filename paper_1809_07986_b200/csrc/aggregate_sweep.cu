@@ -174,7 +174,8 @@ __device__ __forceinline__ uint32_t quads_of(uint32_t lohi) {
 // `rp` are the shared addresses of the scanline's slot and quad range.
 // kPre: the window's cost words were loaded a step early (pre[0..Q-1], from
 // costq + qo + min(k0, nq - 1), see lines_task).
-template <int G, int Q, bool kPre = false>
+// kV128 (G = 1): the window's 4 allocated quads leave as one 128-bit store.
+template <int G, int Q, bool kPre = false, bool kV128 = false>
 __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
                                            uint32_t sb, uint32_t rp, const uint32_t* costq,
                                            uint32_t* out, uint32_t P1x2, uint32_t P2x2,
@@ -194,17 +195,10 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
         // poison 0x3fff; quads past the window (and lanes without a pixel) are
         // poisoned whole. Poisoned levels lose every min and normalise to P2.
         const uint32_t* cw = costq + pm.qo + static_cast<uint32_t>(a0 - q0);
-        // a window's own lane (G = 1): its 4 allocated quads in one 128-bit
-        // load (windows are 16-byte aligned, alloc_quads)
-        uint32_t c4[4] = {0u, 0u, 0u, 0u};
-        if constexpr (G == 1 && !kPre) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(costq + pm.qo));
-            c4[0] = v.x; c4[1] = v.y; c4[2] = v.z; c4[3] = v.w;
-        }
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             act[t] = pix && k0 + t < nq;
-            const uint32_t c = kPre ? pre[t] : (G == 1 ? c4[t] : __ldg(cw + t));
+            const uint32_t c = kPre ? pre[t] : __ldg(cw + t);
             const uint32_t am = act[t] ? 0xffffffffu : 0u;
             // kPoisonQ & (x | ~am): x masked to 14 bits, or the poison when inactive
             CA[t] = kPoisonQ & (prmt_sx(c, 0x9180u) | ~am);
@@ -242,7 +236,7 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
     const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
     const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
     if (G > 1) __syncwarp();  // the group's reads of this slot are done
-    if constexpr (G == 1 && !kPre) {
+    if constexpr (G == 1 && kV128) {
         // the 4 allocated quads in one 128-bit store (the words past the
         // window's last quad are padding nobody reads)
         if (pix) {
@@ -258,7 +252,7 @@ __device__ __forceinline__ void scan_pixel(bool pix, const PixMeta& pm,
         const uint32_t ma = __viaddmin_u16x2(LA[t], neg, P2x2);
         const uint32_t mb = __viaddmin_u16x2(LB[t], neg, P2x2);
         sts32(sb + 4u + 4u * static_cast<uint32_t>(a0 + t), prmt(ma, mb, 0x6420u));
-        if constexpr (!(G == 1 && !kPre)) (out + pm.qo + k0)[t] = prmt(LA[t], LB[t], 0x6420u);
+        if constexpr (!(G == 1 && kV128)) (out + pm.qo + k0)[t] = prmt(LA[t], LB[t], 0x6420u);
     }
     if (pix && lg == 0) sts32(rp, static_cast<uint32_t>(q0) | (static_cast<uint32_t>(q1) << 16));
 }
@@ -369,9 +363,9 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
     const int dx = sp.dx[d], dy = sp.dy[d];
     const int SB = scan_slot_bytes(b.d_max);
     const int gs = lane / GN, lgs = lane % GN;  // the lane's scanline in the warp, rank in its group
-    uint32_t my_sb = wbase + static_cast<uint32_t>(gs) * SB;
-    uint32_t rbase = wbase + static_cast<uint32_t>(SPW * SB);
-    uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(gs);
+    const uint32_t my_sb = wbase + static_cast<uint32_t>(gs) * SB;
+    const uint32_t rbase = wbase + static_cast<uint32_t>(SPW * SB);
+    const uint32_t my_rp = rbase + 4u * static_cast<uint32_t>(gs);
     const uint32_t srcbase = rbase + 4u * SPW;  // 16 group source lanes
     const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
     const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
@@ -387,15 +381,6 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
     const uint32_t* costq = b.costq + b.vqbase[a];
     uint32_t* out = reinterpret_cast<uint32_t*>(
         b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4);
-#ifndef SCAN_PIN
-#define SCAN_PIN 0
-#endif
-#if SCAN_PIN
-    // (tuning: make the loop invariants opaque so they stay in registers
-    // instead of being recomputed every step: 33 instructions per step)
-    asm volatile("" : "+r"(my_sb), "+r"(my_rp), "+r"(rbase));
-    asm volatile("" : "+l"(costq), "+l"(out));
-#endif
 
     // line geometry: horizontal directions sweep x with lane = row; the others
     // sweep y with lane = line c, pixel x = c + sl*y (sl = dx*dy)
@@ -437,6 +422,15 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
     for (int k = 0; k < nsteps; ++k) {
         const bool active = act1;
         const PixMeta mc = m1;
+        // (32 scanlines per warp) the lane's own window — its 4 allocated
+        // quads, 16-byte aligned — loaded here, a whole bookkeeping section
+        // (~110 instructions) before the narrow pass uses it: the first use
+        // of these words held 18% of the kernel's stall samples
+        uint32_t cpre[4] = {0u, 0u, 0u, 0u};
+        if constexpr (SPW == 32) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(costq + mc.qo));
+            cpre[0] = v.x; cpre[1] = v.y; cpre[2] = v.z; cpre[3] = v.w;
+        }
         act1 = act2;
         m1 = m2;
 #ifndef SCAN_PREFETCH
@@ -477,11 +471,11 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
         if (SPW == 32) {
             // windows of <= 4 quads: the lane itself, Q = the warp's widest such window
             if (cls & 0x10u)
-                scan_pixel<1, 4>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+                scan_pixel<1, 4, true, true>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4, cpre);
             else if (cls & 0x8u)
-                scan_pixel<1, 3>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+                scan_pixel<1, 3, true, true>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4, cpre);
             else if (cls & 0x6u)
-                scan_pixel<1, 2>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
+                scan_pixel<1, 2, true, true>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4, cpre);
         } else if (cls & 0x1eu) {
             // windows of <= 4 quads: the scanline's GN lanes x QN quads
             scan_pixel<GN, QN>(narrow, mc, my_sb, my_rp, costq, out, P1x2, P2x2, P2x4);
