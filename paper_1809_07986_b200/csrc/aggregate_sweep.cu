@@ -494,7 +494,7 @@ __device__ __forceinline__ void scan_task(const Bufs& b, const ScanParams& sp, i
             const int gi = lane / G;
             while (bw) {
                 int src, cnt;
-                if constexpr (PER <= 8) {
+                if constexpr (PER <= 4) {
                     // the pass's windows = the lowest PER set bits of bw; group
                     // gi takes the gi-th of them (warp-uniform bit arithmetic:
                     // no shared-memory table, vote or barrier on the chain)
