@@ -26,6 +26,17 @@
 // quad-aligned copy of the ragged layout (qoff); the combine kernel adds the 4
 // or 8 directions into S in the reference's layout. u16 sums never overflow
 // (SgmParams::validate, sgm.cpp:21-22), so the grouping is exact.
+//
+// Layout. Every window is allocated a multiple of 4 quads (alloc_quads,
+// common.cuh), so it starts 16-byte aligned: a narrow window, and a lane's 4
+// quads of a full-range window, move as ONE 128-bit load (costs) and ONE
+// 128-bit store (path costs). The scan is co-limited by integer issue and by
+// the L1/LSU pipe; 4-byte accesses cost it 3x the L1 tag requests.
+//
+// Small batches. Line groups (a fixed group of G lanes per scanline) give
+// more, shorter tasks when few sequences fill the GPU: lines_task keeps the
+// state in shared memory like scan_task; rline_task keeps it in registers
+// (lanes over absolute levels) and is used for the horizontal walks.
 #include "common.cuh"
 
 #include <cstdio>

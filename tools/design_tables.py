@@ -50,7 +50,7 @@ def config_table():
                  f"{c['aggregation_hbm_frac']:.3f} (latency-bound) |")
     L.append(f"| 2: 64 × 30 (the metric) | {c2['cpu_frames_per_s']:.1f} frames/s (full workload, one sequence per core) | "
              f"{c2['gpu_frames_per_s']:.0f} frames/s device-resident, **{c2['gpu_e2e_frames_per_s']:.0f} frames/s e2e** "
-             f"(host frames in, maps out) | **{c2['speedup_e2e']:.0f}× e2e** | **{c2['aggregation_hbm_frac']:.3f}** |")
+             f"(host frames in, maps out) | **{c2['speedup_e2e']:.1f}× e2e** | **{c2['aggregation_hbm_frac']:.3f}** |")
     L.append("| 2 at 32 / 16 / 8 sequences per GPU (2/4/8-GPU shares) | — | "
              + " / ".join(f"{r['gpu_frames_per_s']:.0f}" for r in sh) + " frames/s ("
              + " / ".join(f"{r['share_of_64_sequence_rate']:.2f}" for r in sh) + " of the 64-sequence rate) | — | — |")

@@ -3,7 +3,7 @@
 # launch list + full captures; outputs under gpurun_out/final (summarised into
 # profiles/ by tools/summarize_ncu.py and tools/config_table.py)
 set -x
-D=gpurun_out/final3; mkdir -p $D
+D=gpurun_out/final; mkdir -p $D
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $D/gpu.txt
 nproc >> $D/gpu.txt; grep -m1 "model name" /proc/cpuinfo >> $D/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > $D/pytest_gpu.log 2>&1; echo "pytest rc $?"
