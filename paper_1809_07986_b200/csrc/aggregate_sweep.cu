@@ -81,6 +81,7 @@ struct ScanParams {
     uint32_t full_rng;       // quad range of a full-range window: 0 | (qmax - 1) << 16
     int warp_bytes;          // shared bytes per warp (scan_kernel)
     int rline;               // line groups with register state: 1 = horizontal tasks, 2 = every direction
+    int all_full;            // every window of the launch is [0, d_max - 1] and d_max = 16 G: rfull_task
 };
 
 // Task order (blockIdx order ~ dispatch order): the first nlead directions
@@ -854,6 +855,116 @@ __device__ __forceinline__ void rline_task(const Bufs& b, const ScanParams& sp, 
     }
 }
 
+// rline_task for a batch whose windows are ALL full range [0, d_max - 1] with
+// d_max = 16 G (frames from the empty state: frame 0 of every sequence,
+// config 3's full-range setting, the noise calibration): nothing is read per
+// pixel but its costs. Pixel p's window is the G 16-byte words p*G .. p*G+G-1
+// of the quad layout (every window holds 4G quads, so qoff[p] = 4G*p), lane
+// lg of the scanline's group loads word p*G + lg, updates its 16 levels (no
+// pads, no range tests, no records), and stores word p*G + lg of the
+// direction's path costs. ~90 instructions per step of 32/G scanlines
+// against ~200 in lines_task + scan_pixel_full.
+template <int G>
+__device__ __forceinline__ void rfull_task(const Bufs& b, const ScanParams& sp, int d, int a, int g) {
+    constexpr int Q = 4, PF = 2, LPW = 32 / G;
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    const int lg = lane & (G - 1);
+    const int W = b.W, H = b.H;
+    const int dx = sp.dx[d], dy = sp.dy[d];
+    const bool horiz = dy == 0;
+    const int nsteps = horiz ? W : H;
+    const int sl = dx * dy;
+    const int c = (horiz ? 0 : (sl == 1 ? -(H - 1) : 0)) + LPW * g + lane / G;
+    const uint4* cost4 = reinterpret_cast<const uint4*>(b.costq + b.vqbase[a]) + lg;
+    uint4* out4 = reinterpret_cast<uint4*>(
+        b.pdir + (static_cast<size_t>(d) * b.pool_quads + b.vqbase[a]) * 4) + lg;
+    const uint32_t P1x2 = static_cast<uint32_t>(sp.p1) * 0x10001u;
+    const uint32_t P2x2 = static_cast<uint32_t>(sp.p2) * 0x10001u;
+    // the line's pixels: step k at pixel i0 + k*di for k in [ka, kb)
+    int i0, di, ka = 0, kb = nsteps;
+    if (horiz) {
+        i0 = c * W + (dx < 0 ? 0 : W - 1);
+        di = dx < 0 ? 1 : -1;
+        if (c >= H) kb = 0;
+    } else {
+        const int y0 = dy < 0 ? 0 : H - 1, dyy = dy < 0 ? 1 : -1;
+        i0 = y0 * W + c + sl * y0;
+        di = dyy * (W + sl);
+        if (sl == 0) {
+            if (c < 0 || c >= W) kb = 0;
+        } else {
+            const int x0 = c + sl * y0, dxx = sl * dyy;  // x(k) = x0 + k*dxx in [0, W)
+            if (dxx > 0) {
+                ka = max(0, -x0);
+                kb = min(nsteps, W - x0);
+            } else {
+                ka = max(0, x0 - (W - 1));
+                kb = min(nsteps, x0 + 1);
+            }
+        }
+    }
+    auto cost_at = [&](int k) -> uint4 {
+        if (k < ka || k >= kb) return make_uint4(0u, 0u, 0u, 0u);
+        return __ldg(cost4 + static_cast<long long>(i0 + k * di) * G);
+    };
+    uint4 ring[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) ring[j] = cost_at(ka + j);
+    uint32_t MA[Q], MB[Q];
+#pragma unroll
+    for (int t = 0; t < Q; ++t) MA[t] = MB[t] = 0u;
+    // (every group walks its own [ka, kb): the warp runs the longest walk)
+    const int span = kb - ka;
+    int maxspan = span;
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) maxspan = max(maxspan, __shfl_xor_sync(0xffffffffu, maxspan, o));
+    for (int j0 = 0; j0 < maxspan; j0 += PF) {
+#pragma unroll
+        for (int jj = 0; jj < PF; ++jj) {
+            const int j = j0 + jj;
+            if (j >= maxspan) break;
+            const bool act = j < span;
+            const uint4 cv = ring[jj];
+            ring[jj] = (j + PF < span) ? cost_at(ka + j + PF) : make_uint4(0u, 0u, 0u, 0u);
+            const uint32_t cw[Q] = {cv.x, cv.y, cv.z, cv.w};
+            uint32_t left = P2x2, right = P2x2;
+            {
+                const uint32_t l = __shfl_up_sync(0xffffffffu, MB[Q - 1], 1, G);
+                const uint32_t rr = __shfl_down_sync(0xffffffffu, MA[0], 1, G);
+                if (lg != 0) left = l;
+                if (lg != G - 1) right = rr;
+            }
+            uint32_t LA[Q], LB[Q];
+            uint32_t mn = 0xffffffffu;
+#pragma unroll
+            for (int t = 0; t < Q; ++t) {
+                const uint32_t CA = prmt(cw[t], 0u, 0x4140u);
+                const uint32_t CB = prmt(cw[t], 0u, 0x4342u);
+                const uint32_t lw = t == 0 ? left : MB[t > 0 ? t - 1 : 0];
+                const uint32_t rw = t == Q - 1 ? right : MA[t < Q - 1 ? t + 1 : 0];
+                const uint32_t mma = prmt(lw, MA[t], 0x5432u);
+                const uint32_t mpa = prmt(MA[t], MB[t], 0x5432u);
+                const uint32_t mpb = prmt(MB[t], rw, 0x5432u);
+                LA[t] = mad_u32(__viaddmin_u16x2(__vminu2(mma, mpa), P1x2, MA[t]), 1u, CA);
+                LB[t] = mad_u32(__viaddmin_u16x2(__vminu2(mpa, mpb), P1x2, MB[t]), 1u, CB);
+                mn = __vimin3_u16x2(mn, LA[t], LB[t]);
+            }
+            const uint32_t m = group_min<G>(min(mn & 0xffffu, mn >> 16));
+            const uint32_t neg = ((0x10000u - m) & 0xffffu) * 0x10001u;
+            if (act) {
+#pragma unroll
+                for (int t = 0; t < Q; ++t) {
+                    MA[t] = __viaddmin_u16x2(LA[t], neg, P2x2);
+                    MB[t] = __viaddmin_u16x2(LB[t], neg, P2x2);
+                }
+                out4[static_cast<long long>(i0 + (ka + j) * di) * G] =
+                    make_uint4(prmt(LA[0], LB[0], 0x6420u), prmt(LA[1], LB[1], 0x6420u),
+                               prmt(LA[2], LB[2], 0x6420u), prmt(LA[3], LB[3], 0x6420u));
+            }
+        }
+    }
+}
+
 __host__ __device__ inline int lines_warp_bytes(int d_max, int G) {
     return (32 / G) * (scan_slot_bytes(d_max) + 4);
 }
@@ -868,7 +979,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_kernel(Bufs b, Sca
     decode_task(sp, task, d, a, g);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) +
                            static_cast<uint32_t>(warp) * static_cast<uint32_t>(sp.warp_bytes);
-    if (sp.rline >= (sp.dy[d] == 0 ? 1 : 2)) rline_task<G, 4>(b, sp, d, a, g);
+    if (G >= 2 && sp.all_full) rfull_task<(G >= 2 ? G : 2)>(b, sp, d, a, g);
+    else if (sp.rline >= (sp.dy[d] == 0 ? 1 : 2)) rline_task<G, 4>(b, sp, d, a, g);
     else lines_task<G>(b, sp, d, a, g, wbase);
 }
 
@@ -890,7 +1002,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) scan_lines_mixed_kernel(Bufs 
         if (sp.rline >= 1) rline_task<GH, QH>(b, sp, d, a, g);
         else lines_task<GH, QH>(b, sp, d, a, g, wbase);
     } else {
-        if (sp.rline >= 2) rline_task<G, 4>(b, sp, d, a, g);
+        if (sp.all_full) rfull_task<G>(b, sp, d, a, g);
+        else if (sp.rline >= 2) rline_task<G, 4>(b, sp, d, a, g);
         else lines_task<G, 4>(b, sp, d, a, g, wbase);
     }
 }
@@ -1158,6 +1271,9 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     {
         const char* fr = std::getenv("TSGM_RLINE");
         sp.rline = fr ? std::atoi(fr) : 1;
+        // TSGM_RFULL=0 keeps full-range launches on lines_task (tests compare both)
+        const char* ff = std::getenv("TSGM_RFULL");
+        sp.all_full = (full_range && sp.full_ok && !(ff && std::atoi(ff) == 0)) ? 1 : 0;
     }
     // one or two sequences or full-range frames: the line-group kernel; else
     // the scanline-group kernel (below ~12 sequences with line-group
@@ -1200,6 +1316,10 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
                           4 * G / gh);
         else
             std::snprintf(g_variant, sizeof g_variant, "scan_lines_kernel<%d>", G);
+        if (sp.all_full) {  // (every window full range: rfull_task)
+            const size_t used = std::strlen(g_variant);
+            std::snprintf(g_variant + used, sizeof g_variant - used, "[rfull]");
+        }
         if (gh != G) {
             auto kern = G == 8 ? (gh == 16 ? scan_lines_mixed_kernel<8, 16, 2>
                                            : scan_lines_mixed_kernel<8, 32, 1>)

@@ -248,6 +248,7 @@ struct tsgm_ctx {
     std::string last_kernels;  // aggregation kernels of the last step's last chunk
     int last_chunks = 0;       // volume chunks of the last step
     int last_c0 = 0;           // batch index of the last chunk's first sequence
+    bool last_full = false;    // the last chunk's windows are all full range (every sequence fresh)
     bool stage_timing = false;
     std::vector<cudaEvent_t> tev;
     std::vector<int> tstage;
@@ -690,6 +691,7 @@ void run_step(tsgm_ctx* ctx, int n) {
         }
         for (int a = 0; a < m; ++a) ctx->vol_owner[a] = ctx->h_slots[c0 + a];
         ctx->last_c0 = c0;
+        ctx->last_full = full;
         c0 += m;
     }
     // correct + diff + mask + render, then the export median (A16-A19, A21)
@@ -1077,9 +1079,11 @@ int tsgm_bench_aggregate(tsgm_ctx* ctx, int32_t n, const int32_t* slots, int32_t
         std::vector<double> H(16 * static_cast<size_t>(n), 0.0);
         upload_step(ctx, n, slots, dl.data(), dr.data(), H.data());
         Launch L{ctx->st, &ctx->launches};  // (no stage marks)
-        aggregate(ctx, ctx->b, n, L);  // warm
+        // (the same kernel choice as the step that built these volumes)
+        const bool full = ctx->last_full;
+        aggregate(ctx, ctx->b, n, L, false, true, full);  // warm
         CK(cudaEventRecord(ctx->ev0, ctx->st));
-        for (int r = 0; r < reps; ++r) aggregate(ctx, ctx->b, n, L);
+        for (int r = 0; r < reps; ++r) aggregate(ctx, ctx->b, n, L, false, true, full);
         CK(cudaEventRecord(ctx->ev1, ctx->st));
         CK(cudaEventSynchronize(ctx->ev1));
         float ms = 0.f;

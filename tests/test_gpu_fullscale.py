@@ -79,6 +79,8 @@ def test_config2_bench_workload_64x30(port):
     assert set(chunks) == {1}
     # the reduced frames ran the kernels bench.py times at 64 sequences per GPU
     assert set(kernels[1:]) == {"scan_kernel<32,32>+combine_wta_kernel<8,1>"}, set(kernels)
+    # frame 0 (every sequence fresh: all windows full range) ran the full-range line groups
+    assert kernels[0] == "scan_lines_kernel<8>[rfull]+combine_wta_kernel<8,1>", kernels[0]
 
 
 def test_config1_full_size_30_frames(port):
