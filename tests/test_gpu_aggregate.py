@@ -45,12 +45,18 @@ CASES = [
 
 @pytest.mark.parametrize("kernel", ["groups32", "groups16", "groups8", "groups32h8", "groups32h16",
                                     "groups16h8", "groups32hlines", "groups8hlines", "groups32hlines8", "lines",
-                                    "lines16h", "lines32h", "scanline"])
+                                    "lines16h", "lines32h", "scanline",
+                                    "lines@r0", "lines@r2", "lines32h@r0", "lines32h@r2",
+                                    "groups32hlines@r0", "groups32hlines8@r0"])
 @pytest.mark.parametrize("w,h,d_max,p_full", CASES)
 def test_random_ragged_volumes(port, monkeypatch, kernel, w, h, d_max, p_full):
     """groupsN[hM]: the scanline-group kernel with N scanlines per warp (M for
     the horizontal lines) (batched throughput path); lines: the line-group kernel (single sequences,
-    full-range frames); scanline: the per-direction fallback."""
+    full-range frames); scanline: the per-direction fallback; @rN: TSGM_RLINE=N
+    (line groups with the path state in shared memory / in registers)."""
+    kernel, _, rl = kernel.partition("@r")
+    if rl:  # register line groups: 0 = off, 1 = horizontal tasks (default), 2 = every direction
+        monkeypatch.setenv("TSGM_RLINE", rl)
     if kernel == "scanline":
         monkeypatch.setenv("TSGM_FORCE_SCANLINE_AGG", "1")
     elif kernel.startswith("lines"):

@@ -171,3 +171,29 @@ def test_pipelined_engine_matches_one_context():
         assert pe.launches > 0
         pe.close()
     base.close()
+
+
+@pytest.mark.parametrize("d_max", [32, 64, 128])
+def test_full_range_line_groups_match_the_masked_path(monkeypatch, port, d_max):
+    """Frame 0 of fresh sequences (every window [0, d_max - 1]) runs rfull_task
+    (register line groups, the window compiled in); TSGM_RFULL=0 keeps
+    lines_task + scan_pixel_full. Same S, same WTA, both equal to the oracle's
+    aggregate_paths (sgm.cpp:39-161)."""
+    w, h = 96, 40
+    cfg = SceneConfig.baseline_config(1, width=w, height=h, focal=100.0, cx=47.5, cy=19.5,
+                                      d_max=d_max, seed=3, n_movers=1, frames=1)
+    calib = tsgm.StereoCalib(cfg.focal, cfg.cx, cfg.cy, cfg.baseline, w, h, d_max)
+    L, R, _, _ = render(cfg, 0, 1)
+    params = tsgm.SgmParams(10, 120, 8, 0, d_max)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TSGM_RFULL", mode)
+        eng = tsgm.Engine(tsgm.EngineConfig(calib, params, tsgm.FilterConfig(), max_slots=3))
+        eng.step([0, 1, 2], [L[0]] * 3, [R[0]] * 3, [EYE] * 3)
+        out[mode] = (eng.last_kernels(), eng.fetch(1, "agg"), eng.fetch(1, "meas_d"), eng.fetch(1, "cost"))
+        eng.close()
+    assert "[rfull]" in out["1"][0] and "[rfull]" not in out["0"][0], (out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1]) and np.array_equal(out["1"][2], out["0"][2])
+    lo = np.zeros((h, w), np.uint16)
+    hi = np.full((h, w), d_max - 1, np.uint16)
+    np.testing.assert_array_equal(out["1"][1], port.aggregate(out["1"][3], lo, hi, params))
