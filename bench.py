@@ -263,8 +263,8 @@ def run_ours(args):
 
     # contexts per GPU: the batch split over independent contexts (own
     # streams) so one group's issue-bound scan overlaps the others' DRAM-bound
-    # kernels (tsgm.PipelinedEngine); auto = 2 from 16 sequences per GPU
-    groups = args.groups if args.groups > 0 else (2 if n >= 16 else 1)
+    # kernels (tsgm.PipelinedEngine); auto = 2 for 16..63 sequences per GPU
+    groups = args.groups if args.groups > 0 else (2 if 16 <= n < 64 else 1)
     ecfg = tsgm.EngineConfig(calib, sgm, filt, max_slots=n, device=local, keep_volumes=False)
     eng = tsgm.PipelinedEngine(ecfg, groups) if groups > 1 else tsgm.Engine(ecfg)
     slots = list(range(n))
@@ -657,7 +657,7 @@ def main():
     ap.add_argument("--seqs", type=int, default=N_SEQ)
     ap.add_argument("--frames", type=int, default=N_FRAMES)
     ap.add_argument("--groups", type=int, default=0,
-                    help="contexts per GPU (0 = auto: 2 from 16 sequences per GPU)")
+                    help="contexts per GPU (0 = auto: 2 for 16..63 sequences per GPU)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher/rank plumbing only, no engine (CPU tests)")

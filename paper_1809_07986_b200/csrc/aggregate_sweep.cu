@@ -43,6 +43,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <vector>
+#include <algorithm>
 
 namespace tsgm {
 
@@ -82,6 +84,13 @@ struct ScanParams {
     int warp_bytes;          // shared bytes per warp (scan_kernel)
     int rline;               // line groups with register state: 1 = horizontal tasks, 2 = every direction
     int all_full;            // every window of the launch is [0, d_max - 1] and d_max = 16 G: rfull_task
+    // non-lead tasks split by length (plan_task_order): per slot, n_long tasks
+    // whose 32 lines all cross the whole image (direction i: groups long_g0[i]
+    // .. of long_off[i+1] - long_off[i] tasks), then n_short tasks of the
+    // shorter diagonal lines near the image corners, longest first
+    int n_long, n_short;
+    int long_off[9], long_g0[8];
+    uint8_t short_d[256], short_g[256];
 };
 
 // Task order (blockIdx order ~ dispatch order): the first nlead directions
@@ -89,7 +98,10 @@ struct ScanParams {
 // over all slots, so they start first; then the other directions
 // SEQUENCE-major, so one sequence's downward (and upward) scans are resident
 // together and sweep the same cost / record rows at the same time: those rows
-// are read from L2 instead of DRAM by all but the first of them.
+// are read from L2 instead of DRAM by all but the first of them. The diagonal
+// tasks near the image corners (lines shorter than the image height) come
+// LAST, over all slots, longest first: the kernel's final wave then drains
+// through short tasks instead of full-length ones.
 __device__ __forceinline__ void decode_task(const ScanParams& sp, int task, int& d, int& a, int& g) {
     const int lead = sp.task_off[sp.nlead] * sp.n;
     if (task < lead) {
@@ -99,6 +111,21 @@ __device__ __forceinline__ void decode_task(const ScanParams& sp, int task, int&
         const int groups = sp.task_off[d + 1] - sp.task_off[d];
         a = r / groups;
         g = r % groups;
+    } else if (sp.n_long > 0) {
+        const int t = task - lead;
+        if (t < sp.n_long * sp.n) {
+            a = t / sp.n_long;
+            const int r = t % sp.n_long;
+            d = sp.nlead;
+            while (r >= sp.long_off[d + 1]) ++d;
+            g = sp.long_g0[d] + r - sp.long_off[d];
+        } else {
+            const int u = t - sp.n_long * sp.n;
+            const int si = u / sp.n;
+            a = u % sp.n;
+            d = sp.short_d[si];
+            g = sp.short_g[si];
+        }
     } else {
         const int per = sp.task_off[sp.ndir] - sp.task_off[sp.nlead];  // tasks per slot
         const int t = task - lead;
@@ -1220,6 +1247,63 @@ __global__ void __launch_bounds__(32 * kCwWarps, kLean ? CW_LEAN_MINB : CW_FULL_
 thread_local char g_variant[128];
 const char* last_sweep_variant() { return g_variant; }
 
+// Split the non-lead tasks of a slot into long ones (every line crosses the
+// whole image) and short ones (decode_task); per[i] = lines per task of
+// direction i. Leaves n_long = 0 (one sequence-major list) when the short
+// list does not fit its table or nothing is long.
+static void plan_task_order(ScanParams& sp, int W, int H, const int* per) {
+    sp.n_long = sp.n_short = 0;
+    const char* fo = std::getenv("TSGM_SCAN_ORDER");
+    if (fo && std::strcmp(fo, "flat") == 0) return;
+    struct Short { int len, d, g; };
+    std::vector<Short> shorts;
+    int nl = 0;
+    for (int i = 0; i < sp.ndir; ++i) sp.long_off[i] = 0, sp.long_g0[i] = 0;
+    for (int i = sp.nlead; i < sp.ndir; ++i) {
+        sp.long_off[i] = nl;
+        const int groups = sp.task_off[i + 1] - sp.task_off[i];
+        const int sl = sp.dx[i] * sp.dy[i];
+        if (sp.dy[i] == 0) return;  // (a horizontal direction outside the lead: keep one list)
+        if (sl == 0) {  // vertical: every line is H pixels
+            sp.long_g0[i] = 0;
+            nl += groups;
+            continue;
+        }
+        const int cstart = sl == 1 ? -(H - 1) : 0;
+        const int lo = sl == 1 ? 0 : H - 1, hi = sl == 1 ? W - H : W - 1;  // full-length lines
+        auto line_len = [&](int c) {
+            const int a = sl == 1 ? std::max(0, -c) : std::max(0, c - (W - 1));
+            const int z = sl == 1 ? std::min(H - 1, W - 1 - c) : std::min(H - 1, c);
+            return std::max(0, z - a + 1);
+        };
+        int g0 = -1, cnt = 0;
+        for (int g = 0; g < groups; ++g) {
+            const int c0 = cstart + per[i] * g, c1 = c0 + per[i] - 1;
+            if (c0 >= lo && c1 <= hi) {
+                if (g0 < 0) g0 = g;
+                ++cnt;
+            } else {
+                int len = 0;
+                for (int c = c0; c <= c1; ++c) len = std::max(len, line_len(c));
+                shorts.push_back({len, i, g});
+            }
+        }
+        sp.long_g0[i] = std::max(g0, 0);
+        nl += cnt;
+    }
+    sp.long_off[sp.ndir] = nl;
+    if (nl == 0 || shorts.size() > 256 || shorts.empty()) return;
+    for (const Short& t : shorts)
+        if (t.g > 255) return;
+    std::stable_sort(shorts.begin(), shorts.end(), [](const Short& x, const Short& y) { return x.len > y.len; });
+    for (size_t k = 0; k < shorts.size(); ++k) {
+        sp.short_d[k] = static_cast<uint8_t>(shorts[k].d);
+        sp.short_g[k] = static_cast<uint8_t>(shorts[k].g);
+    }
+    sp.n_long = nl;
+    sp.n_short = static_cast<int>(shorts.size());
+}
+
 void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int path_set,
                             int write_s, int do_wta, Launch L, int subpix, bool full_range) {
     ScanParams sp{};
@@ -1373,6 +1457,11 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
             const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
             const int per = sp.dy[i] == 0 ? (hlines ? 32 / hg : spwh) : spw;
             sp.task_off[i + 1] = sp.task_off[i] + (lines + per - 1) / per;
+        }
+        {
+            int per[8];
+            for (int i = 0; i < k; ++i) per[i] = sp.dy[i] == 0 ? (hlines ? 32 / hg : spwh) : spw;
+            plan_task_order(sp, b.W, b.H, per);
         }
         sp.warp_bytes = std::max(scan_warp_bytes(b.d_max, std::max(spw, spwh)),
                                  hlines ? lines_warp_bytes(b.d_max, hg) : 0);
