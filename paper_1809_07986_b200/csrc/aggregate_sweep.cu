@@ -48,7 +48,10 @@
 
 namespace tsgm {
 
-constexpr int kScanWarps = 2;  // warps per CTA (one task each)
+#ifndef SCAN_WARPS
+#define SCAN_WARPS 2
+#endif
+constexpr int kScanWarps = SCAN_WARPS;  // warps per CTA (one task each)
 
 // slot: quads -1 .. ceil(D/4) (the ends are only ever read masked)
 #ifndef SCAN_SLOT_ODD
