@@ -1362,7 +1362,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         const char* ff = std::getenv("TSGM_RFULL");
         sp.all_full = (full_range && sp.full_ok && !(ff && std::atoi(ff) == 0)) ? 1 : 0;
     }
-    // one or two sequences or full-range frames: the line-group kernel; else
+    // one sequence or full-range frames: the line-group kernel; else
     // the scanline-group kernel (below ~12 sequences with line-group
     // horizontal tasks: 4 sequences 2153 -> 2246 frames/s, 1 sequence equal).
     // TSGM_SCAN_KERNEL=lines|groups forces one (tests).
@@ -1378,7 +1378,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
     const int sms = b.num_sms > 0 ? b.num_sms : 148;  // thresholds measured on a 148-SM B200
     const char* force = std::getenv("TSGM_SCAN_KERNEL");
     const bool lines_mode =
-        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < sms * 5);
+        force ? std::strcmp(force, "lines") == 0 : (full_range || batched_warps < sms * 3);
     if (lines_mode) {
         const int lpw = 32 / G;
         // horizontal lines with GH-lane groups (TSGM_LINES_H=8|16|32; G = 8 or 16 only)
@@ -1446,8 +1446,12 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         // (fewer instructions per step, 4x the warps): 32 up to ~4 sequences
         // (4: 2255 -> 2318 frames/s; 8: 3244 -> 2613); TSGM_MIXED_GH=8|32
         const char* fmg = std::getenv("TSGM_MIXED_GH");
-        const int mgh = fmg ? std::atoi(fmg) : (batched_warps < sms * 9 ? 32 : 8);
-        const int hg = mgh == 32 ? 32 : G;
+        // (with register line groups, frames/s: 2 sequences 2101 (line-group
+        // kernel) -> 2615 (this kernel, 32-lane groups; G-lane groups 2454);
+        // 3: 3157 (32) -> 3230 (G); 4: 3351 (32) -> 3621 (G))
+        const int mgh = fmg ? std::atoi(fmg) : (batched_warps < sms * 5 ? 32 : 8);
+        // (16 lanes x 2 quads for D = 128: two rows per warp, between the two)
+        const int hg = mgh == 32 ? 32 : (mgh == 16 && G == 8) ? 16 : G;
         // (round 2, frames/s: 32 sequences 5759 (8) -> 5948 (16); 16 sequences
         // 5005 (8) vs 4234 (16); 64 equal for 16 and 32)
         int spwh = fspwh ? std::atoi(fspwh)
@@ -1474,7 +1478,7 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         auto kern = scan_kernel<32, 32>;
         if (hlines)
             std::snprintf(g_variant, sizeof g_variant, "scan_mixed_kernel<%d,%d,%d>", hg,
-                          hg == 32 ? 4 * G / 32 : 4, spw);
+                          4 * G / hg, spw);
         else
             std::snprintf(g_variant, sizeof g_variant, "scan_kernel<%d,%d>",
                           spw == 8 ? 8 : spwh, spw);
@@ -1484,6 +1488,9 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
                                                                          : scan_mixed_kernel<32, 1, 32>)
                               : (spw == 8 ? scan_mixed_kernel<32, 2, 8> : spw == 16 ? scan_mixed_kernel<32, 2, 16>
                                                                          : scan_mixed_kernel<32, 2, 32>);
+            else if (hg == 16 && G == 8)
+                kern = spw == 8 ? scan_mixed_kernel<16, 2, 8> : spw == 16 ? scan_mixed_kernel<16, 2, 16>
+                                                                : scan_mixed_kernel<16, 2, 32>;
             else if (G == 8)
                 kern = spw == 8 ? scan_mixed_kernel<8, 4, 8> : spw == 16 ? scan_mixed_kernel<8, 4, 16>
                                                                : scan_mixed_kernel<8, 4, 32>;
