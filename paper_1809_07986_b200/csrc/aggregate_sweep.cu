@@ -1388,6 +1388,9 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
         // 21.1 -> 22.9 ms)
         int gh = flh ? std::atoi(flh) : (batched_warps < sms * 9 ? 32 : G);
         if ((G != 8 && G != 16) || gh <= G || (gh != 16 && gh != 32)) gh = G;
+        // (all windows full range: rfull_task for every direction beats 32-lane
+        // horizontal groups at any batch: 1 sequence 1135 -> 1351 frames/s, 4: 2213 -> 2561)
+        if (sp.all_full && !flh) gh = G;
         sp.task_off[0] = 0;
         for (int i = 0; i < k; ++i) {
             const int lines = sp.dy[i] == 0 ? b.H : b.W + (sp.dx[i] != 0 ? b.H - 1 : 0);
@@ -1437,10 +1440,11 @@ void launch_aggregate_sweep(const Bufs& b, int n, int p1, int p2, int paths, int
                        : !tall ? 32 : batched_warps < sms * 40 ? 8 : batched_warps < sms * 80 ? 16 : 32;
         if (spw != 8 && spw != 16) spw = 32;
         // TSGM_SCAN_SPW_H=lines: horizontal lines as line groups (G = 8 or 16)
-        // (default below ~12 sequences: 8 sequences 2712 -> 3268 frames/s)
+        // (default up to 16 sequences: 8 sequences 2712 -> 3268 frames/s; with
+        // register line groups 12 sequences 4337 -> 4759, 16 equal)
         const char* fspwh = std::getenv("TSGM_SCAN_SPW_H");
         const bool hlines = (fspwh ? std::strcmp(fspwh, "lines") == 0
-                                   : !fspw && !tall && batched_warps < sms * 24) &&
+                                   : !fspw && !tall && batched_warps < sms * 34) &&
                             (G == 8 || G == 16);
         // the line groups' width: G lanes x 4 quads, or 32 lanes x 4G/32 quads
         // (fewer instructions per step, 4x the warps): 32 up to ~4 sequences
